@@ -1,0 +1,185 @@
+"""ctypes binding of the C ABI declared in include/coolchic_b200.h.
+
+The same declarations bind all three libraries that export the ABI: the B200
+product (``libcoolchic_b200.so``) and the two checkers under ``oracle/``.  Only
+the product library is loaded by :func:`load_product`; the checkers are loaded
+by tests/bench through :func:`load_library` with an explicit path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+PKG_DIR = Path(__file__).resolve().parent
+REPO_DIR = PKG_DIR.parent
+PRODUCT_SO = PKG_DIR / "libcoolchic_b200.so"
+
+CC_OK, CC_ERR_CONFIG, CC_ERR_FORMAT, CC_ERR_TRAINING, CC_ERR_CUDA, CC_ERR_STATE = range(6)
+
+
+class DecoderConfigC(C.Structure):
+    _fields_ = [
+        ("preset", C.c_int),
+        ("spatial_ctx", C.c_int),
+        ("ifce_dim", C.c_int),
+        ("arm_width", C.c_int),
+        ("arm_hidden", C.c_int),
+        ("synth_hidden", C.c_int),
+        ("synth_posts", C.c_int),
+        ("use_hyperlatents", C.c_int),
+        ("use_stabilizer", C.c_int),
+    ]
+
+
+class EncoderConfigC(C.Structure):
+    _fields_ = [
+        ("warmup_candidates", C.c_int),
+        ("warmup_keep", C.c_int),
+        ("warmup_iters", C.c_int),
+        ("main_iters", C.c_int),
+        ("hardround_iters", C.c_int),
+        ("lr_start", C.c_double),
+        ("lr_end", C.c_double),
+        ("noise_std_start", C.c_double),
+        ("noise_std_end", C.c_double),
+        ("temp_start", C.c_double),
+        ("temp_end", C.c_double),
+        ("hardround_lr", C.c_double),
+        ("lambda_", C.c_double),
+        ("seed", C.c_uint64),
+        ("use_soap", C.c_int),
+        ("true_cost_interval", C.c_int),
+        ("log_path", C.c_char_p),
+    ]
+
+
+class LayoutC(C.Structure):
+    _fields_ = [
+        ("height", C.c_int),
+        ("width", C.c_int),
+        ("levels", C.c_int),
+        ("hyper_count", C.c_int),
+        ("n_grids", C.c_int),
+        ("n_latents", C.c_int64),
+        ("n_tensors", C.c_int),
+        ("n_params", C.c_int64),
+        ("pad", C.c_int),
+    ]
+
+
+class GridInfoC(C.Structure):
+    _fields_ = [
+        ("level", C.c_int),
+        ("hyper", C.c_int),
+        ("rows", C.c_int),
+        ("cols", C.c_int),
+        ("offset", C.c_int64),
+        ("ifce_slot", C.c_int),
+    ]
+
+
+class ParamInfoC(C.Structure):
+    _fields_ = [
+        ("name", C.c_char * 32),
+        ("rows", C.c_int),
+        ("cols", C.c_int),
+        ("size", C.c_int64),
+        ("offset", C.c_int64),
+    ]
+
+
+class TrainStatsC(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int64),
+        ("true_cost", C.c_double),
+        ("psnr", C.c_double),
+        ("rate_bpp", C.c_double),
+        ("restarts", C.c_int),
+        ("skipped_steps", C.c_int),
+        ("seconds", C.c_double),
+    ]
+
+
+_P = C.c_void_p
+_F = C.POINTER(C.c_float)
+_D = C.POINTER(C.c_double)
+_I64 = C.POINTER(C.c_int64)
+_I32 = C.POINTER(C.c_int32)
+_I = C.POINTER(C.c_int)
+
+# name -> (restype, argtypes); exactly the symbols include/coolchic_b200.h declares
+SIGNATURES = {
+    "cc_last_error": (C.c_char_p, []),
+    "cc_impl_name": (C.c_char_p, []),
+    "cc_decoder_config_preset": (C.c_int, [C.c_char_p, C.POINTER(DecoderConfigC)]),
+    "cc_encoder_config_default": (C.c_int, [C.POINTER(EncoderConfigC)]),
+    "cc_encoder_config_with_total": (C.c_int, [C.c_int, C.POINTER(EncoderConfigC)]),
+    "cc_count_macs_per_pixel": (C.c_double, [C.POINTER(DecoderConfigC), C.c_int, C.c_int]),
+    "cc_make_synthetic_image": (C.c_int, [C.c_int, C.c_int, C.c_uint64, _F]),
+    "cc_trainer_create": (
+        C.c_int,
+        [_F, C.c_int, C.c_int, C.POINTER(EncoderConfigC), C.POINTER(DecoderConfigC), C.c_int,
+         C.POINTER(_P)],
+    ),
+    "cc_trainer_destroy": (None, [_P]),
+    "cc_trainer_upload_image": (C.c_int, [_P, _F]),
+    "cc_trainer_layout": (C.c_int, [_P, C.POINTER(LayoutC)]),
+    "cc_trainer_grid_info": (C.c_int, [_P, C.c_int, C.POINTER(GridInfoC)]),
+    "cc_trainer_param_info": (C.c_int, [_P, C.c_int, C.POINTER(ParamInfoC)]),
+    "cc_trainer_fresh_candidate": (C.c_int, [_P, C.c_int]),
+    "cc_trainer_set_state": (C.c_int, [_P, _F, _F, _F, _F, _I64, _F, _F, _I64]),
+    "cc_trainer_get_state": (C.c_int, [_P, _F, _F, _F, _F, _I64, _F, _F, _I64]),
+    "cc_trainer_get_grads": (C.c_int, [_P, _F, _F]),
+    "cc_trainer_get_q": (C.c_int, [_P, _I32]),
+    "cc_trainer_get_counters": (C.c_int, [_P, _I64, _I]),
+    "cc_trainer_set_counters": (C.c_int, [_P, C.c_int64, C.c_int]),
+    "cc_trainer_proxy_iteration": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, _D]),
+    "cc_trainer_proxy_iterations": (C.c_int, [_P, C.c_int, _D, _D, _D, _D, _I]),
+    "cc_trainer_hardround_iteration": (C.c_int, [_P, C.c_double, C.c_int, _D]),
+    "cc_trainer_true_cost": (C.c_int, [_P, _D, _D, _D]),
+    "cc_trainer_quantize_all": (C.c_int, [_P]),
+    "cc_trainer_load_pads_from_q": (C.c_int, [_P]),
+    "cc_trainer_last_terms": (C.c_int, [_P, _D, _D]),
+    "cc_trainer_snapshot": (C.c_int, [_P, C.c_int, C.c_double]),
+    "cc_trainer_snapshot_cost": (C.c_int, [_P, C.c_int, _D]),
+    "cc_trainer_restore": (C.c_int, [_P, C.c_int]),
+    "cc_trainer_reset_optimizers": (C.c_int, [_P]),
+    "cc_trainer_take_candidate": (C.c_int, [_P, C.c_int, C.c_double]),
+    "cc_trainer_load_candidate": (C.c_int, [_P, C.c_int]),
+    "cc_trainer_candidate_cost": (C.c_int, [_P, C.c_int, _D]),
+    "cc_trainer_warmup": (C.c_int, [_P]),
+    "cc_trainer_train": (C.c_int, [_P, C.POINTER(TrainStatsC), _F, _I32, _F]),
+}
+
+
+def header_symbols() -> list[str]:
+    """Function names declared in include/coolchic_b200.h (parsed, not assumed)."""
+    import re
+
+    text = (REPO_DIR / "include" / "coolchic_b200.h").read_text()
+    return sorted(set(re.findall(r"\b(cc_[a-z_0-9]+)\s*\(", text)))
+
+
+def load_library(path: os.PathLike | str) -> C.CDLL:
+    lib = C.CDLL(str(path))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_PRODUCT = None
+
+
+def load_product() -> C.CDLL:
+    """Load the sm_100a library.  There is no fallback: a missing build is an error."""
+    global _PRODUCT
+    if _PRODUCT is None:
+        if not PRODUCT_SO.exists():
+            raise RuntimeError(
+                f"{PRODUCT_SO} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        _PRODUCT = load_library(PRODUCT_SO)
+    return _PRODUCT

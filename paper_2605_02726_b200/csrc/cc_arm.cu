@@ -1,0 +1,596 @@
+// cc_arm.cu — the auto-regressive entropy model (ARM + IFCE), forward and
+// backward fused into ONE persistent kernel over every grid of the pyramid.
+//
+// Replaces rate_pass (entropy_model.hpp:180-336), i.e. per latent:
+//   gather 14 causal neighbours + IFCE context        entropy_model.hpp:232-248
+//   MLP d -> w -> w -> 2 (+ linear stabilizer)        entropy_model.hpp:250-255
+//   Laplace mu/sigma, bits (rate)                     entropy_model.hpp:257-273
+//   rate backward to (mu, sigma_raw, value)           entropy_model.hpp:276-296
+//   MLP backward (dH2, dH1, dC)                       entropy_model.hpp:298-310
+//   weight gradients dW1..dW3, dstab, IFCE dWf        entropy_model.hpp:301-321
+// In the training proxy nothing is sequential across latents (every ŷ is
+// known), so all grids run in one launch from a tile table.
+//
+// B200 design: one thread owns one latent's data path (context, activations
+// and their gradients stay in registers; the weights sit in shared memory and
+// are read as broadcast LDS.128).  The weight gradients are per-tile small
+// GEMMs over the latent dimension: the per-latent vectors go to shared memory
+// and every thread owns a 2x4 micro-tile of (dW | db), accumulating over the
+// 128 latents of the tile in fp32 and across tiles in fp64 shared memory.
+// CTAs are persistent (grid = SMs x occupancy) and walk the tile table in a
+// fixed stride, so every sum has a fixed order: no float atomics, bitwise
+// deterministic.  The latent-side gradients are NOT scattered: dC (S planes),
+// dF (F planes) and the own-value term are written per latent and gathered by
+// k_latent_grad, the IFCE coarse-grid term through a 2x2 block-sum pyramid
+// (k_pyramid) — W_f^T is linear, so sum-then-multiply equals the reference's
+// multiply-then-scatter (entropy_model.hpp:322-330).
+#include <cuda_runtime.h>
+
+#include "cc_kernels.h"
+#include "cc_math.cuh"
+#include "cc_reduce.cuh"
+
+namespace ccb {
+
+constexpr int kArmTile = 128;  // latents per tile == threads per CTA
+constexpr int kRMax = 12;      // max IFCE source grids (hyper 4 + main 7)
+constexpr int kFMax = 8;       // max IFCE width
+
+__host__ __device__ constexpr int round4(int n) { return (n + 3) / 4 * 4; }
+// row stride (floats) with an odd number of 16-byte chunks: conflict-free LDS.128
+__host__ __device__ constexpr int odd_chunks(int n) {
+    return ((round4(n) / 4) % 2 == 0) ? round4(n) + 4 : round4(n);
+}
+
+template <int DP, int WP>
+struct ArmCfg {
+    static constexpr int LC = odd_chunks(DP + 1);   // context row, ones at DP
+    static constexpr int LH = odd_chunks(WP + 1);   // activation row, ones at WP
+    static constexpr int LDH = odd_chunks(WP);      // activation-gradient row
+    static constexpr int LR = odd_chunks(kRMax + 1);  // IFCE source row, ones at kRMax
+    static constexpr int LF = odd_chunks(kFMax);    // dF row
+    static constexpr int LDR = 4;                   // (dmu, dsigma_raw, 0, 0)
+    // phase A rows: C | H2 | dH1 | draw | R | dF ; phase B rows: H1 | dH2
+    static constexpr int OA_C = 0;
+    static constexpr int OA_H2 = OA_C + kArmTile * LC;
+    static constexpr int OA_DH1 = OA_H2 + kArmTile * LH;
+    static constexpr int OA_DR = OA_DH1 + kArmTile * LDH;
+    static constexpr int OA_R = OA_DR + kArmTile * LDR;
+    static constexpr int OA_DF = OA_R + kArmTile * LR;
+    static constexpr int ACT = OA_DF + kArmTile * LF;
+    static constexpr int OB_H1 = 0;
+    static constexpr int OB_DH2 = kArmTile * LH;
+    static_assert(OB_DH2 + kArmTile * LDH <= ACT, "phase B must fit in phase A");
+    // upper bound of the ARM+IFCE partial region (unpadded dims <= padded)
+    static constexpr int NACC =
+        WP * DP + WP + WP * WP + WP + 2 * WP + 2 + 2 * DP + kMaxSlots * (kFMax * kRMax + kFMax);
+    // micro-tile jobs (2 rows x 4 cols)
+    static constexpr int NJ1 = (WP / 2) * (round4(DP + 1) / 4);  // dH1 x [C|1]
+    static constexpr int NJ3 = round4(WP + 1) / 4;              // draw x [H2|1]
+    static constexpr int NJ4 = round4(DP) / 4;                  // draw x C (stab)
+    static constexpr int NJ5 = (kFMax / 2) * (round4(kRMax + 1) / 4);  // dF x [R|1]
+    static constexpr int NJA = NJ1 + NJ3 + NJ4 + NJ5;
+    static constexpr int NJ2 = (WP / 2) * (round4(WP + 1) / 4);  // dH2 x [H1|1]
+};
+
+template <int DP, int WP>
+struct alignas(16) ArmSmem {
+    using K = ArmCfg<DP, WP>;
+    alignas(16) float W1[WP * DP];
+    alignas(16) float W2[WP * WP];
+    alignas(16) float W3[2 * WP];
+    alignas(16) float stab[2 * DP];
+    alignas(16) float b1[WP];
+    alignas(16) float b2[WP];
+    alignas(16) float b3[4];
+    alignas(16) float Wf[kMaxSlots][kFMax * kRMax];
+    alignas(16) float bf[kMaxSlots][kFMax];
+    alignas(16) float act[K::ACT];
+    alignas(16) double acc[K::NACC];
+    int ctx_dy[kMaxCtx], ctx_dx[kMaxCtx];
+    double red[kArmTile / 32];
+};
+
+// 2x4 outer-product accumulation over the tile's latents.
+template <int LDA, int LDB>
+__device__ __forceinline__ void mt_accum(const float* __restrict__ A, const float* __restrict__ B,
+                                         int a0, int b0, float (&acc)[8]) {
+#pragma unroll 4
+    for (int i = 0; i < kArmTile; ++i) {
+        const float2 av = *reinterpret_cast<const float2*>(A + i * LDA + a0);
+        const float4 bv = *reinterpret_cast<const float4*>(B + i * LDB + b0);
+        acc[0] = fmaf(av.x, bv.x, acc[0]);
+        acc[1] = fmaf(av.x, bv.y, acc[1]);
+        acc[2] = fmaf(av.x, bv.z, acc[2]);
+        acc[3] = fmaf(av.x, bv.w, acc[3]);
+        acc[4] = fmaf(av.y, bv.x, acc[4]);
+        acc[5] = fmaf(av.y, bv.y, acc[5]);
+        acc[6] = fmaf(av.y, bv.z, acc[6]);
+        acc[7] = fmaf(av.y, bv.w, acc[7]);
+    }
+}
+
+// Region index (== flat parameter index; the ARM region starts at arm.l1.w,
+// which is parameter 0) of output (a, b) of job `kind`, or -1 to discard.
+struct OutMap {
+    int w_off, b_off;  // weight / bias parameter offsets (b_off < 0: none)
+    int rows, cols;    // real (unpadded) extents
+    int ones_col;      // column index of the bias "ones" column
+    __device__ __forceinline__ int operator()(int a, int b) const {
+        if (a >= rows) return -1;
+        if (b < cols) return w_off + a * cols + b;
+        if (b == ones_col && b_off >= 0) return b_off + a;
+        return -1;
+    }
+};
+
+template <int DP, int WP, int MODE>
+__global__ void __launch_bounds__(kArmTile) k_arm(const Plan* __restrict__ pp,
+                                                  const int2* __restrict__ tiles, int ntiles) {
+    using K = ArmCfg<DP, WP>;
+    const Plan& P = *pp;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    ArmSmem<DP, WP>& sm = *reinterpret_cast<ArmSmem<DP, WP>*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int D = P.D, Wd = P.Wd, S = P.S, F = P.F;
+    const float* prm = P.params;
+
+    // ---- weights -> shared memory, zero-padded to (WP, DP) ----
+    for (int e = tid; e < WP * DP; e += kArmTile) {
+        const int a = e / DP, b = e - a * DP;
+        sm.W1[e] = (a < Wd && b < D) ? prm[P.off_l1w + a * D + b] : 0.0f;
+    }
+    for (int e = tid; e < WP * WP; e += kArmTile) {
+        const int a = e / WP, b = e - a * WP;
+        sm.W2[e] = (a < Wd && b < Wd) ? prm[P.off_l2w + a * Wd + b] : 0.0f;
+    }
+    for (int e = tid; e < 2 * WP; e += kArmTile) {
+        const int a = e / WP, b = e - a * WP;
+        sm.W3[e] = b < Wd ? prm[P.off_hw + a * Wd + b] : 0.0f;
+    }
+    for (int e = tid; e < 2 * DP; e += kArmTile) {
+        const int a = e / DP, b = e - a * DP;
+        sm.stab[e] = (P.off_astab >= 0 && b < D) ? prm[P.off_astab + a * D + b] : 0.0f;
+    }
+    for (int e = tid; e < WP; e += kArmTile) {
+        sm.b1[e] = e < Wd ? prm[P.off_l1b + e] : 0.0f;
+        sm.b2[e] = e < Wd ? prm[P.off_l2b + e] : 0.0f;
+    }
+    if (tid < 4) sm.b3[tid] = tid < 2 ? prm[P.off_hb + tid] : 0.0f;
+    for (int e = tid; e < kMaxSlots * kFMax * kRMax; e += kArmTile) {
+        const int s = e / (kFMax * kRMax), rem = e - s * kFMax * kRMax;
+        const int f = rem / kRMax, j = rem - f * kRMax;
+        float v = 0.0f;
+        if (s < P.n_slots) {
+            const int rd = P.g[P.slot_gi[s]].rdim;
+            if (f < F && j < rd) v = prm[P.off_ifw[s] + f * rd + j];
+        }
+        sm.Wf[s][f * kRMax + j] = v;
+    }
+    for (int e = tid; e < kMaxSlots * kFMax; e += kArmTile) {
+        const int s = e / kFMax, f = e - s * kFMax;
+        sm.bf[s][f] = (s < P.n_slots && f < F) ? prm[P.off_ifb[s] + f] : 0.0f;
+    }
+    for (int e = tid; e < kMaxCtx; e += kArmTile) {
+        sm.ctx_dy[e] = e < S ? P.ctx_dy[e] : 0;
+        sm.ctx_dx[e] = e < S ? P.ctx_dx[e] : 0;
+    }
+    if (MODE != kArmForward)
+        for (int e = tid; e < K::NACC; e += kArmTile) sm.acc[e] = 0.0;
+    __syncthreads();
+
+    const float upstream = P.rate_upstream;
+    double bits_cta = 0.0;  // thread 0
+
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int2 tile = tiles[t];
+        const GridGeom& g = P.g[tile.x];
+        const int64_t count = int64_t(g.rows) * g.cols;
+        const int64_t li = int64_t(tile.y) + tid;
+        const bool valid = li < count;
+        const int r = valid ? int(li / g.cols) : 0;
+        const int c = valid ? int(li - int64_t(r) * g.cols) : 0;
+        const int slot = g.ifce_slot;
+
+        // ---- context row in shared memory (runtime extents), then registers ----
+        float* myC = sm.act + K::OA_C + tid * K::LC;
+        float* myR = sm.act + K::OA_R + tid * K::LR;
+        {
+            const float* base = P.yhat_pad + g.pad_base + int64_t(r) * g.stride + c;
+            for (int o = 0; o < S; ++o)
+                myC[o] = valid ? __ldg(base + sm.ctx_dy[o] * g.stride + sm.ctx_dx[o]) : 0.0f;
+            if (slot >= 0) {
+                const int rd = g.rdim;
+                for (int j = 0; j < kRMax; ++j) {
+                    float v = 0.0f;
+                    if (valid && j < rd) {
+                        const GridGeom& s = P.g[j];
+                        const int sh = s.level - g.level;
+                        v = __ldg(P.yhat_pad + s.pad_base + int64_t(r >> sh) * s.stride + (c >> sh));
+                    }
+                    myR[j] = v;
+                }
+                myR[kRMax] = valid ? 1.0f : 0.0f;
+                for (int j = kRMax + 1; j < K::LR; ++j) myR[j] = 0.0f;
+                for (int f = 0; f < F; ++f) {
+                    float acc = sm.bf[slot][f];
+                    for (int j = 0; j < kRMax; ++j) acc = fmaf(myR[j], sm.Wf[slot][f * kRMax + j], acc);
+                    myC[S + f] = valid ? acc : 0.0f;
+                }
+            } else {
+                for (int f = 0; f < F; ++f) myC[S + f] = 0.0f;
+                for (int j = 0; j < K::LR; ++j) myR[j] = 0.0f;
+            }
+            for (int o = D; o < K::LC; ++o) myC[o] = (o == DP && valid) ? 1.0f : 0.0f;
+        }
+        float C[DP];
+#pragma unroll
+        for (int o = 0; o < DP; o += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(myC + o);
+            C[o] = v.x; C[o + 1] = v.y; C[o + 2] = v.z; C[o + 3] = v.w;
+        }
+
+        // ---- MLP forward (entropy_model.hpp:250-255) ----
+        float h1[WP], h2[WP];
+#pragma unroll
+        for (int a = 0; a < WP; ++a) {
+            float acc = sm.b1[a];
+#pragma unroll
+            for (int b = 0; b < DP; b += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(&sm.W1[a * DP + b]);
+                acc = fmaf(C[b], w.x, acc);
+                acc = fmaf(C[b + 1], w.y, acc);
+                acc = fmaf(C[b + 2], w.z, acc);
+                acc = fmaf(C[b + 3], w.w, acc);
+            }
+            h1[a] = acc > 0.0f ? acc : 0.0f;
+        }
+#pragma unroll
+        for (int a = 0; a < WP; ++a) {
+            float acc = sm.b2[a];
+#pragma unroll
+            for (int b = 0; b < WP; b += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(&sm.W2[a * WP + b]);
+                acc = fmaf(h1[b], w.x, acc);
+                acc = fmaf(h1[b + 1], w.y, acc);
+                acc = fmaf(h1[b + 2], w.z, acc);
+                acc = fmaf(h1[b + 3], w.w, acc);
+            }
+            h2[a] = acc > 0.0f ? acc : 0.0f;
+        }
+        float raw[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            float acc = sm.b3[j];
+#pragma unroll
+            for (int b = 0; b < WP; b += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(&sm.W3[j * WP + b]);
+                acc = fmaf(h2[b], w.x, acc);
+                acc = fmaf(h2[b + 1], w.y, acc);
+                acc = fmaf(h2[b + 2], w.z, acc);
+                acc = fmaf(h2[b + 3], w.w, acc);
+            }
+#pragma unroll
+            for (int b = 0; b < DP; b += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(&sm.stab[j * DP + b]);
+                acc = fmaf(C[b], w.x, acc);
+                acc = fmaf(C[b + 1], w.y, acc);
+                acc = fmaf(C[b + 2], w.z, acc);
+                acc = fmaf(C[b + 3], w.w, acc);
+            }
+            raw[j] = acc;
+        }
+
+        // ---- Laplace rate (entropy_model.hpp:257-273) ----
+        const float v = valid ? P.yhat_pad[g.pad_base + int64_t(r) * g.stride + c] : 0.0f;
+        const float mu = raw[0];
+        const float sg = sigma_from_raw(raw[1]);
+        const float bsc = sg * kInvSqrt2F;
+        const float u = fabsf(v - mu);
+        const float e1 = cc_exp(-(u + 0.5f) / bsc);
+        const float e2 = cc_exp(-fabsf(u - 0.5f) / bsc);
+        const float p = u >= 0.5f ? 0.5f * (e2 - e1) : 1.0f - 0.5f * (e1 + e2);
+        const float bits = valid ? -(cc_log(std_max(p, kProbFloorF)) * kLog2EF) : 0.0f;
+        {
+            const double tb = block_sum(double(bits), sm.red);
+            if (tid == 0) bits_cta += tb;
+        }
+        if (MODE == kArmForward) continue;
+
+        // ---- rate backward (entropy_model.hpp:276-296) ----
+        float dmu = 0.0f, dsr = 0.0f, gv = 0.0f;
+        if (valid && p > kProbFloorF) {
+            const float tt = v - mu;
+            const float dbits_dp = -1.0f / (p * kLn2F);
+            const float dp_du = (e1 - e2) / (2.0f * bsc);
+            const float sgn = tt > 0.0f ? 1.0f : (tt < 0.0f ? -1.0f : 0.0f);
+            const float dp_db = -((u + 0.5f) * e1 - (u - 0.5f) * e2) / (2.0f * bsc * bsc);
+            const float up = upstream * dbits_dp;
+            dmu = -up * dp_du * sgn;
+            if (sg > kSigmaMinF && sg < kSigmaMaxF) dsr = up * dp_db * kInvSqrt2F * sg;
+            gv = up * dp_du * sgn;
+        }
+
+        // ---- MLP backward (entropy_model.hpp:298-310) ----
+        float dH2[WP];
+#pragma unroll
+        for (int a = 0; a < WP; ++a) {
+            float acc = fmaf(dmu, sm.W3[a], 0.0f);
+            acc = fmaf(dsr, sm.W3[WP + a], acc);
+            dH2[a] = h2[a] > 0.0f ? acc : 0.0f;
+        }
+        float dH1[WP];
+#pragma unroll
+        for (int b = 0; b < WP; ++b) dH1[b] = 0.0f;
+#pragma unroll
+        for (int a = 0; a < WP; ++a) {
+#pragma unroll
+            for (int b = 0; b < WP; b += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(&sm.W2[a * WP + b]);
+                dH1[b] = fmaf(dH2[a], w.x, dH1[b]);
+                dH1[b + 1] = fmaf(dH2[a], w.y, dH1[b + 1]);
+                dH1[b + 2] = fmaf(dH2[a], w.z, dH1[b + 2]);
+                dH1[b + 3] = fmaf(dH2[a], w.w, dH1[b + 3]);
+            }
+        }
+#pragma unroll
+        for (int b = 0; b < WP; ++b) dH1[b] = h1[b] > 0.0f ? dH1[b] : 0.0f;
+        float dC[DP];
+#pragma unroll
+        for (int k = 0; k < DP; ++k) dC[k] = 0.0f;
+#pragma unroll
+        for (int a = 0; a < WP; ++a) {
+#pragma unroll
+            for (int k = 0; k < DP; k += 4) {
+                const float4 w = *reinterpret_cast<const float4*>(&sm.W1[a * DP + k]);
+                dC[k] = fmaf(dH1[a], w.x, dC[k]);
+                dC[k + 1] = fmaf(dH1[a], w.y, dC[k + 1]);
+                dC[k + 2] = fmaf(dH1[a], w.z, dC[k + 2]);
+                dC[k + 3] = fmaf(dH1[a], w.w, dC[k + 3]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < DP; ++k) {
+            dC[k] = fmaf(dmu, sm.stab[k], dC[k]);
+            dC[k] = fmaf(dsr, sm.stab[DP + k], dC[k]);
+        }
+
+        // ---- latent-side outputs (gathered later, no scatter) ----
+        float* myDF = sm.act + K::OA_DF + tid * K::LF;
+        if (MODE == kArmProxy && valid) {
+            P.gown[g.lat_off + li] = gv;
+            float* dcp = P.dctx + g.dctx_off + li;
+#pragma unroll
+            for (int o = 0; o < DP; ++o)
+                if (o < S) dcp[int64_t(o) * count] = dC[o];
+        }
+        if (slot >= 0) {
+            float* dfp = P.dfeat + g.dfeat_off + li;
+#pragma unroll
+            for (int o = 0; o < DP; ++o) {
+                if (o >= S && o < S + F) {
+                    const float vv = valid ? dC[o] : 0.0f;
+                    myDF[o - S] = vv;
+                    if (MODE == kArmProxy && valid) dfp[int64_t(o - S) * count] = vv;
+                }
+            }
+            for (int f = F; f < K::LF; ++f) myDF[f] = 0.0f;
+        }
+
+        // ---- phase A: C | H2 | dH1 | draw | R | dF in shared memory ----
+        {
+            float* myH2 = sm.act + K::OA_H2 + tid * K::LH;
+            float* myDH1 = sm.act + K::OA_DH1 + tid * K::LDH;
+            float* myDR = sm.act + K::OA_DR + tid * K::LDR;
+#pragma unroll
+            for (int a = 0; a < WP; a += 4) {
+                *reinterpret_cast<float4*>(myH2 + a) =
+                    valid ? make_float4(h2[a], h2[a + 1], h2[a + 2], h2[a + 3])
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(myDH1 + a) =
+                    valid ? make_float4(dH1[a], dH1[a + 1], dH1[a + 2], dH1[a + 3])
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            for (int a = WP; a < K::LH; ++a) myH2[a] = (a == WP && valid) ? 1.0f : 0.0f;
+            for (int a = WP; a < K::LDH; ++a) myDH1[a] = 0.0f;
+            *reinterpret_cast<float4*>(myDR) = make_float4(dmu, dsr, 0.f, 0.f);
+        }
+        __syncthreads();
+        for (int job = tid; job < K::NJA; job += kArmTile) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            OutMap om;
+            int a0, b0;
+            if (job < K::NJ1) {
+                constexpr int nq = round4(DP + 1) / 4;
+                a0 = 2 * (job / nq);
+                b0 = 4 * (job % nq);
+                mt_accum<K::LDH, K::LC>(sm.act + K::OA_DH1, sm.act + K::OA_C, a0, b0, acc);
+                om = OutMap{P.off_l1w, P.off_l1b, Wd, D, DP};
+            } else if (job < K::NJ1 + K::NJ3) {
+                a0 = 0;
+                b0 = 4 * (job - K::NJ1);
+                mt_accum<K::LDR, K::LH>(sm.act + K::OA_DR, sm.act + K::OA_H2, a0, b0, acc);
+                om = OutMap{P.off_hw, P.off_hb, 2, Wd, WP};
+            } else if (job < K::NJ1 + K::NJ3 + K::NJ4) {
+                if (P.off_astab < 0) continue;
+                a0 = 0;
+                b0 = 4 * (job - K::NJ1 - K::NJ3);
+                mt_accum<K::LDR, K::LC>(sm.act + K::OA_DR, sm.act + K::OA_C, a0, b0, acc);
+                om = OutMap{P.off_astab, -1, 2, D, -1};
+            } else {
+                if (slot < 0) continue;
+                constexpr int nq = round4(kRMax + 1) / 4;
+                const int jj = job - K::NJ1 - K::NJ3 - K::NJ4;
+                a0 = 2 * (jj / nq);
+                b0 = 4 * (jj % nq);
+                mt_accum<K::LF, K::LR>(sm.act + K::OA_DF, sm.act + K::OA_R, a0, b0, acc);
+                om = OutMap{P.off_ifw[slot], P.off_ifb[slot], F, g.rdim, kRMax};
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int o = om(a0 + (e >> 2), b0 + (e & 3));
+                if (o >= 0) sm.acc[o] += double(acc[e]);
+            }
+        }
+        __syncthreads();
+        // ---- phase B: H1 | dH2 ----
+        {
+            float* myH1 = sm.act + K::OB_H1 + tid * K::LH;
+            float* myDH2 = sm.act + K::OB_DH2 + tid * K::LDH;
+#pragma unroll
+            for (int a = 0; a < WP; a += 4) {
+                *reinterpret_cast<float4*>(myH1 + a) =
+                    valid ? make_float4(h1[a], h1[a + 1], h1[a + 2], h1[a + 3])
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+                *reinterpret_cast<float4*>(myDH2 + a) =
+                    valid ? make_float4(dH2[a], dH2[a + 1], dH2[a + 2], dH2[a + 3])
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            for (int a = WP; a < K::LH; ++a) myH1[a] = (a == WP && valid) ? 1.0f : 0.0f;
+            for (int a = WP; a < K::LDH; ++a) myDH2[a] = 0.0f;
+        }
+        __syncthreads();
+        for (int job = tid; job < K::NJ2; job += kArmTile) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            constexpr int nq = round4(WP + 1) / 4;
+            const int a0 = 2 * (job / nq), b0 = 4 * (job % nq);
+            mt_accum<K::LDH, K::LH>(sm.act + K::OB_DH2, sm.act + K::OB_H1, a0, b0, acc);
+            const OutMap om{P.off_l2w, P.off_l2b, Wd, Wd, WP};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const int o = om(a0 + (e >> 2), b0 + (e & 3));
+                if (o >= 0) sm.acc[o] += double(acc[e]);
+            }
+        }
+        __syncthreads();
+    }
+
+    if (tid == 0) P.bits_part[blockIdx.x] = bits_cta;
+    if (MODE != kArmForward) {
+        const PartialRegion& R = P.region[P.reg_arm];
+        double* row = P.partials + R.base + int64_t(blockIdx.x) * R.count;
+        for (int e = tid; e < R.count; e += kArmTile) row[e] = sm.acc[e];
+    }
+}
+
+// 2x2 block sums of dF for every IFCE-equipped grid, one level per launch.
+__global__ void k_pyramid(const Plan* __restrict__ pp, int level) {
+    const Plan& P = *pp;
+    for (int s = 0; s < P.n_slots; ++s) {
+        if (level > P.slot_smax[s]) continue;
+        const int ri = P.slot_pyr_rows[s][level - 1], ci = P.slot_pyr_cols[s][level - 1];
+        const int ro = P.slot_pyr_rows[s][level], co = P.slot_pyr_cols[s][level];
+        const float* in = P.dfeat + P.slot_pyr_off[s][level - 1];
+        float* out = P.dfeat + P.slot_pyr_off[s][level];
+        const int64_t n = int64_t(P.F) * ro * co;
+        for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
+             e += int64_t(gridDim.x) * blockDim.x) {
+            const int f = int(e / (int64_t(ro) * co));
+            const int rem = int(e - int64_t(f) * ro * co);
+            const int R = rem / co, Cc = rem - R * co;
+            const float* pl = in + int64_t(f) * ri * ci;
+            const int r0 = 2 * R, c0 = 2 * Cc;
+            const float a = pl[int64_t(r0) * ci + c0];
+            const float b = (c0 + 1 < ci) ? pl[int64_t(r0) * ci + c0 + 1] : 0.0f;
+            const float cc = (r0 + 1 < ri) ? pl[int64_t(r0 + 1) * ci + c0] : 0.0f;
+            const float d = (r0 + 1 < ri && c0 + 1 < ci) ? pl[int64_t(r0 + 1) * ci + c0 + 1] : 0.0f;
+            out[int64_t(f) * ro * co + int64_t(R) * co + Cc] = (a + b) + (cc + d);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Instantiated (Dp, Wp) pairs; any decoder whose (D, W) fits one of them runs
+// zero-padded (exact: padded weights and activations are exact zeros).
+struct ArmVariant {
+    int Dp, Wp;
+};
+static const ArmVariant kVariants[] = {{8, 8}, {16, 12}, {20, 20}, {28, 28}, {32, 20}, {40, 40}};
+
+void arm_padded_dims(int D, int W, int* Dp, int* Wp) {
+    for (const auto& v : kVariants)
+        if (D <= v.Dp && W <= v.Wp) {
+            *Dp = v.Dp;
+            *Wp = v.Wp;
+            return;
+        }
+    *Dp = *Wp = -1;
+}
+
+bool arm_dims_supported(int D, int W) {
+    int a, b;
+    arm_padded_dims(D, W, &a, &b);
+    return a > 0;
+}
+
+template <int DP, int WP>
+static size_t arm_smem() {
+    return sizeof(ArmSmem<DP, WP>);
+}
+
+template <int DP, int WP, int MODE>
+static void launch_arm_t(const LaunchCtx& L) {
+    const size_t smem = arm_smem<DP, WP>();
+    k_arm<DP, WP, MODE><<<L.arm_blocks, kArmTile, smem, L.stream>>>(L.plan, L.arm_tiles,
+                                                                    L.arm_ntiles);
+}
+
+template <int DP, int WP>
+static void configure_t() {
+    const int smem = int(arm_smem<DP, WP>());
+    cudaFuncSetAttribute(k_arm<DP, WP, kArmForward>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_arm<DP, WP, kArmHard>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(k_arm<DP, WP, kArmProxy>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+// Opt in to > 48 KB dynamic shared memory on the CURRENT device.
+void arm_configure(int Dp, int Wp) {
+    if (Dp == 8 && Wp == 8) configure_t<8, 8>();
+    else if (Dp == 16 && Wp == 12) configure_t<16, 12>();
+    else if (Dp == 20 && Wp == 20) configure_t<20, 20>();
+    else if (Dp == 28 && Wp == 28) configure_t<28, 28>();
+    else if (Dp == 32 && Wp == 20) configure_t<32, 20>();
+    else configure_t<40, 40>();
+}
+
+template <int DP, int WP>
+static void launch_arm_mode(const LaunchCtx& L, int mode) {
+    if (mode == kArmForward)
+        launch_arm_t<DP, WP, kArmForward>(L);
+    else if (mode == kArmHard)
+        launch_arm_t<DP, WP, kArmHard>(L);
+    else
+        launch_arm_t<DP, WP, kArmProxy>(L);
+}
+
+void launch_arm(const LaunchCtx& L, int mode) {
+    const int Dp = L.host->Dp, Wp = L.host->Wp;
+    if (Dp == 8 && Wp == 8) launch_arm_mode<8, 8>(L, mode);
+    else if (Dp == 16 && Wp == 12) launch_arm_mode<16, 12>(L, mode);
+    else if (Dp == 20 && Wp == 20) launch_arm_mode<20, 20>(L, mode);
+    else if (Dp == 28 && Wp == 28) launch_arm_mode<28, 28>(L, mode);
+    else if (Dp == 32 && Wp == 20) launch_arm_mode<32, 20>(L, mode);
+    else launch_arm_mode<40, 40>(L, mode);
+}
+
+int arm_blocks_per_sm(int Dp, int Wp) {
+    size_t smem;
+    if (Dp == 8 && Wp == 8) smem = arm_smem<8, 8>();
+    else if (Dp == 16 && Wp == 12) smem = arm_smem<16, 12>();
+    else if (Dp == 20 && Wp == 20) smem = arm_smem<20, 20>();
+    else if (Dp == 28 && Wp == 28) smem = arm_smem<28, 28>();
+    else if (Dp == 32 && Wp == 20) smem = arm_smem<32, 20>();
+    else smem = arm_smem<40, 40>();
+    const size_t per_sm = 227 * 1024;
+    int b = int(per_sm / (smem + 1024));
+    return b < 1 ? 1 : (b > 8 ? 8 : b);
+}
+
+void launch_pyramid(const LaunchCtx& L) {
+    int smax = 0;
+    for (int s = 0; s < L.host->n_slots; ++s) smax = smax > L.host->slot_smax[s] ? smax : L.host->slot_smax[s];
+    for (int lv = 1; lv <= smax; ++lv)
+        k_pyramid<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, lv);
+}
+
+}  // namespace ccb

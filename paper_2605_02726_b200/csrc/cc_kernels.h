@@ -1,0 +1,61 @@
+// cc_kernels.h — host-side launchers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "cc_plan.h"
+
+namespace ccb {
+
+struct LaunchCtx {
+    const Plan* plan;      // device copy
+    const Plan* host;      // host copy (same pointers)
+    cudaStream_t stream;
+    int num_sms;
+    int elem_blocks;       // grid for elementwise kernels over the latents
+    int pix_blocks;        // grid for per-pixel kernels
+    // ARM work table
+    const int2* arm_tiles; // (grid index, first latent) per 128-latent tile
+    int arm_ntiles;
+    int arm_blocks;
+    int syn_ntiles;        // 128-pixel tiles of the trunk-backward kernel
+    int syn_blocks;
+    int red_blocks;        // per-CTA partial rows of the small reduction kernels
+};
+
+enum ArmMode { kArmForward = 0, kArmHard = 1, kArmProxy = 2 };
+
+// latent side (cc_latent.cu)
+void launch_softq_fwd(const LaunchCtx& L);
+void launch_quantize(const LaunchCtx& L, int amp);
+void launch_pads_from_q(const LaunchCtx& L);
+void launch_latent_grad(const LaunchCtx& L);
+void launch_adam_latents(const LaunchCtx& L);
+void launch_init_latents(const LaunchCtx& L, uint64_t stream, float amp);
+
+// entropy model (cc_arm.cu)
+bool arm_dims_supported(int D, int W);
+void arm_padded_dims(int D, int W, int* Dp, int* Wp);
+void launch_arm(const LaunchCtx& L, int mode);
+void launch_pyramid(const LaunchCtx& L);
+int arm_blocks_per_sm(int Dp, int Wp);
+void arm_configure(int Dp, int Wp);
+
+// upsampling (cc_ups.cu)
+void launch_ups_forward(const LaunchCtx& L);
+void launch_ups_backward(const LaunchCtx& L, bool latent_grads);
+
+// synthesis (cc_syn.cu)
+void launch_syn_forward(const LaunchCtx& L, bool backward);
+void launch_syn_backward(const LaunchCtx& L);
+int syn_padded_hidden(int F);
+size_t syn_trunk_smem(int FP);
+void syn_configure(int FP);
+
+// optimizer / bookkeeping (cc_step.cu)
+void launch_finalize(const LaunchCtx& L, int mode, int snap_slot);
+void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log);
+void launch_sched_load(const LaunchCtx& L, const double* sched);
+void launch_snapshot_if_better(const LaunchCtx& L, int slot, float* snap_y, float* snap_p);
+
+}  // namespace ccb

@@ -1,0 +1,201 @@
+// cc_latent.cu — elementwise latent kernels (HBM/L2-bound, one thread per
+// latent, grid sized in multiples of the SM count by the host):
+//   k_softq_fwd   soft_quantize_forward over every grid     latent.hpp:120-128,
+//                 softround layers.hpp:557-568, noise encoder.hpp:100-110,213-215
+//   k_quantize    quantize_all                              latent.hpp:86-99
+//   k_pads_from_q load_pads_from_q                          encoder.hpp:170-180
+//   k_latent_grad deterministic gather of every gradient landing on a padded
+//                 latent (own rate term, ARM context scatter, IFCE scatter,
+//                 upsampling) + soft_quantize_backward       latent.hpp:131-139,
+//                 entropy_model.hpp:292,312-331, synthesis.hpp:135-137
+//   k_adam_latents adam_step per grid, double math           optim.hpp:38-53
+//   k_init_latents init_latents_uniform                      latent.hpp:73-80
+#include <cuda_runtime.h>
+
+#include "cc_kernels.h"
+#include "cc_math.cuh"
+
+namespace ccb {
+
+__device__ __forceinline__ int find_grid(const Plan& P, int64_t i) {
+    int gi = 0;
+#pragma unroll 1
+    for (int k = 1; k < P.n_grids; ++k)
+        if (i >= P.g[k].lat_off) gi = k;
+    return gi;
+}
+
+__global__ void k_softq_fwd(const Plan* __restrict__ pp) {
+    const Plan& P = *pp;
+    const float temp = float(P.scal->temp);         // encoder.hpp:98
+    const float noise_std = float(P.scal->noise);   // encoder.hpp:108
+    const int64_t n = P.n_latents;
+    const uint64_t giter = uint64_t(P.scal->global_iter);
+    const float inv_denom = 1.0f / softround_denom(temp);
+    const float inv_t = 1.0f / temp;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int gi = find_grid(P, i);
+        const GridGeom& g = P.g[gi];
+        const int64_t li = i - g.lat_off;
+        const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
+        const float x = P.y[i];
+        float f = floorf(x);
+        float d = x - f - 0.5f;
+        const float t1 = cc_tanh(d * inv_t);
+        float o = f + 0.5f + t1 * inv_denom;
+        if (noise_std > 0.0f) {
+            const uint64_t stream = hash_combine(hash_combine(P.seed, giter), uint64_t(gi));
+            o += noise_std * counter_gauss(stream, uint64_t(li));
+        }
+        f = floorf(o);
+        d = o - f - 0.5f;
+        const float t2 = cc_tanh(d * inv_t);
+        o = f + 0.5f + t2 * inv_denom;
+        P.yhat_pad[g.pad_base + int64_t(r) * g.stride + c] = o;
+        P.th1[i] = t1;
+        P.th2[i] = t2;
+    }
+}
+
+__global__ void k_quantize(const Plan* __restrict__ pp, int amp) {
+    const Plan& P = *pp;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        long q = lroundf(P.y[i]);  // ties away from zero, like std::lround
+        if (q > amp) q = amp;
+        if (q < -amp) q = -amp;
+        P.q[i] = int32_t(q);
+    }
+}
+
+__global__ void k_pads_from_q(const Plan* __restrict__ pp) {
+    const Plan& P = *pp;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int gi = find_grid(P, i);
+        const GridGeom& g = P.g[gi];
+        const int64_t li = i - g.lat_off;
+        const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
+        P.yhat_pad[g.pad_base + int64_t(r) * g.stride + c] = float(P.q[i]);
+    }
+}
+
+// Gradient wrt the padded soft-quantized latent, assembled by GATHER in a
+// fixed order (the reference scatters with +=; the sum is the same set of
+// terms):  own rate term, the S context-gradient planes of the causal
+// successors, the IFCE terms W_f^T * (block sum of dF) from every equipped
+// finer grid, and the upsampling gradient for main grids.  Then the
+// soft-quantize backward chain rule and the per-grid finiteness flag.
+__global__ void k_latent_grad(const Plan* __restrict__ pp) {
+    const Plan& P = *pp;
+    const float temp = float(P.scal->temp);
+    const int cost_ok = P.scal->cost_ok;
+    const float scale = 1.0f / (temp * softround_denom(temp));
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        if (!cost_ok) {  // encoder.hpp:118 returns before the backward chain
+            P.lat_g[i] = 0.0f;
+            continue;
+        }
+        const int gi = find_grid(P, i);
+        const GridGeom& g = P.g[gi];
+        const int64_t cnt = int64_t(g.rows) * g.cols;
+        const int64_t li = i - g.lat_off;
+        const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
+        float acc = P.gown[i];
+        const float* dc = P.dctx + g.dctx_off;
+        for (int o = 0; o < P.S; ++o) {
+            const int rs = r - P.ctx_dy[o], cs = c - P.ctx_dx[o];
+            if (rs >= 0 && rs < g.rows && cs >= 0 && cs < g.cols)
+                acc += dc[int64_t(o) * cnt + int64_t(rs) * g.cols + cs];
+        }
+        for (int s = 0; s < P.n_slots; ++s) {
+            const GridGeom& e = P.g[P.slot_gi[s]];
+            if (gi >= e.rdim) continue;
+            const int sh = g.level - e.level;
+            const float* pyr = P.dfeat + P.slot_pyr_off[s][sh];
+            const int64_t pc = int64_t(P.slot_pyr_rows[s][sh]) * P.slot_pyr_cols[s][sh];
+            const float* wf = P.params + P.off_ifw[s];
+            float dr = 0.0f;
+            for (int f = 0; f < P.F; ++f)
+                dr += wf[f * e.rdim + gi] * pyr[int64_t(f) * pc + int64_t(r) * g.cols + c];
+            acc += dr;
+        }
+        if (g.main_level == 0)
+            acc += P.dz[int64_t(r) * P.W + c];
+        else if (g.main_level > 0)
+            acc += P.dups[i];
+        const float t2 = P.th2[i], t1 = P.th1[i];
+        const float d2 = (1.0f - t2 * t2) * scale;
+        const float d1 = (1.0f - t1 * t1) * scale;
+        const float dy = acc * d2 * d1;
+        P.lat_g[i] = dy;
+        if (!isfinite(dy)) atomicAnd(&P.lat_ok[gi], 0);
+    }
+}
+
+// One Adam step per grid (optim.hpp:38-53) with the per-tensor skip: a grid
+// whose gradient has a non-finite element is left untouched.  bc1/bc2 were
+// computed per grid by k_finalize from lat_t + 1.  Block 0 / thread 0 also
+// advances the step counters (encoder.hpp:129-133).
+__global__ void k_adam_latents(const Plan* __restrict__ pp) {
+    const Plan& P = *pp;
+    const double lr = P.scal->lr;
+    const double* __restrict__ bc = P.bc_lat;
+    const int cost_ok = P.scal->cost_ok;
+    if (!cost_ok) return;
+    const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int gi = find_grid(P, i);
+        if (!P.lat_ok[gi]) continue;
+        const double bc1 = bc[2 * gi], bc2 = bc[2 * gi + 1];
+        const double gv = double(P.lat_g[i]);
+        const double mt = b1 * double(P.lat_m[i]) + (1.0 - b1) * gv;
+        const double vt = b2 * double(P.lat_v[i]) + (1.0 - b2) * gv * gv;
+        P.lat_m[i] = float(mt);
+        P.lat_v[i] = float(vt);
+        P.y[i] = float(double(P.y[i]) - lr * (mt / bc1) / (sqrt(vt / bc2) + eps));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int gi = 0; gi < P.n_grids; ++gi) {
+            if (P.lat_ok[gi])
+                P.lat_t[gi] += 1;
+            else
+                P.scal->skipped += 1;
+        }
+    }
+}
+
+__global__ void k_init_latents(const Plan* __restrict__ pp, uint64_t stream, float amp) {
+    const Plan& P = *pp;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int gi = find_grid(P, i);
+        const uint64_t gs = hash_combine(stream, uint64_t(gi));
+        P.y[i] = counter_uniform(gs, uint64_t(i - P.g[gi].lat_off), -amp, amp);
+    }
+}
+
+// ---------------------------------------------------------------------------
+void launch_softq_fwd(const LaunchCtx& L) {
+    k_softq_fwd<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+}
+void launch_quantize(const LaunchCtx& L, int amp) {
+    k_quantize<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, amp);
+}
+void launch_pads_from_q(const LaunchCtx& L) {
+    k_pads_from_q<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+}
+void launch_latent_grad(const LaunchCtx& L) {
+    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+}
+void launch_adam_latents(const LaunchCtx& L) {
+    k_adam_latents<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+}
+void launch_init_latents(const LaunchCtx& L, uint64_t stream, float amp) {
+    k_init_latents<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, stream, amp);
+}
+
+}  // namespace ccb

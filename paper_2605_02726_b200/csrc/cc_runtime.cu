@@ -1,0 +1,836 @@
+// cc_runtime.cu — the B200 Trainer: geometry (build_latents latent.hpp:46-70,
+// make_model model.hpp:229-272, make_context_offsets entropy_model.hpp:24-45),
+// one device arena per image, and the per-iteration launch sequences captured
+// once into CUDA graphs and replayed (no host work per kernel).
+#include "cc_runtime.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+
+#include "cc_math.cuh"
+
+namespace ccb {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+constexpr int kArmTileHost = 128;
+constexpr int kRMaxHost = 12;
+constexpr int kFMaxHost = 8;
+constexpr int kSnapSlots = 8;
+constexpr float kBicubic[4] = {-0.0234375f, -0.0703125f, 0.2265625f, 0.8671875f};  // model.hpp:276
+
+int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// make_context_offsets (entropy_model.hpp:24-45)
+void context_offsets(int count, std::vector<int>& dy, std::vector<int>& dx, int& pad) {
+    struct Cand {
+        int d2, dy, dx;
+    };
+    std::vector<Cand> c;
+    const int radius = 8;
+    for (int y = -radius; y <= 0; ++y)
+        for (int x = -radius; x <= radius; ++x) {
+            if (y == 0 && x >= 0) continue;
+            c.push_back({y * y + x * x, y, x});
+        }
+    std::sort(c.begin(), c.end(), [](const Cand& a, const Cand& b) {
+        if (a.d2 != b.d2) return a.d2 < b.d2;
+        if (a.dy != b.dy) return a.dy < b.dy;
+        return a.dx < b.dx;
+    });
+    if (count > int(c.size())) throw ConfigError("spatial context too large");
+    pad = 0;
+    dy.clear();
+    dx.clear();
+    for (int i = 0; i < count; ++i) {
+        dy.push_back(c[i].dy);
+        dx.push_back(c[i].dx);
+        pad = std::max({pad, -c[i].dy, std::abs(c[i].dx)});
+    }
+}
+
+}  // namespace
+
+Trainer::Trainer(const float* image, int h, int w, const cc_encoder_config& enc,
+                 const cc_decoder_config& dec, int device)
+    : enc_(enc), dec_(dec), device_(device) {
+    if (h < 1 || w < 1) throw ConfigError("image dimensions must be positive");
+    log_path_ = enc.log_path ? enc.log_path : "";
+    enc_.log_path = nullptr;
+    if (enc.use_soap)
+        throw ConfigError(
+            "use_soap = true is not implemented by the B200 trainer (NN params use Adam, "
+            "EncoderConfig::use_soap = false)");
+    H_.H = h;
+    H_.W = w;
+    CCB_CUDA(cudaSetDevice(device_));
+    cudaDeviceProp prop;
+    CCB_CUDA(cudaGetDeviceProperties(&prop, device_));
+    if (prop.major < 10)
+        throw CudaError("libcoolchic_b200 is built for sm_100a; device " + std::string(prop.name) +
+                        " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
+    num_sms_ = prop.multiProcessorCount;
+    CCB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    build_plan();
+    allocate();
+    upload_image(image);
+}
+
+Trainer::~Trainer() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : cands_) {
+        for (float* p : {kv.second.y, kv.second.m, kv.second.v, kv.second.p, kv.second.nm, kv.second.nv})
+            cudaFree(p);
+    }
+    for (auto& kv : snaps_) {
+        cudaFree(kv.second.y);
+        cudaFree(kv.second.p);
+    }
+    for (void* p : allocs_) cudaFree(p);
+    if (h_scal_) cudaFreeHost(h_scal_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void* Trainer::dalloc(size_t bytes) {
+    void* p = nullptr;
+    CCB_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+    CCB_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+    allocs_.push_back(p);
+    return p;
+}
+
+void Trainer::build_plan() {
+    Plan& P = H_;
+    const int h = P.H, w = P.W;
+    P.L = int64_t(h) * int64_t(w) < 1000000 ? 7 : 8;  // latent_levels, config.hpp:271
+    P.hyper = dec_.use_hyperlatents ? P.L - 4 : 0;     // kHyperCoarsestLevel = 4
+    P.S = dec_.spatial_ctx;
+    P.F = dec_.ifce_dim;
+    P.D = P.S + P.F;
+    P.Wd = dec_.arm_width;
+    P.syn_F = dec_.synth_hidden;
+    P.posts = dec_.synth_posts;
+    P.use_stab_arm = dec_.use_stabilizer;
+    P.use_stab_syn = dec_.use_stabilizer;
+    if (P.S < 0 || P.F < 0 || P.Wd < 1 || P.syn_F < 1)
+        throw ConfigError("decoder dimensions must be positive");
+    if (P.S > kMaxCtx) throw ConfigError("spatial context too large for the B200 kernels");
+    if (P.F > kFMaxHost) throw ConfigError("ifce_dim > 8 is not supported by the B200 kernels");
+    if (P.D < 1) throw ConfigError("ARM input dimension must be positive");
+    arm_padded_dims(P.D, P.Wd, &P.Dp, &P.Wp);
+    if (P.Dp < 0) throw ConfigError("ARM dims (input <= 40, width <= 40) exceeded");
+    if (syn_padded_hidden(P.syn_F) < 0) throw ConfigError("synth_hidden > 64 is not supported");
+    if (P.posts < 0 || P.posts > 2) throw ConfigError("synth_posts must be 0, 1 or 2");
+    P.npix = int64_t(h) * w;
+    P.lambda = enc_.lambda;
+    P.seed = enc_.seed;
+    P.rate_upstream = float(enc_.lambda / double(P.npix));  // encoder.hpp:64
+
+    std::vector<int> dy, dx;
+    int cpad = 0;
+    context_offsets(P.S, dy, dx, cpad);
+    for (int o = 0; o < P.S; ++o) {
+        P.ctx_dy[o] = dy[o];
+        P.ctx_dx[o] = dx[o];
+    }
+    P.P = std::max(1, cpad);  // encoder.hpp:218
+
+    // ---- grids in decode order (latent.hpp:66-68) ----
+    struct G {
+        int level, hyper;
+    };
+    std::vector<G> order;
+    for (int k = P.L - 1; k >= 4 && dec_.use_hyperlatents; --k) order.push_back({k, 1});
+    for (int k = P.L - 1; k >= 0; --k) order.push_back({k, 0});
+    P.n_grids = int(order.size());
+    if (P.n_grids > kMaxGrids) throw ConfigError("too many grids");
+    int64_t pad_cur = 0, lat_cur = 0, dctx_cur = 0;
+    for (int i = 0; i < kMaxLevels; ++i) P.main_gi[i] = -1;
+    for (int gi = 0; gi < P.n_grids; ++gi) {
+        GridGeom& g = P.g[gi];
+        g.level = order[gi].level;
+        g.hyper = order[gi].hyper;
+        g.rows = ceil_div(h, 1 << g.level);
+        g.cols = ceil_div(w, 1 << g.level);
+        g.stride = g.cols + 2 * P.P;
+        g.pad_base = pad_cur + int64_t(P.P) * g.stride + P.P;
+        pad_cur += int64_t(g.rows + 2 * P.P) * g.stride;
+        g.lat_off = lat_cur;
+        lat_cur += int64_t(g.rows) * g.cols;
+        g.dctx_off = dctx_cur;
+        dctx_cur += int64_t(P.S) * g.rows * g.cols;
+        g.main_level = g.hyper ? -1 : g.level;
+        if (!g.hyper) P.main_gi[g.level] = gi;
+        g.ifce_slot = -1;
+        g.rdim = 0;
+        g.dfeat_off = 0;
+        grids_.push_back({g.level, g.hyper, g.rows, g.cols, g.lat_off, -1});
+    }
+    P.n_latents = lat_cur;
+
+    // ---- IFCE slots (model.hpp:244-251): main levels 0..min(3,L)-1 ----
+    P.n_slots = 0;
+    int64_t df_cur = 0;
+    if (P.F > 0) {
+        for (int k = 0; k < std::min(3, P.L); ++k) {
+            const int s = P.n_slots++;
+            const int gi = P.main_gi[k];
+            GridGeom& g = P.g[gi];
+            g.ifce_slot = s;
+            g.rdim = P.hyper + (P.L - 1 - k);  // ifce_source_count, model.hpp:219
+            if (g.rdim > kRMaxHost) throw ConfigError("IFCE source count exceeds 12");
+            if (g.rdim != gi) throw ConfigError("internal: IFCE sources must precede the grid");
+            grids_[gi].ifce_slot = s;
+            P.slot_gi[s] = gi;
+            P.slot_smax[s] = (P.L - 1) - k;
+            int rr = g.rows, cc = g.cols;
+            for (int l = 0; l <= P.slot_smax[s]; ++l) {
+                if (l > 0) {
+                    rr = ceil_div(rr, 2);
+                    cc = ceil_div(cc, 2);
+                }
+                P.slot_pyr_rows[s][l] = rr;
+                P.slot_pyr_cols[s][l] = cc;
+                P.slot_pyr_off[s][l] = df_cur;
+                df_cur += int64_t(P.F) * rr * cc;
+            }
+            g.dfeat_off = P.slot_pyr_off[s][0];
+        }
+    }
+
+    // ---- parameters in for_each_param order (model.hpp:158-171) ----
+    int off = 0;
+    auto add = [&](const std::string& name, int rows, int cols) {
+        TensorInfo t{name, rows, cols, rows * cols, off};
+        tensors_.push_back(t);
+        off += rows * cols;
+        return t.offset;
+    };
+    const int D = P.D, Wd = P.Wd;
+    P.off_l1w = add("arm.l1.w", Wd, D);
+    P.off_l1b = add("arm.l1.b", 1, Wd);
+    P.off_l2w = add("arm.l2.w", Wd, Wd);
+    P.off_l2b = add("arm.l2.b", 1, Wd);
+    P.off_hw = add("arm.head.w", 2, Wd);
+    P.off_hb = add("arm.head.b", 1, 2);
+    P.off_astab = dec_.use_stabilizer ? add("arm.stab", 2, D) : -1;
+    for (int s = 0; s < P.n_slots; ++s) {
+        const int rd = P.g[P.slot_gi[s]].rdim;
+        P.off_ifw[s] = add("ifce" + std::to_string(s) + ".w", P.F, rd);
+        P.off_ifb[s] = add("ifce" + std::to_string(s) + ".b", 1, P.F);
+    }
+    for (int j = 0; j < P.L - 1; ++j) {
+        P.off_tconv[j] = add("ups" + std::to_string(j) + ".tconv", 1, 4);
+        P.off_refine[j] = add("ups" + std::to_string(j) + ".refine", 1, 3);
+    }
+    P.off_c1w = add("syn.c1.w", P.syn_F, P.L);
+    P.off_c1b = add("syn.c1.b", 1, P.syn_F);
+    P.off_c2w = add("syn.c2.w", 3, P.syn_F);
+    P.off_c2b = add("syn.c2.b", 1, 3);
+    for (int i = 0; i < P.posts; ++i) P.off_pw[i] = add("syn.post" + std::to_string(i) + ".w", 3, 27);
+    for (int i = 0; i < P.posts; ++i) P.off_pb[i] = add("syn.post" + std::to_string(i) + ".b", 1, 3);
+    P.off_sstab = dec_.use_stabilizer ? add("syn.stab", 3, P.L) : -1;
+    P.n_params = off;
+    P.n_tensors = int(tensors_.size());
+    if (P.n_tensors > kMaxTensors) throw ConfigError("too many tensors");
+    for (int t = 0; t < P.n_tensors; ++t) {
+        P.tensor_off[t] = tensors_[t].offset;
+        P.tensor_size[t] = tensors_[t].size;
+    }
+
+    // ---- upsampling stages (synthesis.hpp:66-92) ----
+    int64_t ub = 0;
+    int64_t stage_out_off[kMaxLevels][kMaxLevels];  // [k][j]
+    for (int j = 0; j < kMaxLevels; ++j) P.ups_n[j] = 0;
+    for (int k = 1; k < P.L; ++k) {
+        for (int j = k - 1; j >= 0; --j) {
+            UpsStage& st = P.ups[j][P.ups_n[j]++];
+            st.k = k;
+            st.rows_in = ceil_div(h, 1 << (j + 1));
+            st.cols_in = ceil_div(w, 1 << (j + 1));
+            st.rows_out = ceil_div(h, 1 << j);
+            st.cols_out = ceil_div(w, 1 << j);
+            if (j == k - 1) {
+                const GridGeom& g = P.g[P.main_gi[k]];
+                st.in_is_pad = 1;
+                st.in_off = g.pad_base;
+                st.in_stride = g.stride;
+            } else {
+                st.in_is_pad = 0;
+                st.in_off = stage_out_off[k][j + 1];
+                st.in_stride = st.cols_in;
+            }
+            st.row_off = ub;
+            ub += int64_t(st.rows_in) * st.cols_out;
+            st.col_off = ub;
+            ub += int64_t(st.rows_out) * st.cols_out;
+            if (j == 0) {
+                st.out_is_z = 1;
+                st.out_off = int64_t(k) * P.npix;
+            } else {
+                st.out_is_z = 0;
+                st.out_off = ub;
+                ub += int64_t(st.rows_out) * st.cols_out;
+            }
+            stage_out_off[k][j] = st.out_off;
+            // backward wiring
+            st.dout_is_z = j == 0;
+            st.dout_off = st.out_off;  // dz plane k, or ups_grad at the same offset
+            st.din_is_lat = j == k - 1;
+            st.din_off = st.din_is_lat ? P.g[P.main_gi[k]].lat_off : stage_out_off[k][j + 1];
+        }
+    }
+    // stage (k, j+1)'s output offset is known before stage (k, j) is built
+    // because stages are created from j = k-1 downward.
+    const int64_t ups_total = ub;
+
+    // ---- launch geometry ----
+    L_.num_sms = num_sms_;
+    auto cap = [&](int64_t n, int per) {
+        int64_t b = (n + per - 1) / per;
+        b = std::min<int64_t>(b, int64_t(num_sms_) * 8);
+        return int(std::max<int64_t>(b, 1));
+    };
+    L_.elem_blocks = cap(P.n_latents, 256);
+    L_.pix_blocks = cap(P.npix, 256);
+    L_.red_blocks = num_sms_;
+    std::vector<int2> tiles;
+    for (int gi = 0; gi < P.n_grids; ++gi) {
+        const int64_t cnt = int64_t(P.g[gi].rows) * P.g[gi].cols;
+        for (int64_t s = 0; s < cnt; s += kArmTileHost) tiles.push_back(make_int2(gi, int(s)));
+    }
+    L_.arm_ntiles = int(tiles.size());
+    L_.arm_blocks = std::min(L_.arm_ntiles, num_sms_ * arm_blocks_per_sm(P.Dp, P.Wp));
+    const int FP = syn_padded_hidden(P.syn_F);
+    const int64_t syn_tiles = (P.npix + 127) / 128;
+    int syn_per_sm = int((227 * 1024) / (syn_trunk_smem(FP) + 1024));
+    syn_per_sm = std::max(1, std::min(8, syn_per_sm));
+    L_.syn_ntiles = int(syn_tiles);
+    L_.syn_blocks = int(std::min<int64_t>(syn_tiles, int64_t(num_sms_) * syn_per_sm));
+    P.n_bits_part = L_.arm_blocks;
+    P.n_mse_part = L_.pix_blocks;
+
+    // ---- partial regions ----
+    int64_t pbase = 0;
+    P.n_regions = 0;
+    auto region = [&](int param_off, int count, int nblocks) {
+        const int r = P.n_regions++;
+        if (r >= kMaxPartialRegions) throw ConfigError("too many partial regions");
+        P.region[r] = PartialRegion{param_off, count, nblocks, pbase};
+        pbase += int64_t(count) * nblocks;
+        return r;
+    };
+    P.arm_nvals = P.off_tconv[0];
+    P.reg_arm = region(0, P.arm_nvals, L_.arm_blocks);
+    for (int j = 0; j < P.L - 1; ++j) {
+        const int nb = L_.red_blocks * P.ups_n[j];
+        P.reg_ups_rows[j] = region(P.off_tconv[j], 4, nb);
+        P.reg_ups_cols[j] = region(P.off_tconv[j], 4, nb);
+        P.reg_ups_ref[j] = region(P.off_refine[j], 3, nb);
+    }
+    P.syn_nvals = P.n_params - P.off_c1w;
+    P.reg_syn_trunk = region(P.off_c1w, P.syn_nvals, L_.syn_blocks);
+    for (int i = 0; i < P.posts; ++i)
+        P.reg_post[i] = region(P.off_pw[0], P.off_pb[P.posts - 1] + 3 - P.off_pw[0], L_.red_blocks);
+
+    // sizes for allocate()
+    P.g[0].dfeat_off = P.g[0].dfeat_off;  // (no-op; keeps field initialised)
+    allocs_.reserve(64);
+    // stash sizes in the (otherwise unused before allocation) pointer fields via locals
+    sizes_.pad = pad_cur;
+    sizes_.dctx = dctx_cur;
+    sizes_.dfeat = std::max<int64_t>(df_cur, 1);
+    sizes_.ups = std::max<int64_t>(ups_total, 1);
+    sizes_.partials = std::max<int64_t>(pbase, 1);
+    tiles_host_ = tiles;
+}
+
+void Trainer::allocate() {
+    Plan& P = H_;
+    const int64_t nl = P.n_latents, np = P.npix;
+    auto f32 = [&](int64_t n) { return static_cast<float*>(dalloc(sizeof(float) * size_t(n))); };
+    P.yhat_pad = f32(sizes_.pad);
+    P.y = f32(nl);
+    P.lat_m = f32(nl);
+    P.lat_v = f32(nl);
+    P.lat_g = f32(nl);
+    P.th1 = f32(nl);
+    P.th2 = f32(nl);
+    P.gown = f32(nl);
+    P.dups = f32(nl);
+    P.q = static_cast<int32_t*>(dalloc(sizeof(int32_t) * size_t(nl)));
+    P.dctx = f32(std::max<int64_t>(sizes_.dctx, 1));
+    P.dfeat = f32(sizes_.dfeat);
+    P.z = f32(int64_t(P.L) * np);
+    P.dz = f32(int64_t(P.L) * np);
+    P.ups_buf = f32(sizes_.ups);
+    P.ups_grad = f32(sizes_.ups);
+    P.ups_grad2 = nullptr;
+    P.image = f32(3 * np);
+    P.syn_t = f32(3 * np);
+    P.syn_p[0] = f32(3 * np);
+    P.syn_p[1] = f32(3 * np);
+    P.syn_sz = nullptr;
+    P.syn_dx = f32(3 * np);
+    P.syn_dt = f32(3 * np);
+    P.syn_dtmp = f32(3 * np);
+    P.params = f32(P.n_params);
+    P.grads = f32(P.n_params);
+    P.nn_m = f32(P.n_params);
+    P.nn_v = f32(P.n_params);
+    P.partials = static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.partials)));
+    P.bc_lat = static_cast<double*>(dalloc(sizeof(double) * 2 * kMaxGrids));
+    P.bits_part = static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_bits_part)));
+    P.mse_part = static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_mse_part)));
+    P.lat_t = static_cast<int64_t*>(dalloc(sizeof(int64_t) * kMaxGrids));
+    P.nn_t = static_cast<int64_t*>(dalloc(sizeof(int64_t) * kMaxTensors));
+    P.lat_ok = static_cast<int*>(dalloc(sizeof(int) * kMaxGrids));
+    P.scal = static_cast<DevScalars*>(dalloc(sizeof(DevScalars)));
+    d_tiles_ = static_cast<int2*>(dalloc(sizeof(int2) * tiles_host_.size()));
+    CCB_CUDA(cudaMemcpy(d_tiles_, tiles_host_.data(), sizeof(int2) * tiles_host_.size(),
+                        cudaMemcpyHostToDevice));
+    d_plan_ = static_cast<Plan*>(dalloc(sizeof(Plan)));
+    CCB_CUDA(cudaMemcpy(d_plan_, &H_, sizeof(Plan), cudaMemcpyHostToDevice));
+    CCB_CUDA(cudaMallocHost(&h_scal_, sizeof(DevScalars)));
+    std::memset(h_scal_, 0, sizeof(DevScalars));
+    for (int s = 0; s < kSnapSlots; ++s) h_scal_->snap_cost[s] = std::numeric_limits<double>::infinity();
+    CCB_CUDA(cudaMemcpy(P.scal, h_scal_, sizeof(DevScalars), cudaMemcpyHostToDevice));
+
+    L_.plan = d_plan_;
+    L_.host = &H_;
+    L_.stream = stream_;
+    L_.arm_tiles = d_tiles_;
+    arm_configure(P.Dp, P.Wp);
+    syn_configure(syn_padded_hidden(P.syn_F));
+}
+
+void Trainer::synchronize() { CCB_CUDA(cudaStreamSynchronize(stream_)); }
+
+void Trainer::upload_image(const float* image) {
+    CCB_CUDA(cudaSetDevice(device_));
+    CCB_CUDA(cudaMemcpyAsync(H_.image, image, sizeof(float) * 3 * size_t(H_.npix),
+                             cudaMemcpyHostToDevice, stream_));
+    synchronize();
+}
+
+void Trainer::require_loaded() const {
+    if (!loaded_) throw StateError("no candidate loaded (call fresh_candidate/load_candidate)");
+}
+
+void Trainer::zero_pads() {
+    CCB_CUDA(cudaMemsetAsync(H_.yhat_pad, 0, sizeof(float) * size_t(sizes_.pad), stream_));
+}
+
+// init_model (model.hpp:286-305) — host side, bit-exact with the reference's
+// contracted counter_uniform.
+void Trainer::init_params_host(uint64_t stream, std::vector<float>& out) const {
+    const Plan& P = H_;
+    out.assign(size_t(P.n_params), 0.0f);
+    uint64_t ctr = 0;
+    auto sub = [&]() { return hash_combine(stream, ctr++); };
+    auto kaiming = [&](int off, int n, int fan_in, uint64_t s) {
+        const float a = std::sqrt(6.0f / float(fan_in));
+        for (int i = 0; i < n; ++i) out[size_t(off + i)] = counter_uniform(s, uint64_t(i), -a, a);
+    };
+    kaiming(P.off_l1w, P.Wd * P.D, P.D, sub());
+    kaiming(P.off_l2w, P.Wd * P.Wd, P.Wd, sub());
+    kaiming(P.off_hw, 2 * P.Wd, P.Wd, sub());
+    for (int s = 0; s < P.n_slots; ++s) {
+        const int rd = P.g[P.slot_gi[s]].rdim;
+        kaiming(P.off_ifw[s], P.F * rd, rd, sub());
+    }
+    for (int j = 0; j < P.L - 1; ++j) {
+        for (int i = 0; i < 4; ++i) out[size_t(P.off_tconv[j] + i)] = kBicubic[i];
+        out[size_t(P.off_refine[j])] = 1.0f;
+    }
+    kaiming(P.off_c1w, P.syn_F * P.L, P.L, sub());
+    kaiming(P.off_c2w, 3 * P.syn_F, P.syn_F, sub());
+}
+
+void Trainer::fresh_candidate(int index) {
+    CCB_CUDA(cudaSetDevice(device_));
+    launch_init_latents(L_, hash_combine(enc_.seed, uint64_t(0x1000 + index)), 0.3f);
+    std::vector<float> prm;
+    init_params_host(hash_combine(enc_.seed, uint64_t(0x2000 + index)), prm);
+    CCB_CUDA(cudaMemcpyAsync(H_.params, prm.data(), sizeof(float) * prm.size(),
+                             cudaMemcpyHostToDevice, stream_));
+    loaded_ = true;
+    reset_optimizers();
+    zero_pads();
+    cur_cost_ = std::numeric_limits<double>::infinity();
+    synchronize();
+}
+
+void Trainer::reset_optimizers() {
+    require_loaded();
+    const size_t nl = size_t(H_.n_latents), np = size_t(H_.n_params);
+    CCB_CUDA(cudaMemsetAsync(H_.lat_m, 0, sizeof(float) * nl, stream_));
+    CCB_CUDA(cudaMemsetAsync(H_.lat_v, 0, sizeof(float) * nl, stream_));
+    CCB_CUDA(cudaMemsetAsync(H_.nn_m, 0, sizeof(float) * np, stream_));
+    CCB_CUDA(cudaMemsetAsync(H_.nn_v, 0, sizeof(float) * np, stream_));
+    CCB_CUDA(cudaMemsetAsync(H_.lat_t, 0, sizeof(int64_t) * kMaxGrids, stream_));
+    CCB_CUDA(cudaMemsetAsync(H_.nn_t, 0, sizeof(int64_t) * kMaxTensors, stream_));
+}
+
+// ---------------------------------------------------------------- sequences
+// Trainer::proxy_iteration (encoder.hpp:97-135)
+void Trainer::enqueue_proxy(bool batched) {
+    if (batched) launch_sched_load(L_, d_sched_);
+    launch_softq_fwd(L_);
+    launch_arm(L_, kArmProxy);
+    launch_pyramid(L_);
+    launch_ups_forward(L_);
+    launch_syn_forward(L_, true);
+    launch_syn_backward(L_);
+    launch_ups_backward(L_, true);
+    launch_finalize(L_, kArmProxy, -1);
+    launch_latent_grad(L_);
+    launch_adam_latents(L_);
+    launch_nn_step(L_, true, true, batched ? d_rec_ : nullptr);
+}
+
+// Trainer::hardround_iteration (encoder.hpp:141-155)
+void Trainer::enqueue_hardround(int slot) {
+    launch_arm(L_, kArmHard);
+    launch_ups_forward(L_);
+    launch_syn_forward(L_, true);
+    launch_syn_backward(L_);
+    launch_ups_backward(L_, false);
+    launch_finalize(L_, kArmHard, slot);
+    CCB_CUDA(cudaMemsetAsync(H_.lat_g, 0, sizeof(float) * size_t(H_.n_latents), stream_));
+    if (slot >= 0) launch_snapshot_if_better(L_, slot, snaps_.at(slot).y, snaps_.at(slot).p);
+    launch_nn_step(L_, true, true, nullptr);
+}
+
+// Trainer::true_cost (encoder.hpp:158-168)
+void Trainer::enqueue_true_cost() {
+    launch_quantize(L_, 255);
+    launch_pads_from_q(L_);
+    launch_arm(L_, kArmForward);
+    launch_ups_forward(L_);
+    launch_syn_forward(L_, false);
+    launch_finalize(L_, kArmForward, -1);
+}
+
+void Trainer::run_graph(int which, int slot) {
+    const int key = which == 3 ? 100 + slot : which;
+    auto it = graphs_.find(key);
+    if (it == graphs_.end()) {
+        cudaGraph_t g;
+        CCB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        if (which == 0) enqueue_proxy(false);
+        else if (which == 1) enqueue_proxy(true);
+        else if (which == 2) enqueue_true_cost();
+        else enqueue_hardround(slot);
+        CCB_CUDA(cudaStreamEndCapture(stream_, &g));
+        cudaGraphExec_t ex;
+        CCB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+        cudaGraphDestroy(g);
+        it = graphs_.emplace(key, ex).first;
+    }
+    CCB_CUDA(cudaGraphLaunch(it->second, stream_));
+}
+
+void Trainer::read_scalars() {
+    CCB_CUDA(cudaMemcpyAsync(h_scal_, H_.scal, sizeof(DevScalars), cudaMemcpyDeviceToHost, stream_));
+    synchronize();
+}
+
+double Trainer::proxy_iteration(double lr, double temp, double noise_std) {
+    require_loaded();
+    CCB_CUDA(cudaSetDevice(device_));
+    h_scal_->lr = lr;
+    h_scal_->temp = temp;
+    h_scal_->noise = noise_std;
+    CCB_CUDA(cudaMemcpyAsync(&H_.scal->lr, &h_scal_->lr, 3 * sizeof(double),
+                             cudaMemcpyHostToDevice, stream_));
+    run_graph(0);
+    read_scalars();
+    last_mse_ = h_scal_->mse;
+    last_bits_ = h_scal_->bits;
+    return h_scal_->cost;
+}
+
+void Trainer::proxy_iterations(int n, const double* lr, const double* temp, const double* noise,
+                               double* rec) {
+    require_loaded();
+    if (n <= 0) return;
+    CCB_CUDA(cudaSetDevice(device_));
+    if (n > sched_cap_) {
+        synchronize();
+        if (d_sched_) cudaFree(d_sched_);
+        if (d_rec_) cudaFree(d_rec_);
+        CCB_CUDA(cudaMalloc(&d_sched_, sizeof(double) * 3 * size_t(n)));
+        CCB_CUDA(cudaMalloc(&d_rec_, sizeof(double) * 4 * size_t(n)));
+        sched_cap_ = n;
+        auto it = graphs_.find(1);
+        if (it != graphs_.end()) {
+            cudaGraphExecDestroy(it->second);
+            graphs_.erase(it);
+        }
+    }
+    std::vector<double> s(3 * size_t(n));
+    for (int i = 0; i < n; ++i) {
+        s[3 * i] = lr[i];
+        s[3 * i + 1] = temp[i];
+        s[3 * i + 2] = noise[i];
+    }
+    CCB_CUDA(cudaMemcpyAsync(d_sched_, s.data(), sizeof(double) * s.size(), cudaMemcpyHostToDevice,
+                             stream_));
+    CCB_CUDA(cudaMemsetAsync(&H_.scal->sched_pos, 0, sizeof(int64_t), stream_));
+    for (int i = 0; i < n; ++i) run_graph(1);
+    std::vector<double> r(4 * size_t(n));
+    CCB_CUDA(cudaMemcpyAsync(r.data(), d_rec_, sizeof(double) * r.size(), cudaMemcpyDeviceToHost,
+                             stream_));
+    read_scalars();
+    if (rec) std::memcpy(rec, r.data(), sizeof(double) * r.size());
+    last_mse_ = r[4 * size_t(n - 1) + 1];
+    last_bits_ = r[4 * size_t(n - 1) + 2];
+}
+
+void Trainer::ensure_snapshot(int slot) {
+    if (slot < 0 || slot >= kSnapSlots) throw ConfigError("snapshot slot must be in [0, 8)");
+    if (snaps_.count(slot)) return;
+    SnapSlot s;
+    CCB_CUDA(cudaMalloc(&s.y, sizeof(float) * size_t(H_.n_latents)));
+    CCB_CUDA(cudaMalloc(&s.p, sizeof(float) * size_t(H_.n_params)));
+    s.valid = false;
+    snaps_[slot] = s;
+    const double inf = std::numeric_limits<double>::infinity();
+    h_scal_->snap_cost[slot] = inf;
+    CCB_CUDA(cudaMemcpyAsync(&H_.scal->snap_cost[slot], &h_scal_->snap_cost[slot], sizeof(double),
+                             cudaMemcpyHostToDevice, stream_));
+    synchronize();
+}
+
+double Trainer::hardround_iteration(double lr, int best_slot) {
+    require_loaded();
+    CCB_CUDA(cudaSetDevice(device_));
+    if (best_slot >= 0) ensure_snapshot(best_slot);
+    h_scal_->lr = lr;
+    CCB_CUDA(cudaMemcpyAsync(&H_.scal->lr, &h_scal_->lr, sizeof(double), cudaMemcpyHostToDevice,
+                             stream_));
+    run_graph(3, best_slot);
+    read_scalars();
+    last_mse_ = h_scal_->mse;
+    last_bits_ = h_scal_->bits;
+    if (best_slot >= 0 && h_scal_->snap_take) snaps_[best_slot].valid = true;
+    return h_scal_->cost;
+}
+
+double Trainer::true_cost(double* psnr, double* bpp) {
+    require_loaded();
+    CCB_CUDA(cudaSetDevice(device_));
+    run_graph(2);
+    read_scalars();
+    const double mse = h_scal_->mse, bits = h_scal_->bits;
+    if (psnr) *psnr = mse > 0 ? std::min(99.0, -10.0 * std::log10(mse)) : 99.0;  // kPsnrCap
+    if (bpp) *bpp = bits / double(H_.npix);
+    return h_scal_->cost;
+}
+
+void Trainer::quantize_all() {
+    require_loaded();
+    launch_quantize(L_, 255);
+    synchronize();
+}
+
+void Trainer::load_pads_from_q() {
+    require_loaded();
+    launch_pads_from_q(L_);
+    synchronize();
+}
+
+void Trainer::snapshot(int slot, double cost) {
+    require_loaded();
+    ensure_snapshot(slot);
+    SnapSlot& s = snaps_[slot];
+    CCB_CUDA(cudaMemcpyAsync(s.y, H_.y, sizeof(float) * size_t(H_.n_latents),
+                             cudaMemcpyDeviceToDevice, stream_));
+    CCB_CUDA(cudaMemcpyAsync(s.p, H_.params, sizeof(float) * size_t(H_.n_params),
+                             cudaMemcpyDeviceToDevice, stream_));
+    h_scal_->snap_cost[slot] = cost;
+    CCB_CUDA(cudaMemcpyAsync(&H_.scal->snap_cost[slot], &h_scal_->snap_cost[slot], sizeof(double),
+                             cudaMemcpyHostToDevice, stream_));
+    s.valid = true;
+    synchronize();
+}
+
+double Trainer::snapshot_cost(int slot) {
+    if (!snaps_.count(slot)) return std::numeric_limits<double>::infinity();
+    read_scalars();
+    return h_scal_->snap_cost[slot];
+}
+
+void Trainer::restore(int slot) {
+    require_loaded();
+    auto it = snaps_.find(slot);
+    if (it == snaps_.end() || !it->second.valid) throw StateError("empty snapshot slot");
+    CCB_CUDA(cudaMemcpyAsync(H_.y, it->second.y, sizeof(float) * size_t(H_.n_latents),
+                             cudaMemcpyDeviceToDevice, stream_));
+    CCB_CUDA(cudaMemcpyAsync(H_.params, it->second.p, sizeof(float) * size_t(H_.n_params),
+                             cudaMemcpyDeviceToDevice, stream_));
+    synchronize();
+}
+
+void Trainer::take_candidate(int slot, double cost) {
+    require_loaded();
+    CandSlot& c = cands_[slot];
+    const size_t nl = size_t(H_.n_latents), np = size_t(H_.n_params);
+    if (!c.y) {
+        CCB_CUDA(cudaMalloc(&c.y, sizeof(float) * nl));
+        CCB_CUDA(cudaMalloc(&c.m, sizeof(float) * nl));
+        CCB_CUDA(cudaMalloc(&c.v, sizeof(float) * nl));
+        CCB_CUDA(cudaMalloc(&c.p, sizeof(float) * np));
+        CCB_CUDA(cudaMalloc(&c.nm, sizeof(float) * np));
+        CCB_CUDA(cudaMalloc(&c.nv, sizeof(float) * np));
+    }
+    auto cp = [&](void* d, const void* s, size_t b) {
+        CCB_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToDevice, stream_));
+    };
+    cp(c.y, H_.y, sizeof(float) * nl);
+    cp(c.m, H_.lat_m, sizeof(float) * nl);
+    cp(c.v, H_.lat_v, sizeof(float) * nl);
+    cp(c.p, H_.params, sizeof(float) * np);
+    cp(c.nm, H_.nn_m, sizeof(float) * np);
+    cp(c.nv, H_.nn_v, sizeof(float) * np);
+    c.lat_t.resize(kMaxGrids);
+    c.nn_t.resize(kMaxTensors);
+    CCB_CUDA(cudaMemcpyAsync(c.lat_t.data(), H_.lat_t, sizeof(int64_t) * kMaxGrids,
+                             cudaMemcpyDeviceToHost, stream_));
+    CCB_CUDA(cudaMemcpyAsync(c.nn_t.data(), H_.nn_t, sizeof(int64_t) * kMaxTensors,
+                             cudaMemcpyDeviceToHost, stream_));
+    c.cost = cost;
+    synchronize();
+    loaded_ = false;
+}
+
+void Trainer::load_candidate(int slot) {
+    auto it = cands_.find(slot);
+    if (it == cands_.end()) throw StateError("empty candidate slot");
+    CandSlot& c = it->second;
+    const size_t nl = size_t(H_.n_latents), np = size_t(H_.n_params);
+    auto cp = [&](void* d, const void* s, size_t b) {
+        CCB_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToDevice, stream_));
+    };
+    cp(H_.y, c.y, sizeof(float) * nl);
+    cp(H_.lat_m, c.m, sizeof(float) * nl);
+    cp(H_.lat_v, c.v, sizeof(float) * nl);
+    cp(H_.params, c.p, sizeof(float) * np);
+    cp(H_.nn_m, c.nm, sizeof(float) * np);
+    cp(H_.nn_v, c.nv, sizeof(float) * np);
+    CCB_CUDA(cudaMemcpyAsync(H_.lat_t, c.lat_t.data(), sizeof(int64_t) * kMaxGrids,
+                             cudaMemcpyHostToDevice, stream_));
+    CCB_CUDA(cudaMemcpyAsync(H_.nn_t, c.nn_t.data(), sizeof(int64_t) * kMaxTensors,
+                             cudaMemcpyHostToDevice, stream_));
+    zero_pads();  // setup_buffers (encoder.hpp:217-235)
+    synchronize();
+    cur_cost_ = c.cost;
+    for (float* p : {c.y, c.m, c.v, c.p, c.nm, c.nv}) cudaFree(p);
+    cands_.erase(it);
+    loaded_ = true;
+}
+
+void Trainer::discard_candidate(int slot) {
+    auto it = cands_.find(slot);
+    if (it == cands_.end()) return;
+    CandSlot& c = it->second;
+    synchronize();
+    for (float* p : {c.y, c.m, c.v, c.p, c.nm, c.nv}) cudaFree(p);
+    cands_.erase(it);
+}
+
+double Trainer::candidate_cost(int slot) const {
+    auto it = cands_.find(slot);
+    if (it == cands_.end()) throw StateError("empty candidate slot");
+    return it->second.cost;
+}
+
+int64_t Trainer::global_iter() {
+    read_scalars();
+    return h_scal_->global_iter;
+}
+
+int Trainer::skipped_steps() {
+    read_scalars();
+    return h_scal_->skipped;
+}
+
+void Trainer::set_counters(int64_t gi, int skipped) {
+    read_scalars();
+    h_scal_->global_iter = gi;
+    h_scal_->skipped = skipped;
+    CCB_CUDA(cudaMemcpyAsync(H_.scal, h_scal_, sizeof(DevScalars), cudaMemcpyHostToDevice, stream_));
+    synchronize();
+}
+
+void Trainer::set_state(const float* lat, const float* par, const float* lm, const float* lv,
+                        const int64_t* lt, const float* nm, const float* nv, const int64_t* nt) {
+    require_loaded();
+    const size_t nl = size_t(H_.n_latents), np = size_t(H_.n_params);
+    auto up = [&](void* d, const void* s, size_t b) {
+        if (s) CCB_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, stream_));
+    };
+    up(H_.y, lat, sizeof(float) * nl);
+    up(H_.params, par, sizeof(float) * np);
+    up(H_.lat_m, lm, sizeof(float) * nl);
+    up(H_.lat_v, lv, sizeof(float) * nl);
+    up(H_.lat_t, lt, sizeof(int64_t) * size_t(H_.n_grids));
+    up(H_.nn_m, nm, sizeof(float) * np);
+    up(H_.nn_v, nv, sizeof(float) * np);
+    up(H_.nn_t, nt, sizeof(int64_t) * size_t(H_.n_tensors));
+    synchronize();
+}
+
+void Trainer::get_state(float* lat, float* par, float* lm, float* lv, int64_t* lt, float* nm,
+                        float* nv, int64_t* nt) {
+    require_loaded();
+    const size_t nl = size_t(H_.n_latents), np = size_t(H_.n_params);
+    auto dn = [&](void* d, const void* s, size_t b) {
+        if (d) CCB_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToHost, stream_));
+    };
+    dn(lat, H_.y, sizeof(float) * nl);
+    dn(par, H_.params, sizeof(float) * np);
+    dn(lm, H_.lat_m, sizeof(float) * nl);
+    dn(lv, H_.lat_v, sizeof(float) * nl);
+    dn(lt, H_.lat_t, sizeof(int64_t) * size_t(H_.n_grids));
+    dn(nm, H_.nn_m, sizeof(float) * np);
+    dn(nv, H_.nn_v, sizeof(float) * np);
+    dn(nt, H_.nn_t, sizeof(int64_t) * size_t(H_.n_tensors));
+    synchronize();
+}
+
+void Trainer::get_grads(float* lg, float* pg) {
+    require_loaded();
+    if (lg)
+        CCB_CUDA(cudaMemcpyAsync(lg, H_.lat_g, sizeof(float) * size_t(H_.n_latents),
+                                 cudaMemcpyDeviceToHost, stream_));
+    if (pg)
+        CCB_CUDA(cudaMemcpyAsync(pg, H_.grads, sizeof(float) * size_t(H_.n_params),
+                                 cudaMemcpyDeviceToHost, stream_));
+    synchronize();
+}
+
+void Trainer::get_q(int32_t* q) {
+    require_loaded();
+    CCB_CUDA(cudaMemcpyAsync(q, H_.q, sizeof(int32_t) * size_t(H_.n_latents), cudaMemcpyDeviceToHost,
+                             stream_));
+    synchronize();
+}
+
+void Trainer::get_params(float* p) {
+    CCB_CUDA(cudaMemcpyAsync(p, H_.params, sizeof(float) * size_t(H_.n_params),
+                             cudaMemcpyDeviceToHost, stream_));
+    synchronize();
+}
+
+}  // namespace ccb

@@ -1,0 +1,159 @@
+// cc_runtime.h — host side of the B200 trainer: geometry, device arena, the
+// per-iteration launch sequences (captured once as CUDA graphs), and the
+// reference's Trainer surface (encoder.hpp:59-306) on top of them.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/coolchic_b200.h"
+#include "cc_kernels.h"
+#include "cc_plan.h"
+
+namespace ccb {
+
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+#define CCB_CUDA(x) ::ccb::cuda_check((x), #x)
+
+struct TensorInfo {
+    std::string name;
+    int rows, cols;
+    int size, offset;
+};
+
+struct GridInfo {
+    int level, hyper, rows, cols;
+    int64_t offset;
+    int ifce_slot;
+};
+
+// Device buffers of one CandidateState (encoder.hpp:42-48).
+struct CandSlot {
+    float *y = nullptr, *m = nullptr, *v = nullptr, *p = nullptr, *nm = nullptr, *nv = nullptr;
+    std::vector<int64_t> lat_t, nn_t;
+    double cost = 0.0;
+};
+
+struct SnapSlot {
+    float *y = nullptr, *p = nullptr;
+    bool valid = false;
+};
+
+class Trainer {
+public:
+    Trainer(const float* image, int h, int w, const cc_encoder_config& enc,
+            const cc_decoder_config& dec, int device);
+    ~Trainer();
+    Trainer(const Trainer&) = delete;
+    Trainer& operator=(const Trainer&) = delete;
+
+    // ---- reference surface ----
+    void upload_image(const float* image);
+    void fresh_candidate(int index);
+    double proxy_iteration(double lr, double temp, double noise_std);
+    // n iterations without host round trips; rec receives 4 doubles per
+    // iteration (cost, mse, bits, global_iter after the iteration)
+    void proxy_iterations(int n, const double* lr, const double* temp, const double* noise,
+                          double* rec);
+    double hardround_iteration(double lr, int best_slot);
+    double true_cost(double* psnr, double* bpp);
+    void quantize_all();
+    void load_pads_from_q();
+    void snapshot(int slot, double cost);
+    double snapshot_cost(int slot);
+    void restore(int slot);
+    void reset_optimizers();
+    void take_candidate(int slot, double cost);
+    void load_candidate(int slot);
+    void discard_candidate(int slot);
+    double candidate_cost(int slot) const;
+    double last_mse() const { return last_mse_; }
+    double last_bits() const { return last_bits_; }
+    int64_t global_iter();
+    int skipped_steps();
+    void set_counters(int64_t gi, int skipped);
+    double current_cost() const { return cur_cost_; }
+    void set_current_cost(double c) { cur_cost_ = c; }
+
+    // state transfer
+    void set_state(const float* lat, const float* par, const float* lm, const float* lv,
+                   const int64_t* lt, const float* nm, const float* nv, const int64_t* nt);
+    void get_state(float* lat, float* par, float* lm, float* lv, int64_t* lt, float* nm,
+                   float* nv, int64_t* nt);
+    void get_grads(float* lg, float* pg);
+    void get_q(int32_t* q);
+    void get_params(float* p);
+
+    // geometry
+    const Plan& plan() const { return H_; }
+    const std::vector<TensorInfo>& tensors() const { return tensors_; }
+    const std::vector<GridInfo>& grids() const { return grids_; }
+    const cc_encoder_config& enc() const { return enc_; }
+    const std::string& log_path() const { return log_path_; }
+    bool loaded() const { return loaded_; }
+    void synchronize();
+
+private:
+    void build_plan();
+    void allocate();
+    void require_loaded() const;
+    void init_params_host(uint64_t stream, std::vector<float>& out) const;
+    void enqueue_proxy(bool batched);
+    void enqueue_hardround(int slot);
+    void enqueue_true_cost();
+    void run_graph(int which, int slot = -1);
+    void read_scalars();
+    void ensure_snapshot(int slot);
+    void zero_pads();
+    void* dalloc(size_t bytes);
+
+    cc_encoder_config enc_;
+    cc_decoder_config dec_;
+    std::string log_path_;
+    int device_ = 0;
+    int num_sms_ = 148;
+    cudaStream_t stream_ = nullptr;
+    Plan H_{};
+    Plan* d_plan_ = nullptr;
+    LaunchCtx L_{};
+    std::vector<TensorInfo> tensors_;
+    std::vector<GridInfo> grids_;
+    std::vector<void*> allocs_;
+    int2* d_tiles_ = nullptr;
+    double* d_sched_ = nullptr;     // 3 doubles per iteration (batched)
+    double* d_rec_ = nullptr;       // 4 doubles per iteration (batched)
+    int sched_cap_ = 0;
+    DevScalars* h_scal_ = nullptr;  // pinned mirror
+    bool loaded_ = false;
+    double cur_cost_ = 0.0;
+    double last_mse_ = 0.0, last_bits_ = 0.0;
+    std::map<int, CandSlot> cands_;
+    std::map<int, SnapSlot> snaps_;
+    // captured graphs: 0 proxy(single), 1 proxy(batched), 2 true_cost, 100+slot hardround
+    std::map<int, cudaGraphExec_t> graphs_;
+    struct Sizes {
+        int64_t pad = 0, dctx = 0, dfeat = 0, ups = 0, partials = 0;
+    } sizes_;
+    std::vector<int2> tiles_host_;
+};
+
+// warmup / train (encoder.hpp:315-413) over the B200 Trainer.
+void warmup(Trainer& tr);
+void train(Trainer& tr, cc_train_stats* stats);
+
+}  // namespace ccb

@@ -1,0 +1,141 @@
+// cc_step.cu — per-iteration bookkeeping on the device, so an iteration needs
+// no host round trip:
+//   k_finalize       bits / mse partials -> cost (encoder.hpp:111-118, 256;
+//                    rd_loss encoder.hpp:20-22); Adam bias corrections per
+//                    latent grid; snapshot decision (encoder.hpp:151)
+//   k_nn_step        fixed-order reduction of every per-CTA weight-gradient
+//                    partial into ParamTensor::g, per-tensor finiteness and
+//                    Adam (optim.hpp:38-53, NnOptimizer::step optim.hpp:277-286)
+//   k_snapshot_copy  Trainer::snapshot for the hardround "best" slot
+//                    (encoder.hpp:151,182-189)
+#include <cuda_runtime.h>
+
+#include "cc_kernels.h"
+#include "cc_math.cuh"
+
+namespace ccb {
+
+namespace {
+
+__global__ void k_finalize(const Plan* __restrict__ pp, int mode, int snap_slot) {
+    const Plan& P = *pp;
+    double* bc_lat = P.bc_lat;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double bits = 0.0;
+    for (int b = 0; b < P.n_bits_part; ++b) bits += P.bits_part[b];
+    double se = 0.0;
+    for (int b = 0; b < P.n_mse_part; ++b) se += P.mse_part[b];
+    const double mse = se / double(3 * P.npix);
+    const double cost = mse + P.lambda * (bits / double(P.npix));
+    DevScalars* s = P.scal;
+    s->bits = bits;
+    s->mse = mse;
+    s->cost = cost;
+    s->cost_ok = isfinite(cost) ? 1 : 0;
+    if (mode == kArmProxy) {
+        for (int g = 0; g < P.n_grids; ++g) {
+            const double t = double(P.lat_t[g] + 1);
+            bc_lat[2 * g] = 1.0 - pow(0.9, t);
+            bc_lat[2 * g + 1] = 1.0 - pow(0.999, t);
+            P.lat_ok[g] = 1;
+        }
+    }
+    s->snap_take = (snap_slot >= 0 && s->cost_ok && cost < s->snap_cost[snap_slot]) ? 1 : 0;
+}
+
+// One CTA per NN tensor.
+__global__ void __launch_bounds__(256) k_nn_step(const Plan* __restrict__ pp, int do_step,
+                                                 int count_iter, double* __restrict__ cost_log) {
+    const Plan& P = *pp;
+    const double lr = P.scal->lr;
+    const int ti = blockIdx.x;
+    const int off = P.tensor_off[ti], n = P.tensor_size[ti];
+    bool finite = true;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const int p = off + e;
+        double sum = 0.0;
+        for (int r = 0; r < P.n_regions; ++r) {
+            const PartialRegion& R = P.region[r];
+            if (p < R.param_off || p >= R.param_off + R.count) continue;
+            const double* col = P.partials + R.base + (p - R.param_off);
+            for (int b = 0; b < R.nblocks; ++b) sum += col[int64_t(b) * R.count];
+        }
+        const float g = float(sum);
+        P.grads[p] = g;
+        finite = finite && isfinite(g);
+    }
+    finite = __syncthreads_and(finite);
+    DevScalars* s = P.scal;
+    if (do_step && s->cost_ok) {
+        if (finite) {
+            const double t = double(P.nn_t[ti] + 1);
+            const double bc1 = 1.0 - pow(0.9, t), bc2 = 1.0 - pow(0.999, t);
+            const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+            for (int e = threadIdx.x; e < n; e += blockDim.x) {
+                const int p = off + e;
+                const double gv = double(P.grads[p]);
+                const double mt = b1 * double(P.nn_m[p]) + (1.0 - b1) * gv;
+                const double vt = b2 * double(P.nn_v[p]) + (1.0 - b2) * gv * gv;
+                P.nn_m[p] = float(mt);
+                P.nn_v[p] = float(vt);
+                P.params[p] = float(double(P.params[p]) - lr * (mt / bc1) / (sqrt(vt / bc2) + eps));
+            }
+            if (threadIdx.x == 0) P.nn_t[ti] += 1;
+        } else if (threadIdx.x == 0) {
+            atomicAdd(&s->skipped, 1);  // integer counter: order-independent
+        }
+    }
+    if (count_iter && ti == 0 && threadIdx.x == 0 && s->cost_ok) s->global_iter += 1;
+    if (cost_log && ti == 0 && threadIdx.x == 0) {  // batched runs: per-iteration record
+        double* rec = cost_log + 4 * s->sched_pos;
+        rec[0] = s->cost;
+        rec[1] = s->mse;
+        rec[2] = s->bits;
+        rec[3] = double(s->global_iter);
+        s->sched_pos += 1;
+    }
+}
+
+// Batched runs: the scalars of iteration sched_pos (lr, temp, noise_std).
+__global__ void k_sched_load(const Plan* __restrict__ pp, const double* __restrict__ sched) {
+    DevScalars* s = pp->scal;
+    const double* e = sched + 3 * s->sched_pos;
+    s->lr = e[0];
+    s->temp = e[1];
+    s->noise = e[2];
+}
+
+__global__ void k_snapshot_copy(const Plan* __restrict__ pp, int slot, float* __restrict__ sy,
+                                float* __restrict__ sp) {
+    const Plan& P = *pp;
+    DevScalars* s = P.scal;
+    if (!s->snap_take) return;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+         i += int64_t(gridDim.x) * blockDim.x)
+        sy[i] = P.y[i];
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_params;
+         i += int64_t(gridDim.x) * blockDim.x)
+        sp[i] = P.params[i];
+    if (blockIdx.x == 0 && threadIdx.x == 0) s->snap_cost[slot] = s->cost;
+}
+
+}  // namespace
+
+void launch_finalize(const LaunchCtx& L, int mode, int snap_slot) {
+    k_finalize<<<1, 32, 0, L.stream>>>(L.plan, mode, snap_slot);
+}
+
+void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log) {
+    k_nn_step<<<L.host->n_tensors, 256, 0, L.stream>>>(L.plan, do_step ? 1 : 0,
+                                                       count_iter ? 1 : 0, cost_log);
+}
+
+void launch_sched_load(const LaunchCtx& L, const double* sched) {
+    k_sched_load<<<1, 1, 0, L.stream>>>(L.plan, sched);
+}
+
+void launch_snapshot_if_better(const LaunchCtx& L, int slot, float* snap_y, float* snap_p) {
+    k_snapshot_copy<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, slot, snap_y, snap_p);
+}
+
+}  // namespace ccb
