@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py — Cool-chic 5.0 encode iterations on B200 (driver contract).
+
+One step = one proxy_iteration (soft-quantise, ARM+IFCE rate fwd/bwd,
+upsampling fwd/bwd, synthesis fwd + MSE + bwd, Adam on latents and NN params;
+encoder.hpp:97-135) over one 512x768 synthetic image per GPU (BASELINE.json
+configs[1], HOP decoder).  Multi-GPU = independent images, one per rank, no
+collective on the data path (weak scaling); timing is the max over ranks.
+
+  python bench.py [--gpus N --steps K --warmup W]          B200 arm
+  python bench.py --impl reference [...]                   reference CPU arm
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+from paper_2605_02726_b200 import capi  # noqa: E402
+from paper_2605_02726_b200.trainer import (  # noqa: E402
+    DecoderConfig, EncoderConfig, Trainer, make_synthetic_image,
+)
+
+METRIC = "encode Gpix-iter/s (proxy_iteration fwd+bwd+Adam) at 512x768, HOP decoder"
+UNIT = "Gpix-iter/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--height", type=int, default=512)
+    ap.add_argument("--width", type=int, default=768)
+    ap.add_argument("--preset", default="hop")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def schedule(enc: EncoderConfig, n: int, start: int = 0):
+    """Main-stage scalars of with_total(10000) (config.hpp:301-309)."""
+    lr_s, t_s, n_s = enc.schedules()
+    its = range(start, start + n)
+    return (np.array([lr_s.value(i) for i in its]), np.array([t_s.value(i) for i in its]),
+            np.array([n_s.value(i) for i in its]))
+
+
+def _dp(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,uuid,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuid: str | None):
+        self.uuid = uuid
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+               "-lms", "100"]
+        if self.uuid:
+            cmd += ["-i", self.uuid]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        time.sleep(0.3)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 10:
+                self.rows.append(parts)
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        mx = [float(r[3]) for r in self.rows if r[3].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[6 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def load_ref_lib():
+    from tests.oracle_util import load_reference
+
+    lib = load_reference()
+    fn = lib.ccref_parallel_proxy
+    fn.restype = C.c_int
+    fn.argtypes = [C.POINTER(C.c_float), C.c_int, C.c_int, C.POINTER(capi.EncoderConfigC),
+                   C.POINTER(capi.DecoderConfigC), C.c_int, C.c_int, C.c_int,
+                   C.POINTER(C.c_double)]
+    return lib
+
+
+def cpu_reference_run(h, w, preset, seed, threads, warm, iters):
+    """The UNMODIFIED reference (oracle/_ref, built from /root/reference headers):
+    `threads` independent detail::Trainer instances, one image each, on std::threads
+    (the reference's only multi-core mode, tools/coolcodec.cpp:150-171)."""
+    lib = load_ref_lib()
+    img = np.empty((3, h, w), np.float32)
+    lib.cc_make_synthetic_image(h, w, seed, img.ctypes.data_as(C.POINTER(C.c_float)))
+    enc = EncoderConfig.with_total(10000)
+    enc.lmbda, enc.seed, enc.use_soap = 1e-3, seed, False
+    ec, dc = enc.to_c(), DecoderConfig.from_name(preset).to_c()
+    secs = C.c_double()
+    rc = lib.ccref_parallel_proxy(img.ctypes.data_as(C.POINTER(C.c_float)), h, w, C.byref(ec),
+                                  C.byref(dc), threads, warm, iters, C.byref(secs))
+    if rc != 0:
+        raise RuntimeError(lib.cc_last_error().decode())
+    return secs.value
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    h, w = args.height, args.width
+    # each step = one proxy_iteration on every thread (~0.8 s wall); cap the
+    # timed steps so the whole arm ends within a couple of minutes
+    steps = max(1, min(args.steps, 60))
+    warm = max(0, min(args.warmup, 1))
+    secs = cpu_reference_run(h, w, args.preset, args.seed, threads, warm, steps)
+    value = threads * steps * h * w / secs / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "warmup": warm, "steps_requested": args.steps,
+        "ms_per_step": 1e3 * secs / steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(args, threads_cpu=threads),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{threads} independent detail::Trainer (oracle/_ref, reference "
+                                   f"headers, -O3 -ffp-contract=fast) x {steps} proxy_iteration "
+                                   f"each after {warm} warm-up, {h}x{w} {args.preset}"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(args, threads_cpu=None):
+    d = {
+        "workload": f"cfg2: one {args.height}x{args.width} RGB synthetic image per GPU, "
+                    f"{args.preset.upper()} decoder, proxy_iteration (NN params Adam)",
+        "height": args.height, "width": args.width, "decoder": args.preset,
+        "images_per_gpu": 1, "lambda": 1e-3,
+        "schedule": "EncoderConfig::with_total(10000) main-stage lr/T/sigma",
+        "parallelism": f"image-sharded x{args.gpus} (no collective)",
+        "l2": "back-to-back iterations, per-iteration working set ~150 MB > 126 MB L2; "
+              "value_l2_flushed = same steps with a 512 MB L2 flush before each",
+    }
+    if threads_cpu:
+        d["cpu_threads"] = threads_cpu
+    return d
+
+
+def run_b200(args, rank, world, local_rank):
+    import torch
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+    lib = capi.load_product()
+    h, w = args.height, args.width
+    img = make_synthetic_image(h, w, args.seed + rank, lib)
+    enc = EncoderConfig.with_total(10000)
+    enc.lmbda, enc.seed, enc.use_soap = 1e-3, args.seed + rank, False
+    dcfg = DecoderConfig.from_name(args.preset)
+    tr = Trainer(img, enc, dcfg, lib=lib, device=local_rank)
+    tr.fresh_candidate(0)
+    # a real (non-legacy) stream: the library launches on it, the events below
+    # are recorded on it, so they bracket exactly the library's work
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
+    if lib.cc_trainer_set_stream(tr._h, C.c_void_p(stream.cuda_stream)) != 0:
+        raise RuntimeError(lib.cc_last_error().decode())
+    K, W = args.steps, max(3, args.warmup)
+    lr, tp, ns = schedule(enc, W + K)
+
+    def enqueue(a, b):
+        rc = lib.cc_trainer_enqueue_proxy_iterations(tr._h, b - a, _dp(lr[a:b].copy()),
+                                                     _dp(tp[a:b].copy()), _dp(ns[a:b].copy()))
+        if rc != 0:
+            raise RuntimeError(lib.cc_last_error().decode())
+
+    enqueue(0, W)
+    torch.cuda.synchronize(dev)
+    kpi = C.c_int()
+    lib.ccb_kernels_per_iteration(tr._h, C.byref(kpi))
+
+    # ---------------- timed region (device events, max over ranks) --------
+    uuid = None
+    try:
+        uuid = str(torch.cuda.get_device_properties(dev).uuid)
+        if uuid and not uuid.startswith("GPU-"):
+            uuid = "GPU-" + uuid
+    except Exception:
+        uuid = None
+    sampler = ClockSampler(uuid)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    enqueue(W, W + K)
+    e1.record(stream)
+    e1.synchronize()
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    rec = np.empty(4 * K, np.float64)
+    lib.cc_trainer_last_records(tr._h, K, _dp(rec))
+    finite = bool(np.all(np.isfinite(rec[0::4])))
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * h * w * K / (ms_max / 1e3) / 1e9
+
+    # ---------------- same steps with an L2 flush before each -------------
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    Kf = min(K, 50)
+    tot = 0.0
+    for i in range(Kf):
+        flush.zero_()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        enqueue(W + i, W + i + 1)
+        a1.record(stream)
+        a1.synchronize()
+        tot += a0.elapsed_time(a1)
+    t = torch.tensor([tot / Kf], device=dev, dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    value_flushed = world * h * w / (float(t.item()) / 1e3) / 1e9
+    del flush
+
+    # ---------------- per-stage profile and the roofline ------------------
+    stage_ms = np.zeros(8, np.float64)
+    lib.ccb_profile_stages(tr._h, 20, lr[W], tp[W], ns[W], _dp(stage_ms))
+    stages = {lib.ccb_stage_name(s).decode(): round(float(stage_ms[s]), 5) for s in range(8)}
+    arm_flops = lib.ccb_arm_flops(tr._h)
+    peak, pk_ms = C.c_double(), C.c_double()
+    lib.ccb_fp32_peak(local_rank, C.byref(peak), C.byref(pk_ms))
+    achieved = arm_flops / (stage_ms[1] / 1e3) / 1e12
+    traffic = None
+    tf = REPO / "profiles" / "arm_traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "fp32", "kernel": "k_arm (fused ARM+IFCE fwd/bwd)",
+                "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+                "frac": achieved / peak.value, "traffic": traffic,
+                "flops_per_launch": arm_flops,
+                "peak_source": "FFMA peak measured in-run by ccb_fp32_peak (MEASURED_PEAKS.json "
+                               "has no fp32 entry)",
+                "stage_ms": stages,
+                "macs_per_px": capi_macs(lib, dcfg, h, w)}
+
+    # ---------------- end to end through the public API -------------------
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.empty((3, h, w), dtype=torch.float32, pin_memory=True)
+        pinned.numpy()[...] = img
+        Ke = min(K, 100)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        tr.upload_image(pinned.numpy())
+        costs = [tr.proxy_iteration(lr[W + i], tp[W + i], ns[W + i]) for i in range(Ke)]
+        b1.record(stream)
+        b1.synchronize()
+        t = torch.tensor([b0.elapsed_time(b1)], device=dev, dtype=torch.float64)
+        if dist:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * h * w * Ke / (float(t.item()) / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": (3 * h * w * 4 + Ke * 24) / Ke,
+               "d2h_bytes_per_step": 144,
+               "steps": Ke,
+               "api": "cc_trainer_upload_image + cc_trainer_proxy_iteration (synchronous, returns "
+                      "the RD cost to the host)"}
+        finite = finite and all(math.isfinite(c) for c in costs)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        iters = 2
+        try:
+            secs = cpu_reference_run(h, w, args.preset, args.seed, threads, 1, iters)
+            cpu = {"value": threads * iters * h * w / secs / 1e9, "unit": UNIT, "cores": threads,
+                   "kind": "reference",
+                   "sample": f"{threads} independent detail::Trainer x {iters} proxy_iteration "
+                             f"after 1 warm-up, {h}x{w} {args.preset}, oracle/_ref"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": threads, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": config_dict(args),
+            "it_per_s_per_image": K / (ms_max / 1e3),
+            "value_l2_flushed": value_flushed,
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(kpi.value) * K, "kernels_per_step": int(kpi.value),
+            "clocks": clocks, "costs_finite": finite,
+        }
+        print(json.dumps(line), flush=True)
+    tr.close()
+
+
+def capi_macs(lib, dcfg, h, w):
+    dc = dcfg.to_c()
+    return lib.cc_count_macs_per_pixel(C.byref(dc), h, w)
+
+
+def main():
+    args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_b200(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

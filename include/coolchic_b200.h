@@ -206,6 +206,19 @@ int cc_trainer_take_candidate(cc_trainer* tr, int slot, double cost);
 int cc_trainer_load_candidate(cc_trainer* tr, int slot);
 int cc_trainer_candidate_cost(cc_trainer* tr, int slot, double* cost);
 
+/* ---- asynchronous use (no reference counterpart; the reference is a
+ * synchronous CPU library).  Launch on the caller's CUDA stream (a
+ * cudaStream_t passed as void*; NULL = the trainer's own stream), enqueue n
+ * proxy iterations without waiting, and wait for them.  Costs of enqueued
+ * iterations are readable with cc_trainer_last_records after synchronize. */
+int cc_trainer_set_stream(cc_trainer* tr, void* cuda_stream);
+int cc_trainer_enqueue_proxy_iterations(cc_trainer* tr, int n, const double* lr,
+                                        const double* temp, const double* noise_std);
+int cc_trainer_synchronize(cc_trainer* tr);
+/* records of the last batched run: 4 doubles per iteration
+ * (cost, mse, bits, global_iter after the iteration). */
+int cc_trainer_last_records(cc_trainer* tr, int n, double* rec);
+
 /* warmup(tr, enc) + load_candidate (encoder.hpp:315-342, 352). */
 int cc_trainer_warmup(cc_trainer* tr);
 /* train(img, enc, dcfg) (encoder.hpp:349-413) on an existing trainer (image

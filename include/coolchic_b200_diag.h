@@ -1,0 +1,48 @@
+/*
+ * coolchic_b200_diag.h — measurement hooks of the B200 library (used by
+ * bench.py and the profiling notes; not part of the reference surface).
+ */
+#ifndef COOLCHIC_B200_DIAG_H
+#define COOLCHIC_B200_DIAG_H
+
+#include "coolchic_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CCB_NUM_STAGES 8
+/* Stage names, in launch order of one proxy iteration:
+ * 0 softq_fwd, 1 arm (fused ARM+IFCE fwd/bwd), 2 pyramid, 3 ups_fwd,
+ * 4 syn_fwd, 5 syn_bwd, 6 ups_bwd, 7 tail (finalize, gather, Adam). */
+const char* ccb_stage_name(int stage);
+
+/* Run n proxy iterations (lr/temp/noise fixed) WITHOUT the graph, with CUDA
+ * events between stages on the trainer's stream; ms[s] receives the average
+ * duration of stage s per iteration. */
+int ccb_profile_stages(cc_trainer* tr, int n, double lr, double temp, double noise, double* ms);
+
+/* Number of kernel nodes in one captured proxy iteration (graph). */
+int ccb_kernels_per_iteration(cc_trainer* tr, int* count);
+
+/* Algorithmic FLOPs of one launch of the fused ARM kernel (proxy mode):
+ * 6 x (ARM + IFCE MACs of count_macs_per_pixel) x npix, SURVEY 8(d). */
+double ccb_arm_flops(cc_trainer* tr);
+
+/* FP32 FFMA peak of `device` measured by a register-only FMA kernel
+ * (TFLOP/s, 2 flops per FMA), ms = device time of the measurement. */
+int ccb_fp32_peak(int device, double* tflops, double* ms);
+
+/* Device evaluation of the parity-critical element functions on n inputs:
+ * fn 0 cc_exp(a), 1 cc_log(a), 2 cc_tanh(a), 3 softround_value(a, T=b),
+ * 4 laplace_bits(a, mu=b, sigma=c), 5 quantize_value(a, 255),
+ * 6 softround derivative at (a, T=b).  b/c may be NULL (zeros). */
+int ccb_eval_math(int fn, int n, const float* a, const float* b, const float* c, float* out);
+/* counter_gauss(stream, idx0 + i) for i < n, on the device. */
+int ccb_counter_gauss(uint64_t stream, uint64_t idx0, int n, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* COOLCHIC_B200_DIAG_H */

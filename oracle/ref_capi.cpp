@@ -133,6 +133,7 @@ struct cc_trainer {
     LatentSet shape_lat;
     DecoderModel shape_model;
     size_t n_latents = 0, n_params = 0;
+    std::vector<double> records;
 
     detail::CandidateState& cur() {
         if (tr->current().lat.grids.empty())
@@ -395,6 +396,33 @@ int cc_trainer_proxy_iterations(cc_trainer* t, int n, const double* lr, const do
     });
 }
 
+int cc_trainer_set_stream(cc_trainer*, void*) { return CC_OK; }
+
+int cc_trainer_enqueue_proxy_iterations(cc_trainer* t, int n, const double* lr,
+                                        const double* temp, const double* noise_std) {
+    return guarded([&] {
+        t->cur();
+        t->records.assign(4 * size_t(std::max(n, 0)), 0.0);
+        for (int i = 0; i < n; ++i) {
+            const double c = t->tr->proxy_iteration(lr[i], temp[i], noise_std[i]);
+            double* r = &t->records[4 * size_t(i)];
+            r[0] = c;
+            r[1] = t->tr->last_mse();
+            r[2] = t->tr->last_bits();
+            r[3] = double(t->tr->global_iter);
+        }
+        return CC_OK;
+    });
+}
+
+int cc_trainer_synchronize(cc_trainer*) { return CC_OK; }
+
+int cc_trainer_last_records(cc_trainer* t, int n, double* rec) {
+    if (size_t(n) * 4 > t->records.size()) return fail(CC_ERR_CONFIG, "no such records");
+    std::copy(t->records.begin(), t->records.begin() + 4 * size_t(n), rec);
+    return CC_OK;
+}
+
 int cc_trainer_hardround_iteration(cc_trainer* t, double lr, int best_slot, double* cost) {
     return guarded([&] {
         t->cur();
@@ -527,6 +555,40 @@ int cc_trainer_train(cc_trainer* t, cc_train_stats* stats, float* latents, int32
         });
         return CC_OK;
     });
+}
+
+// ---------------------------------------------------------------------------
+// Element-level hooks into the reference's numerics (tests pin the oracle and
+// compare the device restatements against these):
+//   fn 0 cc_exp(a)  1 cc_log(a)  2 cc_tanh(a)  3 softround_value(a, T=b)
+//   4 laplace_bits(a, mu=b, sigma=c)  5 quantize_value(a, amp=255)
+//   6 softround derivative (1-tanh^2(d/T)) / (T * 2tanh(1/2T)) at (a, T=b)
+// ---------------------------------------------------------------------------
+int ccref_eval_math(int fn, int n, const float* a, const float* b, const float* c, float* out) {
+    for (int i = 0; i < n; ++i) {
+        switch (fn) {
+            case 0: out[i] = cc_exp(a[i]); break;
+            case 1: out[i] = cc_log(a[i]); break;
+            case 2: out[i] = cc_tanh(a[i]); break;
+            case 3: out[i] = softround_value(a[i], b[i]); break;
+            case 4: out[i] = laplace_bits(a[i], b[i], c[i]); break;
+            case 5: out[i] = float(quantize_value(a[i], 255)); break;
+            case 6: {
+                float x = a[i], y, th, dx = 0.0f, dy = 1.0f;
+                softround_forward(&x, &y, &th, 1, b[i]);
+                softround_backward(&dy, &th, &dx, 1, b[i]);
+                out[i] = dx;
+                break;
+            }
+            default: return fail(CC_ERR_CONFIG, "unknown math function");
+        }
+    }
+    return CC_OK;
+}
+
+int ccref_counter_gauss(uint64_t stream, uint64_t idx0, int n, float* out) {
+    for (int i = 0; i < n; ++i) out[i] = counter_gauss(stream, idx0 + uint64_t(i));
+    return CC_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -41,7 +41,7 @@ def build_product(verbose: bool = False, ptxas_v: bool = False) -> Path:
     nvcc = _nvcc()
     BUILD.mkdir(exist_ok=True)
     headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list((REPO / "include").glob("*.h"))
-    objs = []
+    objs, cmds = [], []
     for src in sorted(CSRC.glob("*.cu")):
         obj = BUILD / (src.stem + ".o")
         objs.append(obj)
@@ -49,9 +49,17 @@ def build_product(verbose: bool = False, ptxas_v: bool = False) -> Path:
             cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
             if ptxas_v:
                 cmd.insert(1, "-Xptxas=-v")
+            cmds.append(cmd)
+    if cmds:
+        from concurrent.futures import ThreadPoolExecutor
+
+        def run(cmd):
             if verbose:
                 print(" ".join(cmd), flush=True)
             subprocess.run(cmd, check=True)
+
+        with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+            list(ex.map(run, cmds))
     if _newer(OUT, objs):
         cmd = [nvcc, *ARCH, "-shared", "-o", str(OUT), *map(str, objs), "-lcudart"]
         if verbose:

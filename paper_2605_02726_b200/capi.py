@@ -150,20 +150,40 @@ SIGNATURES = {
     "cc_trainer_candidate_cost": (C.c_int, [_P, C.c_int, _D]),
     "cc_trainer_warmup": (C.c_int, [_P]),
     "cc_trainer_train": (C.c_int, [_P, C.POINTER(TrainStatsC), _F, _I32, _F]),
+    "cc_trainer_set_stream": (C.c_int, [_P, C.c_void_p]),
+    "cc_trainer_enqueue_proxy_iterations": (C.c_int, [_P, C.c_int, _D, _D, _D]),
+    "cc_trainer_synchronize": (C.c_int, [_P]),
+    "cc_trainer_last_records": (C.c_int, [_P, C.c_int, _D]),
+}
+
+# include/coolchic_b200_diag.h (product library only)
+DIAG_SIGNATURES = {
+    "ccb_stage_name": (C.c_char_p, [C.c_int]),
+    "ccb_profile_stages": (C.c_int, [_P, C.c_int, C.c_double, C.c_double, C.c_double, _D]),
+    "ccb_kernels_per_iteration": (C.c_int, [_P, _I]),
+    "ccb_arm_flops": (C.c_double, [_P]),
+    "ccb_fp32_peak": (C.c_int, [C.c_int, _D, _D]),
+    "ccb_eval_math": (C.c_int, [C.c_int, C.c_int, _F, _F, _F, _F]),
+    "ccb_counter_gauss": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, _F]),
 }
 
 
-def header_symbols() -> list[str]:
-    """Function names declared in include/coolchic_b200.h (parsed, not assumed)."""
+def header_symbols(header: str = "coolchic_b200.h") -> list[str]:
+    """Function names declared in include/<header> (parsed, not assumed)."""
     import re
 
-    text = (REPO_DIR / "include" / "coolchic_b200.h").read_text()
-    return sorted(set(re.findall(r"\b(cc_[a-z_0-9]+)\s*\(", text)))
+    text = (REPO_DIR / "include" / header).read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)  # drop comments
+    text = re.sub(r"//[^\n]*", "", text)
+    return sorted(set(re.findall(r"\b((?:cc|ccb)_[a-z_0-9]+)\s*\(", text)))
 
 
-def load_library(path: os.PathLike | str) -> C.CDLL:
+def load_library(path: os.PathLike | str, diag: bool = False) -> C.CDLL:
     lib = C.CDLL(str(path))
-    for name, (res, args) in SIGNATURES.items():
+    table = dict(SIGNATURES)
+    if diag:
+        table.update(DIAG_SIGNATURES)
+    for name, (res, args) in table.items():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
@@ -181,5 +201,5 @@ def load_product() -> C.CDLL:
             raise RuntimeError(
                 f"{PRODUCT_SO} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
             )
-        _PRODUCT = load_library(PRODUCT_SO)
+        _PRODUCT = load_library(PRODUCT_SO, diag=True)
     return _PRODUCT

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/coolchic_b200.h"
+#include "../../include/coolchic_b200_diag.h"
 #include "../../include/coolchic_synth.h"
 #include "cc_runtime.h"
 
@@ -554,6 +555,90 @@ int cc_trainer_load_candidate(cc_trainer* t, int slot) {
 int cc_trainer_candidate_cost(cc_trainer* t, int slot, double* cost) {
     return guarded([&] {
         *cost = t->tr->candidate_cost(slot);
+        return CC_OK;
+    });
+}
+
+int cc_trainer_set_stream(cc_trainer* t, void* stream) {
+    return guarded([&] {
+        t->tr->set_stream(static_cast<cudaStream_t>(stream));
+        return CC_OK;
+    });
+}
+
+int cc_trainer_enqueue_proxy_iterations(cc_trainer* t, int n, const double* lr,
+                                        const double* temp, const double* noise_std) {
+    return guarded([&] {
+        t->tr->enqueue_proxy_iterations(n, lr, temp, noise_std);
+        return CC_OK;
+    });
+}
+
+int cc_trainer_synchronize(cc_trainer* t) {
+    return guarded([&] {
+        t->tr->synchronize();
+        return CC_OK;
+    });
+}
+
+int cc_trainer_last_records(cc_trainer* t, int n, double* rec) {
+    return guarded([&] {
+        t->tr->last_records(n, rec);
+        return CC_OK;
+    });
+}
+
+// ---- diagnostics (include/coolchic_b200_diag.h) ----
+const char* ccb_stage_name(int s) {
+    static const char* names[] = {"softq_fwd", "arm", "pyramid", "ups_fwd",
+                                  "syn_fwd",   "syn_bwd", "ups_bwd", "tail"};
+    return (s >= 0 && s < 8) ? names[s] : "?";
+}
+
+int ccb_profile_stages(cc_trainer* t, int n, double lr, double temp, double noise, double* ms) {
+    return guarded([&] {
+        t->tr->profile_stages(n, lr, temp, noise, ms);
+        return CC_OK;
+    });
+}
+
+int ccb_kernels_per_iteration(cc_trainer* t, int* count) {
+    return guarded([&] {
+        *count = t->tr->kernels_per_iteration();
+        return CC_OK;
+    });
+}
+
+double ccb_arm_flops(cc_trainer* t) {
+    const ccb::Plan& P = t->tr->plan();
+    double macs = 0.0;
+    const double per = double(P.D) * P.Wd + double(P.Wd) * P.Wd + 2.0 * P.Wd +
+                       (P.off_astab >= 0 ? 2.0 * P.D : 0.0);
+    for (int gi = 0; gi < P.n_grids; ++gi) {
+        const double cnt = double(P.g[gi].rows) * P.g[gi].cols;
+        macs += cnt * per;
+        if (P.g[gi].ifce_slot >= 0) macs += cnt * double(P.g[gi].rdim) * P.F;
+    }
+    return 6.0 * macs;
+}
+
+int ccb_fp32_peak(int device, double* tflops, double* ms) {
+    return guarded([&] {
+        ccb::fp32_peak(device, tflops, ms);
+        return CC_OK;
+    });
+}
+
+int ccb_eval_math(int fn, int n, const float* a, const float* b, const float* c, float* out) {
+    return guarded([&] {
+        ccb::eval_math(fn, n, a, b, c, out);
+        return CC_OK;
+    });
+}
+
+int ccb_counter_gauss(uint64_t stream, uint64_t idx0, int n, float* out) {
+    return guarded([&] {
+        ccb::gauss(stream, idx0, n, out);
         return CC_OK;
     });
 }

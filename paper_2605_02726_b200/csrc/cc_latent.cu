@@ -127,8 +127,8 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp) {
         else if (g.main_level > 0)
             acc += P.dups[i];
         const float t2 = P.th2[i], t1 = P.th1[i];
-        const float d2 = (1.0f - t2 * t2) * scale;
-        const float d1 = (1.0f - t1 * t1) * scale;
+        const float d2 = fmaf(-t2, t2, 1.0f) * scale;
+        const float d1 = fmaf(-t1, t1, 1.0f) * scale;
         const float dy = acc * d2 * d1;
         P.lat_g[i] = dy;
         if (!isfinite(dy)) atomicAnd(&P.lat_ok[gi], 0);

@@ -53,16 +53,17 @@ __device__ __forceinline__ float cc_exp(float x) {
     const float kLn2 = 0.69314718055994531f;
     const float kInvLn2 = 1.44269504088896341f;
     x = std_min(88.0f, std_max(-87.0f, x));
-    const float z = x * kInvLn2;
-    const float nf = floorf(z + 0.5f);
-    const float t = (z - nf) * kLn2;
+    // z = x*log2(e) feeds two add/subs; the reference build (-ffp-contract=fast)
+    // fuses both into FMAs, so the restatement spells them out.
+    const float nf = floorf(fmaf(x, kInvLn2, 0.5f));
+    const float t = fmaf(x, kInvLn2, -nf) * kLn2;
     float p = 0.0013888889f;
-    p = 0.008333334f + t * p;
-    p = 0.041666668f + t * p;
-    p = 0.16666667f + t * p;
-    p = 0.5f + t * p;
-    p = 1.0f + t * p;
-    p = 1.0f + t * p;
+    p = fmaf(t, p, 0.008333334f);
+    p = fmaf(t, p, 0.041666668f);
+    p = fmaf(t, p, 0.16666667f);
+    p = fmaf(t, p, 0.5f);
+    p = fmaf(t, p, 1.0f);
+    p = fmaf(t, p, 1.0f);
     const float s = __int_as_float((int(nf) + 127) << 23);
     return p * s;
 }
@@ -79,11 +80,11 @@ __device__ __forceinline__ float cc_log(float x) {
     const float s = (m - 1.0f) / (m + 1.0f);
     const float s2 = s * s;
     float p = 0.11111111f;
-    p = 0.14285715f + s2 * p;
-    p = 0.2f + s2 * p;
-    p = 0.33333333f + s2 * p;
-    p = 1.0f + s2 * p;
-    return 2.0f * s * p + float(e) * 0.69314718f;
+    p = fmaf(s2, p, 0.14285715f);
+    p = fmaf(s2, p, 0.2f);
+    p = fmaf(s2, p, 0.33333333f);
+    p = fmaf(s2, p, 1.0f);
+    return fmaf(2.0f * s, p, float(e) * 0.69314718f);
 }
 
 // mathutil.hpp:88-94

@@ -152,6 +152,7 @@ struct Plan {
     int64_t* lat_t;           // per grid
     int64_t* nn_t;            // per tensor
     int* lat_ok;              // per grid: grads finite
+    int* tensor_ok;           // per NN tensor: grads finite
     // device scalars (see DevScalars)
     struct DevScalars* scal;
 };

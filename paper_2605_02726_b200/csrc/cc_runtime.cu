@@ -77,7 +77,8 @@ Trainer::Trainer(const float* image, int h, int w, const cc_encoder_config& enc,
         throw CudaError("libcoolchic_b200 is built for sm_100a; device " + std::string(prop.name) +
                         " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
     num_sms_ = prop.multiProcessorCount;
-    CCB_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    CCB_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+    stream_ = own_stream_;
     build_plan();
     allocate();
     upload_image(image);
@@ -97,7 +98,9 @@ Trainer::~Trainer() {
     }
     for (void* p : allocs_) cudaFree(p);
     if (h_scal_) cudaFreeHost(h_scal_);
-    if (stream_) cudaStreamDestroy(stream_);
+    if (d_sched_) cudaFree(d_sched_);
+    if (d_rec_) cudaFree(d_rec_);
+    if (own_stream_) cudaStreamDestroy(own_stream_);
 }
 
 void* Trainer::dalloc(size_t bytes) {
@@ -394,6 +397,7 @@ void Trainer::allocate() {
     P.lat_t = static_cast<int64_t*>(dalloc(sizeof(int64_t) * kMaxGrids));
     P.nn_t = static_cast<int64_t*>(dalloc(sizeof(int64_t) * kMaxTensors));
     P.lat_ok = static_cast<int*>(dalloc(sizeof(int) * kMaxGrids));
+    P.tensor_ok = static_cast<int*>(dalloc(sizeof(int) * kMaxTensors));
     P.scal = static_cast<DevScalars*>(dalloc(sizeof(DevScalars)));
     d_tiles_ = static_cast<int2*>(dalloc(sizeof(int2) * tiles_host_.size()));
     CCB_CUDA(cudaMemcpy(d_tiles_, tiles_host_.data(), sizeof(int2) * tiles_host_.size(),
@@ -562,6 +566,31 @@ double Trainer::proxy_iteration(double lr, double temp, double noise_std) {
 
 void Trainer::proxy_iterations(int n, const double* lr, const double* temp, const double* noise,
                                double* rec) {
+    enqueue_proxy_iterations(n, lr, temp, noise);
+    if (n <= 0) return;
+    std::vector<double> r(4 * size_t(n));
+    last_records(n, r.data());
+    if (rec) std::memcpy(rec, r.data(), sizeof(double) * r.size());
+}
+
+void Trainer::last_records(int n, double* rec) {
+    if (n <= 0) return;
+    if (n > sched_cap_) throw ConfigError("more records requested than the last batch holds");
+    CCB_CUDA(cudaMemcpyAsync(rec, d_rec_, sizeof(double) * 4 * size_t(n), cudaMemcpyDeviceToHost,
+                             stream_));
+    read_scalars();
+    last_mse_ = rec[4 * size_t(n - 1) + 1];
+    last_bits_ = rec[4 * size_t(n - 1) + 2];
+}
+
+void Trainer::set_stream(cudaStream_t s) {
+    synchronize();
+    stream_ = s ? s : own_stream_;
+    L_.stream = stream_;
+}
+
+void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* temp,
+                                       const double* noise) {
     require_loaded();
     if (n <= 0) return;
     CCB_CUDA(cudaSetDevice(device_));
@@ -588,13 +617,71 @@ void Trainer::proxy_iterations(int n, const double* lr, const double* temp, cons
                              stream_));
     CCB_CUDA(cudaMemsetAsync(&H_.scal->sched_pos, 0, sizeof(int64_t), stream_));
     for (int i = 0; i < n; ++i) run_graph(1);
-    std::vector<double> r(4 * size_t(n));
-    CCB_CUDA(cudaMemcpyAsync(r.data(), d_rec_, sizeof(double) * r.size(), cudaMemcpyDeviceToHost,
-                             stream_));
-    read_scalars();
-    if (rec) std::memcpy(rec, r.data(), sizeof(double) * r.size());
-    last_mse_ = r[4 * size_t(n - 1) + 1];
-    last_bits_ = r[4 * size_t(n - 1) + 2];
+}
+
+// Stage-by-stage replay of one proxy iteration with events in between
+// (diagnostics; same kernels as the graph).
+void Trainer::profile_stages(int n, double lr, double temp, double noise, double* ms) {
+    require_loaded();
+    CCB_CUDA(cudaSetDevice(device_));
+    h_scal_->lr = lr;
+    h_scal_->temp = temp;
+    h_scal_->noise = noise;
+    CCB_CUDA(cudaMemcpyAsync(&H_.scal->lr, &h_scal_->lr, 3 * sizeof(double),
+                             cudaMemcpyHostToDevice, stream_));
+    constexpr int NS = 8;
+    cudaEvent_t ev[NS + 1];
+    for (auto& e : ev) CCB_CUDA(cudaEventCreate(&e));
+    double acc[NS] = {0};
+    for (int it = 0; it < n; ++it) {
+        CCB_CUDA(cudaEventRecord(ev[0], stream_));
+        launch_softq_fwd(L_);
+        CCB_CUDA(cudaEventRecord(ev[1], stream_));
+        launch_arm(L_, kArmProxy);
+        CCB_CUDA(cudaEventRecord(ev[2], stream_));
+        launch_pyramid(L_);
+        CCB_CUDA(cudaEventRecord(ev[3], stream_));
+        launch_ups_forward(L_);
+        CCB_CUDA(cudaEventRecord(ev[4], stream_));
+        launch_syn_forward(L_, true);
+        CCB_CUDA(cudaEventRecord(ev[5], stream_));
+        launch_syn_backward(L_);
+        CCB_CUDA(cudaEventRecord(ev[6], stream_));
+        launch_ups_backward(L_, true);
+        CCB_CUDA(cudaEventRecord(ev[7], stream_));
+        launch_finalize(L_, kArmProxy, -1);
+        launch_latent_grad(L_);
+        launch_adam_latents(L_);
+        launch_nn_step(L_, true, true, nullptr);
+        CCB_CUDA(cudaEventRecord(ev[8], stream_));
+        CCB_CUDA(cudaEventSynchronize(ev[8]));
+        for (int s = 0; s < NS; ++s) {
+            float t = 0.f;
+            CCB_CUDA(cudaEventElapsedTime(&t, ev[s], ev[s + 1]));
+            acc[s] += t;
+        }
+    }
+    for (int s = 0; s < NS; ++s) ms[s] = acc[s] / std::max(1, n);
+    for (auto& e : ev) cudaEventDestroy(e);
+}
+
+int Trainer::kernels_per_iteration() {
+    cudaGraph_t g;
+    CCB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    enqueue_proxy(false);
+    CCB_CUDA(cudaStreamEndCapture(stream_, &g));
+    size_t n = 0;
+    CCB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CCB_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+    int k = 0;
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        CCB_CUDA(cudaGraphNodeGetType(nd, &t));
+        if (t == cudaGraphNodeTypeKernel) ++k;
+    }
+    cudaGraphDestroy(g);
+    return k;
 }
 
 void Trainer::ensure_snapshot(int slot) {

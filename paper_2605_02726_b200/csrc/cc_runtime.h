@@ -70,6 +70,11 @@ public:
     // iteration (cost, mse, bits, global_iter after the iteration)
     void proxy_iterations(int n, const double* lr, const double* temp, const double* noise,
                           double* rec);
+    void enqueue_proxy_iterations(int n, const double* lr, const double* temp, const double* noise);
+    void last_records(int n, double* rec);
+    void set_stream(cudaStream_t s);
+    void profile_stages(int n, double lr, double temp, double noise, double* ms);
+    int kernels_per_iteration();
     double hardround_iteration(double lr, int best_slot);
     double true_cost(double* psnr, double* bpp);
     void quantize_all();
@@ -128,6 +133,7 @@ private:
     int device_ = 0;
     int num_sms_ = 148;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t own_stream_ = nullptr;
     Plan H_{};
     Plan* d_plan_ = nullptr;
     LaunchCtx L_{};
@@ -151,6 +157,10 @@ private:
     } sizes_;
     std::vector<int2> tiles_host_;
 };
+
+void fp32_peak(int device, double* tflops, double* ms);
+void eval_math(int fn, int n, const float* a, const float* b, const float* c, float* out);
+void gauss(uint64_t stream, uint64_t idx0, int n, float* out);
 
 // warmup / train (encoder.hpp:315-413) over the B200 Trainer.
 void warmup(Trainer& tr);

@@ -12,19 +12,26 @@
 
 #include "cc_kernels.h"
 #include "cc_math.cuh"
+#include "cc_reduce.cuh"
 
 namespace ccb {
 
 namespace {
 
-__global__ void k_finalize(const Plan* __restrict__ pp, int mode, int snap_slot) {
+// one CTA of 256 threads: strided partial sums, then a fixed-order tree
+__global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, int mode,
+                                                  int snap_slot) {
     const Plan& P = *pp;
     double* bc_lat = P.bc_lat;
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    double bits = 0.0;
-    for (int b = 0; b < P.n_bits_part; ++b) bits += P.bits_part[b];
-    double se = 0.0;
-    for (int b = 0; b < P.n_mse_part; ++b) se += P.mse_part[b];
+    __shared__ double red[8];
+    double b_loc = 0.0, s_loc = 0.0;
+    for (int b = threadIdx.x; b < P.n_bits_part; b += blockDim.x) b_loc += P.bits_part[b];
+    for (int b = threadIdx.x; b < P.n_mse_part; b += blockDim.x) s_loc += P.mse_part[b];
+    const double bits_all = block_sum(b_loc, red);
+    const double se_all = block_sum(s_loc, red);
+    for (int t = threadIdx.x; t < P.n_tensors; t += blockDim.x) P.tensor_ok[t] = 1;
+    if (threadIdx.x != 0) return;
+    const double bits = bits_all, se = se_all;
     const double mse = se / double(3 * P.npix);
     const double cost = mse + P.lambda * (bits / double(P.npix));
     DevScalars* s = P.scal;
@@ -43,28 +50,46 @@ __global__ void k_finalize(const Plan* __restrict__ pp, int mode, int snap_slot)
     s->snap_take = (snap_slot >= 0 && s->cost_ok && cost < s->snap_cost[snap_slot]) ? 1 : 0;
 }
 
-// One CTA per NN tensor.
-__global__ void __launch_bounds__(256) k_nn_step(const Plan* __restrict__ pp, int do_step,
-                                                 int count_iter, double* __restrict__ cost_log) {
+// Wide reduction: one warp per parameter over the whole grid; lanes stride the
+// per-CTA partial rows, fixed shuffle tree, regions in index order.  Writes
+// ParamTensor::g and clears the tensor's finiteness flag on a non-finite grad.
+__global__ void __launch_bounds__(256) k_nn_reduce(const Plan* __restrict__ pp,
+                                                   int* __restrict__ tensor_ok) {
     const Plan& P = *pp;
-    const double lr = P.scal->lr;
-    const int ti = blockIdx.x;
-    const int off = P.tensor_off[ti], n = P.tensor_size[ti];
-    bool finite = true;
-    for (int e = threadIdx.x; e < n; e += blockDim.x) {
-        const int p = off + e;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int p = gw; p < P.n_params; p += nw) {
         double sum = 0.0;
         for (int r = 0; r < P.n_regions; ++r) {
             const PartialRegion& R = P.region[r];
             if (p < R.param_off || p >= R.param_off + R.count) continue;
             const double* col = P.partials + R.base + (p - R.param_off);
-            for (int b = 0; b < R.nblocks; ++b) sum += col[int64_t(b) * R.count];
+            double s = 0.0;
+            for (int b = lane; b < R.nblocks; b += 32) s += col[int64_t(b) * R.count];
+            sum += warp_sum(s);
         }
-        const float g = float(sum);
-        P.grads[p] = g;
-        finite = finite && isfinite(g);
+        if (lane == 0) {
+            const float g = float(sum);
+            P.grads[p] = g;
+            if (!isfinite(g)) {
+                int ti = 0;
+                while (ti + 1 < P.n_tensors && P.tensor_off[ti + 1] <= p) ++ti;
+                atomicAnd(&tensor_ok[ti], 0);
+            }
+        }
     }
-    finite = __syncthreads_and(finite);
+}
+
+// One CTA per NN tensor: Adam with the per-tensor skip (optim.hpp:38-41).
+__global__ void __launch_bounds__(256) k_nn_step(const Plan* __restrict__ pp, int do_step,
+                                                 int count_iter, double* __restrict__ cost_log,
+                                                 const int* __restrict__ tensor_ok) {
+    const Plan& P = *pp;
+    const double lr = P.scal->lr;
+    const int ti = blockIdx.x;
+    const int off = P.tensor_off[ti], n = P.tensor_size[ti];
+    const bool finite = tensor_ok[ti] != 0;
     DevScalars* s = P.scal;
     if (do_step && s->cost_ok) {
         if (finite) {
@@ -122,12 +147,16 @@ __global__ void k_snapshot_copy(const Plan* __restrict__ pp, int slot, float* __
 }  // namespace
 
 void launch_finalize(const LaunchCtx& L, int mode, int snap_slot) {
-    k_finalize<<<1, 32, 0, L.stream>>>(L.plan, mode, snap_slot);
+    k_finalize<<<1, 256, 0, L.stream>>>(L.plan, mode, snap_slot);
 }
 
 void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log) {
+    const int warps = L.host->n_params;
+    const int blocks = (warps + 7) / 8;
+    k_nn_reduce<<<blocks, 256, 0, L.stream>>>(L.plan, L.host->tensor_ok);
     k_nn_step<<<L.host->n_tensors, 256, 0, L.stream>>>(L.plan, do_step ? 1 : 0,
-                                                       count_iter ? 1 : 0, cost_log);
+                                                       count_iter ? 1 : 0, cost_log,
+                                                       L.host->tensor_ok);
 }
 
 void launch_sched_load(const LaunchCtx& L, const double* sched) {

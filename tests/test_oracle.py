@@ -1,0 +1,196 @@
+"""The oracle, pinned (CPU only).
+
+1. The reference checker (oracle/_ref) reproduces the reference's own
+   known-answer tests (proj/tests/*.cpp) — so the checker is the reference.
+2. The committed golden fixtures are reproducible from the reference build.
+3. The plain-C restatement (oracle/libccport.so) matches the golden fixtures
+   within the north-star tolerance and the known answers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+
+from paper_2605_02726_b200 import capi
+from paper_2605_02726_b200.trainer import DecoderConfig, EncoderConfig, Trainer
+from tests import golden_util
+from tests.conftest import make_image
+
+
+def _math(lib, prefix, fn, a, b=None, c=None):
+    f = getattr(lib, f"{prefix}_eval_math")
+    f.restype = C.c_int
+    f.argtypes = [C.c_int, C.c_int, capi._F, capi._F, capi._F, capi._F]
+    n = len(a)
+    a = np.ascontiguousarray(a, np.float32)
+    b = np.ascontiguousarray(b if b is not None else np.zeros(n), np.float32)
+    c = np.ascontiguousarray(c if c is not None else np.zeros(n), np.float32)
+    out = np.empty(n, np.float32)
+    assert f(fn, n, a.ctypes.data_as(capi._F), b.ctypes.data_as(capi._F),
+             c.ctypes.data_as(capi._F), out.ctypes.data_as(capi._F)) == 0
+    return out
+
+
+def ref_softround(x, t):  # tests/testutil.hpp:18-22
+    f = math.floor(x)
+    return f + 0.5 + math.tanh((x - f - 0.5) / t) / (2.0 * math.tanh(1.0 / (2.0 * t)))
+
+
+def ref_laplace_bits(v, mu, sigma):  # tests/testutil.hpp:24-33
+    b = sigma / math.sqrt(2.0)
+
+    def cdf(x):
+        return 0.5 * math.exp((x - mu) / b) if x < mu else 1.0 - 0.5 * math.exp(-(x - mu) / b)
+
+    p = cdf(v + 0.5) - cdf(v - 0.5)
+    return -math.log2(max(p, 1.0 / 65536.0))
+
+
+@pytest.fixture(params=["ref", "port"])
+def checker(request, ref_lib, port_lib):
+    return (ref_lib, "ccref") if request.param == "ref" else (port_lib, "ccport")
+
+
+def test_softround_known_answers(checker):
+    # tests/test_numerics.cpp:57-71
+    lib, pre = checker
+    want = ref_softround(0.3, 0.35)
+    assert want == pytest.approx(0.2103, abs=2e-4)
+    assert _math(lib, pre, 3, [0.3], [0.35])[0] == pytest.approx(want, abs=1e-4)
+    dwant = 1.0 / (2.0 * 0.35 * math.tanh(1.0 / 0.7))
+    assert dwant == pytest.approx(1.603, abs=2e-3)
+    assert _math(lib, pre, 6, [0.5], [0.35])[0] == pytest.approx(dwant, rel=1e-5)
+
+
+def test_laplace_known_answers(checker):
+    # tests/test_entropy.cpp:156-174
+    lib, pre = checker
+    want = ref_laplace_bits(0.0, 0.0, math.sqrt(2.0))
+    assert want == pytest.approx(1.3457, abs=1e-4)
+    assert _math(lib, pre, 4, [0.0], [0.0], [math.sqrt(2.0)])[0] == pytest.approx(want, abs=1e-4)
+    rng = np.random.default_rng(5)
+    mu = rng.uniform(-3, 3, 50).astype(np.float32)
+    sg = rng.uniform(0.2, 5, 50).astype(np.float32)
+    v = np.trunc(rng.uniform(-8, 8, 50)).astype(np.float32)
+    a = _math(lib, pre, 4, v, mu, sg)
+    b = _math(lib, pre, 4, 2 * mu - v, mu, sg)
+    assert np.allclose(a, b, rtol=1e-4)
+    assert _math(lib, pre, 4, [100.0], [0.0], [0.06])[0] == pytest.approx(16.0, abs=1e-6)
+    # against the independent double-precision oracle
+    ref = np.array([ref_laplace_bits(float(x), float(m), float(s)) for x, m, s in zip(v, mu, sg)])
+    assert np.allclose(a, ref, rtol=2e-4, atol=2e-4)
+
+
+def test_quantizer_known_answers(checker):
+    # tests/test_latent.cpp:64-81
+    lib, pre = checker
+    x = [0.49, 0.51, -1.5, 1.5, -0.49, 300.0, -300.0] + [float(v) for v in range(-10, 11)]
+    want = [0, 1, -2, 2, 0, 255, -255] + list(range(-10, 11))
+    assert list(_math(lib, pre, 5, x).astype(int)) == want
+    rng = np.random.default_rng(1)
+    xs = rng.uniform(-20, 20, 1000).astype(np.float32)
+    q = _math(lib, pre, 5, xs)
+    assert np.array_equal(_math(lib, pre, 5, q), q)
+
+
+def test_fast_math_accuracy(checker):
+    # tests/test_numerics.cpp:451-459: polynomial exp/log/tanh vs libm
+    lib, pre = checker
+    x = np.linspace(-20, 20, 2001).astype(np.float32)
+    assert np.allclose(_math(lib, pre, 0, x), np.exp(x.astype(np.float64)), rtol=2e-6)
+    xp = np.linspace(1e-3, 100, 2001).astype(np.float32)
+    assert np.allclose(_math(lib, pre, 1, xp), np.log(xp.astype(np.float64)), rtol=2e-6, atol=2e-7)
+    assert np.allclose(_math(lib, pre, 2, x / 4), np.tanh(x.astype(np.float64) / 4), atol=2e-7)
+
+
+def test_math_vectors_reproduce(ref_lib):
+    g = dict(np.load(golden_util.GOLDEN / "math_vectors.npz"))
+    for f in range(7):
+        out = _math(ref_lib, "ccref", f, g[f"fn{f}_a"], g[f"fn{f}_b"], g[f"fn{f}_c"])
+        assert np.array_equal(out, g[f"fn{f}_out"]), f
+
+
+def test_port_math_vectors(port_lib):
+    g = dict(np.load(golden_util.GOLDEN / "math_vectors.npz"))
+    for f in range(7):
+        out = _math(port_lib, "ccport", f, g[f"fn{f}_a"], g[f"fn{f}_b"], g[f"fn{f}_c"])
+        ref = g[f"fn{f}_out"]
+        if f == 0:  # polynomial exp: 98 % bit-identical, the rest within 1 ulp
+            assert np.allclose(out, ref, rtol=1e-6, atol=0.0), f
+        else:       # log, tanh, softround, Laplace bits, quantiser, derivative
+            assert np.array_equal(out, ref), f
+
+
+def test_context_offsets_hop(ref_lib):
+    # HOP causal offsets nearest-first — observed through the layout
+    img = make_image(ref_lib, 16, 16)
+    with Trainer(img, EncoderConfig(), DecoderConfig.hop(), lib=ref_lib) as tr:
+        assert tr.layout.pad == 3
+    with Trainer(img, EncoderConfig(), DecoderConfig(spatial_ctx=26), lib=ref_lib) as tr:
+        assert tr.layout.pad == 4
+
+
+@pytest.mark.parametrize("h,w,n_lat", [(256, 256, 87712), (512, 768, 526272)])
+def test_grid_shapes(ref_lib, port_lib, h, w, n_lat):
+    # SURVEY 8(a) sizes (build_latents, latent.hpp:46-70)
+    img = np.zeros((3, h, w), np.float32)
+    for lib in (ref_lib, port_lib):
+        with Trainer(img, EncoderConfig(), DecoderConfig.hop(), lib=lib) as tr:
+            assert tr.n_latents == n_lat
+            assert tr.n_params == 1846
+            assert [g.level for g in tr.grids] == [6, 5, 4, 6, 5, 4, 3, 2, 1, 0]
+            assert [g.hyper for g in tr.grids] == [True] * 3 + [False] * 7
+            assert [g.ifce_slot for g in tr.grids] == [-1] * 7 + [2, 1, 0]
+
+
+def test_zero_arm_rate_on_1x1(ref_lib, port_lib):
+    # tests/test_entropy.cpp:176-189 (zero params: every grid costs bits(0;0,1))
+    img = np.full((3, 1, 1), 0.5, np.float32)
+    per = ref_laplace_bits(0.0, 0.0, 1.0)
+    for lib in (ref_lib, port_lib):
+        with Trainer(img, EncoderConfig(), DecoderConfig.hop(), lib=lib) as tr:
+            tr.fresh_candidate(0)
+            st = tr.get_state()
+            st["latents"][:] = 0
+            st["params"][:] = 0
+            tr.set_state(st)
+            tr.true_cost()
+            _, bits = 0, None
+            c, psnr, bpp = tr.true_cost()
+            assert bpp == pytest.approx(per * len(tr.grids), rel=1e-4)
+
+
+@pytest.mark.parametrize("case", golden_util.CASES)
+def test_reference_reproduces_golden(ref_lib, case):
+    rep = golden_util.replay(ref_lib, case, iters=2)
+    assert rep.init_latents_exact and rep.init_params_exact
+    assert max(rep.scalars) <= 1e-9
+    assert max(rep.param_grad) <= 1e-6 and max(rep.lat_grad) <= 1e-6
+    assert rep.q_exact
+
+
+@pytest.mark.parametrize("case", golden_util.CASES)
+def test_port_matches_golden(port_lib, case):
+    rep = golden_util.replay(port_lib, case, iters=3)
+    golden_util.assert_report(rep, exact_init=True)
+
+
+def test_port_matches_reference_cfg1_prefix(port_lib):
+    """Config 1 (256x256 HOP, zero latents): first 10 free-running iterations of
+    the port against the reference's per-iteration scalars (golden)."""
+    g = dict(np.load(golden_util.GOLDEN / "cfg1_scalars.npz"))
+    with Trainer(g["image"], EncoderConfig(lmbda=1e-3, seed=0), DecoderConfig.hop(),
+                 lib=port_lib) as tr:
+        tr.fresh_candidate(0)
+        st = tr.get_state()
+        st["latents"][:] = 0
+        tr.set_state(st)
+        for i in range(10):
+            c = tr.proxy_iteration(1e-2, 0.35, 0.22)
+            m, b = tr.last_terms()
+            ref = g["scalars"][i]
+            assert abs(c - ref[0]) / ref[0] <= 1e-5
+            assert abs(b - ref[2]) / ref[2] <= 1e-5
