@@ -473,6 +473,51 @@ __global__ void __launch_bounds__(kArmTile) k_arm(const Plan* __restrict__ pp,
     }
 }
 
+// 2x2 block sums of dF for every IFCE-equipped grid, ALL levels in one
+// launch: CTA (coarse block, slot*F + f) loads the 2^smax x 2^smax fine
+// block of channel f (zeros past the grid edge) and halves it level by level
+// in shared memory, writing each level.  Summation order ((a+b)+(c+d)) is
+// the same at every level, so results do not depend on the blocking.
+__global__ void __launch_bounds__(256) k_pyramid_fused(const Plan* __restrict__ pp) {
+    const Plan& P = *pp;
+    extern __shared__ float pbuf[];
+    const int s = blockIdx.y / P.F, f = blockIdx.y - s * P.F;
+    const int smax = P.slot_smax[s];
+    const int B = 1 << smax;
+    const int cr = P.slot_pyr_rows[s][smax], ccn = P.slot_pyr_cols[s][smax];
+    const int R = blockIdx.x / ccn, Cc = blockIdx.x - R * ccn;
+    if (R >= cr) return;
+    float* a = pbuf;
+    float* b = pbuf + B * B;
+    {
+        const int rows = P.slot_pyr_rows[s][0], cols = P.slot_pyr_cols[s][0];
+        const float* in = P.dfeat + P.slot_pyr_off[s][0] + int64_t(f) * rows * cols;
+        for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
+            const int y = e >> smax, x = e & (B - 1);
+            const int gy = R * B + y, gx = Cc * B + x;
+            a[e] = (gy < rows && gx < cols) ? in[int64_t(gy) * cols + gx] : 0.0f;
+        }
+    }
+    __syncthreads();
+    for (int l = 1; l <= smax; ++l) {
+        const int n = B >> l;  // edge of this level's block
+        const int rows = P.slot_pyr_rows[s][l], cols = P.slot_pyr_cols[s][l];
+        float* out = P.dfeat + P.slot_pyr_off[s][l] + int64_t(f) * rows * cols;
+        for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+            const int y = e / n, x = e - y * n;
+            const float* src = a + (2 * y) * (2 * n) + 2 * x;
+            const float v = (src[0] + src[1]) + (src[2 * n] + src[2 * n + 1]);
+            b[e] = v;
+            const int gy = R * n + y, gx = Cc * n + x;
+            if (gy < rows && gx < cols) out[int64_t(gy) * cols + gx] = v;
+        }
+        __syncthreads();
+        float* t = a;
+        a = b;
+        b = t;
+    }
+}
+
 // 2x2 block sums of dF for every IFCE-equipped grid, one level per launch.
 __global__ void k_pyramid(const Plan* __restrict__ pp, int level) {
     const Plan& P = *pp;
@@ -586,11 +631,25 @@ int arm_blocks_per_sm(int Dp, int Wp) {
     return b < 1 ? 1 : (b > 8 ? 8 : b);
 }
 
-void launch_pyramid(const LaunchCtx& L) {
+static size_t pyramid_smem(const Plan& H) {
     int smax = 0;
-    for (int s = 0; s < L.host->n_slots; ++s) smax = smax > L.host->slot_smax[s] ? smax : L.host->slot_smax[s];
-    for (int lv = 1; lv <= smax; ++lv)
-        k_pyramid<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, lv);
+    for (int s = 0; s < H.n_slots; ++s) smax = smax > H.slot_smax[s] ? smax : H.slot_smax[s];
+    const size_t B = size_t(1) << smax;
+    return sizeof(float) * (B * B + (B / 2) * (B / 2));
+}
+
+void pyramid_configure(const Plan& H) {
+    cudaFuncSetAttribute(k_pyramid_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(pyramid_smem(H)));
+}
+
+void launch_pyramid(const LaunchCtx& L) {
+    const Plan& H = *L.host;
+    if (H.n_slots == 0 || H.F == 0) return;
+    // every slot's deepest level is the coarsest grid: same coarse block count
+    const int nblk = H.slot_pyr_rows[0][H.slot_smax[0]] * H.slot_pyr_cols[0][H.slot_smax[0]];
+    const dim3 grid(nblk, H.n_slots * H.F);
+    k_pyramid_fused<<<grid, 256, pyramid_smem(H), L.stream>>>(L.plan);
 }
 
 }  // namespace ccb

@@ -40,10 +40,13 @@ void launch_arm(const LaunchCtx& L, int mode);
 void launch_pyramid(const LaunchCtx& L);
 int arm_blocks_per_sm(int Dp, int Wp);
 void arm_configure(int Dp, int Wp);
+void pyramid_configure(const Plan& H);
 
 // upsampling (cc_ups.cu)
 void launch_ups_forward(const LaunchCtx& L);
 void launch_ups_backward(const LaunchCtx& L, bool latent_grads);
+int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward);
+void ups_configure();
 
 // synthesis (cc_syn.cu)
 void launch_syn_forward(const LaunchCtx& L, bool backward);
@@ -51,6 +54,8 @@ void launch_syn_backward(const LaunchCtx& L);
 int syn_padded_hidden(int F);
 size_t syn_trunk_smem(int FP);
 void syn_configure(int FP);
+void syn_post_configure();
+int syn_post_tiles(int H, int W);
 
 // optimizer / bookkeeping (cc_step.cu)
 void launch_finalize(const LaunchCtx& L, int mode, int snap_slot);

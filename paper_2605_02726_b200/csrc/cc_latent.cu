@@ -92,6 +92,13 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp) {
     const float temp = float(P.scal->temp);
     const int cost_ok = P.scal->cost_ok;
     const float scale = 1.0f / (temp * softround_denom(temp));
+    __shared__ int s_dy[kMaxCtx], s_dx[kMaxCtx];
+    const int S = P.S;
+    for (int o = threadIdx.x; o < kMaxCtx; o += blockDim.x) {
+        s_dy[o] = P.ctx_dy[o];
+        s_dx[o] = P.ctx_dx[o];
+    }
+    __syncthreads();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
         if (!cost_ok) {  // encoder.hpp:118 returns before the backward chain
@@ -105,8 +112,10 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp) {
         const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
         float acc = P.gown[i];
         const float* dc = P.dctx + g.dctx_off;
-        for (int o = 0; o < P.S; ++o) {
-            const int rs = r - P.ctx_dy[o], cs = c - P.ctx_dx[o];
+        // causal successors' context gradients, fixed offset order
+#pragma unroll 4
+        for (int o = 0; o < S; ++o) {
+            const int rs = r - s_dy[o], cs = c - s_dx[o];
             if (rs >= 0 && rs < g.rows && cs >= 0 && cs < g.cols)
                 acc += dc[int64_t(o) * cnt + int64_t(rs) * g.cols + cs];
         }

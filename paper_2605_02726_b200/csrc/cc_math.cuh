@@ -101,6 +101,26 @@ __device__ __forceinline__ float softround_denom(float temp) {
     return 2.0f * cc_tanh(1.0f / (2.0f * temp));
 }
 
+// e / n for small non-negative ints (e < 2^22, n >= 1) without an integer
+// division (tile index splits in the stencil kernels): (e + 0.5) / n is at
+// least 0.5/n away from an integer, far above the fp32 rounding error.
+struct FDiv {
+    float inv;
+    int n;
+    __device__ __forceinline__ explicit FDiv(int n_) : inv(1.0f / float(n_)), n(n_) {}
+    __device__ __forceinline__ int div(int e) const { return int((float(e) + 0.5f) * inv); }
+};
+
+// Asynchronous 4-byte global -> shared copy (LDGSTS): window staging keeps
+// every load of a tile in flight at once instead of load/wait/store.
+__device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // Laplace sigma head (entropy_model.hpp:260, layers.hpp:591-592).
 __device__ __forceinline__ float sigma_from_raw(float raw1) {
     return std_min(kSigmaMaxF, std_max(kSigmaMinF, cc_exp(raw1)));

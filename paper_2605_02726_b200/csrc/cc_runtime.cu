@@ -320,7 +320,8 @@ void Trainer::build_plan() {
     L_.syn_ntiles = int(syn_tiles);
     L_.syn_blocks = int(std::min<int64_t>(syn_tiles, int64_t(num_sms_) * syn_per_sm));
     P.n_bits_part = L_.arm_blocks;
-    P.n_mse_part = L_.pix_blocks;
+    // k_syn_post: persistent, one 16x16 tile at a time, one MSE/post-grad row per CTA
+    P.n_mse_part = std::max(1, std::min(syn_post_tiles(h, w), 3 * num_sms_));
 
     // ---- partial regions ----
     int64_t pbase = 0;
@@ -335,15 +336,16 @@ void Trainer::build_plan() {
     P.arm_nvals = P.off_tconv[0];
     P.reg_arm = region(0, P.arm_nvals, L_.arm_blocks);
     for (int j = 0; j < P.L - 1; ++j) {
-        const int nb = L_.red_blocks * P.ups_n[j];
+        // k_ups_bwd writes one row per CTA: dk4 (row + column passes) and dr3
+        const int nb = ups_blocks_x(P, j, num_sms_, false) * P.ups_n[j];
         P.reg_ups_rows[j] = region(P.off_tconv[j], 4, nb);
-        P.reg_ups_cols[j] = region(P.off_tconv[j], 4, nb);
+        P.reg_ups_cols[j] = -1;
         P.reg_ups_ref[j] = region(P.off_refine[j], 3, nb);
     }
     P.syn_nvals = P.n_params - P.off_c1w;
     P.reg_syn_trunk = region(P.off_c1w, P.syn_nvals, L_.syn_blocks);
     for (int i = 0; i < P.posts; ++i)
-        P.reg_post[i] = region(P.off_pw[0], P.off_pb[P.posts - 1] + 3 - P.off_pw[0], L_.red_blocks);
+        P.reg_post[i] = region(P.off_pw[0], P.off_pb[P.posts - 1] + 3 - P.off_pw[0], P.n_mse_part);
 
     // sizes for allocate()
     P.g[0].dfeat_off = P.g[0].dfeat_off;  // (no-op; keeps field initialised)
@@ -382,7 +384,7 @@ void Trainer::allocate() {
     P.syn_t = f32(3 * np);
     P.syn_p[0] = f32(3 * np);
     P.syn_p[1] = f32(3 * np);
-    P.syn_sz = nullptr;
+    P.syn_sz = f32(3 * np);
     P.syn_dx = f32(3 * np);
     P.syn_dt = f32(3 * np);
     P.syn_dtmp = f32(3 * np);
@@ -415,6 +417,9 @@ void Trainer::allocate() {
     L_.arm_tiles = d_tiles_;
     arm_configure(P.Dp, P.Wp);
     syn_configure(syn_padded_hidden(P.syn_F));
+    ups_configure();
+    syn_post_configure();
+    pyramid_configure(H_);
 }
 
 void Trainer::synchronize() { CCB_CUDA(cudaStreamSynchronize(stream_)); }

@@ -3,13 +3,15 @@
 // Replaces synthesize_forward / synthesize_backward (synthesis.hpp:191-233),
 // conv1x1_* (layers.hpp:196-250), conv3x3_* (layers.hpp:257-343), mse_*
 // (layers.hpp:643-657) and the straight-through clamp (layers.hpp:661-664,
-// synthesis.hpp:215).
+// synthesis.hpp:215).  Three kernels per iteration:
 //
-//   k_syn_trunk_fwd   z -> relu(c1) -> c2 = t (3 planes); the F-wide hidden
-//                     layer h1 never leaves registers (663 MAC/px HOP)
-//   k_syn_post_fwd    residual 3x3 post filter i (replicate padding)
-//   k_syn_out         + stabilizer, clamp, MSE partial (fp64), dx̂
-//   k_syn_post_bwd    post filter i backward: gather-transposed conv + dW
+//   k_syn_trunk_fwd   per pixel: z -> relu(c1) -> c2 = t, and the linear
+//                     stabilizer term s = stab·z (3 + 3 planes); the F-wide
+//                     hidden layer never leaves registers (663 MAC/px HOP)
+//   k_syn_post        per 16x16 tile, in shared memory on replicate-clamped
+//                     halos: residual 3x3 posts forward, clamp, MSE (fp64,
+//                     owned pixels), dx̂, posts backward (transposed conv by
+//                     gather), post weight gradients -> dt
 //   k_syn_trunk_bwd   recompute h1, dh1, dz, and the c1/c2/stab weight
 //                     gradients as per-tile shared-memory GEMMs (persistent
 //                     CTAs, fixed-order fp64 accumulation; no atomics)
@@ -34,7 +36,7 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 // ---------------------------------------------------------------- trunk fwd
 __global__ void __launch_bounds__(256) k_syn_trunk_fwd(const Plan* __restrict__ pp) {
     const Plan& P = *pp;
-    __shared__ float c1w[64 * kLZ], c1b[64], c2w[3 * 64], c2b[4];
+    __shared__ float c1w[64 * kLZ], c1b[64], c2w[3 * 64], c2b[4], st[3 * kLZ];
     const int L = P.L, F = P.syn_F;
     for (int e = threadIdx.x; e < 64 * kLZ; e += blockDim.x) {
         const int f = e / kLZ, k = e - f * kLZ;
@@ -46,6 +48,10 @@ __global__ void __launch_bounds__(256) k_syn_trunk_fwd(const Plan* __restrict__ 
         c2w[e] = f < F ? P.params[P.off_c2w + co * F + f] : 0.0f;
     }
     if (threadIdx.x < 4) c2b[threadIdx.x] = threadIdx.x < 3 ? P.params[P.off_c2b + threadIdx.x] : 0.0f;
+    if (threadIdx.x < 3 * kLZ) {
+        const int co = threadIdx.x / kLZ, k = threadIdx.x - co * kLZ;
+        st[threadIdx.x] = (P.off_sstab >= 0 && k < L) ? P.params[P.off_sstab + co * L + k] : 0.0f;
+    }
     __syncthreads();
     const int64_t np = P.npix;
     for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < np;
@@ -66,165 +72,292 @@ __global__ void __launch_bounds__(256) k_syn_trunk_fwd(const Plan* __restrict__ 
         P.syn_t[p] = t0;
         P.syn_t[np + p] = t1;
         P.syn_t[2 * np + p] = t2;
-    }
-}
-
-// ---------------------------------------------------------- residual posts
-__device__ __forceinline__ const float* post_in(const Plan& P, int i) {
-    return i == 0 ? P.syn_t : P.syn_p[i - 1];
-}
-
-// conv3x3_forward (layers.hpp:257-300) + residual (synthesis.hpp:204-209)
-__global__ void k_syn_post_fwd(const Plan* __restrict__ pp, int i) {
-    const Plan& P = *pp;
-    __shared__ float w[81], b[3];
-    if (threadIdx.x < 81) w[threadIdx.x] = P.params[P.off_pw[i] + threadIdx.x];
-    if (threadIdx.x < 3) b[threadIdx.x] = P.params[P.off_pb[i] + threadIdx.x];
-    __syncthreads();
-    const float* in = post_in(P, i);
-    float* out = P.syn_p[i];
-    const int H = P.H, W = P.W;
-    const int64_t np = P.npix;
-    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < np;
-         p += int64_t(gridDim.x) * blockDim.x) {
-        const int r = int(p / W), c = int(p - int64_t(r) * W);
-        const int rm = r > 0 ? r - 1 : 0, rp = r < H - 1 ? r + 1 : H - 1;
-        const int cm = c > 0 ? c - 1 : 0, cp = c < W - 1 ? c + 1 : W - 1;
+        // stabilizer s = stab·z (synthesis.hpp:211; zero padding is exact)
 #pragma unroll
         for (int co = 0; co < 3; ++co) {
-            float acc = b[co];
+            float a = 0.0f;
 #pragma unroll
-            for (int ci = 0; ci < 3; ++ci) {
-                const float* k = w + (co * 3 + ci) * 9;
-                const float* x = in + int64_t(ci) * np;
-                const float* x0 = x + int64_t(rm) * W;
-                const float* x1 = x + int64_t(r) * W;
-                const float* x2 = x + int64_t(rp) * W;
-                acc += k[0] * x0[cm] + k[1] * x0[c] + k[2] * x0[cp] + k[3] * x1[cm] + k[4] * x1[c] +
-                       k[5] * x1[cp] + k[6] * x2[cm] + k[7] * x2[c] + k[8] * x2[cp];
-            }
-            out[int64_t(co) * np + p] = acc + in[int64_t(co) * np + p];
+            for (int k = 0; k < kLZ; ++k) a = fmaf(st[co * kLZ + k], zv[k], a);
+            P.syn_sz[co * np + p] = a;
         }
     }
 }
 
-// x̂ = clamp01(posts + stab·z); MSE (double) and dx̂ = 2(x̂ - x)/(3HW)
-// (synthesis.hpp:210-212, layers.hpp:643-657, encoder.hpp:256-260).
-__global__ void __launch_bounds__(256) k_syn_out(const Plan* __restrict__ pp, int with_grad) {
+// ------------------------------------------------- fused posts + MSE (NP posts)
+// On replicate-clamped windows W_h (the 16x16 tile grown by h, cut at the
+// image border):
+//   p_0 = t on W_2NP,  p_i = p_{i-1} + conv_i(p_{i-1}) on W_{2NP-i}
+//   x̂ = clamp01(p_NP + s) on W_NP, dx̂ = 2(x̂ - x)/(3HW)        (encoder.hpp:256-260)
+//   d_i = d_{i+1} + conv_iᵀ(d_{i+1}) on W_i, d_NP = dx̂           (synthesis.hpp:222-228)
+// so dt = d_0 on the tile.  MSE and the post weight gradients sum over OWNED
+// pixels only.
+constexpr int kPT = 16;
+
+template <int NP>
+struct PostSmem {
+    static constexpr int PW = kPT + 4 * NP;   // p_0 window edge
+    static constexpr int DW = kPT + 2 * NP;   // d_NP window edge
+    float p[NP + 1][3][PW * PW];
+    float d[NP + 1][3][DW * DW];
+    float sz[3][DW * DW];   // stabilizer term on W_NP
+    float img[3][DW * DW];  // target on W_NP
+    double red[8];
+};
+
+struct PWin {
+    int r0, r1, c0, c1;  // inclusive, clamped
+    __device__ __forceinline__ int w() const { return c1 - c0 + 1; }
+    __device__ __forceinline__ int n() const { return (r1 - r0 + 1) * (c1 - c0 + 1); }
+};
+
+template <int NP>
+__global__ void __launch_bounds__(256, 2) k_syn_post(const Plan* __restrict__ pp, int with_grad) {
     const Plan& P = *pp;
-    __shared__ float st[3 * kLZ];
-    __shared__ double red[8];
-    const int L = P.L;
-    if (threadIdx.x < 3 * kLZ) {
-        const int co = threadIdx.x / kLZ, k = threadIdx.x - co * kLZ;
-        st[threadIdx.x] = (P.off_sstab >= 0 && k < L) ? P.params[P.off_sstab + co * L + k] : 0.0f;
-    }
-    __syncthreads();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PostSmem<NP>& sm = *reinterpret_cast<PostSmem<NP>*>(smem_raw);
+    __shared__ float w[2][81], bb[2][3];
+    const int H = P.H, W = P.W;
     const int64_t np = P.npix;
-    const float* pl = P.posts > 0 ? P.syn_p[P.posts - 1] : P.syn_t;
+    for (int i = 0; i < NP; ++i) {
+        if (threadIdx.x < 81) w[i][threadIdx.x] = P.params[P.off_pw[i] + threadIdx.x];
+        if (threadIdx.x < 3) bb[i][threadIdx.x] = P.params[P.off_pb[i] + threadIdx.x];
+    }
     const float s = float(2.0 / double(3 * np));
-    double acc = 0.0;
-    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < np;
-         p += int64_t(gridDim.x) * blockDim.x) {
-        float zv[kLZ];
+    float wacc[2][10];
 #pragma unroll
-        for (int k = 0; k < kLZ; ++k) zv[k] = k < L ? P.z[int64_t(k) * np + p] : 0.0f;
+    for (int k = 0; k < 10; ++k) wacc[0][k] = wacc[1][k] = 0.0f;
+    double mse = 0.0;
+    const int tiles_x = (W + kPT - 1) / kPT;
+    const int ntiles = tiles_x * ((H + kPT - 1) / kPT);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int y0 = (tile / tiles_x) * kPT, x0 = (tile % tiles_x) * kPT;
+        auto win = [&](int h) {
+            return PWin{max(y0 - h, 0), min(y0 + kPT - 1 + h, H - 1), max(x0 - h, 0),
+                        min(x0 + kPT - 1 + h, W - 1)};
+        };
+        __syncthreads();
+        {  // stage p_0 = t on W_2NP, and s, x on W_NP (all loads in flight)
+            const PWin a = win(2 * NP);
+            const FDiv fa(a.w());
+            for (int e = threadIdx.x; e < a.n(); e += 256) {
+                const int q_ = fa.div(e);
+                const int64_t p = int64_t(a.r0 + q_) * W + (a.c0 + (e - q_ * a.w()));
 #pragma unroll
-        for (int co = 0; co < 3; ++co) {
-            float x = pl[int64_t(co) * np + p];
-            if (P.off_sstab >= 0) {
-#pragma unroll
-                for (int k = 0; k < kLZ; ++k)
-                    if (k < L) x += st[co * kLZ + k] * zv[k];
+                for (int ch = 0; ch < 3; ++ch) cp_async4(&sm.p[0][ch][e], P.syn_t + ch * np + p);
             }
-            x = std_min(1.0f, std_max(0.0f, x));
-            const float tgt = P.image[int64_t(co) * np + p];
-            const double d = double(x) - double(tgt);
-            acc += d * d;
-            if (with_grad) P.syn_dx[int64_t(co) * np + p] = s * (x - tgt);
+            const PWin b = win(NP);
+            const FDiv fb(b.w());
+            for (int e = threadIdx.x; e < b.n(); e += 256) {
+                const int q_ = fb.div(e);
+                const int64_t p = int64_t(b.r0 + q_) * W + (b.c0 + (e - q_ * b.w()));
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) {
+                    cp_async4(&sm.sz[ch][e], P.syn_sz + ch * np + p);
+                    cp_async4(&sm.img[ch][e], P.image + ch * np + p);
+                }
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // forward posts: conv3x3_forward (layers.hpp:257-300) + residual (synthesis.hpp:207)
+#pragma unroll
+        for (int i = 1; i <= NP; ++i) {
+            const PWin a = win(2 * NP - i + 1), b = win(2 * NP - i);
+            const int aw = a.w();
+            for (int e = threadIdx.x; e < b.n(); e += 256) {
+                const int q_ = FDiv(b.w()).div(e);
+                const int r = b.r0 + q_, c = b.c0 + (e - q_ * b.w());
+                const int rm = max(r - 1, 0) - a.r0, r0 = r - a.r0, rp = min(r + 1, H - 1) - a.r0;
+                const int cm = max(c - 1, 0) - a.c0, c0 = c - a.c0, cp = min(c + 1, W - 1) - a.c0;
+                float x[3][9];
+#pragma unroll
+                for (int ci = 0; ci < 3; ++ci) {
+                    const float* xs = sm.p[i - 1][ci];
+                    x[ci][0] = xs[rm * aw + cm]; x[ci][1] = xs[rm * aw + c0]; x[ci][2] = xs[rm * aw + cp];
+                    x[ci][3] = xs[r0 * aw + cm]; x[ci][4] = xs[r0 * aw + c0]; x[ci][5] = xs[r0 * aw + cp];
+                    x[ci][6] = xs[rp * aw + cm]; x[ci][7] = xs[rp * aw + c0]; x[ci][8] = xs[rp * aw + cp];
+                }
+#pragma unroll
+                for (int co = 0; co < 3; ++co) {
+                    float v = bb[i - 1][co];
+#pragma unroll
+                    for (int ci = 0; ci < 3; ++ci) {
+                        const float* k = w[i - 1] + (co * 3 + ci) * 9;
+                        v += k[0] * x[ci][0] + k[1] * x[ci][1] + k[2] * x[ci][2] + k[3] * x[ci][3] +
+                             k[4] * x[ci][4] + k[5] * x[ci][5] + k[6] * x[ci][6] + k[7] * x[ci][7] +
+                             k[8] * x[ci][8];
+                    }
+                    sm.p[i][co][e] = v + x[co][4];
+                }
+            }
+            __syncthreads();
+        }
+        {  // x̂, MSE (owned), dx̂ on W_NP  (synthesis.hpp:210-212, layers.hpp:643-657)
+            const PWin a = win(NP);
+            for (int e = threadIdx.x; e < a.n(); e += 256) {
+                const int q_ = FDiv(a.w()).div(e);
+                const int r = a.r0 + q_, c = a.c0 + (e - q_ * a.w());
+                const int64_t p = int64_t(r) * W + c;
+                const bool own = r >= y0 && r < y0 + kPT && c >= x0 && c < x0 + kPT;
+#pragma unroll
+                for (int co = 0; co < 3; ++co) {
+                    float x = sm.p[NP][co][e] + sm.sz[co][e];
+                    x = std_min(1.0f, std_max(0.0f, x));
+                    const float tgt = sm.img[co][e];
+                    if (own) {
+                        const double dd = double(x) - double(tgt);
+                        mse += dd * dd;
+                    }
+                    const float g = s * (x - tgt);
+                    sm.d[NP][co][e] = g;
+                    if (own && with_grad) P.syn_dx[co * np + p] = g;
+                }
+            }
+        }
+        if (!with_grad) continue;
+        __syncthreads();
+        // backward posts: transposed conv by gather (layers.hpp:302-343)
+#pragma unroll
+        for (int i = NP - 1; i >= 0; --i) {
+            const PWin a = win(i + 1), b = win(i);
+            const int aw = a.w();
+            for (int e = threadIdx.x; e < b.n(); e += 256) {
+                const int q_ = FDiv(b.w()).div(e);
+                const int r = b.r0 + q_, c = b.c0 + (e - q_ * b.w());
+                const int ra = r - a.r0, ca = c - a.c0;
+                float sum[3] = {0.0f, 0.0f, 0.0f};
+                if (r >= 1 && r <= H - 2 && c >= 1 && c <= W - 2) {
+                    // interior: the exact flipped-kernel correlation
+#pragma unroll
+                    for (int co = 0; co < 3; ++co) {
+                        const float* g = sm.d[i + 1][co];
+                        float gv[9];
+#pragma unroll
+                        for (int q = 0; q < 9; ++q)
+                            gv[q] = g[(ra - (q / 3 - 1)) * aw + (ca - (q % 3 - 1))];
+#pragma unroll
+                        for (int ci = 0; ci < 3; ++ci) {
+                            const float* k = w[i] + (co * 3 + ci) * 9;
+#pragma unroll
+                            for (int q = 0; q < 9; ++q) sum[ci] = fmaf(k[q], gv[q], sum[ci]);
+                        }
+                    }
+                } else {
+                    // border: every (r', tap) with clamp(r' + dr) == r
+                    int rr[3], dr[3], cc[3], dc[3];
+                    int nr = 0, nc = 0;
+                    for (int q = r - 1; q <= r + 1; ++q) {
+                        if (q < 0 || q >= H) continue;
+                        for (int d = -1; d <= 1; ++d)
+                            if (clampi(q + d, 0, H - 1) == r && nr < 3) { rr[nr] = q - a.r0; dr[nr] = d; ++nr; }
+                    }
+                    for (int q = c - 1; q <= c + 1; ++q) {
+                        if (q < 0 || q >= W) continue;
+                        for (int d = -1; d <= 1; ++d)
+                            if (clampi(q + d, 0, W - 1) == c && nc < 3) { cc[nc] = q - a.c0; dc[nc] = d; ++nc; }
+                    }
+                    for (int co = 0; co < 3; ++co) {
+                        const float* g = sm.d[i + 1][co];
+                        for (int u = 0; u < nr; ++u)
+                            for (int v = 0; v < nc; ++v) {
+                                const float gv = g[rr[u] * aw + cc[v]];
+                                const int tap = (dr[u] + 1) * 3 + (dc[v] + 1);
+#pragma unroll
+                                for (int ci = 0; ci < 3; ++ci) sum[ci] += w[i][(co * 3 + ci) * 9 + tap] * gv;
+                            }
+                    }
+                }
+#pragma unroll
+                for (int ci = 0; ci < 3; ++ci) {
+                    const float dv = sum[ci] + sm.d[i + 1][ci][ra * aw + ca];  // residual path
+                    sm.d[i][ci][e] = dv;
+                    if (i == 0) P.syn_dt[ci * np + int64_t(r) * W + c] = dv;
+                }
+            }
+            __syncthreads();
+        }
+        if (NP == 0) {  // dt = dx̂
+            const PWin a = win(0);
+            for (int e = threadIdx.x; e < a.n(); e += 256) {
+                const int q_ = FDiv(a.w()).div(e);
+                const int r = a.r0 + q_, c = a.c0 + (e - q_ * a.w());
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) P.syn_dt[ch * np + int64_t(r) * W + c] = sm.d[0][ch][e];
+            }
+        }
+        // post weight gradients over OWNED pixels: thread (column c, slot s)
+        // walks the 16 rows of column c for pairs s and s+16 of the NP*9
+        // (post, co, ci) pairs: 9 tap sums each (+ the bias sum, used when
+        // ci == 0).  A warp reads 16 consecutive columns: no bank conflicts.
+        if constexpr (NP > 0) {
+            const int cc = threadIdx.x % kPT, slot = threadIdx.x / kPT;
+            const int c = x0 + cc;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int pair = slot + 16 * h;
+                if (pair >= NP * 9 || c >= W) continue;
+                const int i = pair / 9, co = (pair % 9) / 3, ci = pair % 3;
+                const PWin a = win(i + 1), x = win(2 * NP - i);
+                const int aw = a.w(), xw = x.w();
+                const float* g = sm.d[i + 1][co];
+                const float* xs = sm.p[i][ci];
+                const int cm = max(c - 1, 0) - x.c0, c0 = c - x.c0, cp = min(c + 1, W - 1) - x.c0;
+                const int rend = min(kPT, H - y0);
+                for (int rr = 0; rr < rend; ++rr) {
+                    const int r = y0 + rr;
+                    const int rm = max(r - 1, 0) - x.r0, r0 = r - x.r0, rp = min(r + 1, H - 1) - x.r0;
+                    const float gv = g[(r - a.r0) * aw + (c - a.c0)];
+                    float* wa = wacc[h];
+                    wa[0] = fmaf(gv, xs[rm * xw + cm], wa[0]);
+                    wa[1] = fmaf(gv, xs[rm * xw + c0], wa[1]);
+                    wa[2] = fmaf(gv, xs[rm * xw + cp], wa[2]);
+                    wa[3] = fmaf(gv, xs[r0 * xw + cm], wa[3]);
+                    wa[4] = fmaf(gv, xs[r0 * xw + c0], wa[4]);
+                    wa[5] = fmaf(gv, xs[r0 * xw + cp], wa[5]);
+                    wa[6] = fmaf(gv, xs[rp * xw + cm], wa[6]);
+                    wa[7] = fmaf(gv, xs[rp * xw + c0], wa[7]);
+                    wa[8] = fmaf(gv, xs[rp * xw + cp], wa[8]);
+                    wa[9] += gv;
+                }
+            }
         }
     }
-    const double tot = block_sum(acc, red);
-    if (threadIdx.x == 0) P.mse_part[blockIdx.x] = tot;
-}
-
-// conv3x3_backward (layers.hpp:302-343) + residual path (synthesis.hpp:222-228)
-__global__ void __launch_bounds__(256) k_syn_post_bwd(const Plan* __restrict__ pp, int i,
-                                                      const float* __restrict__ dcur,
-                                                      float* __restrict__ dprev) {
-    const Plan& P = *pp;
-    __shared__ float w[81];
-    __shared__ double sbuf[84 * 8];
-    __shared__ double tot[84];
-    if (threadIdx.x < 81) w[threadIdx.x] = P.params[P.off_pw[i] + threadIdx.x];
-    __syncthreads();
-    const float* in = post_in(P, i);
-    const int H = P.H, W = P.W;
-    const int64_t np = P.npix;
-    float acc[84];
-#pragma unroll
-    for (int k = 0; k < 84; ++k) acc[k] = 0.0f;
-    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < np;
-         p += int64_t(gridDim.x) * blockDim.x) {
-        const int r = int(p / W), c = int(p - int64_t(r) * W);
-        const int rm = r > 0 ? r - 1 : 0, rp = r < H - 1 ? r + 1 : H - 1;
-        const int cm = c > 0 ? c - 1 : 0, cp = c < W - 1 ? c + 1 : W - 1;
-        // weight gradients (forward-direction loop)
-#pragma unroll
-        for (int co = 0; co < 3; ++co) {
-            const float g = dcur[int64_t(co) * np + p];
-            acc[81 + co] += g;
-#pragma unroll
-            for (int ci = 0; ci < 3; ++ci) {
-                const float* x = in + int64_t(ci) * np;
-                const float* x0 = x + int64_t(rm) * W;
-                const float* x1 = x + int64_t(r) * W;
-                const float* x2 = x + int64_t(rp) * W;
-                float* dk = acc + (co * 3 + ci) * 9;
-                dk[0] += g * x0[cm]; dk[1] += g * x0[c]; dk[2] += g * x0[cp];
-                dk[3] += g * x1[cm]; dk[4] += g * x1[c]; dk[5] += g * x1[cp];
-                dk[6] += g * x2[cm]; dk[7] += g * x2[c]; dk[8] += g * x2[cp];
+    // fixed-order reductions: MSE partial + per-post weight-gradient partial rows
+    const double mtot = block_sum(mse, sm.red);
+    if (threadIdx.x == 0) P.mse_part[blockIdx.x] = mtot;
+    if constexpr (NP > 0) {
+        if (!with_grad) return;
+        __syncthreads();
+        float* scratch = &sm.p[0][0][0];  // [pair][column][10]
+        {
+            const int cc = threadIdx.x % kPT, slot = threadIdx.x / kPT;
+            for (int h = 0; h < 2; ++h) {
+                const int pair = slot + 16 * h;
+                if (pair < NP * 9)
+                    for (int k = 0; k < 10; ++k) scratch[(pair * kPT + cc) * 10 + k] = wacc[h][k];
             }
         }
-        // input gradient by gather over the replicate-clamped neighbourhood
-        int rr[3], dr[3], cc[3], dc[3];
-        int nr = 0, nc = 0;
-        for (int q = r - 1; q <= r + 1; ++q) {
-            if (q < 0 || q >= H) continue;
-            for (int d = -1; d <= 1; ++d)
-                if (clampi(q + d, 0, H - 1) == r && nr < 3) { rr[nr] = q; dr[nr] = d; ++nr; }
-        }
-        for (int q = c - 1; q <= c + 1; ++q) {
-            if (q < 0 || q >= W) continue;
-            for (int d = -1; d <= 1; ++d)
-                if (clampi(q + d, 0, W - 1) == c && nc < 3) { cc[nc] = q; dc[nc] = d; ++nc; }
-        }
-#pragma unroll
-        for (int ci = 0; ci < 3; ++ci) {
-            float s = 0.0f;
-            for (int co = 0; co < 3; ++co) {
-                const float* k = w + (co * 3 + ci) * 9;
-                const float* g = dcur + int64_t(co) * np;
-                for (int a = 0; a < nr; ++a)
-                    for (int b = 0; b < nc; ++b)
-                        s += k[(dr[a] + 1) * 3 + (dc[b] + 1)] * g[int64_t(rr[a]) * W + cc[b]];
+        __syncthreads();
+        for (int i = 0; i < NP; ++i) {
+            const PartialRegion& R = P.region[P.reg_post[i]];
+            double* row = P.partials + R.base + int64_t(blockIdx.x) * R.count;
+            for (int e = threadIdx.x; e < R.count; e += blockDim.x) {
+                const int pidx = R.param_off + e;
+                double v = 0.0;
+                int pair = -1, k = 0;
+                if (pidx >= P.off_pw[i] && pidx < P.off_pw[i] + 81) {
+                    const int q = pidx - P.off_pw[i];  // (co*3 + ci)*9 + tap
+                    pair = i * 9 + q / 9;
+                    k = q % 9;
+                } else if (pidx >= P.off_pb[i] && pidx < P.off_pb[i] + 3) {
+                    pair = i * 9 + (pidx - P.off_pb[i]) * 3;  // (co, ci = 0) carries the bias
+                    k = 9;
+                }
+                if (pair >= 0)
+                    for (int gq = 0; gq < kPT; ++gq) v += double(scratch[(pair * kPT + gq) * 10 + k]);
+                row[e] = v;
             }
-            dprev[int64_t(ci) * np + p] = s + dcur[int64_t(ci) * np + p];  // residual path
         }
-    }
-    double dacc[84];
-#pragma unroll
-    for (int k = 0; k < 84; ++k) dacc[k] = double(acc[k]);
-    block_sum_vec<84>(dacc, sbuf, tot);
-    __syncthreads();
-    const PartialRegion& R = P.region[P.reg_post[i]];
-    double* row = P.partials + R.base + int64_t(blockIdx.x) * R.count;
-    for (int e = threadIdx.x; e < R.count; e += blockDim.x) {
-        const int pidx = R.param_off + e;
-        double v = 0.0;
-        if (pidx >= P.off_pw[i] && pidx < P.off_pw[i] + 81) v = tot[pidx - P.off_pw[i]];
-        else if (pidx >= P.off_pb[i] && pidx < P.off_pb[i] + 3) v = tot[81 + pidx - P.off_pb[i]];
-        row[e] = v;
     }
 }
 
@@ -332,28 +465,52 @@ __global__ void __launch_bounds__(kSynTile) k_syn_trunk_bwd(const Plan* __restri
             a = fmaf(sm.st[2 * kLZ + k], dx[2], a);
             dz[k] = P.off_sstab >= 0 ? a : 0.0f;
         }
-#pragma unroll 4
-        for (int f = 0; f < FP; ++f) {
-            float acc = sm.c1b[f];
+#pragma unroll 2
+        for (int f0 = 0; f0 < FP; f0 += 4) {
+            float hv[4], dv[4];
 #pragma unroll
-            for (int k = 0; k < kLZ; ++k) acc = fmaf(zv[k], sm.c1w[f * kLZ + k], acc);
-            const float h = acc > 0.0f ? acc : 0.0f;
-            float d = 0.0f;
-            d = fmaf(sm.c2w[f], dt[0], d);
-            d = fmaf(sm.c2w[FP + f], dt[1], d);
-            d = fmaf(sm.c2w[2 * FP + f], dt[2], d);
-            d = h > 0.0f ? d : 0.0f;
-#pragma unroll
-            for (int k = 0; k < kLZ; ++k) dz[k] = fmaf(sm.c1w[f * kLZ + k], d, dz[k]);
-            myH[f] = valid ? h : 0.0f;
-            myDH[f] = valid ? d : 0.0f;
+            for (int q = 0; q < 4; ++q) {
+                const int f = f0 + q;
+                const float4 wa = *reinterpret_cast<const float4*>(&sm.c1w[f * kLZ]);
+                const float4 wb = *reinterpret_cast<const float4*>(&sm.c1w[f * kLZ + 4]);
+                float acc = sm.c1b[f];
+                acc = fmaf(zv[0], wa.x, acc);
+                acc = fmaf(zv[1], wa.y, acc);
+                acc = fmaf(zv[2], wa.z, acc);
+                acc = fmaf(zv[3], wa.w, acc);
+                acc = fmaf(zv[4], wb.x, acc);
+                acc = fmaf(zv[5], wb.y, acc);
+                acc = fmaf(zv[6], wb.z, acc);
+                acc = fmaf(zv[7], wb.w, acc);
+                const float h = acc > 0.0f ? acc : 0.0f;
+                float d = 0.0f;
+                d = fmaf(sm.c2w[f], dt[0], d);
+                d = fmaf(sm.c2w[FP + f], dt[1], d);
+                d = fmaf(sm.c2w[2 * FP + f], dt[2], d);
+                d = h > 0.0f ? d : 0.0f;
+                dz[0] = fmaf(wa.x, d, dz[0]);
+                dz[1] = fmaf(wa.y, d, dz[1]);
+                dz[2] = fmaf(wa.z, d, dz[2]);
+                dz[3] = fmaf(wa.w, d, dz[3]);
+                dz[4] = fmaf(wb.x, d, dz[4]);
+                dz[5] = fmaf(wb.y, d, dz[5]);
+                dz[6] = fmaf(wb.z, d, dz[6]);
+                dz[7] = fmaf(wb.w, d, dz[7]);
+                hv[q] = valid ? h : 0.0f;
+                dv[q] = valid ? d : 0.0f;
+            }
+            *reinterpret_cast<float4*>(myH + f0) = make_float4(hv[0], hv[1], hv[2], hv[3]);
+            *reinterpret_cast<float4*>(myDH + f0) = make_float4(dv[0], dv[1], dv[2], dv[3]);
         }
         if (valid) {
 #pragma unroll
             for (int k = 0; k < kLZ; ++k)
                 if (k < L) P.dz[int64_t(k) * np + p] = dz[k];
         }
-        for (int k = 0; k < K::LZ; ++k) myZ[k] = k < kLZ ? zv[k] : ((k == kLZ && valid) ? 1.0f : 0.0f);
+        *reinterpret_cast<float4*>(myZ) = make_float4(zv[0], zv[1], zv[2], zv[3]);
+        *reinterpret_cast<float4*>(myZ + 4) = make_float4(zv[4], zv[5], zv[6], zv[7]);
+        *reinterpret_cast<float4*>(myZ + 8) = make_float4(valid ? 1.0f : 0.0f, 0.f, 0.f, 0.f);
+        for (int k = 12; k < K::LZ; ++k) myZ[k] = 0.0f;
         for (int f = FP; f < K::LH; ++f) myH[f] = (f == FP && valid) ? 1.0f : 0.0f;
         for (int f = FP; f < K::LDH; ++f) myDH[f] = 0.0f;
         *reinterpret_cast<float4*>(myDT) = make_float4(dt[0], dt[1], dt[2], 0.0f);
@@ -466,28 +623,35 @@ void syn_configure(int FP) {
     }
 }
 
+void syn_post_configure() {
+    cudaFuncSetAttribute(k_syn_post<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem<0>)));
+    cudaFuncSetAttribute(k_syn_post<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem<1>)));
+    cudaFuncSetAttribute(k_syn_post<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem<2>)));
+}
+
+int syn_post_tiles(int H, int W) { return ((H + kPT - 1) / kPT) * ((W + kPT - 1) / kPT); }
+
 void launch_syn_forward(const LaunchCtx& L, bool backward) {
     const Plan& H = *L.host;
     k_syn_trunk_fwd<<<L.pix_blocks, 256, 0, L.stream>>>(L.plan);
-    for (int i = 0; i < H.posts; ++i) k_syn_post_fwd<<<L.pix_blocks, 256, 0, L.stream>>>(L.plan, i);
-    k_syn_out<<<H.n_mse_part, 256, 0, L.stream>>>(L.plan, backward ? 1 : 0);
+    const int g = H.n_mse_part;
+    const int wg = backward ? 1 : 0;
+    switch (H.posts) {
+        case 0: k_syn_post<0><<<g, 256, sizeof(PostSmem<0>), L.stream>>>(L.plan, wg); break;
+        case 1: k_syn_post<1><<<g, 256, sizeof(PostSmem<1>), L.stream>>>(L.plan, wg); break;
+        default: k_syn_post<2><<<g, 256, sizeof(PostSmem<2>), L.stream>>>(L.plan, wg); break;
+    }
 }
 
 void launch_syn_backward(const LaunchCtx& L) {
     const Plan& H = *L.host;
-    const float* dcur = H.syn_dx;
-    for (int i = H.posts - 1; i >= 0; --i) {
-        float* dprev = (i == 0) ? H.syn_dt : H.syn_dtmp;
-        if (i > 0 && dcur == H.syn_dtmp) dprev = H.syn_dt;  // ping-pong (posts <= 2)
-        k_syn_post_bwd<<<L.red_blocks, 256, 0, L.stream>>>(L.plan, i, dcur, dprev);
-        dcur = dprev;
-    }
+    const float* dt = H.syn_dt;
     const int FP = syn_padded_hidden(H.syn_F);
     switch (FP) {
-        case 8: launch_trunk_bwd_t<8>(L, dcur); break;
-        case 16: launch_trunk_bwd_t<16>(L, dcur); break;
-        case 48: launch_trunk_bwd_t<48>(L, dcur); break;
-        default: launch_trunk_bwd_t<64>(L, dcur); break;
+        case 8: launch_trunk_bwd_t<8>(L, dt); break;
+        case 16: launch_trunk_bwd_t<16>(L, dt); break;
+        case 48: launch_trunk_bwd_t<48>(L, dt); break;
+        default: launch_trunk_bwd_t<64>(L, dt); break;
     }
 }
 

@@ -3,12 +3,19 @@
 // Replaces upsample_forward / upsample_backward (synthesis.hpp:55-139) built
 // from tconv2x_rows/cols (layers.hpp:353-460) and conv3x3_sym
 // (layers.hpp:467-515).  Main grid k >= 1 is lifted through stages
-// j = k-1 .. 0 (stage parameters ups[j] are shared by every grid passing
-// through it).  All grids that are at stage j run in ONE launch per sub-op
-// (blockIdx.y = grid), so the chain costs 3 launches per stage regardless of
-// the number of grids.  The backward is written as deterministic GATHERS over
-// the replicate-clamped index maps (the reference scatters with +=), and the
-// tap gradients dk4 / dr3 are per-CTA fp64 partials reduced in fixed order.
+// j = k-1 .. 0; stage j's parameters are shared by every grid passing it.
+//
+// B200 design: ONE kernel per stage and direction, all grids at that stage in
+// the same launch (blockIdx.y = grid).  A CTA owns a 2-D tile; the row pass,
+// the column pass and the 3x3 refinement run back to back in shared memory on
+// the tile plus its replicate-clamped halo, so the intermediates (rowtmp,
+// coltmp) never touch HBM — the backward recomputes them from the stage input
+// instead of reading caches.  The backward is a chain of deterministic
+// GATHERS (transposed refine -> transposed column pass -> transposed row
+// pass); each level-j position is "owned" by exactly one CTA (the one owning
+// its parent at level j+1), which is where its contribution to the tap
+// gradients dk4 / dr3 is summed (fp64, fixed-order block reduction, per-CTA
+// partial rows).
 #include <cuda_runtime.h>
 
 #include "cc_kernels.h"
@@ -19,10 +26,13 @@ namespace ccb {
 
 namespace {
 
+constexpr int kFT = 32;   // forward output tile (level j), square
+constexpr int kBT = 16;   // backward input tile (level j+1), square
+constexpr int kThreads = 256;
+
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-// Polyphase tap table of the symmetric x2 transposed conv (layers.hpp:346-351):
-// output t reads inputs idx[0..3] with taps tap[0..3].
+// Polyphase tap table (layers.hpp:346-351): output t reads idx[q] with tap[q].
 __device__ __forceinline__ void tconv_map(int t, int last, int (&idx)[4], int (&tap)[4]) {
     const int u = t >> 1;
     if ((t & 1) == 0) {
@@ -40,6 +50,16 @@ __device__ __forceinline__ void tconv_map(int t, int last, int (&idx)[4], int (&
     }
 }
 
+// A clamped index window [lo, hi] of one axis, stored densely in smem.
+struct Win {
+    int lo, hi;
+    __device__ __forceinline__ int n() const { return hi - lo + 1; }
+};
+// window of the tconv inputs read by outputs in [a, b] (clamped to [0, last])
+__device__ __forceinline__ Win tconv_src(Win out, int last) {
+    return Win{clampi((out.lo >> 1) - 2, 0, last), clampi((out.hi >> 1) + 2, 0, last)};
+}
+
 __device__ __forceinline__ const float* stage_in(const Plan& P, const UpsStage& s) {
     return s.in_is_pad ? P.yhat_pad + s.in_off : P.ups_buf + s.in_off;
 }
@@ -54,74 +74,73 @@ __device__ __forceinline__ float* stage_din(const Plan& P, const UpsStage& s) {
 }
 
 // ---------------------------------------------------------------- forward
-// tconv2x_rows_forward (layers.hpp:353-376): rowtmp[u][t], u < rows_in.
-__global__ void k_ups_rows_fwd(const Plan* __restrict__ pp, int j) {
+// One CTA = one kFT x kFT output tile of stage j for grid blockIdx.y.
+constexpr int kFC = kFT + 2;              // coltmp window (tile + refine halo)
+constexpr int kFR = kFC / 2 + 6;          // rowtmp rows / input rows
+__global__ void __launch_bounds__(kThreads) k_ups_fwd(const Plan* __restrict__ pp, int j) {
     const Plan& P = *pp;
     const UpsStage& s = P.ups[j][blockIdx.y];
+    const int ro = s.rows_out, co = s.cols_out, ri = s.rows_in, ci = s.cols_in;
+    const int tiles_x = (co + kFT - 1) / kFT;
+    const int ntiles = tiles_x * ((ro + kFT - 1) / kFT);
+    __shared__ float s_in[kFR * kFR];
+    __shared__ float s_row[kFR * kFC];
+    __shared__ float s_col[kFC * kFC];
     const float* k4 = P.params + P.off_tconv[j];
-    const float k0 = k4[0], k1 = k4[1], k2 = k4[2], k3 = k4[3];
-    const float* in = stage_in(P, s);
-    float* out = P.ups_buf + s.row_off;
-    const int64_t n = int64_t(s.rows_in) * s.cols_out;
-    const int last = s.cols_in - 1;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int r = int(e / s.cols_out), t = int(e - int64_t(r) * s.cols_out);
-        const float* xi = in + int64_t(r) * s.in_stride;
-        const int u = t >> 1;
-        float y;
-        if ((t & 1) == 0) {
-            const int a = u >= 2 ? u - 2 : 0, b = u >= 1 ? u - 1 : 0, d = u < last ? u + 1 : last;
-            y = k0 * xi[a] + k2 * xi[b] + k3 * xi[u] + k1 * xi[d];
-        } else {
-            const int a = u >= 1 ? u - 1 : 0, b = u < last ? u + 1 : last;
-            const int d = u + 2 < last ? u + 2 : last;
-            y = k1 * xi[a] + k3 * xi[u] + k2 * xi[b] + k0 * xi[d];
-        }
-        out[e] = y;
-    }
-}
-
-// tconv2x_cols_forward (layers.hpp:407-429): coltmp[t][c], t < rows_out.
-__global__ void k_ups_cols_fwd(const Plan* __restrict__ pp, int j) {
-    const Plan& P = *pp;
-    const UpsStage& s = P.ups[j][blockIdx.y];
-    const float* k4 = P.params + P.off_tconv[j];
-    const float* in = P.ups_buf + s.row_off;
-    float* out = P.ups_buf + s.col_off;
-    const int w = s.cols_out;
-    const int64_t n = int64_t(s.rows_out) * w;
-    const int last = s.rows_in - 1;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int t = int(e / w), c = int(e - int64_t(t) * w);
-        int idx[4], tap[4];
-        tconv_map(t, last, idx, tap);
-        out[e] = k4[tap[0]] * in[int64_t(idx[0]) * w + c] + k4[tap[1]] * in[int64_t(idx[1]) * w + c] +
-                 k4[tap[2]] * in[int64_t(idx[2]) * w + c] + k4[tap[3]] * in[int64_t(idx[3]) * w + c];
-    }
-}
-
-// conv3x3_sym_forward (layers.hpp:467-483), replicate padding.
-__global__ void k_ups_refine_fwd(const Plan* __restrict__ pp, int j) {
-    const Plan& P = *pp;
-    const UpsStage& s = P.ups[j][blockIdx.y];
     const float* r3 = P.params + P.off_refine[j];
+    const float t0 = k4[0], t1 = k4[1], t2 = k4[2], t3 = k4[3];
     const float kc = r3[0], ke = r3[1], ko = r3[2];
-    const float* in = P.ups_buf + s.col_off;
+    const float* in = stage_in(P, s);
     float* out = stage_out(P, s);
-    const int h = s.rows_out, w = s.cols_out;
-    const int64_t n = int64_t(h) * w;
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int r = int(e / w), c = int(e - int64_t(r) * w);
-        const int rm = r > 0 ? r - 1 : 0, rp = r < h - 1 ? r + 1 : h - 1;
-        const int cm = c > 0 ? c - 1 : 0, cp = c < w - 1 ? c + 1 : w - 1;
-        const float* x0 = in + int64_t(rm) * w;
-        const float* x1 = in + int64_t(r) * w;
-        const float* x2 = in + int64_t(rp) * w;
-        out[e] = kc * x1[c] + ke * (x0[c] + x2[c] + x1[cm] + x1[cp]) +
-                 ko * (x0[cm] + x0[cp] + x2[cm] + x2[cp]);
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int y0 = (tile / tiles_x) * kFT, x0 = (tile % tiles_x) * kFT;
+        const Win cr{clampi(y0 - 1, 0, ro - 1), clampi(y0 + kFT, 0, ro - 1)};   // coltmp rows
+        const Win cc{clampi(x0 - 1, 0, co - 1), clampi(x0 + kFT, 0, co - 1)};   // coltmp cols
+        const Win rr = tconv_src(cr, ri - 1);                                  // rowtmp/input rows
+        const Win ic = tconv_src(cc, ci - 1);                                  // input cols
+        __syncthreads();
+        for (int e = threadIdx.x; e < rr.n() * ic.n(); e += kThreads) {
+            const int a = FDiv(ic.n()).div(e), b = e - a * ic.n();
+            cp_async4(&s_in[a * kFR + b], in + int64_t(rr.lo + a) * s.in_stride + (ic.lo + b));
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // tconv2x_rows_forward (layers.hpp:353-376)
+        for (int e = threadIdx.x; e < rr.n() * cc.n(); e += kThreads) {
+            const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
+            const int t = cc.lo + b;
+            int idx[4], tap[4];
+            tconv_map(t, ci - 1, idx, tap);
+            const float* x = s_in + a * kFR - ic.lo;
+            const float kk[4] = {t0, t1, t2, t3};
+            s_row[a * kFC + b] = kk[tap[0]] * x[idx[0]] + kk[tap[1]] * x[idx[1]] +
+                                 kk[tap[2]] * x[idx[2]] + kk[tap[3]] * x[idx[3]];
+        }
+        __syncthreads();
+        // tconv2x_cols_forward (layers.hpp:407-429)
+        for (int e = threadIdx.x; e < cr.n() * cc.n(); e += kThreads) {
+            const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
+            const int t = cr.lo + a;
+            int idx[4], tap[4];
+            tconv_map(t, ri - 1, idx, tap);
+            const float kk[4] = {t0, t1, t2, t3};
+            const float* xr = s_row + b - rr.lo * kFC;
+            s_col[a * kFC + b] = kk[tap[0]] * xr[idx[0] * kFC] + kk[tap[1]] * xr[idx[1] * kFC] +
+                                 kk[tap[2]] * xr[idx[2] * kFC] + kk[tap[3]] * xr[idx[3] * kFC];
+        }
+        __syncthreads();
+        // conv3x3_sym_forward (layers.hpp:467-483)
+        for (int e = threadIdx.x; e < kFT * kFT; e += kThreads) {
+            const int r = y0 + e / kFT, c = x0 + (e % kFT);
+            if (r >= ro || c >= co) continue;
+            const int rm = (r > 0 ? r - 1 : 0) - cr.lo, r0 = r - cr.lo, rp = (r < ro - 1 ? r + 1 : ro - 1) - cr.lo;
+            const int cm = (c > 0 ? c - 1 : 0) - cc.lo, c0 = c - cc.lo, cp = (c < co - 1 ? c + 1 : co - 1) - cc.lo;
+            const float* x0r = s_col + rm * kFC;
+            const float* x1r = s_col + r0 * kFC;
+            const float* x2r = s_col + rp * kFC;
+            out[int64_t(r) * co + c] = kc * x1r[c0] + ke * (x0r[c0] + x2r[c0] + x1r[cm] + x1r[cp]) +
+                                       ko * (x0r[cm] + x0r[cp] + x2r[cm] + x2r[cp]);
+        }
     }
 }
 
@@ -137,14 +156,15 @@ __global__ void k_copy_z0(const Plan* __restrict__ pp) {
 }
 
 // --------------------------------------------------------------- backward
-// (r', d) pairs with clamp(r' + d, 0, n-1) == r, d in {-1, 0, 1}, r' in [0, n).
-__device__ __forceinline__ int nbr_pairs(int r, int n, int (&rr)[4], int (&dd)[4]) {
+// (r', d) pairs with clamp(r' + d) == r, r' in [0, n): the transposed
+// replicate-padded 3-tap stencil.
+__device__ __forceinline__ int nbr_pairs(int r, int n, int (&rr)[3], int (&dd)[3]) {
     int k = 0;
-    for (int rp = r - 1; rp <= r + 1; ++rp) {
-        if (rp < 0 || rp >= n) continue;
+    for (int q = r - 1; q <= r + 1; ++q) {
+        if (q < 0 || q >= n) continue;
         for (int d = -1; d <= 1; ++d)
-            if (clampi(rp + d, 0, n - 1) == r && k < 4) {
-                rr[k] = rp;
+            if (clampi(q + d, 0, n - 1) == r && k < 3) {
+                rr[k] = q;
                 dd[k] = d;
                 ++k;
             }
@@ -152,171 +172,246 @@ __device__ __forceinline__ int nbr_pairs(int r, int n, int (&rr)[4], int (&dd)[4
     return k;
 }
 
-// conv3x3_sym_backward (layers.hpp:486-515): dcol by gather, dr3 partials.
-__global__ void k_ups_refine_bwd(const Plan* __restrict__ pp, int j) {
+// windows of the backward tile (input tile [U0,U0+kBT) x [V0,V0+kBT))
+constexpr int kBO = 2 * kBT;              // owned level-j span
+constexpr int kBD = kBO + 10;             // dcol / drow-column window
+constexpr int kBG = kBD + 2;              // dOut window
+constexpr int kBC = kBO + 2;              // coltmp window (owned + refine halo)
+constexpr int kBR = kBC / 2 + 6;          // rowtmp rows / input rows
+constexpr int kBI = kBD / 2 + 8;          // input cols window
+
+struct BwdSmem {
+    float dout[kBG * kBG];
+    float dcol[kBD * kBD];
+    float drow[kBT * kBD];
+    float in[kBR * kBI];
+    float row[kBR * kBC];
+    float col[kBC * kBC];
+    double red[7 * (kThreads / 32)];
+    double tot[7];
+};
+
+__global__ void __launch_bounds__(kThreads) k_ups_bwd(const Plan* __restrict__ pp, int j,
+                                                      int write_lat) {
     const Plan& P = *pp;
     const UpsStage& s = P.ups[j][blockIdx.y];
+    const int ro = s.rows_out, co = s.cols_out, ri = s.rows_in, ci = s.cols_in;
+    const int tiles_x = (ci + kBT - 1) / kBT;
+    const int ntiles = tiles_x * ((ri + kBT - 1) / kBT);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
+    const float* k4 = P.params + P.off_tconv[j];
     const float* r3 = P.params + P.off_refine[j];
+    const float kk[4] = {k4[0], k4[1], k4[2], k4[3]};
     const float kc = r3[0], ke = r3[1], ko = r3[2];
-    const float* x = P.ups_buf + s.col_off;
-    const float* dout = stage_dout(P, s);
-    float* dcol = P.ups_grad + s.col_off;
-    const int h = s.rows_out, w = s.cols_out;
-    const int64_t n = int64_t(h) * w;
-    double acc[3] = {0.0, 0.0, 0.0};
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int r = int(e / w), c = int(e - int64_t(r) * w);
-        // dr3 partials, as written by the forward-direction loop
-        const int rm = r > 0 ? r - 1 : 0, rp = r < h - 1 ? r + 1 : h - 1;
-        const int cm = c > 0 ? c - 1 : 0, cp = c < w - 1 ? c + 1 : w - 1;
-        const float* x0 = x + int64_t(rm) * w;
-        const float* x1 = x + int64_t(r) * w;
-        const float* x2 = x + int64_t(rp) * w;
-        const float g = dout[e];
-        acc[0] += double(g) * double(x1[c]);
-        acc[1] += double(g) * double(x0[c] + x2[c] + x1[cm] + x1[cp]);
-        acc[2] += double(g) * double(x0[cm] + x0[cp] + x2[cm] + x2[cp]);
-        // dcol gather
-        int rr[4], dr[4], cc[4], dc[4];
-        const int nr = nbr_pairs(r, h, rr, dr), nc = nbr_pairs(c, w, cc, dc);
-        float sum = 0.0f;
-        for (int a = 0; a < nr; ++a)
-            for (int b = 0; b < nc; ++b) {
-                const int cls = (dr[a] != 0) + (dc[b] != 0);
-                const float kw = cls == 0 ? kc : (cls == 1 ? ke : ko);
-                sum += kw * dout[int64_t(rr[a]) * w + cc[b]];
-            }
-        dcol[e] = sum;
-    }
-    __shared__ double sbuf[3 * 8];
-    __shared__ double tot[3];
-    block_sum_vec<3>(acc, sbuf, tot);
-    __syncthreads();
-    const PartialRegion& R = P.region[P.reg_ups_ref[j]];
-    const int row = blockIdx.y * gridDim.x + blockIdx.x;
-    if (threadIdx.x < 3) P.partials[R.base + int64_t(row) * R.count + threadIdx.x] = tot[threadIdx.x];
-}
-
-// tconv2x_cols_backward (layers.hpp:432-460): drow by gather over the column
-// (row-index) map, dk4 partials from rowtmp.
-__global__ void k_ups_cols_bwd(const Plan* __restrict__ pp, int j) {
-    const Plan& P = *pp;
-    const UpsStage& s = P.ups[j][blockIdx.y];
-    const float* k4 = P.params + P.off_tconv[j];
-    const float* rowtmp = P.ups_buf + s.row_off;
-    const float* dcol = P.ups_grad + s.col_off;
-    float* drow = P.ups_grad + s.row_off;
-    const int w = s.cols_out, hin = s.rows_in, hout = s.rows_out;
-    const int last = hin - 1;
-    const int64_t nA = int64_t(hin) * w, nB = int64_t(hout) * w;
-    const int64_t n = nA > nB ? nA : nB;
-    const int vmax = (hout - 1) >> 1;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        if (e < nB) {  // dk4 from output row t
-            const int t = int(e / w), c = int(e - int64_t(t) * w);
-            int idx[4], tap[4];
-            tconv_map(t, last, idx, tap);
-            const double g = double(dcol[e]);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[tap[q]] += g * double(rowtmp[int64_t(idx[q]) * w + c]);
-        }
-        if (e < nA) {  // drow[u][c]
-            const int u = int(e / w), c = int(e - int64_t(u) * w);
-            float sum = 0.0f;
-            const int v0 = u - 2 < 0 ? 0 : u - 2, v1 = u + 2 > vmax ? vmax : u + 2;
-            for (int v = v0; v <= v1; ++v)
-                for (int par = 0; par < 2; ++par) {
-                    const int t = 2 * v + par;
-                    if (t >= hout) continue;
-                    int idx[4], tap[4];
-                    tconv_map(t, last, idx, tap);
-                    const float g = dcol[int64_t(t) * w + c];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (idx[q] == u) sum += k4[tap[q]] * g;
-                }
-            drow[e] = sum;
-        }
-    }
-    __shared__ double sbuf[4 * 8];
-    __shared__ double tot[4];
-    block_sum_vec<4>(acc, sbuf, tot);
-    __syncthreads();
-    const PartialRegion& R = P.region[P.reg_ups_cols[j]];
-    const int row = blockIdx.y * gridDim.x + blockIdx.x;
-    if (threadIdx.x < 4) P.partials[R.base + int64_t(row) * R.count + threadIdx.x] = tot[threadIdx.x];
-}
-
-// tconv2x_rows_backward (layers.hpp:378-405): din by gather, dk4 partials from
-// the stage input.
-__global__ void k_ups_rows_bwd(const Plan* __restrict__ pp, int j, int write_din) {
-    const Plan& P = *pp;
-    const UpsStage& s = P.ups[j][blockIdx.y];
-    const float* k4 = P.params + P.off_tconv[j];
     const float* in = stage_in(P, s);
-    const float* drow = P.ups_grad + s.row_off;
+    const float* dout = stage_dout(P, s);
     float* din = stage_din(P, s);
-    const int win = s.cols_in, wout = s.cols_out, h = s.rows_in;
-    const int last = win - 1;
-    const int64_t nA = int64_t(h) * win, nB = int64_t(h) * wout;
-    const int64_t n = nA > nB ? nA : nB;
-    const int vmax = (wout - 1) >> 1;
-    const bool wd = write_din || !s.din_is_lat;
-    double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        if (e < nB) {
-            const int r = int(e / wout), t = int(e - int64_t(r) * wout);
-            int idx[4], tap[4];
-            tconv_map(t, last, idx, tap);
-            const double g = double(drow[e]);
-            const float* xi = in + int64_t(r) * s.in_stride;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[tap[q]] += g * double(xi[idx[q]]);
+    const bool wd = write_lat || !s.din_is_lat;
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // dk4[0..3] (rows+cols passes), dr3[0..2]
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int U0 = (tile / tiles_x) * kBT, V0 = (tile % tiles_x) * kBT;
+        const int U1 = min(U0 + kBT, ri) - 1, V1 = min(V0 + kBT, ci) - 1;  // inclusive
+        // owned level-j positions: parents in the tile
+        const Win own_r{2 * U0, min(2 * U1 + 1, ro - 1)};
+        const Win own_c{2 * V0, min(2 * V1 + 1, co - 1)};
+        // level-j rows/cols whose transposed-tconv reaches the tile: t with
+        // any idx(t, q) in [U0, U1]  ->  t in [2U0 - 4, 2U1 + 5]
+        const Win dr{clampi(2 * U0 - 4, 0, ro - 1), clampi(2 * U1 + 5, 0, ro - 1)};
+        const Win dc{clampi(2 * V0 - 4, 0, co - 1), clampi(2 * V1 + 5, 0, co - 1)};
+        const Win gr{clampi(dr.lo - 1, 0, ro - 1), clampi(dr.hi + 1, 0, ro - 1)};
+        const Win gc{clampi(dc.lo - 1, 0, co - 1), clampi(dc.hi + 1, 0, co - 1)};
+        // recomputed forward intermediates over the owned region + refine halo
+        const Win cr{clampi(own_r.lo - 1, 0, ro - 1), clampi(own_r.hi + 1, 0, ro - 1)};
+        const Win cc{clampi(own_c.lo - 1, 0, co - 1), clampi(own_c.hi + 1, 0, co - 1)};
+        const Win rr = tconv_src(cr, ri - 1);  // rowtmp rows (also covers rows U0..U1)
+        const Win rw{min(rr.lo, U0), max(rr.hi, U1)};
+        // input columns: for rowtmp over cc, and for the row-pass dk4 over own_c
+        const Win ic = tconv_src(Win{min(cc.lo, own_c.lo), max(cc.hi, own_c.hi)}, ci - 1);
+        __syncthreads();
+        for (int e = threadIdx.x; e < gr.n() * gc.n(); e += kThreads) {
+            const int a = FDiv(gc.n()).div(e), b = e - a * gc.n();
+            cp_async4(&sm.dout[a * kBG + b], dout + int64_t(gr.lo + a) * co + (gc.lo + b));
         }
-        if (wd && e < nA) {
-            const int r = int(e / win), u = int(e - int64_t(r) * win);
-            const float* go = drow + int64_t(r) * wout;
+        for (int e = threadIdx.x; e < rw.n() * ic.n(); e += kThreads) {
+            const int a = FDiv(ic.n()).div(e), b = e - a * ic.n();
+            cp_async4(&sm.in[a * kBI + b], in + int64_t(rw.lo + a) * s.in_stride + (ic.lo + b));
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        // rowtmp over rows rw, cols cc (recompute of tconv2x_rows_forward)
+        for (int e = threadIdx.x; e < rw.n() * cc.n(); e += kThreads) {
+            const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
+            int idx[4], tap[4];
+            tconv_map(cc.lo + b, ci - 1, idx, tap);
+            const float* x = sm.in + a * kBI - ic.lo;
+            sm.row[a * kBC + b] = kk[tap[0]] * x[idx[0]] + kk[tap[1]] * x[idx[1]] +
+                                  kk[tap[2]] * x[idx[2]] + kk[tap[3]] * x[idx[3]];
+        }
+        // dcol over (dr, dc): transposed refine (conv3x3_sym_backward, layers.hpp:486-515)
+        for (int e = threadIdx.x; e < dr.n() * dc.n(); e += kThreads) {
+            const int a = FDiv(dc.n()).div(e), b = e - a * dc.n();
+            const int r = dr.lo + a, c = dc.lo + b;
+            if (r >= 1 && r <= ro - 2 && c >= 1 && c <= co - 2) {
+                // interior: the symmetric stencil is its own transpose
+                const float* g = sm.dout + (r - gr.lo) * kBG + (c - gc.lo);
+                sm.dcol[a * kBD + b] = kc * g[0] + ke * (g[-kBG] + g[kBG] + g[-1] + g[1]) +
+                                       ko * (g[-kBG - 1] + g[-kBG + 1] + g[kBG - 1] + g[kBG + 1]);
+                continue;
+            }
+            int rp[3], rd[3], cp[3], cd[3];
+            const int nr = nbr_pairs(r, ro, rp, rd), nc = nbr_pairs(c, co, cp, cd);
             float sum = 0.0f;
-            const int v0 = u - 2 < 0 ? 0 : u - 2, v1 = u + 2 > vmax ? vmax : u + 2;
+            for (int x = 0; x < nr; ++x)
+                for (int y = 0; y < nc; ++y) {
+                    const int cls = (rd[x] != 0) + (cd[y] != 0);
+                    const float w = cls == 0 ? kc : (cls == 1 ? ke : ko);
+                    sum += w * sm.dout[(rp[x] - gr.lo) * kBG + (cp[y] - gc.lo)];
+                }
+            sm.dcol[a * kBD + b] = sum;
+        }
+        __syncthreads();
+        // coltmp over (cr, cc) (recompute of tconv2x_cols_forward)
+        for (int e = threadIdx.x; e < cr.n() * cc.n(); e += kThreads) {
+            const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
+            int idx[4], tap[4];
+            tconv_map(cr.lo + a, ri - 1, idx, tap);
+            const float* xr = sm.row + b - rw.lo * kBC;
+            sm.col[a * kBC + b] = kk[tap[0]] * xr[idx[0] * kBC] + kk[tap[1]] * xr[idx[1] * kBC] +
+                                  kk[tap[2]] * xr[idx[2] * kBC] + kk[tap[3]] * xr[idx[3] * kBC];
+        }
+        // drow[u][t'] for u in tile rows, t' in dc: transposed column pass
+        const int vmax_r = (ro - 1) >> 1;
+        const int ufast_hi = min(ri - 2, (ro - 5) / 2);
+        for (int e = threadIdx.x; e < (U1 - U0 + 1) * dc.n(); e += kThreads) {
+            const int a = FDiv(dc.n()).div(e), b = e - a * dc.n();
+            const int u = U0 + a;
+            if (u >= 2 && u <= ufast_hi) {
+                // interior: outputs 2u-3 .. 2u+4 reach u with fixed taps
+                const float* g = sm.dcol + (2 * u - dr.lo) * kBD + b;
+                sm.drow[a * kBD + b] = kk[0] * (g[4 * kBD] + g[-3 * kBD]) + kk[1] * (g[-2 * kBD] + g[3 * kBD]) +
+                                       kk[2] * (g[2 * kBD] + g[-kBD]) + kk[3] * (g[0] + g[kBD]);
+                continue;
+            }
+            float sum = 0.0f;
+            const int v0 = max(u - 2, 0), v1 = min(u + 2, vmax_r);
             for (int v = v0; v <= v1; ++v)
                 for (int par = 0; par < 2; ++par) {
                     const int t = 2 * v + par;
-                    if (t >= wout) continue;
+                    if (t >= ro) continue;
                     int idx[4], tap[4];
-                    tconv_map(t, last, idx, tap);
-                    const float g = go[t];
+                    tconv_map(t, ri - 1, idx, tap);
+                    const float g = sm.dcol[(t - dr.lo) * kBD + b];
 #pragma unroll
                     for (int q = 0; q < 4; ++q)
-                        if (idx[q] == u) sum += k4[tap[q]] * g;
+                        if (idx[q] == u) sum += kk[tap[q]] * g;
                 }
-            // main-grid targets are flat unpadded (dups); intermediate ones too
-            din[e] = sum;
+            sm.drow[a * kBD + b] = sum;
+        }
+        __syncthreads();
+        // din[u][v]: transposed row pass (tconv2x_rows_backward, layers.hpp:378-405)
+        if (wd) {
+            const int vmax_c = (co - 1) >> 1;
+            const int vfast_hi = min(ci - 2, (co - 5) / 2);
+            for (int e = threadIdx.x; e < (U1 - U0 + 1) * (V1 - V0 + 1); e += kThreads) {
+                const int a = FDiv(V1 - V0 + 1).div(e), b = e - a * (V1 - V0 + 1);
+                const int u = V0 + b;
+                if (u >= 2 && u <= vfast_hi) {
+                    const float* g = sm.drow + a * kBD + (2 * u - dc.lo);
+                    din[int64_t(U0 + a) * ci + u] = kk[0] * (g[4] + g[-3]) + kk[1] * (g[-2] + g[3]) +
+                                                    kk[2] * (g[2] + g[-1]) + kk[3] * (g[0] + g[1]);
+                    continue;
+                }
+                float sum = 0.0f;
+                const int w0 = max(u - 2, 0), w1 = min(u + 2, vmax_c);
+                for (int w = w0; w <= w1; ++w)
+                    for (int par = 0; par < 2; ++par) {
+                        const int t = 2 * w + par;
+                        if (t >= co) continue;
+                        int idx[4], tap[4];
+                        tconv_map(t, ci - 1, idx, tap);
+                        const float g = sm.drow[a * kBD + (t - dc.lo)];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (idx[q] == u) sum += kk[tap[q]] * g;
+                    }
+                din[int64_t(U0 + a) * ci + u] = sum;
+            }
+        }
+        // tap gradients over owned positions
+        for (int e = threadIdx.x; e < own_r.n() * own_c.n(); e += kThreads) {
+            const int a = FDiv(own_c.n()).div(e), b = e - a * own_c.n();
+            const int r = own_r.lo + a, c = own_c.lo + b;
+            // refine: dOut x coltmp neighbourhood (layers.hpp:504-506)
+            const float g = sm.dout[(r - gr.lo) * kBG + (c - gc.lo)];
+            const int rm = (r > 0 ? r - 1 : 0) - cr.lo, r0 = r - cr.lo, rp = (r < ro - 1 ? r + 1 : ro - 1) - cr.lo;
+            const int cm = (c > 0 ? c - 1 : 0) - cc.lo, c0 = c - cc.lo, cp = (c < co - 1 ? c + 1 : co - 1) - cc.lo;
+            const float* x0 = sm.col + rm * kBC;
+            const float* x1 = sm.col + r0 * kBC;
+            const float* x2 = sm.col + rp * kBC;
+            acc[4] += double(g) * double(x1[c0]);
+            acc[5] += double(g) * double(x0[c0] + x2[c0] + x1[cm] + x1[cp]);
+            acc[6] += double(g) * double(x0[cm] + x0[cp] + x2[cm] + x2[cp]);
+            // column pass: dcol x rowtmp (layers.hpp:452-457)
+            int idx[4], tap[4];
+            tconv_map(r, ri - 1, idx, tap);
+            const double gc2 = double(sm.dcol[(r - dr.lo) * kBD + (c - dc.lo)]);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                acc[tap[q]] += gc2 * double(sm.row[(idx[q] - rw.lo) * kBC + (c - cc.lo)]);
+        }
+        // row pass: drow x input over (u in tile, t' owned) (layers.hpp:395,401)
+        for (int e = threadIdx.x; e < (U1 - U0 + 1) * own_c.n(); e += kThreads) {
+            const int a = FDiv(own_c.n()).div(e), b = e - a * own_c.n();
+            const int t = own_c.lo + b;
+            int idx[4], tap[4];
+            tconv_map(t, ci - 1, idx, tap);
+            const double g = double(sm.drow[a * kBD + (t - dc.lo)]);
+            const float* x = sm.in + (U0 + a - rw.lo) * kBI - ic.lo;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[tap[q]] += g * double(x[idx[q]]);
         }
     }
-    __shared__ double sbuf[4 * 8];
-    __shared__ double tot[4];
-    block_sum_vec<4>(acc, sbuf, tot);
+    block_sum_vec<7>(acc, sm.red, sm.tot);
     __syncthreads();
-    const PartialRegion& R = P.region[P.reg_ups_rows[j]];
     const int row = blockIdx.y * gridDim.x + blockIdx.x;
-    if (threadIdx.x < 4) P.partials[R.base + int64_t(row) * R.count + threadIdx.x] = tot[threadIdx.x];
+    if (threadIdx.x < 4) {
+        const PartialRegion& R = P.region[P.reg_ups_rows[j]];
+        P.partials[R.base + int64_t(row) * R.count + threadIdx.x] = sm.tot[threadIdx.x];
+    } else if (threadIdx.x < 7) {
+        const PartialRegion& R = P.region[P.reg_ups_ref[j]];
+        P.partials[R.base + int64_t(row) * R.count + (threadIdx.x - 4)] = sm.tot[threadIdx.x];
+    }
 }
 
 }  // namespace
+
+int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward) {
+    // enough CTAs to cover the largest grid of the stage, capped at ~2 waves
+    int best = 1;
+    for (int i = 0; i < H.ups_n[j]; ++i) {
+        const UpsStage& s = H.ups[j][i];
+        const int t = forward ? ((s.rows_out + kFT - 1) / kFT) * ((s.cols_out + kFT - 1) / kFT)
+                              : ((s.rows_in + kBT - 1) / kBT) * ((s.cols_in + kBT - 1) / kBT);
+        best = t > best ? t : best;
+    }
+    const int cap = (2 * num_sms * 8 + H.ups_n[j] - 1) / (H.ups_n[j] > 0 ? H.ups_n[j] : 1);
+    return best < cap ? best : cap;
+}
+
+size_t ups_bwd_smem() { return sizeof(BwdSmem); }
+
+void ups_configure() {
+    cudaFuncSetAttribute(k_ups_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
+}
 
 void launch_ups_forward(const LaunchCtx& L) {
     const Plan& H = *L.host;
     k_copy_z0<<<L.pix_blocks, 256, 0, L.stream>>>(L.plan);
     for (int j = H.L - 2; j >= 0; --j) {
         if (H.ups_n[j] == 0) continue;
-        const dim3 grid(L.red_blocks, H.ups_n[j]);
-        k_ups_rows_fwd<<<grid, 256, 0, L.stream>>>(L.plan, j);
-        k_ups_cols_fwd<<<grid, 256, 0, L.stream>>>(L.plan, j);
-        k_ups_refine_fwd<<<grid, 256, 0, L.stream>>>(L.plan, j);
+        const dim3 grid(ups_blocks_x(H, j, L.num_sms, true), H.ups_n[j]);
+        k_ups_fwd<<<grid, kThreads, 0, L.stream>>>(L.plan, j);
     }
 }
 
@@ -324,10 +419,8 @@ void launch_ups_backward(const LaunchCtx& L, bool latent_grads) {
     const Plan& H = *L.host;
     for (int j = 0; j <= H.L - 2; ++j) {
         if (H.ups_n[j] == 0) continue;
-        const dim3 grid(L.red_blocks, H.ups_n[j]);
-        k_ups_refine_bwd<<<grid, 256, 0, L.stream>>>(L.plan, j);
-        k_ups_cols_bwd<<<grid, 256, 0, L.stream>>>(L.plan, j);
-        k_ups_rows_bwd<<<grid, 256, 0, L.stream>>>(L.plan, j, latent_grads ? 1 : 0);
+        const dim3 grid(ups_blocks_x(H, j, L.num_sms, false), H.ups_n[j]);
+        k_ups_bwd<<<grid, kThreads, sizeof(BwdSmem), L.stream>>>(L.plan, j, latent_grads ? 1 : 0);
     }
 }
 
