@@ -78,7 +78,7 @@ def build_oracle(verbose: bool = False) -> None:
         raise RuntimeError("make not found")
     targets = ["port"]
     if Path("/root/reference/proj/include/coolcodec/encoder.hpp").exists():
-        targets.append("ref")
+        targets += ["ref", "dropin"]
     subprocess.run([make, "-s", "-C", str(odir), *targets], check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
 

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 
@@ -78,6 +79,9 @@ Trainer::Trainer(const float* image, int h, int w, const cc_encoder_config& enc,
                         " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
     num_sms_ = prop.multiProcessorCount;
     CCB_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+    CCB_CUDA(cudaStreamCreateWithFlags(&side_stream_, cudaStreamNonBlocking));
+    CCB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+    CCB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     stream_ = own_stream_;
     build_plan();
     allocate();
@@ -100,6 +104,10 @@ Trainer::~Trainer() {
     if (h_scal_) cudaFreeHost(h_scal_);
     if (d_sched_) cudaFree(d_sched_);
     if (d_rec_) cudaFree(d_rec_);
+    if (side_stream_) cudaStreamSynchronize(side_stream_);
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (side_stream_) cudaStreamDestroy(side_stream_);
     if (own_stream_) cudaStreamDestroy(own_stream_);
 }
 
@@ -312,7 +320,9 @@ void Trainer::build_plan() {
         for (int64_t s = 0; s < cnt; s += kArmTileHost) tiles.push_back(make_int2(gi, int(s)));
     }
     L_.arm_ntiles = int(tiles.size());
-    L_.arm_blocks = std::min(L_.arm_ntiles, num_sms_ * arm_blocks_per_sm(P.Dp, P.Wp));
+    int arm_occ = arm_blocks_per_sm(P.Dp, P.Wp);
+    if (const char* e = std::getenv("CCB_ARM_OCC")) arm_occ = std::max(1, std::min(arm_occ, std::atoi(e)));
+    L_.arm_blocks = std::min(L_.arm_ntiles, num_sms_ * arm_occ);
     const int FP = syn_padded_hidden(P.syn_F);
     const int64_t syn_tiles = (P.npix + 127) / 128;
     int syn_per_sm = int((227 * 1024) / (syn_trunk_smem(FP) + 1024));
@@ -492,15 +502,35 @@ void Trainer::reset_optimizers() {
 
 // ---------------------------------------------------------------- sequences
 // Trainer::proxy_iteration (encoder.hpp:97-135)
+// The rate branch (ARM + IFCE, dF pyramid) and the distortion branch
+// (upsampling, synthesis, their backward) only share ŷ as input, so they run
+// as two concurrent branches of the graph and join before the gradient
+// assembly.
+void Trainer::fork() {
+    CCB_CUDA(cudaEventRecord(ev_fork_, stream_));
+    CCB_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
+}
+void Trainer::join() {
+    CCB_CUDA(cudaEventRecord(ev_join_, side_stream_));
+    CCB_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+}
+LaunchCtx Trainer::side() const {
+    LaunchCtx s = L_;
+    s.stream = side_stream_;
+    return s;
+}
+
 void Trainer::enqueue_proxy(bool batched) {
     if (batched) launch_sched_load(L_, d_sched_);
     launch_softq_fwd(L_);
-    launch_arm(L_, kArmProxy);
-    launch_pyramid(L_);
+    fork();
+    launch_arm(side(), kArmProxy);
+    launch_pyramid(side());
     launch_ups_forward(L_);
     launch_syn_forward(L_, true);
     launch_syn_backward(L_);
     launch_ups_backward(L_, true);
+    join();
     launch_finalize(L_, kArmProxy, -1);
     launch_latent_grad(L_);
     launch_adam_latents(L_);
@@ -509,11 +539,13 @@ void Trainer::enqueue_proxy(bool batched) {
 
 // Trainer::hardround_iteration (encoder.hpp:141-155)
 void Trainer::enqueue_hardround(int slot) {
-    launch_arm(L_, kArmHard);
+    fork();
+    launch_arm(side(), kArmHard);
     launch_ups_forward(L_);
     launch_syn_forward(L_, true);
     launch_syn_backward(L_);
     launch_ups_backward(L_, false);
+    join();
     launch_finalize(L_, kArmHard, slot);
     CCB_CUDA(cudaMemsetAsync(H_.lat_g, 0, sizeof(float) * size_t(H_.n_latents), stream_));
     if (slot >= 0) launch_snapshot_if_better(L_, slot, snaps_.at(slot).y, snaps_.at(slot).p);
@@ -524,9 +556,11 @@ void Trainer::enqueue_hardround(int slot) {
 void Trainer::enqueue_true_cost() {
     launch_quantize(L_, 255);
     launch_pads_from_q(L_);
-    launch_arm(L_, kArmForward);
+    fork();
+    launch_arm(side(), kArmForward);
     launch_ups_forward(L_);
     launch_syn_forward(L_, false);
+    join();
     launch_finalize(L_, kArmForward, -1);
 }
 

@@ -119,6 +119,9 @@ private:
     void require_loaded() const;
     void init_params_host(uint64_t stream, std::vector<float>& out) const;
     void enqueue_proxy(bool batched);
+    void fork();
+    void join();
+    LaunchCtx side() const;
     void enqueue_hardround(int slot);
     void enqueue_true_cost();
     void run_graph(int which, int slot = -1);
@@ -134,6 +137,8 @@ private:
     int num_sms_ = 148;
     cudaStream_t stream_ = nullptr;
     cudaStream_t own_stream_ = nullptr;
+    cudaStream_t side_stream_ = nullptr;  // concurrent rate branch
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     Plan H_{};
     Plan* d_plan_ = nullptr;
     LaunchCtx L_{};

@@ -28,7 +28,8 @@ namespace {
 
 constexpr int kFT = 32;   // forward output tile (level j), square
 constexpr int kBT = 16;   // backward input tile (level j+1), square
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;     // big stages
+constexpr int kThreadsWide = 512; // stages with few tiles: shorter per-CTA phase chains
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
@@ -77,7 +78,7 @@ __device__ __forceinline__ float* stage_din(const Plan& P, const UpsStage& s) {
 // One CTA = one kFT x kFT output tile of stage j for grid blockIdx.y.
 constexpr int kFC = kFT + 2;              // coltmp window (tile + refine halo)
 constexpr int kFR = kFC / 2 + 6;          // rowtmp rows / input rows
-__global__ void __launch_bounds__(kThreads) k_ups_fwd(const Plan* __restrict__ pp, int j) {
+__global__ void __launch_bounds__(kThreadsWide) k_ups_fwd(const Plan* __restrict__ pp, int j) {
     const Plan& P = *pp;
     const UpsStage& s = P.ups[j][blockIdx.y];
     const int ro = s.rows_out, co = s.cols_out, ri = s.rows_in, ci = s.cols_in;
@@ -99,14 +100,14 @@ __global__ void __launch_bounds__(kThreads) k_ups_fwd(const Plan* __restrict__ p
         const Win rr = tconv_src(cr, ri - 1);                                  // rowtmp/input rows
         const Win ic = tconv_src(cc, ci - 1);                                  // input cols
         __syncthreads();
-        for (int e = threadIdx.x; e < rr.n() * ic.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < rr.n() * ic.n(); e += blockDim.x) {
             const int a = FDiv(ic.n()).div(e), b = e - a * ic.n();
             cp_async4(&s_in[a * kFR + b], in + int64_t(rr.lo + a) * s.in_stride + (ic.lo + b));
         }
         cp_async_wait_all();
         __syncthreads();
         // tconv2x_rows_forward (layers.hpp:353-376)
-        for (int e = threadIdx.x; e < rr.n() * cc.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < rr.n() * cc.n(); e += blockDim.x) {
             const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
             const int t = cc.lo + b;
             int idx[4], tap[4];
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_ups_fwd(const Plan* __restrict__ p
         }
         __syncthreads();
         // tconv2x_cols_forward (layers.hpp:407-429)
-        for (int e = threadIdx.x; e < cr.n() * cc.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < cr.n() * cc.n(); e += blockDim.x) {
             const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
             const int t = cr.lo + a;
             int idx[4], tap[4];
@@ -130,7 +131,7 @@ __global__ void __launch_bounds__(kThreads) k_ups_fwd(const Plan* __restrict__ p
         }
         __syncthreads();
         // conv3x3_sym_forward (layers.hpp:467-483)
-        for (int e = threadIdx.x; e < kFT * kFT; e += kThreads) {
+        for (int e = threadIdx.x; e < kFT * kFT; e += blockDim.x) {
             const int r = y0 + e / kFT, c = x0 + (e % kFT);
             if (r >= ro || c >= co) continue;
             const int rm = (r > 0 ? r - 1 : 0) - cr.lo, r0 = r - cr.lo, rp = (r < ro - 1 ? r + 1 : ro - 1) - cr.lo;
@@ -187,11 +188,11 @@ struct BwdSmem {
     float in[kBR * kBI];
     float row[kBR * kBC];
     float col[kBC * kBC];
-    double red[7 * (kThreads / 32)];
+    double red[7 * (kThreadsWide / 32)];
     double tot[7];
 };
 
-__global__ void __launch_bounds__(kThreads) k_ups_bwd(const Plan* __restrict__ pp, int j,
+__global__ void __launch_bounds__(kThreadsWide) k_ups_bwd(const Plan* __restrict__ pp, int j,
                                                       int write_lat) {
     const Plan& P = *pp;
     const UpsStage& s = P.ups[j][blockIdx.y];
@@ -229,18 +230,18 @@ __global__ void __launch_bounds__(kThreads) k_ups_bwd(const Plan* __restrict__ p
         // input columns: for rowtmp over cc, and for the row-pass dk4 over own_c
         const Win ic = tconv_src(Win{min(cc.lo, own_c.lo), max(cc.hi, own_c.hi)}, ci - 1);
         __syncthreads();
-        for (int e = threadIdx.x; e < gr.n() * gc.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < gr.n() * gc.n(); e += blockDim.x) {
             const int a = FDiv(gc.n()).div(e), b = e - a * gc.n();
             cp_async4(&sm.dout[a * kBG + b], dout + int64_t(gr.lo + a) * co + (gc.lo + b));
         }
-        for (int e = threadIdx.x; e < rw.n() * ic.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < rw.n() * ic.n(); e += blockDim.x) {
             const int a = FDiv(ic.n()).div(e), b = e - a * ic.n();
             cp_async4(&sm.in[a * kBI + b], in + int64_t(rw.lo + a) * s.in_stride + (ic.lo + b));
         }
         cp_async_wait_all();
         __syncthreads();
         // rowtmp over rows rw, cols cc (recompute of tconv2x_rows_forward)
-        for (int e = threadIdx.x; e < rw.n() * cc.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < rw.n() * cc.n(); e += blockDim.x) {
             const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
             int idx[4], tap[4];
             tconv_map(cc.lo + b, ci - 1, idx, tap);
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(kThreads) k_ups_bwd(const Plan* __restrict__ p
                                   kk[tap[2]] * x[idx[2]] + kk[tap[3]] * x[idx[3]];
         }
         // dcol over (dr, dc): transposed refine (conv3x3_sym_backward, layers.hpp:486-515)
-        for (int e = threadIdx.x; e < dr.n() * dc.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < dr.n() * dc.n(); e += blockDim.x) {
             const int a = FDiv(dc.n()).div(e), b = e - a * dc.n();
             const int r = dr.lo + a, c = dc.lo + b;
             if (r >= 1 && r <= ro - 2 && c >= 1 && c <= co - 2) {
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kThreads) k_ups_bwd(const Plan* __restrict__ p
         }
         __syncthreads();
         // coltmp over (cr, cc) (recompute of tconv2x_cols_forward)
-        for (int e = threadIdx.x; e < cr.n() * cc.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < cr.n() * cc.n(); e += blockDim.x) {
             const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
             int idx[4], tap[4];
             tconv_map(cr.lo + a, ri - 1, idx, tap);
@@ -283,7 +284,7 @@ __global__ void __launch_bounds__(kThreads) k_ups_bwd(const Plan* __restrict__ p
         // drow[u][t'] for u in tile rows, t' in dc: transposed column pass
         const int vmax_r = (ro - 1) >> 1;
         const int ufast_hi = min(ri - 2, (ro - 5) / 2);
-        for (int e = threadIdx.x; e < (U1 - U0 + 1) * dc.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < (U1 - U0 + 1) * dc.n(); e += blockDim.x) {
             const int a = FDiv(dc.n()).div(e), b = e - a * dc.n();
             const int u = U0 + a;
             if (u >= 2 && u <= ufast_hi) {
@@ -313,7 +314,7 @@ __global__ void __launch_bounds__(kThreads) k_ups_bwd(const Plan* __restrict__ p
         if (wd) {
             const int vmax_c = (co - 1) >> 1;
             const int vfast_hi = min(ci - 2, (co - 5) / 2);
-            for (int e = threadIdx.x; e < (U1 - U0 + 1) * (V1 - V0 + 1); e += kThreads) {
+            for (int e = threadIdx.x; e < (U1 - U0 + 1) * (V1 - V0 + 1); e += blockDim.x) {
                 const int a = FDiv(V1 - V0 + 1).div(e), b = e - a * (V1 - V0 + 1);
                 const int u = V0 + b;
                 if (u >= 2 && u <= vfast_hi) {
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(kThreads) k_ups_bwd(const Plan* __restrict__ p
             }
         }
         // tap gradients over owned positions
-        for (int e = threadIdx.x; e < own_r.n() * own_c.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < own_r.n() * own_c.n(); e += blockDim.x) {
             const int a = FDiv(own_c.n()).div(e), b = e - a * own_c.n();
             const int r = own_r.lo + a, c = own_c.lo + b;
             // refine: dOut x coltmp neighbourhood (layers.hpp:504-506)
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kThreads) k_ups_bwd(const Plan* __restrict__ p
                 acc[tap[q]] += gc2 * double(sm.row[(idx[q] - rw.lo) * kBC + (c - cc.lo)]);
         }
         // row pass: drow x input over (u in tile, t' owned) (layers.hpp:395,401)
-        for (int e = threadIdx.x; e < (U1 - U0 + 1) * own_c.n(); e += kThreads) {
+        for (int e = threadIdx.x; e < (U1 - U0 + 1) * own_c.n(); e += blockDim.x) {
             const int a = FDiv(own_c.n()).div(e), b = e - a * own_c.n();
             const int t = own_c.lo + b;
             int idx[4], tap[4];
@@ -411,7 +412,8 @@ void launch_ups_forward(const LaunchCtx& L) {
     for (int j = H.L - 2; j >= 0; --j) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, true), H.ups_n[j]);
-        k_ups_fwd<<<grid, kThreads, 0, L.stream>>>(L.plan, j);
+        const int nt = int(grid.x * grid.y) < 2 * L.num_sms ? kThreadsWide : kThreads;
+        k_ups_fwd<<<grid, nt, 0, L.stream>>>(L.plan, j);
     }
 }
 
@@ -420,7 +422,8 @@ void launch_ups_backward(const LaunchCtx& L, bool latent_grads) {
     for (int j = 0; j <= H.L - 2; ++j) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, false), H.ups_n[j]);
-        k_ups_bwd<<<grid, kThreads, sizeof(BwdSmem), L.stream>>>(L.plan, j, latent_grads ? 1 : 0);
+        const int nt = int(grid.x * grid.y) < 2 * L.num_sms ? kThreadsWide : kThreads;
+        k_ups_bwd<<<grid, nt, sizeof(BwdSmem), L.stream>>>(L.plan, j, latent_grads ? 1 : 0);
     }
 }
 

@@ -1,0 +1,26 @@
+"""The C++ drop-in (include/coolchic_b200.hpp) used the way a coolcodec
+encoder would use it: coolcodec::gpu::train vs coolcodec::train on the same
+image.  The test binary is compiled against the reference headers
+(`make -C oracle dropin`, where /root/reference exists) and travels with the
+repo."""
+from __future__ import annotations
+
+import json
+import subprocess
+
+import pytest
+
+from tests.oracle_util import REF_DIR
+
+pytestmark = pytest.mark.gpu
+
+
+def test_cpp_dropin_train_matches_reference(gpu_lib):
+    exe = REF_DIR / "dropin_train"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/dropin_train not built (needs /root/reference once)")
+    out = subprocess.run([str(exe), "40", "48", "600"], capture_output=True, text=True,
+                         timeout=600, check=True).stdout
+    r = json.loads(out.strip().splitlines()[-1])
+    assert r["gpu_iters"] == r["ref_iters"] == 600
+    assert abs(r["gpu_cost"] - r["ref_cost"]) / r["ref_cost"] <= 5e-3
