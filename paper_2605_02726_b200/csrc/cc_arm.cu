@@ -26,13 +26,15 @@
 // multiply-then-scatter (entropy_model.hpp:322-330).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "cc_kernels.h"
 #include "cc_math.cuh"
 #include "cc_reduce.cuh"
 
 namespace ccb {
 
-constexpr int kArmTile = 128;  // latents per tile == threads per CTA
+// kArmTile (latents per tile == threads per CTA) lives in cc_plan.h
 constexpr int kRMax = 12;      // max IFCE source grids (hyper 4 + main 7)
 constexpr int kFMax = 8;       // max IFCE width
 
@@ -589,7 +591,23 @@ static void configure_t() {
 }
 
 // Opt in to > 48 KB dynamic shared memory on the CURRENT device.
+// The register-tiled kernel (cc_arm2.cu) is the default for every variant it
+// instantiates; CCB_ARM_V1=1 selects this per-latent kernel (A/B comparison).
+bool arm2_supported(int Dp, int Wp);
+size_t arm2_smem_bytes(int Dp, int Wp);
+void arm2_configure(int Dp, int Wp);
+void launch_arm2(const LaunchCtx& L, int mode);
+
+static bool use_arm2(int Dp, int Wp) {
+    static const bool v1 = [] {
+        const char* e = std::getenv("CCB_ARM_V1");
+        return e && e[0] == '1';
+    }();
+    return !v1 && arm2_supported(Dp, Wp);
+}
+
 void arm_configure(int Dp, int Wp) {
+    if (use_arm2(Dp, Wp)) arm2_configure(Dp, Wp);
     if (Dp == 8 && Wp == 8) configure_t<8, 8>();
     else if (Dp == 16 && Wp == 12) configure_t<16, 12>();
     else if (Dp == 20 && Wp == 20) configure_t<20, 20>();
@@ -610,6 +628,7 @@ static void launch_arm_mode(const LaunchCtx& L, int mode) {
 
 void launch_arm(const LaunchCtx& L, int mode) {
     const int Dp = L.host->Dp, Wp = L.host->Wp;
+    if (use_arm2(Dp, Wp)) return launch_arm2(L, mode);
     if (Dp == 8 && Wp == 8) launch_arm_mode<8, 8>(L, mode);
     else if (Dp == 16 && Wp == 12) launch_arm_mode<16, 12>(L, mode);
     else if (Dp == 20 && Wp == 20) launch_arm_mode<20, 20>(L, mode);
@@ -619,6 +638,10 @@ void launch_arm(const LaunchCtx& L, int mode) {
 }
 
 int arm_blocks_per_sm(int Dp, int Wp) {
+    if (use_arm2(Dp, Wp)) {  // __launch_bounds__(128, 2)
+        const int b = int((227 * 1024) / (arm2_smem_bytes(Dp, Wp) + 1024));
+        return b < 1 ? 1 : (b > 2 ? 2 : b);
+    }
     size_t smem;
     if (Dp == 8 && Wp == 8) smem = arm_smem<8, 8>();
     else if (Dp == 16 && Wp == 12) smem = arm_smem<16, 12>();

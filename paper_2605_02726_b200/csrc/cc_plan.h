@@ -32,6 +32,8 @@ constexpr int kMaxTensors = 64;
 constexpr int kMaxSlots = 3;
 constexpr int kMaxPartialRegions = 48;
 constexpr int kMaxUpsGrids = 8;
+constexpr int kArmTile = 128;  // latents per ARM tile == threads per ARM CTA
+constexpr int kSynTile = 128;  // pixels per trunk-backward tile == threads per CTA
 
 struct GridGeom {
     int level, hyper, rows, cols;

@@ -21,7 +21,7 @@ void cuda_check(cudaError_t e, const char* what) {
 
 namespace {
 
-constexpr int kArmTileHost = 128;
+constexpr int kArmTileHost = kArmTile;
 constexpr int kRMaxHost = 12;
 constexpr int kFMaxHost = 8;
 constexpr int kSnapSlots = 8;
@@ -324,7 +324,7 @@ void Trainer::build_plan() {
     if (const char* e = std::getenv("CCB_ARM_OCC")) arm_occ = std::max(1, std::min(arm_occ, std::atoi(e)));
     L_.arm_blocks = std::min(L_.arm_ntiles, num_sms_ * arm_occ);
     const int FP = syn_padded_hidden(P.syn_F);
-    const int64_t syn_tiles = (P.npix + 127) / 128;
+    const int64_t syn_tiles = (P.npix + kSynTile - 1) / kSynTile;
     int syn_per_sm = int((227 * 1024) / (syn_trunk_smem(FP) + 1024));
     syn_per_sm = std::max(1, std::min(8, syn_per_sm));
     L_.syn_ntiles = int(syn_tiles);

@@ -26,7 +26,7 @@ namespace ccb {
 namespace {
 
 constexpr int kLZ = kMaxLevels;  // z vector padded to 8 channels
-constexpr int kSynTile = 128;
+// kSynTile (pixels per trunk-backward tile) lives in cc_plan.h
 
 __host__ __device__ constexpr int r4(int n) { return (n + 3) / 4 * 4; }
 __host__ __device__ constexpr int oddc(int n) { return ((r4(n) / 4) % 2 == 0) ? r4(n) + 4 : r4(n); }
