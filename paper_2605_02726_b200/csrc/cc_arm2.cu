@@ -1,27 +1,31 @@
 // cc_arm2.cu — the auto-regressive entropy model (ARM + IFCE) as a chain of
-// register-tiled tile-GEMMs.  Same math and summation orders as cc_arm.cu
-// (entropy_model.hpp:180-336); different execution shape:
+// register-tiled tile-GEMMs.  Same math and per-output summation orders as
+// cc_arm.cu (entropy_model.hpp:180-336); different execution shape:
 //
-//   * a CTA (128 threads) owns a tile of 128 latents of one grid; every
-//     activation lives FEATURE-MAJOR in shared memory ([feature][latent],
-//     latents contiguous), so a thread reads 4 latents of a feature with one
-//     LDS.128 (conflict-free across the warp);
+//   * a CTA (256 threads, 8 warps) owns a tile of 128 latents of one grid;
+//     every activation lives FEATURE-MAJOR in shared memory ([feature][latent],
+//     latents contiguous), so a thread reads 2 latents of a feature with one
+//     LDS.64 (conflict-free across the warp);
 //   * every dense layer (forward l1, l2; backward dH1 = W2ᵀdH2, dC = W1ᵀdH1 +
 //     stabᵀ·draw) is a [128 x K] x [K x N] tile GEMM in which thread
-//     (quad q = lane, group g = warp) computes 4 latents x N/4 outputs: per K
-//     step one LDS.128 of activations + two LDS.128 of (broadcast) weights
-//     feed 4·N/4 FMAs;
-//   * the per-latent scalar work (head, Laplace rate and its backward, ReLU
-//     masks of the head) runs one thread per latent;
+//     (latent pair p, output group g) computes 2 latents x N/4 outputs with
+//     packed FFMA2 (the two latents are the two lanes, the weight is the
+//     FFMA2 broadcast operand);
+//   * the per-latent work (causal-context gather, IFCE, the two head outputs,
+//     Laplace rate and its backward) runs on one or two threads per latent;
 //   * the weight gradients are 4x4 register micro-tiles of
 //     [dH1|dH2|draw|dF] x [C|1, H1|1, H2|1, R|1] over the latent axis, split
-//     in thirds of the tile so that all 128 threads carry (nearly) the same
-//     work, and accumulated in REGISTERS across all tiles of the persistent
-//     CTA (fp32 per thread, fp64 at the final per-CTA reduction) — no
-//     per-tile shared-memory accumulation, no atomics, fixed order.
-//   The IFCE weight gradient (whose output depends on the tile's grid) is
-//   staged per tile and added to an fp64 shared accumulator in fixed order.
+//     in thirds of the tile so that the 256 threads carry (nearly) the same
+//     work, accumulated in REGISTERS across all tiles of the persistent CTA
+//     (fp32 per thread, fp64 at the final per-CTA reduction) — no per-tile
+//     shared-memory accumulation, no atomics, fixed order.  The IFCE weight
+//     gradient (whose output depends on the tile's grid) is staged per tile
+//     and added to an fp64 shared accumulator in fixed order;
+//   * the gather of tile t + grid is issued with cp.async (zero-fill past the
+//     grid) into a second set of buffers while tile t computes.
 #include <cuda_runtime.h>
+
+#pragma nv_diag_suppress 128  // forward-only instantiations skip the backward phases
 
 #include "cc_kernels.h"
 #include "cc_math.cuh"
@@ -31,7 +35,8 @@ namespace ccb {
 
 namespace {
 
-constexpr int T = kArmTile;   // latents per tile == threads per CTA (128)
+constexpr int T = kArmTile;   // latents per tile (128)
+constexpr int NT = 2 * T;     // threads per CTA
 constexpr int LT = T + 4;     // shared-memory row length (floats)
 constexpr int kRM = 12;       // max IFCE source grids
 constexpr int kFM = 8;        // max IFCE width
@@ -57,8 +62,9 @@ struct A2 {
     static constexpr int O_DR = O_DH2 + RDH * LT;
     static constexpr int O_R = O_DR + RDR * LT;
     static constexpr int O_DF = O_R + RR * LT;
-    static constexpr int O_C2 = O_DF + RF * LT;  // second C / R buffers: the
-    static constexpr int O_R2 = O_C2 + RC * LT;  // next tile's gather lands here
+    static constexpr int O_RAW = O_DF + RF * LT;   // head outputs (mu, sigma-raw)
+    static constexpr int O_C2 = O_RAW + 2 * LT;    // second C / R buffers: the
+    static constexpr int O_R2 = O_C2 + RC * LT;    // next tile's gather lands here
     static constexpr int ACT = O_R2 + RR * LT;
     // weight-gradient jobs (4x4 micro-tiles) and units (job x latent third)
     static constexpr int J1 = (WP / 4) * (DP / 4 + 1);   // dH1 x [C|1]
@@ -69,8 +75,9 @@ struct A2 {
     static constexpr int NU = 3 * NJ;                    // register-accumulated units
     static constexpr int J5 = (kFM / 4) * (kRM / 4 + 1); // dF x [R|1] (per tile)
     static constexpr int NU5 = 3 * J5;
-    static constexpr int MAXU = (NU + NU5 + T - 1) / T;  // units per thread (upper bound)
+    static constexpr int MAXU = (NU + NU5 + NT - 1) / NT;  // units per thread (upper bound)
     static constexpr int NACC5 = kMaxSlots * kFM * (kRM + 1);
+    static_assert(NU * 16 <= ACT, "epilogue staging fits in the activation buffers");
 };
 
 template <int DP, int WP>
@@ -93,7 +100,7 @@ struct alignas(16) A2Smem {
     double acc5[K::NACC5];  // IFCE dW (+db), per slot, fp64
     GridGeom geo[kMaxGrids];
     int ctx_dy[kMaxCtx], ctx_dx[kMaxCtx];
-    double red[T / 32];
+    double red[NT / 32];
 };
 
 // 4x4 outer-product micro-tile over latents [i0, i1), step 4: FFMA2 lanes
@@ -125,14 +132,17 @@ __device__ __forceinline__ void dw_tile(const float* __restrict__ A, const float
     for (int e = 0; e < 16; ++e) acc[e] += p[e].x + p[e].y;
 }
 
-// one K step of a tile GEMM: 4 latents (x) x N outputs (w, broadcast);
-// lo / hi hold latents {0,1} / {2,3} of every output in FFMA2 lanes
-template <int N>
-__device__ __forceinline__ void gemm_step(const float4& x, const float* w, float2 (&lo)[N], float2 (&hi)[N]) {
+// a tile GEMM over K rows of X (feature-major, LT stride): thread's 2 latents
+// at column 2p, N outputs of group g; acc holds (latent 2p, latent 2p+1)
+template <int N, int K>
+__device__ __forceinline__ void tile_gemm(const float* __restrict__ X, const float (*W)[32], int p, int g,
+                                          float2 (&acc)[N]) {
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+        const float2 x = *reinterpret_cast<const float2*>(X + k * LT + 2 * p);
+        const float* w = &W[k][g * 8];
 #pragma unroll
-    for (int n = 0; n < N; ++n) {
-        lo[n] = ffma2(make_float2(x.x, x.y), w[n], lo[n]);
-        hi[n] = ffma2(make_float2(x.z, x.w), w[n], hi[n]);
+        for (int n = 0; n < N; ++n) acc[n] = ffma2(x, w[n], acc[n]);
     }
 }
 
@@ -146,26 +156,30 @@ __device__ __forceinline__ void cp_async4_zfill(float* smem, const float* gmem, 
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(full ? 4 : 0)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 
-// Asynchronous gather of tile t (thread = latent): the S causal-context
-// values, the latent's own value (row DP+1) and, on IFCE grids, the kRM
-// co-located coarser-grid values (zero-filled past rdim / past the grid).
+// Asynchronous gather of one tile.  Threads [0,128) (latent lt): the S causal
+// context values and the latent's own value (row DP+1); threads [128,256): on
+// IFCE grids, the kRM co-located coarser-grid values (zero past rdim / past
+// the grid).  Always commits one cp.async group.
 template <int DP>
 __device__ __forceinline__ void issue_gather(const Plan& P, const GridGeom* geo, int2 tile,
                                              const int* cdy, const int* cdx, float* sCb, float* sRb,
-                                             int tid) {
+                                             int half, int lt) {
     const GridGeom& g = geo[tile.x];
     const int64_t count = int64_t(g.rows) * g.cols;
-    const int64_t li = int64_t(tile.y) + tid;
+    const int64_t li = int64_t(tile.y) + lt;
     const bool valid = li < count;
     const int r = valid ? int(li / g.cols) : 0;
     const int c = valid ? int(li - int64_t(r) * g.cols) : 0;
-    const float* base = P.yhat_pad + g.pad_base + int64_t(r) * g.stride + c;
-    const int S = P.S;
+    if (half == 0) {
+        const float* base = P.yhat_pad + g.pad_base + int64_t(r) * g.stride + c;
+        const int S = P.S;
 #pragma unroll 4
-    for (int o = 0; o < S; ++o) cp_async4_zfill(sCb + o * LT + tid, base + cdy[o] * g.stride + cdx[o], valid);
-    cp_async4_zfill(sCb + (DP + 1) * LT + tid, base, valid);
-    if (g.ifce_slot >= 0) {
+        for (int o = 0; o < S; ++o)
+            cp_async4_zfill(sCb + o * LT + lt, base + cdy[o] * g.stride + cdx[o], valid);
+        cp_async4_zfill(sCb + (DP + 1) * LT + lt, base, valid);
+    } else if (g.ifce_slot >= 0) {
         const int rd = g.rdim;
 #pragma unroll
         for (int j = 0; j < kRM; ++j) {
@@ -176,10 +190,10 @@ __device__ __forceinline__ void issue_gather(const Plan& P, const GridGeom* geo,
                 const int sh = sg.level - g.level;
                 src = P.yhat_pad + sg.pad_base + int64_t(r >> sh) * sg.stride + (c >> sh);
             }
-            cp_async4_zfill(sRb + j * LT + tid, src, on);
+            cp_async4_zfill(sRb + j * LT + lt, src, on);
         }
     }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    cp_async_commit();
 }
 
 __device__ __forceinline__ void swap_bufs(float*& a, float*& b, float*& c, float*& d) {
@@ -188,24 +202,25 @@ __device__ __forceinline__ void swap_bufs(float*& a, float*& b, float*& c, float
 }
 
 template <int DP, int WP, int MODE>
-__global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
-                                               const int2* __restrict__ tiles, int ntiles) {
+__global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
+                                                const int2* __restrict__ tiles, int ntiles) {
     using K = A2<DP, WP>;
     const Plan& P = *pp;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     A2Smem<DP, WP>& sm = *reinterpret_cast<A2Smem<DP, WP>*>(smem_raw);
     const int tid = threadIdx.x;
-    const int lane = tid & 31, grp = tid >> 5;
+    const int half = tid >> 7, lt = tid & (T - 1);   // per-latent roles
+    const int pr = tid & 63, grp = tid >> 6;         // tile-GEMM roles
     const int D = P.D, Wd = P.Wd, S = P.S, F = P.F;
     const float* prm = P.params;
 
     // ---------------- weights -> shared memory (zero padded) ----------------
-    for (int e = tid; e < DP * 32; e += T) {
+    for (int e = tid; e < DP * 32; e += NT) {
         const int k = e / 32, c = e % 32, g = c / 8, n = c % 8;
         const int a = g * K::NW + n;  // output of l1 (W-wide)
         sm.W1T[k][c] = (n < K::NW && a < Wd && k < D) ? prm[P.off_l1w + a * D + k] : 0.0f;
     }
-    for (int e = tid; e < WP * 32; e += T) {
+    for (int e = tid; e < WP * 32; e += NT) {
         const int a = e / 32, c = e % 32, g = c / 8, n = c % 8;
         const int k = g * K::ND + n;  // output of dC (D-wide)
         sm.W1[a][c] = (n < K::ND && a < Wd && k < D) ? prm[P.off_l1w + a * D + k] : 0.0f;
@@ -213,25 +228,25 @@ __global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
         sm.W2T[a][c] = (n < K::NW && a < Wd && b < Wd) ? prm[P.off_l2w + b * Wd + a] : 0.0f;
         sm.W2[a][c] = (n < K::NW && a < Wd && b < Wd) ? prm[P.off_l2w + a * Wd + b] : 0.0f;
     }
-    for (int e = tid; e < 2 * 32; e += T) {
+    for (int e = tid; e < 2 * 32; e += NT) {
         const int j = e / 32, c = e % 32, g = c / 8, n = c % 8;
         const int k = g * K::ND + n;
         sm.ST[j][c] = (n < K::ND && k < D && P.off_astab >= 0) ? prm[P.off_astab + j * D + k] : 0.0f;
     }
-    for (int e = tid; e < 2 * WP; e += T) {
+    for (int e = tid; e < 2 * WP; e += NT) {
         const int j = e / WP, a = e % WP;
         sm.W3[j][a] = a < Wd ? prm[P.off_hw + j * Wd + a] : 0.0f;
     }
-    for (int e = tid; e < 2 * DP; e += T) {
+    for (int e = tid; e < 2 * DP; e += NT) {
         const int j = e / DP, k = e % DP;
         sm.stab[j][k] = (P.off_astab >= 0 && k < D) ? prm[P.off_astab + j * D + k] : 0.0f;
     }
-    for (int e = tid; e < WP; e += T) {
+    for (int e = tid; e < WP; e += NT) {
         sm.b1[e] = e < Wd ? prm[P.off_l1b + e] : 0.0f;
         sm.b2[e] = e < Wd ? prm[P.off_l2b + e] : 0.0f;
     }
     if (tid < 4) sm.b3[tid] = tid < 2 ? prm[P.off_hb + tid] : 0.0f;
-    for (int e = tid; e < kMaxSlots * kFM * kRM; e += T) {
+    for (int e = tid; e < kMaxSlots * kFM * kRM; e += NT) {
         const int s = e / (kFM * kRM), r = e % (kFM * kRM), f = r / kRM, j = r % kRM;
         float v = 0.0f;
         if (s < P.n_slots) {
@@ -240,35 +255,36 @@ __global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
         }
         sm.Wf[s][f][j] = v;
     }
-    for (int e = tid; e < kMaxSlots * kFM; e += T) {
+    for (int e = tid; e < kMaxSlots * kFM; e += NT) {
         const int s = e / kFM, f = e % kFM;
         sm.bf[s][f] = (s < P.n_slots && f < F) ? prm[P.off_ifb[s] + f] : 0.0f;
     }
-    for (int e = tid; e < kMaxCtx; e += T) {
+    for (int e = tid; e < kMaxCtx; e += NT) {
         sm.ctx_dy[e] = e < S ? P.ctx_dy[e] : 0;
         sm.ctx_dx[e] = e < S ? P.ctx_dx[e] : 0;
     }
-    for (int e = tid; e < K::NACC5; e += T) sm.acc5[e] = 0.0;
-    for (int e = tid; e < P.n_grids; e += T) sm.geo[e] = P.g[e];
+    for (int e = tid; e < K::NACC5; e += NT) sm.acc5[e] = 0.0;
+    for (int e = tid; e < P.n_grids; e += NT) sm.geo[e] = P.g[e];
     // constant rows: zero padding of every activation array (written once)
-    for (int e = tid; e < K::ACT; e += T) sm.act[e] = 0.0f;
+    for (int e = tid; e < K::ACT; e += NT) sm.act[e] = 0.0f;
     __syncthreads();
 
     float* sC = sm.act + K::O_C;
+    float* sR = sm.act + K::O_R;
+    float* sCn = sm.act + K::O_C2;
+    float* sRn = sm.act + K::O_R2;
     float* const sH1 = sm.act + K::O_H1;
     float* const sH2 = sm.act + K::O_H2;
     float* const sDH1 = sm.act + K::O_DH1;
     float* const sDH2 = sm.act + K::O_DH2;
     float* const sDR = sm.act + K::O_DR;
-    float* sR = sm.act + K::O_R;
-    float* sCn = sm.act + K::O_C2;
-    float* sRn = sm.act + K::O_R2;
+    float* const sDF = sm.act + K::O_DF;
+    float* const sRaw = sm.act + K::O_RAW;
     // tile records run two ahead of the tile being computed (register
     // prefetch); the gather of tile t+grid is issued while tile t computes
     int2 cur = blockIdx.x < ntiles ? tiles[blockIdx.x] : make_int2(0, 0);
     int2 nxt = blockIdx.x + gridDim.x < ntiles ? tiles[blockIdx.x + gridDim.x] : make_int2(0, 0);
-    if (blockIdx.x < ntiles) issue_gather<DP>(P, sm.geo, cur, sm.ctx_dy, sm.ctx_dx, sC, sR, tid);
-    float* const sDF = sm.act + K::O_DF;
+    if (blockIdx.x < ntiles) issue_gather<DP>(P, sm.geo, cur, sm.ctx_dy, sm.ctx_dx, sC, sR, half, lt);
 
     // persistent weight-gradient accumulators of this thread's units
     float uacc[K::MAXU][16];
@@ -285,106 +301,99 @@ __global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
         const GridGeom& g = sm.geo[tile.x];
         const int64_t count = int64_t(g.rows) * g.cols;
         const int slot = g.ifce_slot;
-
-        // ---- P0/P1: per-latent gather (thread = latent) + IFCE forward ----
-        const int64_t li = int64_t(tile.y) + tid;
+        const int64_t li = int64_t(tile.y) + lt;
         const bool valid = li < count;
+
+        // ---- P0: prefetch the next tile (its buffers' last readers finished
+        // at the previous tile's closing barrier), land the current one ----
+        if (t + int(gridDim.x) < ntiles)
+            issue_gather<DP>(P, sm.geo, nxt, sm.ctx_dy, sm.ctx_dx, sCn, sRn, half, lt);
+        else
+            cp_async_commit();
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncthreads();
+
+        // ---- P1: IFCE forward (two threads per latent) + constant rows ----
         {
-            // prefetch the next tile into the other buffers (their last readers
-            // finished at the previous tile's closing barrier), then wait for
-            // this thread's own columns of the current tile
-            if (t + int(gridDim.x) < ntiles)
-                issue_gather<DP>(P, sm.geo, nxt, sm.ctx_dy, sm.ctx_dx, sCn, sRn, tid);
-            else
-                asm volatile("cp.async.commit_group;\n" ::: "memory");
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            constexpr int FH = kFM / 2;
             if (slot >= 0) {
                 float rv[kRM];
 #pragma unroll
-                for (int j = 0; j < kRM; ++j) rv[j] = sR[j * LT + tid];
-                sR[kRM * LT + tid] = valid ? 1.0f : 0.0f;
-                for (int f = 0; f < F; ++f) {  // gemm_xwt_fast order: bias, then j
-                    float a = sm.bf[slot][f];
+                for (int j = 0; j < kRM; ++j) rv[j] = sR[j * LT + lt];
 #pragma unroll
-                    for (int j = 0; j < kRM; ++j) a = fmaf(rv[j], sm.Wf[slot][f][j], a);
-                    sC[(S + f) * LT + tid] = valid ? a : 0.0f;
+                for (int ff = 0; ff < FH; ++ff) {  // gemm_xwt_fast order: bias, then j
+                    const int f = half * FH + ff;
+                    if (f < F) {
+                        float a = sm.bf[slot][f];
+#pragma unroll
+                        for (int j = 0; j < kRM; ++j) a = fmaf(rv[j], sm.Wf[slot][f][j], a);
+                        sC[(S + f) * LT + lt] = valid ? a : 0.0f;
+                    }
                 }
+                if (half) sR[kRM * LT + lt] = valid ? 1.0f : 0.0f;
             } else {
-                for (int f = 0; f < F; ++f) sC[(S + f) * LT + tid] = 0.0f;
+#pragma unroll
+                for (int ff = 0; ff < FH; ++ff) {
+                    const int f = half * FH + ff;
+                    if (f < F) sC[(S + f) * LT + lt] = 0.0f;
+                }
             }
-            sC[DP * LT + tid] = valid ? 1.0f : 0.0f;
-            sH1[WP * LT + tid] = valid ? 1.0f : 0.0f;
-            sH2[WP * LT + tid] = valid ? 1.0f : 0.0f;
+            if (half == 0) {
+                sC[DP * LT + lt] = valid ? 1.0f : 0.0f;
+                sH1[WP * LT + lt] = valid ? 1.0f : 0.0f;
+            } else {
+                sH2[WP * LT + lt] = valid ? 1.0f : 0.0f;
+            }
         }
         __syncthreads();
 
-        // ---- P2: H1 = relu(b1 + W1·C)   (tile GEMM, 4 latents x NW outputs) ----
+        // ---- P2: H1 = relu(b1 + W1·C) ----
         {
-            float2 lo[K::NW], hi[K::NW];
+            float2 acc[K::NW];
 #pragma unroll
             for (int n = 0; n < K::NW; ++n) {
                 const float b = sm.b1[grp * K::NW + n];
-                lo[n] = hi[n] = make_float2(b, b);
+                acc[n] = make_float2(b, b);
             }
-#pragma unroll 4
-            for (int k = 0; k < DP; ++k) {
-                const float4 x = *reinterpret_cast<const float4*>(sC + k * LT + 4 * lane);
-                const float* w = &sm.W1T[k][grp * 8];
-                gemm_step<K::NW>(x, w, lo, hi);
-            }
+            tile_gemm<K::NW, DP>(sC, sm.W1T, pr, grp, acc);
 #pragma unroll
             for (int n = 0; n < K::NW; ++n) {
-                const int a = grp * K::NW + n;
-                float4 h;
-                h.x = lo[n].x > 0.0f ? lo[n].x : 0.0f;
-                h.y = lo[n].y > 0.0f ? lo[n].y : 0.0f;
-                h.z = hi[n].x > 0.0f ? hi[n].x : 0.0f;
-                h.w = hi[n].y > 0.0f ? hi[n].y : 0.0f;
-                *reinterpret_cast<float4*>(sH1 + a * LT + 4 * lane) = h;
+                const float2 h = make_float2(acc[n].x > 0.0f ? acc[n].x : 0.0f, acc[n].y > 0.0f ? acc[n].y : 0.0f);
+                *reinterpret_cast<float2*>(sH1 + (grp * K::NW + n) * LT + 2 * pr) = h;
             }
         }
         __syncthreads();
         // ---- P3: H2 = relu(b2 + W2·H1) ----
         {
-            float2 lo[K::NW], hi[K::NW];
+            float2 acc[K::NW];
 #pragma unroll
             for (int n = 0; n < K::NW; ++n) {
                 const float b = sm.b2[grp * K::NW + n];
-                lo[n] = hi[n] = make_float2(b, b);
+                acc[n] = make_float2(b, b);
             }
-#pragma unroll 4
-            for (int k = 0; k < WP; ++k) {
-                const float4 x = *reinterpret_cast<const float4*>(sH1 + k * LT + 4 * lane);
-                const float* w = &sm.W2T[k][grp * 8];
-                gemm_step<K::NW>(x, w, lo, hi);
-            }
+            tile_gemm<K::NW, WP>(sH1, sm.W2T, pr, grp, acc);
 #pragma unroll
             for (int n = 0; n < K::NW; ++n) {
-                const int a = grp * K::NW + n;
-                float4 h;
-                h.x = lo[n].x > 0.0f ? lo[n].x : 0.0f;
-                h.y = lo[n].y > 0.0f ? lo[n].y : 0.0f;
-                h.z = hi[n].x > 0.0f ? hi[n].x : 0.0f;
-                h.w = hi[n].y > 0.0f ? hi[n].y : 0.0f;
-                *reinterpret_cast<float4*>(sH2 + a * LT + 4 * lane) = h;
+                const float2 h = make_float2(acc[n].x > 0.0f ? acc[n].x : 0.0f, acc[n].y > 0.0f ? acc[n].y : 0.0f);
+                *reinterpret_cast<float2*>(sH2 + (grp * K::NW + n) * LT + 2 * pr) = h;
             }
         }
         __syncthreads();
-        // ---- P4/P5: head, Laplace rate + its backward, dH2 (thread = latent) ----
+        // ---- P4a: head output `half` (mu / sigma-raw) of latent lt ----
         {
-            float raw[2];
+            float a = sm.b3[half];
 #pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                float a = sm.b3[j];
+            for (int k = 0; k < WP; ++k) a = fmaf(sH2[k * LT + lt], sm.W3[half][k], a);
 #pragma unroll
-                for (int k = 0; k < WP; ++k) a = fmaf(sH2[k * LT + tid], sm.W3[j][k], a);
-#pragma unroll
-                for (int k = 0; k < DP; ++k) a = fmaf(sC[k * LT + tid], sm.stab[j][k], a);
-                raw[j] = a;
-            }
-            const float v = sC[(DP + 1) * LT + tid];
-            const float mu = raw[0];
-            const float sg = sigma_from_raw(raw[1]);
+            for (int k = 0; k < DP; ++k) a = fmaf(sC[k * LT + lt], sm.stab[half][k], a);
+            sRaw[half * LT + lt] = a;
+        }
+        __syncthreads();
+        // ---- P4b: Laplace rate + its backward, dH2 (threads [0,128)) ----
+        if (half == 0) {
+            const float v = sC[(DP + 1) * LT + lt];
+            const float mu = sRaw[lt];
+            const float sg = sigma_from_raw(sRaw[LT + lt]);
             const float bsc = sg * kInvSqrt2F;
             const float u = fabsf(v - mu);
             const float e1 = cc_exp(-(u + 0.5f) / bsc);
@@ -405,92 +414,63 @@ __global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
                     gv = up * dp_du * sgn;
                 }
                 if (MODE == kArmProxy && valid) P.gown[g.lat_off + li] = gv;
-                sDR[0 * LT + tid] = dmu;
-                sDR[1 * LT + tid] = dsr;
+                sDR[0 * LT + lt] = dmu;
+                sDR[1 * LT + lt] = dsr;
 #pragma unroll
                 for (int a = 0; a < WP; ++a) {  // dH2 = (W3ᵀ draw) ⊙ relu'(H2)
                     float d = fmaf(dmu, sm.W3[0][a], 0.0f);
                     d = fmaf(dsr, sm.W3[1][a], d);
-                    sDH2[a * LT + tid] = sH2[a * LT + tid] > 0.0f ? d : 0.0f;
+                    sDH2[a * LT + lt] = sH2[a * LT + lt] > 0.0f ? d : 0.0f;
                 }
             }
         }
+        __syncthreads();
         if (MODE == kArmForward) {
-            __syncthreads();  // activations are rewritten by the next tile
             swap_bufs(sC, sCn, sR, sRn);
             cur = nxt;
             nxt = nxt2;
             continue;
         }
-        __syncthreads();
         // ---- P6: dH1 = (W2ᵀ·dH2) ⊙ relu'(H1) ----
         {
-            float2 lo[K::NW], hi[K::NW];
+            float2 acc[K::NW];
 #pragma unroll
-            for (int n = 0; n < K::NW; ++n)
-                lo[n] = hi[n] = make_float2(0.0f, 0.0f);
-#pragma unroll 4
-            for (int a = 0; a < WP; ++a) {
-                const float4 x = *reinterpret_cast<const float4*>(sDH2 + a * LT + 4 * lane);
-                const float* w = &sm.W2[a][grp * 8];
-                gemm_step<K::NW>(x, w, lo, hi);
-            }
+            for (int n = 0; n < K::NW; ++n) acc[n] = make_float2(0.0f, 0.0f);
+            tile_gemm<K::NW, WP>(sDH2, sm.W2, pr, grp, acc);
 #pragma unroll
             for (int n = 0; n < K::NW; ++n) {
                 const int b = grp * K::NW + n;
-                const float4 h = *reinterpret_cast<const float4*>(sH1 + b * LT + 4 * lane);
-                float4 d;
-                d.x = h.x > 0.0f ? lo[n].x : 0.0f;
-                d.y = h.y > 0.0f ? lo[n].y : 0.0f;
-                d.z = h.z > 0.0f ? hi[n].x : 0.0f;
-                d.w = h.w > 0.0f ? hi[n].y : 0.0f;
-                *reinterpret_cast<float4*>(sDH1 + b * LT + 4 * lane) = d;
+                const float2 h = *reinterpret_cast<const float2*>(sH1 + b * LT + 2 * pr);
+                const float2 d = make_float2(h.x > 0.0f ? acc[n].x : 0.0f, h.y > 0.0f ? acc[n].y : 0.0f);
+                *reinterpret_cast<float2*>(sDH1 + b * LT + 2 * pr) = d;
             }
         }
         __syncthreads();
         // ---- P7: dC = W1ᵀ·dH1 + stabᵀ·draw -> dctx / dF ----
         {
-            float2 lo[K::ND], hi[K::ND];
+            float2 acc[K::ND];
 #pragma unroll
-            for (int n = 0; n < K::ND; ++n)
-                lo[n] = hi[n] = make_float2(0.0f, 0.0f);
-#pragma unroll 4
-            for (int a = 0; a < WP; ++a) {
-                const float4 x = *reinterpret_cast<const float4*>(sDH1 + a * LT + 4 * lane);
-                const float* w = &sm.W1[a][grp * 8];
-                gemm_step<K::ND>(x, w, lo, hi);
-            }
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const float4 x = *reinterpret_cast<const float4*>(sDR + j * LT + 4 * lane);
-                const float* w = &sm.ST[j][grp * 8];
-                gemm_step<K::ND>(x, w, lo, hi);
-            }
-            const int64_t l0 = int64_t(tile.y) + 4 * lane;
+            for (int n = 0; n < K::ND; ++n) acc[n] = make_float2(0.0f, 0.0f);
+            tile_gemm<K::ND, WP>(sDH1, sm.W1, pr, grp, acc);
+            tile_gemm<K::ND, 2>(sDR, sm.ST, pr, grp, acc);
+            const int64_t l0 = int64_t(tile.y) + 2 * pr;
+            const bool v0 = l0 < count, v1 = l0 + 1 < count;
 #pragma unroll
             for (int n = 0; n < K::ND; ++n) {
                 const int k = grp * K::ND + n;
                 if (k < S) {
                     if (MODE == kArmProxy) {
                         float* dcp = P.dctx + g.dctx_off + int64_t(k) * count + l0;
-                        const float vv[4] = {lo[n].x, lo[n].y, hi[n].x, hi[n].y};
-#pragma unroll
-                        for (int l = 0; l < 4; ++l)
-                            if (l0 + l < count) dcp[l] = vv[l];
+                        if (v0) dcp[0] = acc[n].x;
+                        if (v1) dcp[1] = acc[n].y;
                     }
                 } else if (k < S + F && slot >= 0) {
-                    float4 dv = make_float4(lo[n].x, lo[n].y, hi[n].x, hi[n].y);
-                    if (l0 + 0 >= count) dv.x = 0.0f;
-                    if (l0 + 1 >= count) dv.y = 0.0f;
-                    if (l0 + 2 >= count) dv.z = 0.0f;
-                    if (l0 + 3 >= count) dv.w = 0.0f;
-                    *reinterpret_cast<float4*>(sDF + (k - S) * LT + 4 * lane) = dv;
+                    const float2 dv = make_float2(v0 ? acc[n].x : 0.0f, v1 ? acc[n].y : 0.0f);
+                    *reinterpret_cast<float2*>(sDF + (k - S) * LT + 2 * pr) = dv;
                     if (MODE == kArmProxy) {
                         float* dfp = P.dfeat + g.dfeat_off + int64_t(k - S) * count + l0;
-                        const float vv[4] = {dv.x, dv.y, dv.z, dv.w};
-#pragma unroll
-                        for (int l = 0; l < 4; ++l)
-                            if (l0 + l < count) dfp[l] = vv[l];
+                        if (v0) dfp[0] = dv.x;
+                        if (v1) dfp[1] = dv.y;
                     }
                 }
             }
@@ -499,7 +479,7 @@ __global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
         // ---- P8: weight gradients (register micro-tiles, balanced units) ----
 #pragma unroll
         for (int m = 0; m < K::MAXU; ++m) {
-            const int u = tid + m * T;
+            const int u = tid + m * NT;
             if (u < K::NU) {
                 const int j = u / 3;
                 int i0, i1;
@@ -539,14 +519,14 @@ __global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
         __syncthreads();
         if (slot >= 0) {  // IFCE dW: thirds summed in order, then fp64 accumulate
             constexpr int nq = kRM / 4 + 1;
-            for (int e = tid; e < K::J5 * 16; e += T) {
+            for (int e = tid; e < K::J5 * 16; e += NT) {
                 const int j = e / 16, q = e % 16;
                 const float v = (sm.stage5[3 * j][q] + sm.stage5[3 * j + 1][q]) + sm.stage5[3 * j + 2][q];
                 const int a = 4 * (j / nq) + q / 4, b = 4 * (j % nq) + q % 4;
                 if (b <= kRM) sm.acc5[(slot * kFM + a) * (kRM + 1) + b] += double(v);
             }
+            // stage5 is rewritten only after the next tile's five barriers
         }
-        __syncthreads();
         swap_bufs(sC, sCn, sR, sRn);
         cur = nxt;
         nxt = nxt2;
@@ -554,7 +534,7 @@ __global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 
     // ---------------- per-CTA results ----------------
-    const double tb = block_sum(bits_thr, sm.red);
+    const double tb = block_sum(bits_thr, sm.red);  // (its barriers also close the last tile)
     if (tid == 0) P.bits_part[blockIdx.x] = tb;
     if (MODE == kArmForward) return;
     const PartialRegion& R = P.region[P.reg_arm];
@@ -565,13 +545,13 @@ __global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
     float* stage = sm.act;
 #pragma unroll
     for (int m = 0; m < K::MAXU; ++m) {
-        const int u = tid + m * T;
+        const int u = tid + m * NT;
         if (u < K::NU)
 #pragma unroll
             for (int e = 0; e < 16; ++e) stage[u * 16 + e] = uacc[m][e];
     }
     __syncthreads();
-    for (int x = tid; x < K::NJ * 16; x += T) {
+    for (int x = tid; x < K::NJ * 16; x += NT) {
         const int j = x / 16, q = x % 16;
         const double v = (double(stage[(3 * j) * 16 + q]) + double(stage[(3 * j + 1) * 16 + q])) +
                          double(stage[(3 * j + 2) * 16 + q]);
@@ -596,7 +576,7 @@ __global__ void __launch_bounds__(T, 2) k_arm2(const Plan* __restrict__ pp,
     }
     for (int s = 0; s < P.n_slots; ++s) {
         const int rd = P.g[P.slot_gi[s]].rdim;
-        for (int e = tid; e < F * (rd + 1); e += T) {
+        for (int e = tid; e < F * (rd + 1); e += NT) {
             const int f = e / (rd + 1), b = e % (rd + 1);
             const double v = sm.acc5[(s * kFM + f) * (kRM + 1) + (b < rd ? b : kRM)];
             const int o = b < rd ? P.off_ifw[s] + f * rd + b : P.off_ifb[s] + f;
@@ -612,8 +592,8 @@ size_t arm2_smem() {
 
 template <int DP, int WP, int MODE>
 void launch_t(const LaunchCtx& L) {
-    k_arm2<DP, WP, MODE><<<L.arm_blocks, T, arm2_smem<DP, WP>(), L.stream>>>(L.plan, L.arm_tiles,
-                                                                              L.arm_ntiles);
+    k_arm2<DP, WP, MODE><<<L.arm_blocks, NT, arm2_smem<DP, WP>(), L.stream>>>(L.plan, L.arm_tiles,
+                                                                               L.arm_ntiles);
 }
 
 template <int DP, int WP>
