@@ -30,6 +30,7 @@
 #include "cc_kernels.h"
 #include "cc_math.cuh"
 #include "cc_reduce.cuh"
+#include "cc_tile.cuh"
 
 namespace ccb {
 
@@ -103,33 +104,9 @@ struct alignas(16) A2Smem {
     double red[NT / 32];
 };
 
-// 4x4 outer-product micro-tile over latents [i0, i1), step 4: FFMA2 lanes
-// carry the even / odd latents, folded into acc (+= even + odd) at the end.
 __device__ __forceinline__ void dw_tile(const float* __restrict__ A, const float* __restrict__ B,
                                         int i0, int i1, float (&acc)[16]) {
-    float2 p[16];
-#pragma unroll
-    for (int e = 0; e < 16; ++e) p[e] = make_float2(0.0f, 0.0f);
-#pragma unroll 2
-    for (int i = i0; i < i1; i += 4) {
-        float4 av[4], bv[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            av[r] = *reinterpret_cast<const float4*>(A + r * LT + i);
-            bv[r] = *reinterpret_cast<const float4*>(B + r * LT + i);
-        }
-#pragma unroll
-        for (int r = 0; r < 4; ++r)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                float2 a = p[r * 4 + c];
-                a = ffma2(make_float2(av[r].x, av[r].y), make_float2(bv[c].x, bv[c].y), a);
-                a = ffma2(make_float2(av[r].z, av[r].w), make_float2(bv[c].z, bv[c].w), a);
-                p[r * 4 + c] = a;
-            }
-    }
-#pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] += p[e].x + p[e].y;
+    dw_tile4x4<LT>(A, B, i0, i1, acc);
 }
 
 // a tile GEMM over K rows of X (feature-major, LT stride): thread's 2 latents

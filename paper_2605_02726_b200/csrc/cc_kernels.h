@@ -48,11 +48,12 @@ void launch_ups_backward(const LaunchCtx& L, bool latent_grads);
 int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward);
 void ups_configure();
 
-// synthesis (cc_syn.cu)
+// synthesis (cc_syn.cu, cc_syn_trunk.cu)
 void launch_syn_forward(const LaunchCtx& L, bool backward);
 void launch_syn_backward(const LaunchCtx& L);
 int syn_padded_hidden(int F);
 size_t syn_trunk_smem(int FP);
+int syn_trunk_blocks_per_sm(int FP);
 void syn_configure(int FP);
 void syn_post_configure();
 int syn_post_tiles(int H, int W);

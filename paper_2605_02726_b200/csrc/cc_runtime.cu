@@ -325,8 +325,7 @@ void Trainer::build_plan() {
     L_.arm_blocks = std::min(L_.arm_ntiles, num_sms_ * arm_occ);
     const int FP = syn_padded_hidden(P.syn_F);
     const int64_t syn_tiles = (P.npix + kSynTile - 1) / kSynTile;
-    int syn_per_sm = int((227 * 1024) / (syn_trunk_smem(FP) + 1024));
-    syn_per_sm = std::max(1, std::min(8, syn_per_sm));
+    const int syn_per_sm = syn_trunk_blocks_per_sm(FP);
     L_.syn_ntiles = int(syn_tiles);
     L_.syn_blocks = int(std::min<int64_t>(syn_tiles, int64_t(num_sms_) * syn_per_sm));
     P.n_bits_part = L_.arm_blocks;

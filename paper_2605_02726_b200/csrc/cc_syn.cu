@@ -12,9 +12,8 @@
 //                     halos: residual 3x3 posts forward, clamp, MSE (fp64,
 //                     owned pixels), dx̂, posts backward (transposed conv by
 //                     gather), post weight gradients -> dt
-//   k_syn_trunk_bwd   recompute h1, dh1, dz, and the c1/c2/stab weight
-//                     gradients as per-tile shared-memory GEMMs (persistent
-//                     CTAs, fixed-order fp64 accumulation; no atomics)
+//   k_syn_trunk_bwd2  (cc_syn_trunk.cu) recompute h1, dh1, dz and the
+//                     c1/c2/stab weight gradients
 #include <cuda_runtime.h>
 
 #include "cc_kernels.h"
@@ -28,8 +27,6 @@ namespace {
 constexpr int kLZ = kMaxLevels;  // z vector padded to 8 channels
 // kSynTile (pixels per trunk-backward tile) lives in cc_plan.h
 
-__host__ __device__ constexpr int r4(int n) { return (n + 3) / 4 * 4; }
-__host__ __device__ constexpr int oddc(int n) { return ((r4(n) / 4) % 2 == 0) ? r4(n) + 4 : r4(n); }
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
@@ -361,267 +358,7 @@ __global__ void __launch_bounds__(256, 2) k_syn_post(const Plan* __restrict__ pp
     }
 }
 
-// ----------------------------------------------------------- trunk backward
-template <int FP>
-struct TrunkCfg {
-    static constexpr int LZ = oddc(kLZ + 1);   // z row, ones at kLZ
-    static constexpr int LH = oddc(FP + 1);    // h1 row, ones at FP
-    static constexpr int LDH = oddc(FP);       // dh1 row
-    static constexpr int LT = 4;               // dt / dx̂ rows
-    static constexpr int O_Z = 0;
-    static constexpr int O_H = O_Z + kSynTile * LZ;
-    static constexpr int O_DH = O_H + kSynTile * LH;
-    static constexpr int O_DT = O_DH + kSynTile * LDH;
-    static constexpr int O_DX = O_DT + kSynTile * LT;
-    static constexpr int ACT = O_DX + kSynTile * LT;
-    static constexpr int NJ1 = (FP / 2) * (r4(kLZ + 1) / 4);  // dh1 x [z|1]
-    static constexpr int NJ2 = 2 * (r4(FP + 1) / 4);          // dt x [h1|1]
-    static constexpr int NJ3 = 2 * (kLZ / 4);                 // dx̂ x z
-    static constexpr int NJ = NJ1 + NJ2 + NJ3;
-    static constexpr int NACC = FP * kLZ + FP + 3 * FP + 3 + 3 * kLZ;
-};
-
-template <int FP>
-struct alignas(16) TrunkSmem {
-    using K = TrunkCfg<FP>;
-    alignas(16) float c1w[FP * kLZ];
-    alignas(16) float c1b[FP];
-    alignas(16) float c2w[3 * FP];
-    alignas(16) float st[3 * kLZ];
-    alignas(16) float act[K::ACT];
-    alignas(16) double acc[K::NACC];
-};
-
-template <int LDA, int LDB>
-__device__ __forceinline__ void syn_mt(const float* __restrict__ A, const float* __restrict__ B,
-                                       int a0, int b0, float (&acc)[8]) {
-#pragma unroll 4
-    for (int i = 0; i < kSynTile; ++i) {
-        const float2 av = *reinterpret_cast<const float2*>(A + i * LDA + a0);
-        const float4 bv = *reinterpret_cast<const float4*>(B + i * LDB + b0);
-        acc[0] = fmaf(av.x, bv.x, acc[0]);
-        acc[1] = fmaf(av.x, bv.y, acc[1]);
-        acc[2] = fmaf(av.x, bv.z, acc[2]);
-        acc[3] = fmaf(av.x, bv.w, acc[3]);
-        acc[4] = fmaf(av.y, bv.x, acc[4]);
-        acc[5] = fmaf(av.y, bv.y, acc[5]);
-        acc[6] = fmaf(av.y, bv.z, acc[6]);
-        acc[7] = fmaf(av.y, bv.w, acc[7]);
-    }
-}
-
-// accumulator index layout: [c1w F*8 | c1b F | c2w 3*F | c2b 3 | st 3*8] (padded dims)
-template <int FP>
-__global__ void __launch_bounds__(kSynTile) k_syn_trunk_bwd(const Plan* __restrict__ pp,
-                                                            const float* __restrict__ dt_in) {
-    using K = TrunkCfg<FP>;
-    const Plan& P = *pp;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    TrunkSmem<FP>& sm = *reinterpret_cast<TrunkSmem<FP>*>(smem_raw);
-    const int tid = threadIdx.x;
-    const int L = P.L, F = P.syn_F;
-    for (int e = tid; e < FP * kLZ; e += kSynTile) {
-        const int f = e / kLZ, k = e - f * kLZ;
-        sm.c1w[e] = (f < F && k < L) ? P.params[P.off_c1w + f * L + k] : 0.0f;
-    }
-    for (int e = tid; e < FP; e += kSynTile) sm.c1b[e] = e < F ? P.params[P.off_c1b + e] : 0.0f;
-    for (int e = tid; e < 3 * FP; e += kSynTile) {
-        const int co = e / FP, f = e - co * FP;
-        sm.c2w[e] = f < F ? P.params[P.off_c2w + co * F + f] : 0.0f;
-    }
-    for (int e = tid; e < 3 * kLZ; e += kSynTile) {
-        const int co = e / kLZ, k = e - co * kLZ;
-        sm.st[e] = (P.off_sstab >= 0 && k < L) ? P.params[P.off_sstab + co * L + k] : 0.0f;
-    }
-    for (int e = tid; e < K::NACC; e += kSynTile) sm.acc[e] = 0.0;
-    __syncthreads();
-
-    const int64_t np = P.npix;
-    const int64_t ntiles = (np + kSynTile - 1) / kSynTile;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t p = t * kSynTile + tid;
-        const bool valid = p < np;
-        float zv[kLZ];
-#pragma unroll
-        for (int k = 0; k < kLZ; ++k) zv[k] = (valid && k < L) ? P.z[int64_t(k) * np + p] : 0.0f;
-        float dt[3], dx[3];
-#pragma unroll
-        for (int co = 0; co < 3; ++co) {
-            dt[co] = valid ? dt_in[int64_t(co) * np + p] : 0.0f;
-            dx[co] = valid ? P.syn_dx[int64_t(co) * np + p] : 0.0f;
-        }
-        float* myZ = sm.act + K::O_Z + tid * K::LZ;
-        float* myH = sm.act + K::O_H + tid * K::LH;
-        float* myDH = sm.act + K::O_DH + tid * K::LDH;
-        float* myDT = sm.act + K::O_DT + tid * K::LT;
-        float* myDX = sm.act + K::O_DX + tid * K::LT;
-        // dz accumulates the stabilizer term first, then c1 (synthesis.hpp:220,232)
-        float dz[kLZ];
-#pragma unroll
-        for (int k = 0; k < kLZ; ++k) {
-            float a = 0.0f;
-            a = fmaf(sm.st[k], dx[0], a);
-            a = fmaf(sm.st[kLZ + k], dx[1], a);
-            a = fmaf(sm.st[2 * kLZ + k], dx[2], a);
-            dz[k] = P.off_sstab >= 0 ? a : 0.0f;
-        }
-#pragma unroll 2
-        for (int f0 = 0; f0 < FP; f0 += 4) {
-            float hv[4], dv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int f = f0 + q;
-                const float4 wa = *reinterpret_cast<const float4*>(&sm.c1w[f * kLZ]);
-                const float4 wb = *reinterpret_cast<const float4*>(&sm.c1w[f * kLZ + 4]);
-                float acc = sm.c1b[f];
-                acc = fmaf(zv[0], wa.x, acc);
-                acc = fmaf(zv[1], wa.y, acc);
-                acc = fmaf(zv[2], wa.z, acc);
-                acc = fmaf(zv[3], wa.w, acc);
-                acc = fmaf(zv[4], wb.x, acc);
-                acc = fmaf(zv[5], wb.y, acc);
-                acc = fmaf(zv[6], wb.z, acc);
-                acc = fmaf(zv[7], wb.w, acc);
-                const float h = acc > 0.0f ? acc : 0.0f;
-                float d = 0.0f;
-                d = fmaf(sm.c2w[f], dt[0], d);
-                d = fmaf(sm.c2w[FP + f], dt[1], d);
-                d = fmaf(sm.c2w[2 * FP + f], dt[2], d);
-                d = h > 0.0f ? d : 0.0f;
-                dz[0] = fmaf(wa.x, d, dz[0]);
-                dz[1] = fmaf(wa.y, d, dz[1]);
-                dz[2] = fmaf(wa.z, d, dz[2]);
-                dz[3] = fmaf(wa.w, d, dz[3]);
-                dz[4] = fmaf(wb.x, d, dz[4]);
-                dz[5] = fmaf(wb.y, d, dz[5]);
-                dz[6] = fmaf(wb.z, d, dz[6]);
-                dz[7] = fmaf(wb.w, d, dz[7]);
-                hv[q] = valid ? h : 0.0f;
-                dv[q] = valid ? d : 0.0f;
-            }
-            *reinterpret_cast<float4*>(myH + f0) = make_float4(hv[0], hv[1], hv[2], hv[3]);
-            *reinterpret_cast<float4*>(myDH + f0) = make_float4(dv[0], dv[1], dv[2], dv[3]);
-        }
-        if (valid) {
-#pragma unroll
-            for (int k = 0; k < kLZ; ++k)
-                if (k < L) P.dz[int64_t(k) * np + p] = dz[k];
-        }
-        *reinterpret_cast<float4*>(myZ) = make_float4(zv[0], zv[1], zv[2], zv[3]);
-        *reinterpret_cast<float4*>(myZ + 4) = make_float4(zv[4], zv[5], zv[6], zv[7]);
-        *reinterpret_cast<float4*>(myZ + 8) = make_float4(valid ? 1.0f : 0.0f, 0.f, 0.f, 0.f);
-        for (int k = 12; k < K::LZ; ++k) myZ[k] = 0.0f;
-        for (int f = FP; f < K::LH; ++f) myH[f] = (f == FP && valid) ? 1.0f : 0.0f;
-        for (int f = FP; f < K::LDH; ++f) myDH[f] = 0.0f;
-        *reinterpret_cast<float4*>(myDT) = make_float4(dt[0], dt[1], dt[2], 0.0f);
-        *reinterpret_cast<float4*>(myDX) = make_float4(dx[0], dx[1], dx[2], 0.0f);
-        __syncthreads();
-        for (int job = tid; job < K::NJ; job += kSynTile) {
-            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-            int a0, b0, kind;
-            if (job < K::NJ1) {
-                constexpr int nq = r4(kLZ + 1) / 4;
-                a0 = 2 * (job / nq);
-                b0 = 4 * (job % nq);
-                kind = 0;
-                syn_mt<K::LDH, K::LZ>(sm.act + K::O_DH, sm.act + K::O_Z, a0, b0, acc);
-            } else if (job < K::NJ1 + K::NJ2) {
-                constexpr int nq = r4(FP + 1) / 4;
-                const int jj = job - K::NJ1;
-                a0 = 2 * (jj / nq);
-                b0 = 4 * (jj % nq);
-                kind = 1;
-                syn_mt<K::LT, K::LH>(sm.act + K::O_DT, sm.act + K::O_H, a0, b0, acc);
-            } else {
-                constexpr int nq = kLZ / 4;
-                const int jj = job - K::NJ1 - K::NJ2;
-                a0 = 2 * (jj / nq);
-                b0 = 4 * (jj % nq);
-                kind = 2;
-                syn_mt<K::LT, K::LZ>(sm.act + K::O_DX, sm.act + K::O_Z, a0, b0, acc);
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int a = a0 + (e >> 2), b = b0 + (e & 3);
-                int o = -1;
-                if (kind == 0) {
-                    if (b < kLZ) o = a * kLZ + b;
-                    else if (b == kLZ) o = FP * kLZ + a;
-                } else if (kind == 1) {
-                    if (a < 3) {
-                        if (b < FP) o = FP * kLZ + FP + a * FP + b;
-                        else if (b == FP) o = FP * kLZ + FP + 3 * FP + a;
-                    }
-                } else {
-                    if (a < 3 && b < kLZ) o = FP * kLZ + FP + 3 * FP + 3 + a * kLZ + b;
-                }
-                if (o >= 0) sm.acc[o] += double(acc[e]);
-            }
-        }
-        __syncthreads();
-    }
-    // scatter the padded accumulators into this CTA's partial row
-    const PartialRegion& R = P.region[P.reg_syn_trunk];
-    double* row = P.partials + R.base + int64_t(blockIdx.x) * R.count;
-    for (int e = tid; e < R.count; e += kSynTile) {
-        const int pidx = R.param_off + e;
-        double v = 0.0;
-        if (pidx >= P.off_c1w && pidx < P.off_c1w + F * L) {
-            const int q = pidx - P.off_c1w, f = q / L, k = q - f * L;
-            v = sm.acc[f * kLZ + k];
-        } else if (pidx >= P.off_c1b && pidx < P.off_c1b + F) {
-            v = sm.acc[FP * kLZ + (pidx - P.off_c1b)];
-        } else if (pidx >= P.off_c2w && pidx < P.off_c2w + 3 * F) {
-            const int q = pidx - P.off_c2w, co = q / F, f = q - co * F;
-            v = sm.acc[FP * kLZ + FP + co * FP + f];
-        } else if (pidx >= P.off_c2b && pidx < P.off_c2b + 3) {
-            v = sm.acc[FP * kLZ + FP + 3 * FP + (pidx - P.off_c2b)];
-        } else if (P.off_sstab >= 0 && pidx >= P.off_sstab && pidx < P.off_sstab + 3 * L) {
-            const int q = pidx - P.off_sstab, co = q / L, k = q - co * L;
-            v = sm.acc[FP * kLZ + FP + 3 * FP + 3 + co * kLZ + k];
-        }
-        row[e] = v;
-    }
-}
-
-template <int FP>
-size_t trunk_smem() {
-    return sizeof(TrunkSmem<FP>);
-}
-
-template <int FP>
-void launch_trunk_bwd_t(const LaunchCtx& L, const float* dt) {
-    k_syn_trunk_bwd<FP><<<L.syn_blocks, kSynTile, trunk_smem<FP>(), L.stream>>>(L.plan, dt);
-}
-
 }  // namespace
-
-int syn_padded_hidden(int F) {
-    if (F <= 8) return 8;
-    if (F <= 16) return 16;
-    if (F <= 48) return 48;
-    if (F <= 64) return 64;
-    return -1;
-}
-
-size_t syn_trunk_smem(int FP) {
-    switch (FP) {
-        case 8: return trunk_smem<8>();
-        case 16: return trunk_smem<16>();
-        case 48: return trunk_smem<48>();
-        default: return trunk_smem<64>();
-    }
-}
-
-void syn_configure(int FP) {
-    const int smem = int(syn_trunk_smem(FP));
-    switch (FP) {
-        case 8: cudaFuncSetAttribute(k_syn_trunk_bwd<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-        case 16: cudaFuncSetAttribute(k_syn_trunk_bwd<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-        case 48: cudaFuncSetAttribute(k_syn_trunk_bwd<48>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-        default: cudaFuncSetAttribute(k_syn_trunk_bwd<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); break;
-    }
-}
 
 void syn_post_configure() {
     cudaFuncSetAttribute(k_syn_post<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(PostSmem<0>)));
@@ -640,18 +377,6 @@ void launch_syn_forward(const LaunchCtx& L, bool backward) {
         case 0: k_syn_post<0><<<g, 256, sizeof(PostSmem<0>), L.stream>>>(L.plan, wg); break;
         case 1: k_syn_post<1><<<g, 256, sizeof(PostSmem<1>), L.stream>>>(L.plan, wg); break;
         default: k_syn_post<2><<<g, 256, sizeof(PostSmem<2>), L.stream>>>(L.plan, wg); break;
-    }
-}
-
-void launch_syn_backward(const LaunchCtx& L) {
-    const Plan& H = *L.host;
-    const float* dt = H.syn_dt;
-    const int FP = syn_padded_hidden(H.syn_F);
-    switch (FP) {
-        case 8: launch_trunk_bwd_t<8>(L, dt); break;
-        case 16: launch_trunk_bwd_t<16>(L, dt); break;
-        case 48: launch_trunk_bwd_t<48>(L, dt); break;
-        default: launch_trunk_bwd_t<64>(L, dt); break;
     }
 }
 

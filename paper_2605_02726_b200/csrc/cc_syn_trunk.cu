@@ -1,0 +1,315 @@
+// cc_syn_trunk.cu — synthesis trunk backward (conv1x1 c1 -> ReLU -> conv1x1
+// c2, plus the linear stabilizer): synthesize_backward's trunk part
+// (synthesis.hpp:216-233; conv1x1_backward layers.hpp:216-250).
+//
+// Per tile of 128 pixels, 256 threads (persistent CTAs, 2 per SM):
+//   phase A  two threads per pixel, each owning half of the F hidden units:
+//            recompute pre-activations (bias, then z in channel order),
+//            h1 = relu, dh1 = (c2ᵀ·dt) ⊙ relu'(h1), and dz = stabᵀ·dx̂ + c1ᵀ·dh1
+//            with FFMA2 (pairs of hidden units / pairs of z channels); h1,
+//            dh1, z, dt, dx̂ are written FEATURE-MAJOR to shared memory;
+//   phase B  the weight gradients [dh1 | dt | dx̂] x [z|1, h1|1, z] as 4x4
+//            register micro-tiles over the pixel axis, each job split in
+//            NPART pixel ranges so that every thread owns ~one unit; the
+//            accumulators stay in registers across all tiles of the CTA and
+//            are summed (ranges in fixed order, fp64) once at the end.
+// Deterministic: fixed thread->work mapping, no atomics.
+#include <cuda_runtime.h>
+
+#include "cc_kernels.h"
+#include "cc_math.cuh"
+#include "cc_tile.cuh"
+
+namespace ccb {
+
+namespace {
+
+constexpr int T = kSynTile;   // pixels per tile (128)
+constexpr int NT = 2 * T;     // threads per CTA
+constexpr int LT = T + 4;     // feature-major row stride (floats)
+constexpr int kLZ = kMaxLevels;
+
+template <int FP>
+struct TB {
+    static_assert(T == 128 && FP % 4 == 0, "tile mapping");
+    static constexpr int FH = FP / 2;  // hidden units per phase-A thread
+    static constexpr int RZ = 12;      // z 0..7, ones at 8
+    static constexpr int RH = FP + 4;  // h1, ones at FP
+    static constexpr int O_Z = 0;
+    static constexpr int O_H = O_Z + RZ * LT;
+    static constexpr int O_DH = O_H + RH * LT;
+    static constexpr int O_DT = O_DH + FP * LT;
+    static constexpr int O_DX = O_DT + 4 * LT;
+    static constexpr int O_DZ = O_DX + 4 * LT;   // second half's partial dz
+    static constexpr int ACT = O_DZ + kLZ * LT;
+    static constexpr int J1 = (FP / 4) * 3;      // dh1 x [z|1]
+    static constexpr int J2 = FP / 4 + 1;        // dt x [h1|1]
+    static constexpr int J3 = 2;                 // dx̂ x z (stabilizer)
+    static constexpr int NJ = J1 + J2 + J3;
+    static constexpr int NPART = NT / NJ > 8 ? 8 : (NT / NJ < 1 ? 1 : NT / NJ);
+    static constexpr int PS = 4 * ((T / 4 + NPART - 1) / NPART);  // pixels per range
+    static constexpr int NU = NJ * NPART;
+    static constexpr int MAXU = (NU + NT - 1) / NT;
+    static_assert(NU * 16 <= ACT, "epilogue staging fits");
+};
+
+template <int FP>
+struct alignas(16) TBSmem {
+    using K = TB<FP>;
+    alignas(16) float W1T[kLZ][FP];  // c1.w as [k][f]: pre-activation pairs (f, f+1)
+    alignas(16) float W1[FP][kLZ];   // c1.w as [f][k]: dz pairs (k, k+1)
+    alignas(16) float c1b[FP];
+    alignas(16) float c2w[3][FP];
+    alignas(16) float st[3][kLZ];
+    alignas(16) float act[K::ACT];
+};
+
+template <int FP>
+__global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict__ pp,
+                                                          const float* __restrict__ dt_in) {
+    using K = TB<FP>;
+    const Plan& P = *pp;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    TBSmem<FP>& sm = *reinterpret_cast<TBSmem<FP>*>(smem_raw);
+    const int tid = threadIdx.x;
+    const int px = tid & (T - 1), half = tid >> 7;
+    const int L = P.L, F = P.syn_F;
+    const bool has_stab = P.off_sstab >= 0;
+    for (int e = tid; e < FP * kLZ; e += NT) {
+        const int f = e / kLZ, k = e - f * kLZ;
+        const float w = (f < F && k < L) ? P.params[P.off_c1w + f * L + k] : 0.0f;
+        sm.W1[f][k] = w;
+        sm.W1T[k][f] = w;
+    }
+    for (int e = tid; e < FP; e += NT) sm.c1b[e] = e < F ? P.params[P.off_c1b + e] : 0.0f;
+    for (int e = tid; e < 3 * FP; e += NT) {
+        const int co = e / FP, f = e - co * FP;
+        sm.c2w[co][f] = f < F ? P.params[P.off_c2w + co * F + f] : 0.0f;
+    }
+    for (int e = tid; e < 3 * kLZ; e += NT) {
+        const int co = e / kLZ, k = e - co * kLZ;
+        sm.st[co][k] = (has_stab && k < L) ? P.params[P.off_sstab + co * L + k] : 0.0f;
+    }
+    for (int e = tid; e < K::ACT; e += NT) sm.act[e] = 0.0f;
+    __syncthreads();
+
+    float* const sZ = sm.act + K::O_Z;
+    float* const sH = sm.act + K::O_H;
+    float* const sDH = sm.act + K::O_DH;
+    float* const sDT = sm.act + K::O_DT;
+    float* const sDX = sm.act + K::O_DX;
+    float* const sDZ = sm.act + K::O_DZ;
+
+    float uacc[K::MAXU][16];
+#pragma unroll
+    for (int m = 0; m < K::MAXU; ++m)
+#pragma unroll
+        for (int e = 0; e < 16; ++e) uacc[m][e] = 0.0f;
+
+    const int64_t np = P.npix;
+    const int64_t ntiles = (np + T - 1) / T;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t p = t * T + px;
+        const bool valid = p < np;
+        // ---- phase A ----
+        float z[kLZ];
+#pragma unroll
+        for (int k = 0; k < kLZ; ++k) z[k] = (valid && k < L) ? __ldg(P.z + int64_t(k) * np + p) : 0.0f;
+        float dt[3], dx[3];
+#pragma unroll
+        for (int co = 0; co < 3; ++co) {
+            dt[co] = valid ? __ldg(dt_in + int64_t(co) * np + p) : 0.0f;
+            dx[co] = valid ? __ldg(P.syn_dx + int64_t(co) * np + p) : 0.0f;
+        }
+        // dz starts with the stabilizer term (synthesis.hpp:220), then c1 (:232)
+        float2 dzp[kLZ / 2];
+#pragma unroll
+        for (int kp = 0; kp < kLZ / 2; ++kp) {
+            float2 a = make_float2(0.0f, 0.0f);
+            if (half == 0 && has_stab) {
+                a.x = fmaf(sm.st[0][2 * kp], dx[0], 0.0f);
+                a.x = fmaf(sm.st[1][2 * kp], dx[1], a.x);
+                a.x = fmaf(sm.st[2][2 * kp], dx[2], a.x);
+                a.y = fmaf(sm.st[0][2 * kp + 1], dx[0], 0.0f);
+                a.y = fmaf(sm.st[1][2 * kp + 1], dx[1], a.y);
+                a.y = fmaf(sm.st[2][2 * kp + 1], dx[2], a.y);
+            }
+            dzp[kp] = a;
+        }
+        const int f0 = half * K::FH;
+#pragma unroll 4
+        for (int fp = 0; fp < K::FH / 2; ++fp) {
+            const int f = f0 + 2 * fp;
+            float2 acc = *reinterpret_cast<const float2*>(&sm.c1b[f]);
+#pragma unroll
+            for (int k = 0; k < kLZ; ++k)
+                acc = ffma2(*reinterpret_cast<const float2*>(&sm.W1T[k][f]), z[k], acc);
+            const float2 h = make_float2(acc.x > 0.0f ? acc.x : 0.0f, acc.y > 0.0f ? acc.y : 0.0f);
+            float2 d = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int co = 0; co < 3; ++co) d = ffma2(*reinterpret_cast<const float2*>(&sm.c2w[co][f]), dt[co], d);
+            d.x = h.x > 0.0f ? d.x : 0.0f;
+            d.y = h.y > 0.0f ? d.y : 0.0f;
+#pragma unroll
+            for (int kp = 0; kp < kLZ / 2; ++kp)
+                dzp[kp] = ffma2(*reinterpret_cast<const float2*>(&sm.W1[f][2 * kp]), d.x, dzp[kp]);
+#pragma unroll
+            for (int kp = 0; kp < kLZ / 2; ++kp)
+                dzp[kp] = ffma2(*reinterpret_cast<const float2*>(&sm.W1[f + 1][2 * kp]), d.y, dzp[kp]);
+            sH[f * LT + px] = valid ? h.x : 0.0f;
+            sH[(f + 1) * LT + px] = valid ? h.y : 0.0f;
+            sDH[f * LT + px] = d.x;
+            sDH[(f + 1) * LT + px] = d.y;
+        }
+        if (half == 0) {
+#pragma unroll
+            for (int k = 0; k < kLZ; ++k) sZ[k * LT + px] = z[k];
+            sZ[kLZ * LT + px] = valid ? 1.0f : 0.0f;
+        } else {
+#pragma unroll
+            for (int co = 0; co < 3; ++co) {
+                sDT[co * LT + px] = dt[co];
+                sDX[co * LT + px] = dx[co];
+            }
+            sH[FP * LT + px] = valid ? 1.0f : 0.0f;
+#pragma unroll
+            for (int kp = 0; kp < kLZ / 2; ++kp) {
+                sDZ[(2 * kp) * LT + px] = dzp[kp].x;
+                sDZ[(2 * kp + 1) * LT + px] = dzp[kp].y;
+            }
+        }
+        __syncthreads();
+        if (half == 0 && valid) {
+#pragma unroll
+            for (int kp = 0; kp < kLZ / 2; ++kp) {
+                if (2 * kp < L) P.dz[int64_t(2 * kp) * np + p] = dzp[kp].x + sDZ[(2 * kp) * LT + px];
+                if (2 * kp + 1 < L) P.dz[int64_t(2 * kp + 1) * np + p] = dzp[kp].y + sDZ[(2 * kp + 1) * LT + px];
+            }
+        }
+        // ---- phase B: weight gradients ----
+#pragma unroll
+        for (int m = 0; m < K::MAXU; ++m) {
+            const int u = tid + m * NT;
+            if (u < K::NU) {
+                const int j = u / K::NPART, s = u - j * K::NPART;
+                const int i0 = s * K::PS, i1 = min(i0 + K::PS, T);
+                const float* A;
+                const float* B;
+                if (j < K::J1) {
+                    A = sDH + 4 * (j / 3) * LT;
+                    B = sZ + 4 * (j % 3) * LT;
+                } else if (j < K::J1 + K::J2) {
+                    A = sDT;
+                    B = sH + 4 * (j - K::J1) * LT;
+                } else {
+                    A = sDX;
+                    B = sZ + 4 * (j - K::J1 - K::J2) * LT;
+                }
+                if (i0 < i1) dw_tile4x4<LT>(A, B, i0, i1, uacc[m]);
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- epilogue: stage the units, sum ranges in order, one row per CTA ----
+    float* stage = sm.act;
+#pragma unroll
+    for (int m = 0; m < K::MAXU; ++m) {
+        const int u = tid + m * NT;
+        if (u < K::NU)
+#pragma unroll
+            for (int e = 0; e < 16; ++e) stage[u * 16 + e] = uacc[m][e];
+    }
+    __syncthreads();
+    const PartialRegion& R = P.region[P.reg_syn_trunk];
+    double* row = P.partials + R.base + int64_t(blockIdx.x) * R.count;
+    for (int e = tid; e < R.count; e += NT) {
+        const int pidx = R.param_off + e;
+        int job = -1, q = 0;
+        if (pidx >= P.off_c1w && pidx < P.off_c1w + F * L) {
+            const int r = pidx - P.off_c1w, f = r / L, k = r - f * L;
+            job = (f / 4) * 3 + k / 4;
+            q = (f % 4) * 4 + k % 4;
+        } else if (pidx >= P.off_c1b && pidx < P.off_c1b + F) {
+            const int f = pidx - P.off_c1b;
+            job = (f / 4) * 3 + 2;
+            q = (f % 4) * 4;
+        } else if (pidx >= P.off_c2w && pidx < P.off_c2w + 3 * F) {
+            const int r = pidx - P.off_c2w, co = r / F, f = r - co * F;
+            job = K::J1 + f / 4;
+            q = co * 4 + f % 4;
+        } else if (pidx >= P.off_c2b && pidx < P.off_c2b + 3) {
+            job = K::J1 + FP / 4;
+            q = (pidx - P.off_c2b) * 4;
+        } else if (has_stab && pidx >= P.off_sstab && pidx < P.off_sstab + 3 * L) {
+            const int r = pidx - P.off_sstab, co = r / L, k = r - co * L;
+            job = K::J1 + K::J2 + k / 4;
+            q = co * 4 + k % 4;
+        }
+        double v = 0.0;
+        if (job >= 0)
+            for (int s = 0; s < K::NPART; ++s) v += double(stage[(job * K::NPART + s) * 16 + q]);
+        row[e] = v;
+    }
+}
+
+template <int FP>
+size_t tb_smem() {
+    return sizeof(TBSmem<FP>);
+}
+
+template <int FP>
+void launch_t(const LaunchCtx& L, const float* dt) {
+    k_syn_trunk_bwd2<FP><<<L.syn_blocks, NT, tb_smem<FP>(), L.stream>>>(L.plan, dt);
+}
+
+template <int FP>
+void configure_t() {
+    cudaFuncSetAttribute(k_syn_trunk_bwd2<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tb_smem<FP>()));
+}
+
+}  // namespace
+
+int syn_padded_hidden(int F) {
+    if (F <= 8) return 8;
+    if (F <= 16) return 16;
+    if (F <= 48) return 48;
+    if (F <= 64) return 64;
+    return -1;
+}
+
+size_t syn_trunk_smem(int FP) {
+    switch (FP) {
+        case 8: return tb_smem<8>();
+        case 16: return tb_smem<16>();
+        case 48: return tb_smem<48>();
+        default: return tb_smem<64>();
+    }
+}
+
+int syn_trunk_blocks_per_sm(int FP) {  // __launch_bounds__(256, 2)
+    const int b = int((227 * 1024) / (syn_trunk_smem(FP) + 1024));
+    return b < 1 ? 1 : (b > 2 ? 2 : b);
+}
+
+void syn_configure(int FP) {
+    switch (FP) {
+        case 8: configure_t<8>(); break;
+        case 16: configure_t<16>(); break;
+        case 48: configure_t<48>(); break;
+        default: configure_t<64>(); break;
+    }
+}
+
+void launch_syn_backward(const LaunchCtx& L) {
+    const Plan& H = *L.host;
+    const float* dt = H.syn_dt;
+    switch (syn_padded_hidden(H.syn_F)) {
+        case 8: launch_t<8>(L, dt); break;
+        case 16: launch_t<16>(L, dt); break;
+        case 48: launch_t<48>(L, dt); break;
+        default: launch_t<64>(L, dt); break;
+    }
+}
+
+}  // namespace ccb
