@@ -41,7 +41,10 @@ struct TB {
     static constexpr int O_DT = O_DH + FP * LT;
     static constexpr int O_DX = O_DT + 4 * LT;
     static constexpr int O_DZ = O_DX + 4 * LT;   // second half's partial dz
-    static constexpr int ACT = O_DZ + kLZ * LT;
+    static constexpr int O_Z2 = O_DZ + kLZ * LT; // next tile's z / dt / dx̂ (cp.async)
+    static constexpr int O_DT2 = O_Z2 + RZ * LT;
+    static constexpr int O_DX2 = O_DT2 + 4 * LT;
+    static constexpr int ACT = O_DX2 + 4 * LT;
     static constexpr int J1 = (FP / 4) * 3;      // dh1 x [z|1]
     static constexpr int J2 = FP / 4 + 1;        // dt x [h1|1]
     static constexpr int J3 = 2;                 // dx̂ x z (stabilizer)
@@ -63,6 +66,54 @@ struct alignas(16) TBSmem {
     alignas(16) float st[3][kLZ];
     alignas(16) float act[K::ACT];
 };
+
+__device__ __forceinline__ void cp_async16_zfill(float* smem, const float* gmem, int bytes) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async4_zfill(float* smem, const float* gmem, bool full) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(full ? 4 : 0) : "memory");
+}
+
+// Asynchronous load of tile t's inputs into feature-major rows: z planes
+// 0..7 (zero past L), dt 0..2, dx̂ 0..2; zero past the last pixel.  16-byte
+// copies when every plane is 16-byte aligned (npix % 4 == 0).  Always commits
+// one cp.async group.
+__device__ __forceinline__ void issue_tile(const Plan& P, const float* __restrict__ dt_in, int64_t t,
+                                           float* bZ, float* bDT, float* bDX, int tid) {
+    const int64_t np = P.npix, p0 = t * T;
+    const bool vec = (np & 3) == 0;
+    for (int c = tid; c < 14 * (T / 4); c += NT) {
+        const int row = c / (T / 4), q = c % (T / 4);
+        const int64_t p = p0 + 4 * q;
+        const float* src;
+        float* dst;
+        bool ok;
+        if (row < kLZ) {
+            src = P.z + int64_t(row) * np + p;
+            dst = bZ + row * LT + 4 * q;
+            ok = row < P.L;
+        } else if (row < kLZ + 3) {
+            src = dt_in + int64_t(row - kLZ) * np + p;
+            dst = bDT + (row - kLZ) * LT + 4 * q;
+            ok = true;
+        } else {
+            src = P.syn_dx + int64_t(row - kLZ - 3) * np + p;
+            dst = bDX + (row - kLZ - 3) * LT + 4 * q;
+            ok = true;
+        }
+        const int64_t left = np - p;
+        const int n = ok ? (left >= 4 ? 4 : (left > 0 ? int(left) : 0)) : 0;
+        if (vec) {
+            cp_async16_zfill(dst, n > 0 ? src : P.z, 4 * n);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) cp_async4_zfill(dst + i, i < n ? src + i : P.z, i < n);
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
 
 template <int FP>
 __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict__ pp,
@@ -93,11 +144,14 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
     for (int e = tid; e < K::ACT; e += NT) sm.act[e] = 0.0f;
     __syncthreads();
 
-    float* const sZ = sm.act + K::O_Z;
+    float* sZ = sm.act + K::O_Z;
+    float* sDT = sm.act + K::O_DT;
+    float* sDX = sm.act + K::O_DX;
+    float* nZ = sm.act + K::O_Z2;
+    float* nDT = sm.act + K::O_DT2;
+    float* nDX = sm.act + K::O_DX2;
     float* const sH = sm.act + K::O_H;
     float* const sDH = sm.act + K::O_DH;
-    float* const sDT = sm.act + K::O_DT;
-    float* const sDX = sm.act + K::O_DX;
     float* const sDZ = sm.act + K::O_DZ;
 
     float uacc[K::MAXU][16];
@@ -108,18 +162,26 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
 
     const int64_t np = P.npix;
     const int64_t ntiles = (np + T - 1) / T;
+    if (blockIdx.x < ntiles) issue_tile(P, dt_in, blockIdx.x, sZ, sDT, sDX, tid);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int64_t p = t * T + px;
         const bool valid = p < np;
+        // the next tile's inputs land in the other buffers while this one computes
+        if (t + gridDim.x < ntiles)
+            issue_tile(P, dt_in, t + gridDim.x, nZ, nDT, nDX, tid);
+        else
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        __syncthreads();
         // ---- phase A ----
         float z[kLZ];
 #pragma unroll
-        for (int k = 0; k < kLZ; ++k) z[k] = (valid && k < L) ? __ldg(P.z + int64_t(k) * np + p) : 0.0f;
+        for (int k = 0; k < kLZ; ++k) z[k] = sZ[k * LT + px];
         float dt[3], dx[3];
 #pragma unroll
         for (int co = 0; co < 3; ++co) {
-            dt[co] = valid ? __ldg(dt_in + int64_t(co) * np + p) : 0.0f;
-            dx[co] = valid ? __ldg(P.syn_dx + int64_t(co) * np + p) : 0.0f;
+            dt[co] = sDT[co * LT + px];
+            dx[co] = sDX[co * LT + px];
         }
         // dz starts with the stabilizer term (synthesis.hpp:220), then c1 (:232)
         float2 dzp[kLZ / 2];
@@ -162,15 +224,8 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
             sDH[(f + 1) * LT + px] = d.y;
         }
         if (half == 0) {
-#pragma unroll
-            for (int k = 0; k < kLZ; ++k) sZ[k * LT + px] = z[k];
             sZ[kLZ * LT + px] = valid ? 1.0f : 0.0f;
         } else {
-#pragma unroll
-            for (int co = 0; co < 3; ++co) {
-                sDT[co * LT + px] = dt[co];
-                sDX[co * LT + px] = dx[co];
-            }
             sH[FP * LT + px] = valid ? 1.0f : 0.0f;
 #pragma unroll
             for (int kp = 0; kp < kLZ / 2; ++kp) {
@@ -209,7 +264,12 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
             }
         }
         __syncthreads();
+        float* x = sZ; sZ = nZ; nZ = x;
+        x = sDT; sDT = nDT; nDT = x;
+        x = sDX; sDX = nDX; nDX = x;
     }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
 
     // ---- epilogue: stage the units, sum ranges in order, one row per CTA ----
     float* stage = sm.act;
