@@ -56,6 +56,7 @@ size_t syn_trunk_smem(int FP);
 int syn_trunk_blocks_per_sm(int FP);
 void syn_configure(int FP);
 void syn_post_configure();
+void launch_syn_post(const LaunchCtx& L, bool backward);  // cc_syn_post.cu
 int syn_post_tiles(int H, int W);
 
 // optimizer / bookkeeping (cc_step.cu)
