@@ -192,6 +192,142 @@ struct BwdSmem {
     double tot[7];
 };
 
+// ---- interior fast path of the backward tile --------------------------
+// For tiles whose every window is in range (no replicate clamp, no crop, no
+// tconv index clamp) the stencils have fixed taps and fixed geometry, so each
+// phase is a flat loop over a compile-time window.  a = 2·U0, b = 2·V0.
+constexpr int FO = 2 * kBT;    // owned level-j span (32)
+constexpr int FDO = FO + 10;   // dOut window: a-5 .. a+36
+constexpr int FDC = FO + 8;    // dcol window: a-4 .. a+35
+constexpr int FX = kBT + 6;    // input window: U0-3 .. U0+18
+constexpr int FRC = FO + 4;    // rowtmp columns: b-2 .. b+33 (rows = input rows)
+constexpr int FC = FO + 2;     // coltmp window: a-1 .. a+32
+struct FastSmem {
+    float dout[FDO * FDO];
+    float dcol[FDC * FDC];
+    float x[FX * FX];
+    float r[FX * FRC];
+    float c[FC * FC];
+    float drow[kBT * FDC];
+};
+static_assert(sizeof(FastSmem) <= sizeof(BwdSmem) - sizeof(double) * 7 * (kThreadsWide / 32 + 1),
+              "fast-path windows overlay the generic ones");
+
+__device__ __forceinline__ bool bwd_interior(int U0, int V0, int ri, int ci, int ro, int co) {
+    return U0 >= kBT && V0 >= kBT && U0 + kBT + 2 <= ri - 1 && V0 + kBT + 2 <= ci - 1 &&
+           2 * U0 + FO + 4 <= ro - 1 && 2 * V0 + FO + 4 <= co - 1;
+}
+
+__device__ __forceinline__ void bwd_tile_fast(const float* __restrict__ in, int in_stride,
+                                              const float* __restrict__ dout, int co,
+                                              float* __restrict__ din, int ci, bool wd, int U0, int V0,
+                                              const float (&kk)[4], float kc, float ke, float ko,
+                                              FastSmem& f, double (&acc)[7]) {
+    const int a = 2 * U0, b = 2 * V0;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+    __syncthreads();
+    for (int i = ty; i < FDO; i += ny)
+    for (int j = tx; j < FDO; j += 32) {
+        const int e = i * FDO + j;
+        cp_async4(&f.dout[e], dout + int64_t(a - 5 + i) * co + (b - 5 + j));
+    }
+    for (int i = ty; i < FX; i += ny)
+    for (int j = tx; j < FX; j += 32) {
+        const int e = i * FX + j;
+        cp_async4(&f.x[e], in + int64_t(U0 - 3 + i) * in_stride + (V0 - 3 + j));
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // dcol = refineᵀ(dOut) (symmetric interior stencil), rowtmp recompute
+    for (int i = ty; i < FDC; i += ny)
+    for (int j = tx; j < FDC; j += 32) {
+        const int e = i * FDC + j;
+        const float* g = &f.dout[(i + 1) * FDO + (j + 1)];
+        f.dcol[e] = kc * g[0] + ke * (g[-FDO] + g[FDO] + g[-1] + g[1]) +
+                    ko * (g[-FDO - 1] + g[-FDO + 1] + g[FDO - 1] + g[FDO + 1]);
+    }
+    for (int i = ty; i < FX; i += ny)
+    for (int j = tx; j < FRC; j += 32) {
+        const int e = i * FRC + j;
+        const float* x = &f.x[i * FX + (j >> 1) + 2];
+        f.r[e] = (j & 1) == 0 ? kk[0] * x[-2] + kk[2] * x[-1] + kk[3] * x[0] + kk[1] * x[1]
+                              : kk[1] * x[-1] + kk[3] * x[0] + kk[2] * x[1] + kk[0] * x[2];
+    }
+    __syncthreads();
+    // coltmp recompute; drow = colᵀ(dcol) on the tile's input rows
+    for (int i = ty; i < FC; i += ny)
+    for (int j = tx; j < FC; j += 32) {
+        const int e = i * FC + j;
+        const int tr = i - 1;                 // output row a + tr
+        const int v = (tr >> 1) + 3;          // R row (local) of v = U0 + floor(tr/2)
+        const float* rr = &f.r[v * FRC + j + 1];
+        f.c[e] = (tr & 1) == 0 ? kk[0] * rr[-2 * FRC] + kk[2] * rr[-FRC] + kk[3] * rr[0] + kk[1] * rr[FRC]
+                               : kk[1] * rr[-FRC] + kk[3] * rr[0] + kk[2] * rr[FRC] + kk[0] * rr[2 * FRC];
+    }
+    for (int i = ty; i < kBT; i += ny)
+    for (int j = tx; j < FDC; j += 32) {
+        const int e = i * FDC + j;
+        const float* g = &f.dcol[(2 * i + 4) * FDC + j];
+        f.drow[e] = kk[0] * (g[4 * FDC] + g[-3 * FDC]) + kk[1] * (g[-2 * FDC] + g[3 * FDC]) +
+                    kk[2] * (g[2 * FDC] + g[-FDC]) + kk[3] * (g[0] + g[FDC]);
+    }
+    __syncthreads();
+    float fa[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    // din = rowᵀ(drow)
+    if (wd) {
+        for (int i = ty; i < kBT; i += ny)
+        for (int j = tx; j < kBT; j += 32) {
+            const float* g = &f.drow[i * FDC + 2 * j + 4];
+            din[int64_t(U0 + i) * ci + V0 + j] = kk[0] * (g[4] + g[-3]) + kk[1] * (g[-2] + g[3]) +
+                                                 kk[2] * (g[2] + g[-1]) + kk[3] * (g[0] + g[1]);
+        }
+    }
+    // refine taps over the owned outputs: dOut x coltmp neighbourhoods
+    for (int i = ty; i < FO; i += ny)
+    for (int j = tx; j < FO; j += 32) {
+        const float g = f.dout[(i + 5) * FDO + j + 5];
+        const float* x0 = &f.c[i * FC + j];
+        const float* x1 = x0 + FC;
+        const float* x2 = x1 + FC;
+        fa[4] = fmaf(g, x1[1], fa[4]);
+        fa[5] = fmaf(g, x0[1] + x2[1] + x1[0] + x1[2], fa[5]);
+        fa[6] = fmaf(g, x0[0] + x0[2] + x2[0] + x2[2], fa[6]);
+        // column pass: dcol x rowtmp (owned output (a+i, b+j))
+        const float gc = f.dcol[(i + 4) * FDC + j + 4];
+        const float* rr = &f.r[((i >> 1) + 3) * FRC + j + 2];
+        if ((i & 1) == 0) {
+            fa[0] = fmaf(gc, rr[-2 * FRC], fa[0]);
+            fa[2] = fmaf(gc, rr[-FRC], fa[2]);
+            fa[3] = fmaf(gc, rr[0], fa[3]);
+            fa[1] = fmaf(gc, rr[FRC], fa[1]);
+        } else {
+            fa[1] = fmaf(gc, rr[-FRC], fa[1]);
+            fa[3] = fmaf(gc, rr[0], fa[3]);
+            fa[2] = fmaf(gc, rr[FRC], fa[2]);
+            fa[0] = fmaf(gc, rr[2 * FRC], fa[0]);
+        }
+    }
+    // row pass: drow x input (input rows of the tile, owned output columns)
+    for (int i = ty; i < kBT; i += ny)
+    for (int j = tx; j < FO; j += 32) {
+        const float g = f.drow[i * FDC + j + 4];
+        const float* x = &f.x[(i + 3) * FX + (j >> 1) + 3];
+        if ((j & 1) == 0) {
+            fa[0] = fmaf(g, x[-2], fa[0]);
+            fa[2] = fmaf(g, x[-1], fa[2]);
+            fa[3] = fmaf(g, x[0], fa[3]);
+            fa[1] = fmaf(g, x[1], fa[1]);
+        } else {
+            fa[1] = fmaf(g, x[-1], fa[1]);
+            fa[3] = fmaf(g, x[0], fa[3]);
+            fa[2] = fmaf(g, x[1], fa[2]);
+            fa[0] = fmaf(g, x[2], fa[0]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 7; ++k) acc[k] += double(fa[k]);
+}
+
 __global__ void __launch_bounds__(kThreadsWide) k_ups_bwd(const Plan* __restrict__ pp, int j,
                                                       int write_lat) {
     const Plan& P = *pp;
@@ -212,6 +348,11 @@ __global__ void __launch_bounds__(kThreadsWide) k_ups_bwd(const Plan* __restrict
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // dk4[0..3] (rows+cols passes), dr3[0..2]
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int U0 = (tile / tiles_x) * kBT, V0 = (tile % tiles_x) * kBT;
+        if (bwd_interior(U0, V0, ri, ci, ro, co)) {
+            bwd_tile_fast(in, s.in_stride, dout, co, din, ci, wd, U0, V0, kk, kc, ke, ko,
+                          *reinterpret_cast<FastSmem*>(smem_raw), acc);
+            continue;
+        }
         const int U1 = min(U0 + kBT, ri) - 1, V1 = min(V0 + kBT, ci) - 1;  // inclusive
         // owned level-j positions: parents in the tile
         const Win own_r{2 * U0, min(2 * U1 + 1, ro - 1)};
