@@ -95,6 +95,45 @@ __global__ void __launch_bounds__(kThreadsWide) k_ups_fwd(const Plan* __restrict
     float* out = stage_out(P, s);
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int y0 = (tile / tiles_x) * kFT, x0 = (tile % tiles_x) * kFT;
+        if (y0 >= kFT && x0 >= kFT && y0 / 2 + 18 <= ri - 1 && x0 / 2 + 18 <= ci - 1 && y0 + kFT <= ro - 1 &&
+            x0 + kFT <= co - 1) {
+            // interior tile: fixed taps and geometry, 2D thread mapping
+            constexpr int XW = 22, RW = kFT + 2, CW = kFT + 2;
+            const int U = y0 / 2, V = x0 / 2;
+            const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+            const float kk[4] = {t0, t1, t2, t3};
+            __syncthreads();
+            for (int i = ty; i < XW; i += ny)
+                for (int j = tx; j < XW; j += 32)
+                    cp_async4(&s_in[i * XW + j], in + int64_t(U - 3 + i) * s.in_stride + (V - 3 + j));
+            cp_async_wait_all();
+            __syncthreads();
+            for (int i = ty; i < XW; i += ny)
+                for (int j = tx; j < RW; j += 32) {
+                    const float* x = &s_in[i * XW + ((j - 1) >> 1) + 3];
+                    s_row[i * RW + j] = ((j - 1) & 1) == 0
+                                            ? kk[0] * x[-2] + kk[2] * x[-1] + kk[3] * x[0] + kk[1] * x[1]
+                                            : kk[1] * x[-1] + kk[3] * x[0] + kk[2] * x[1] + kk[0] * x[2];
+                }
+            __syncthreads();
+            for (int i = ty; i < CW; i += ny)
+                for (int j = tx; j < CW; j += 32) {
+                    const float* rr = &s_row[(((i - 1) >> 1) + 3) * RW + j];
+                    s_col[i * CW + j] = ((i - 1) & 1) == 0
+                                            ? kk[0] * rr[-2 * RW] + kk[2] * rr[-RW] + kk[3] * rr[0] + kk[1] * rr[RW]
+                                            : kk[1] * rr[-RW] + kk[3] * rr[0] + kk[2] * rr[RW] + kk[0] * rr[2 * RW];
+                }
+            __syncthreads();
+            for (int i = ty; i < kFT; i += ny) {
+                const float* x0r = &s_col[i * CW + 1];
+                const float* x1r = x0r + CW;
+                const float* x2r = x1r + CW;
+                const int j = tx;
+                out[int64_t(y0 + i) * co + x0 + j] = kc * x1r[j] + ke * (x0r[j] + x2r[j] + x1r[j - 1] + x1r[j + 1]) +
+                                                     ko * (x0r[j - 1] + x0r[j + 1] + x2r[j - 1] + x2r[j + 1]);
+            }
+            continue;
+        }
         const Win cr{clampi(y0 - 1, 0, ro - 1), clampi(y0 + kFT, 0, ro - 1)};   // coltmp rows
         const Win cc{clampi(x0 - 1, 0, co - 1), clampi(x0 + kFT, 0, co - 1)};   // coltmp cols
         const Win rr = tconv_src(cr, ri - 1);                                  // rowtmp/input rows
