@@ -172,7 +172,7 @@ __global__ void k_adam_latents(const Plan* __restrict__ pp) {
             if (P.lat_ok[gi])
                 P.lat_t[gi] += 1;
             else
-                P.scal->skipped += 1;
+                atomicAdd(&P.scal->skipped, 1);  // k_nn_step counts concurrently
         }
     }
 }

@@ -531,9 +531,17 @@ void Trainer::enqueue_proxy(bool batched) {
     launch_ups_backward(L_, true);
     join();
     launch_finalize(L_, kArmProxy, -1);
+    // gradient assembly: the NN-gradient reduction runs beside the latent
+    // gather; the NN Adam step waits for the gather (it reads the IFCE
+    // weights) and runs beside the latent Adam step
+    fork();
+    launch_nn_reduce(side());
     launch_latent_grad(L_);
+    join();
+    fork();
+    launch_nn_apply(side(), true, true, batched ? d_rec_ : nullptr);
     launch_adam_latents(L_);
-    launch_nn_step(L_, true, true, batched ? d_rec_ : nullptr);
+    join();
 }
 
 // Trainer::hardround_iteration (encoder.hpp:141-155)

@@ -30,6 +30,14 @@ __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, i
     const double bits_all = block_sum(b_loc, red);
     const double se_all = block_sum(s_loc, red);
     for (int t = threadIdx.x; t < P.n_tensors; t += blockDim.x) P.tensor_ok[t] = 1;
+    if (mode == kArmProxy) {  // Adam bias corrections of every latent grid, one thread each
+        for (int g = threadIdx.x; g < P.n_grids; g += blockDim.x) {
+            const double t = double(P.lat_t[g] + 1);
+            bc_lat[2 * g] = 1.0 - pow(0.9, t);
+            bc_lat[2 * g + 1] = 1.0 - pow(0.999, t);
+            P.lat_ok[g] = 1;
+        }
+    }
     if (threadIdx.x != 0) return;
     const double bits = bits_all, se = se_all;
     const double mse = se / double(3 * P.npix);
@@ -39,14 +47,6 @@ __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, i
     s->mse = mse;
     s->cost = cost;
     s->cost_ok = isfinite(cost) ? 1 : 0;
-    if (mode == kArmProxy) {
-        for (int g = 0; g < P.n_grids; ++g) {
-            const double t = double(P.lat_t[g] + 1);
-            bc_lat[2 * g] = 1.0 - pow(0.9, t);
-            bc_lat[2 * g + 1] = 1.0 - pow(0.999, t);
-            P.lat_ok[g] = 1;
-        }
-    }
     s->snap_take = (snap_slot >= 0 && s->cost_ok && cost < s->snap_cost[snap_slot]) ? 1 : 0;
 }
 
@@ -150,13 +150,21 @@ void launch_finalize(const LaunchCtx& L, int mode, int snap_slot) {
     k_finalize<<<1, 256, 0, L.stream>>>(L.plan, mode, snap_slot);
 }
 
-void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log) {
+void launch_nn_reduce(const LaunchCtx& L) {
     const int warps = L.host->n_params;
     const int blocks = (warps + 7) / 8;
     k_nn_reduce<<<blocks, 256, 0, L.stream>>>(L.plan, L.host->tensor_ok);
+}
+
+void launch_nn_apply(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log) {
     k_nn_step<<<L.host->n_tensors, 256, 0, L.stream>>>(L.plan, do_step ? 1 : 0,
                                                        count_iter ? 1 : 0, cost_log,
                                                        L.host->tensor_ok);
+}
+
+void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log) {
+    launch_nn_reduce(L);
+    launch_nn_apply(L, do_step, count_iter, cost_log);
 }
 
 void launch_sched_load(const LaunchCtx& L, const double* sched) {
