@@ -12,21 +12,31 @@
 //   k_init_latents init_latents_uniform                      latent.hpp:73-80
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #include "cc_kernels.h"
 #include "cc_math.cuh"
 
 namespace ccb {
 
-__device__ __forceinline__ int find_grid(const Plan& P, int64_t i) {
+// Grid of flat latent index i: latent offsets cached in shared memory (unused
+// slots hold INT64_MAX), counted branch-free.
+#define CCB_GRID_CACHE(P)                                                                      \
+    __shared__ int64_t s_off[kMaxGrids];                                                       \
+    if (threadIdx.x < kMaxGrids)                                                               \
+        s_off[threadIdx.x] = int(threadIdx.x) < (P).n_grids ? (P).g[threadIdx.x].lat_off : INT64_MAX; \
+    __syncthreads()
+
+__device__ __forceinline__ int find_grid(const int64_t* s_off, int64_t i) {
     int gi = 0;
-#pragma unroll 1
-    for (int k = 1; k < P.n_grids; ++k)
-        if (i >= P.g[k].lat_off) gi = k;
+#pragma unroll
+    for (int k = 1; k < kMaxGrids; ++k) gi += i >= s_off[k] ? 1 : 0;
     return gi;
 }
 
 __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
     const Plan& P = *pp;
+    CCB_GRID_CACHE(P);
     const float temp = float(P.scal->temp);         // encoder.hpp:98
     const float noise_std = float(P.scal->noise);   // encoder.hpp:108
     const int64_t n = P.n_latents;
@@ -35,7 +45,7 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
     const float inv_t = 1.0f / temp;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
-        const int gi = find_grid(P, i);
+        const int gi = find_grid(s_off, i);
         const GridGeom& g = P.g[gi];
         const int64_t li = i - g.lat_off;
         const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
@@ -71,9 +81,10 @@ __global__ void k_quantize(const Plan* __restrict__ pp, int amp) {
 
 __global__ void k_pads_from_q(const Plan* __restrict__ pp) {
     const Plan& P = *pp;
+    CCB_GRID_CACHE(P);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
-        const int gi = find_grid(P, i);
+        const int gi = find_grid(s_off, i);
         const GridGeom& g = P.g[gi];
         const int64_t li = i - g.lat_off;
         const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
@@ -89,15 +100,18 @@ __global__ void k_pads_from_q(const Plan* __restrict__ pp) {
 // soft-quantize backward chain rule and the per-grid finiteness flag.
 __global__ void k_latent_grad(const Plan* __restrict__ pp) {
     const Plan& P = *pp;
+    CCB_GRID_CACHE(P);
     const float temp = float(P.scal->temp);
     const int cost_ok = P.scal->cost_ok;
     const float scale = 1.0f / (temp * softround_denom(temp));
     __shared__ int s_dy[kMaxCtx], s_dx[kMaxCtx];
+    __shared__ GridGeom s_geo[kMaxGrids];
     const int S = P.S;
     for (int o = threadIdx.x; o < kMaxCtx; o += blockDim.x) {
         s_dy[o] = P.ctx_dy[o];
         s_dx[o] = P.ctx_dx[o];
     }
+    for (int k = threadIdx.x; k < P.n_grids; k += blockDim.x) s_geo[k] = P.g[k];
     __syncthreads();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -105,22 +119,31 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp) {
             P.lat_g[i] = 0.0f;
             continue;
         }
-        const int gi = find_grid(P, i);
-        const GridGeom& g = P.g[gi];
+        const int gi = find_grid(s_off, i);
+        const GridGeom& g = s_geo[gi];
         const int64_t cnt = int64_t(g.rows) * g.cols;
         const int64_t li = i - g.lat_off;
         const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
         float acc = P.gown[i];
         const float* dc = P.dctx + g.dctx_off;
-        // causal successors' context gradients, fixed offset order
-#pragma unroll 4
-        for (int o = 0; o < S; ++o) {
-            const int rs = r - s_dy[o], cs = c - s_dx[o];
-            if (rs >= 0 && rs < g.rows && cs >= 0 && cs < g.cols)
-                acc += dc[int64_t(o) * cnt + int64_t(rs) * g.cols + cs];
+        // causal successors' context gradients, fixed offset order; the loads
+        // of a chunk of 8 offsets are all in flight before the ordered sum
+        for (int o0 = 0; o0 < S; o0 += 8) {
+            float v[8];
+            bool in[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int o = o0 + k;
+                const int rs = r - (o < S ? s_dy[o] : 0), cs = c - (o < S ? s_dx[o] : 0);
+                in[k] = o < S && rs >= 0 && rs < g.rows && cs >= 0 && cs < g.cols;
+                v[k] = in[k] ? __ldg(dc + int64_t(o) * cnt + int64_t(rs) * g.cols + cs) : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+                if (in[k]) acc += v[k];
         }
         for (int s = 0; s < P.n_slots; ++s) {
-            const GridGeom& e = P.g[P.slot_gi[s]];
+            const GridGeom& e = s_geo[P.slot_gi[s]];
             if (gi >= e.rdim) continue;
             const int sh = g.level - e.level;
             const float* pyr = P.dfeat + P.slot_pyr_off[s][sh];
@@ -150,6 +173,7 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp) {
 // advances the step counters (encoder.hpp:129-133).
 __global__ void k_adam_latents(const Plan* __restrict__ pp) {
     const Plan& P = *pp;
+    CCB_GRID_CACHE(P);
     const double lr = P.scal->lr;
     const double* __restrict__ bc = P.bc_lat;
     const int cost_ok = P.scal->cost_ok;
@@ -157,7 +181,7 @@ __global__ void k_adam_latents(const Plan* __restrict__ pp) {
     const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
-        const int gi = find_grid(P, i);
+        const int gi = find_grid(s_off, i);
         if (!P.lat_ok[gi]) continue;
         const double bc1 = bc[2 * gi], bc2 = bc[2 * gi + 1];
         const double gv = double(P.lat_g[i]);
@@ -179,9 +203,10 @@ __global__ void k_adam_latents(const Plan* __restrict__ pp) {
 
 __global__ void k_init_latents(const Plan* __restrict__ pp, uint64_t stream, float amp) {
     const Plan& P = *pp;
+    CCB_GRID_CACHE(P);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
-        const int gi = find_grid(P, i);
+        const int gi = find_grid(s_off, i);
         const uint64_t gs = hash_combine(stream, uint64_t(gi));
         P.y[i] = counter_uniform(gs, uint64_t(i - P.g[gi].lat_off), -amp, amp);
     }
