@@ -157,6 +157,20 @@ SIGNATURES = {
 }
 
 # include/coolchic_b200_diag.h (product library only)
+# include/coolchic_b200_band.h (product only): row-band decomposition (cfg5)
+BAND_SIGNATURES = {
+    "cc_band_window": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _I, _I]),
+    "cc_band_trainer_create": (C.c_int, [_F, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(EncoderConfigC), C.POINTER(DecoderConfigC),
+                                         C.c_int, C.POINTER(C.c_void_p)]),
+    "cc_band_grid_rows": (C.c_int, [_P, C.c_int, _I]),
+    "cc_band_rows": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _F, C.c_int]),
+    "cc_band_forward_backward": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, _D, _D]),
+    "cc_band_nn_partial": (C.c_int, [_P, _D]),
+    "cc_band_finish": (C.c_int, [_P, _D, C.c_double, C.c_double, _D, _I]),
+    "cc_band_step": (C.c_int, [_P, _I]),
+}
+
 DIAG_SIGNATURES = {
     "ccb_stage_name": (C.c_char_p, [C.c_int]),
     "ccb_profile_stages": (C.c_int, [_P, C.c_int, C.c_double, C.c_double, C.c_double, _D]),
@@ -183,6 +197,7 @@ def load_library(path: os.PathLike | str, diag: bool = False) -> C.CDLL:
     table = dict(SIGNATURES)
     if diag:
         table.update(DIAG_SIGNATURES)
+        table.update(BAND_SIGNATURES)
     for name, (res, args) in table.items():
         fn = getattr(lib, name)
         fn.restype = res

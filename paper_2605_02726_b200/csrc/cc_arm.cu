@@ -26,6 +26,7 @@
 // multiply-then-scatter (entropy_model.hpp:322-330).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "cc_kernels.h"
@@ -492,12 +493,15 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(const Plan* __restrict__ 
     float* a = pbuf;
     float* b = pbuf + B * B;
     {
+        // level 0 is dF in the grid's local rows; the pyramid's blocks are
+        // aligned to global rows (origin slot_pyr_a): local = aligned - off
         const int rows = P.slot_pyr_rows[s][0], cols = P.slot_pyr_cols[s][0];
+        const int off = P.g[P.slot_gi[s]].row0 - P.slot_pyr_a[s];
         const float* in = P.dfeat + P.slot_pyr_off[s][0] + int64_t(f) * rows * cols;
         for (int e = threadIdx.x; e < B * B; e += blockDim.x) {
             const int y = e >> smax, x = e & (B - 1);
-            const int gy = R * B + y, gx = Cc * B + x;
-            a[e] = (gy < rows && gx < cols) ? in[int64_t(gy) * cols + gx] : 0.0f;
+            const int gy = R * B + y - off, gx = Cc * B + x;
+            a[e] = (gy >= 0 && gy < rows && gx < cols) ? in[int64_t(gy) * cols + gx] : 0.0f;
         }
     }
     __syncthreads();
@@ -606,6 +610,8 @@ static bool use_arm2(int Dp, int Wp) {
     return !v1 && arm2_supported(Dp, Wp);
 }
 
+bool arm_uses_v2(int Dp, int Wp) { return use_arm2(Dp, Wp); }
+
 void arm_configure(int Dp, int Wp) {
     if (use_arm2(Dp, Wp)) arm2_configure(Dp, Wp);
     if (Dp == 8 && Wp == 8) configure_t<8, 8>();
@@ -670,7 +676,9 @@ void launch_pyramid(const LaunchCtx& L) {
     const Plan& H = *L.host;
     if (H.n_slots == 0 || H.F == 0) return;
     // every slot's deepest level is the coarsest grid: same coarse block count
-    const int nblk = H.slot_pyr_rows[0][H.slot_smax[0]] * H.slot_pyr_cols[0][H.slot_smax[0]];
+    int nblk = 0;
+    for (int s = 0; s < H.n_slots; ++s)
+        nblk = std::max(nblk, H.slot_pyr_rows[s][H.slot_smax[s]] * H.slot_pyr_cols[s][H.slot_smax[s]]);
     const dim3 grid(nblk, H.n_slots * H.F);
     k_pyramid_fused<<<grid, 256, pyramid_smem(H), L.stream>>>(L.plan);
 }

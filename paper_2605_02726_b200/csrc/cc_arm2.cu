@@ -162,10 +162,11 @@ __device__ __forceinline__ void issue_gather(const Plan& P, const GridGeom* geo,
         for (int j = 0; j < kRM; ++j) {
             const bool on = valid && j < rd;
             const float* src = P.yhat_pad;
-            if (on) {
+            if (on) {  // co-located coarser latent, in global rows (row bands)
                 const GridGeom& sg = geo[j];
                 const int sh = sg.level - g.level;
-                src = P.yhat_pad + sg.pad_base + int64_t(r >> sh) * sg.stride + (c >> sh);
+                const int rs = min(max(((g.row0 + r) >> sh) - sg.row0, 0), sg.rows - 1);
+                src = P.yhat_pad + sg.pad_base + int64_t(rs) * sg.stride + (c >> sh);
             }
             cp_async4_zfill(sRb + j * LT + lt, src, on);
         }
@@ -280,6 +281,8 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
         const int slot = g.ifce_slot;
         const int64_t li = int64_t(tile.y) + lt;
         const bool valid = li < count;
+        // rate terms only for owned rows (row bands; whole images own all rows)
+        const bool own = valid && li >= int64_t(g.own_lo) * g.cols && li < int64_t(g.own_hi) * g.cols;
 
         // ---- P0: prefetch the next tile (its buffers' last readers finished
         // at the previous tile's closing barrier), land the current one ----
@@ -376,10 +379,10 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
             const float e1 = cc_exp(-(u + 0.5f) / bsc);
             const float e2 = cc_exp(-fabsf(u - 0.5f) / bsc);
             const float p = u >= 0.5f ? 0.5f * (e2 - e1) : 1.0f - 0.5f * (e1 + e2);
-            if (valid) bits_thr += double(-(cc_log(std_max(p, kProbFloorF)) * kLog2EF));
+            if (own) bits_thr += double(-(cc_log(std_max(p, kProbFloorF)) * kLog2EF));
             if (MODE != kArmForward) {
                 float dmu = 0.0f, dsr = 0.0f, gv = 0.0f;
-                if (valid && p > kProbFloorF) {
+                if (own && p > kProbFloorF) {
                     const float tt = v - mu;
                     const float dbits_dp = -1.0f / (p * kLn2F);
                     const float dp_du = (e1 - e2) / (2.0f * bsc);

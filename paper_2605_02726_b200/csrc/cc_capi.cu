@@ -670,3 +670,87 @@ int cc_trainer_train(cc_trainer* t, cc_train_stats* stats, float* latents, int32
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- row bands
+#include "../../include/coolchic_b200_band.h"
+
+extern "C" {
+
+int cc_band_window(int h, int w, int r0, int r1, int halo, int* w0, int* w1) {
+    return guarded([&] {
+        Trainer::band_window(h, w, r0, r1, halo, w0, w1);
+        return CC_OK;
+    });
+}
+
+int cc_band_trainer_create(const float* image_window, int h, int w, int r0, int r1, int halo,
+                           const cc_encoder_config* enc, const cc_decoder_config* dec, int device,
+                           cc_trainer** out) {
+    return guarded([&] {
+        int w0 = 0, w1 = 0;
+        Trainer::band_window(h, w, r0, r1, halo, &w0, &w1);
+        auto t = std::make_unique<cc_trainer>();
+        t->h = w1 - w0;
+        t->w = w;
+        t->enc = *enc;
+        t->log_path = "";
+        t->enc.log_path = nullptr;
+        t->dec = *dec;
+        t->device = device;
+        t->image.assign(image_window, image_window + size_t(3) * size_t(w1 - w0) * size_t(w));
+        t->tr = std::make_unique<Trainer>(image_window, h, w, r0, r1, halo, t->enc, *dec, device);
+        *out = t.release();
+        return CC_OK;
+    });
+}
+
+int cc_band_grid_rows(cc_trainer* t, int gi, int* out4) {
+    return guarded([&] {
+        if (gi < 0 || gi >= t->tr->plan().n_grids) throw ccb::ConfigError("grid index out of range");
+        t->tr->band_grid_rows(gi, out4);
+        return CC_OK;
+    });
+}
+
+int cc_band_rows(cc_trainer* t, int which, int gi, int rb, int re, float* buf, int mode) {
+    return guarded([&] {
+        t->tr->band_rows(which, gi, rb, re, buf, mode);
+        return CC_OK;
+    });
+}
+
+int cc_band_forward_backward(cc_trainer* t, double lr, double temp, double noise_std, double* bits,
+                             double* sq_err) {
+    return guarded([&] {
+        double b = 0.0, s = 0.0;
+        t->tr->band_forward_backward(lr, temp, noise_std, &b, &s);
+        if (bits) *bits = b;
+        if (sq_err) *sq_err = s;
+        return CC_OK;
+    });
+}
+
+int cc_band_nn_partial(cc_trainer* t, double* out) {
+    return guarded([&] {
+        t->tr->band_nn_partial(out);
+        return CC_OK;
+    });
+}
+
+int cc_band_finish(cc_trainer* t, const double* nn_sums, double bits, double sq_err, double* cost,
+                   int* lat_ok_own) {
+    return guarded([&] {
+        const double c = t->tr->band_finish(nn_sums, bits, sq_err, lat_ok_own);
+        if (cost) *cost = c;
+        return CC_OK;
+    });
+}
+
+int cc_band_step(cc_trainer* t, const int* lat_ok) {
+    return guarded([&] {
+        t->tr->band_step(lat_ok);
+        return CC_OK;
+    });
+}
+
+}  // extern "C"

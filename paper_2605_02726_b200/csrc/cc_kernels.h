@@ -30,6 +30,8 @@ void launch_softq_fwd(const LaunchCtx& L);
 void launch_quantize(const LaunchCtx& L, int amp);
 void launch_pads_from_q(const LaunchCtx& L);
 void launch_latent_grad(const LaunchCtx& L);
+void launch_latent_grad_partial(const LaunchCtx& L);  // row bands: ignore the local cost flag
+void launch_band_own_finite(const LaunchCtx& L);
 void launch_adam_latents(const LaunchCtx& L);
 void launch_init_latents(const LaunchCtx& L, uint64_t stream, float amp);
 
@@ -40,6 +42,7 @@ void launch_arm(const LaunchCtx& L, int mode);
 void launch_pyramid(const LaunchCtx& L);
 int arm_blocks_per_sm(int Dp, int Wp);
 void arm_configure(int Dp, int Wp);
+bool arm_uses_v2(int Dp, int Wp);  // the register-tiled kernel (cc_arm2.cu) is selected
 void pyramid_configure(const Plan& H);
 
 // upsampling (cc_ups.cu)

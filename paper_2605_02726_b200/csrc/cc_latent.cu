@@ -56,7 +56,7 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
         float o = f + 0.5f + t1 * inv_denom;
         if (noise_std > 0.0f) {
             const uint64_t stream = hash_combine(hash_combine(P.seed, giter), uint64_t(gi));
-            o += noise_std * counter_gauss(stream, uint64_t(li));
+            o += noise_std * counter_gauss(stream, uint64_t(li + int64_t(g.row0) * g.cols));  // global raster index
         }
         f = floorf(o);
         d = o - f - 0.5f;
@@ -98,11 +98,11 @@ __global__ void k_pads_from_q(const Plan* __restrict__ pp) {
 // successors, the IFCE terms W_f^T * (block sum of dF) from every equipped
 // finer grid, and the upsampling gradient for main grids.  Then the
 // soft-quantize backward chain rule and the per-grid finiteness flag.
-__global__ void k_latent_grad(const Plan* __restrict__ pp) {
+__global__ void k_latent_grad(const Plan* __restrict__ pp, int force) {
     const Plan& P = *pp;
     CCB_GRID_CACHE(P);
     const float temp = float(P.scal->temp);
-    const int cost_ok = P.scal->cost_ok;
+    const int cost_ok = force || P.scal->cost_ok;  // bands: partial grads regardless
     const float scale = 1.0f / (temp * softround_denom(temp));
     __shared__ int s_dy[kMaxCtx], s_dx[kMaxCtx];
     __shared__ GridGeom s_geo[kMaxGrids];
@@ -149,13 +149,16 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp) {
             const float* pyr = P.dfeat + P.slot_pyr_off[s][sh];
             const int64_t pc = int64_t(P.slot_pyr_rows[s][sh]) * P.slot_pyr_cols[s][sh];
             const float* wf = P.params + P.off_ifw[s];
+            // pyramid rows are aligned to global rows from slot_pyr_a
+            const int R = g.row0 + r - (P.slot_pyr_a[s] >> sh);
+            if (R < 0 || R >= P.slot_pyr_rows[s][sh]) continue;
             float dr = 0.0f;
             for (int f = 0; f < P.F; ++f)
-                dr += wf[f * e.rdim + gi] * pyr[int64_t(f) * pc + int64_t(r) * g.cols + c];
+                dr += wf[f * e.rdim + gi] * pyr[int64_t(f) * pc + int64_t(R) * g.cols + c];
             acc += dr;
         }
         if (g.main_level == 0)
-            acc += P.dz[int64_t(r) * P.W + c];
+            acc += P.dz[P.zpix[0] + int64_t(r) * P.W + c];
         else if (g.main_level > 0)
             acc += P.dups[i];
         const float t2 = P.th2[i], t1 = P.th1[i];
@@ -208,7 +211,7 @@ __global__ void k_init_latents(const Plan* __restrict__ pp, uint64_t stream, flo
          i += int64_t(gridDim.x) * blockDim.x) {
         const int gi = find_grid(s_off, i);
         const uint64_t gs = hash_combine(stream, uint64_t(gi));
-        P.y[i] = counter_uniform(gs, uint64_t(i - P.g[gi].lat_off), -amp, amp);
+        P.y[i] = counter_uniform(gs, uint64_t(i - P.g[gi].lat_off + int64_t(P.g[gi].row0) * P.g[gi].cols), -amp, amp);
     }
 }
 
@@ -223,7 +226,32 @@ void launch_pads_from_q(const LaunchCtx& L) {
     k_pads_from_q<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
 }
 void launch_latent_grad(const LaunchCtx& L) {
-    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 0);
+}
+void launch_latent_grad_partial(const LaunchCtx& L) {
+    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 1);
+}
+
+// Row bands: per-grid finiteness of the OWN rows' (complete) latent gradients,
+// the per-tensor check of adam_step (optim.hpp:38-41) restricted to this band.
+__global__ void k_ok_reset(const Plan* __restrict__ pp) {
+    if (threadIdx.x < kMaxGrids) pp->lat_ok[threadIdx.x] = 1;
+}
+__global__ void k_band_own_finite(const Plan* __restrict__ pp) {
+    const Plan& P = *pp;
+    CCB_GRID_CACHE(P);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int gi = find_grid(s_off, i);
+        const GridGeom& g = P.g[gi];
+        const int64_t li = i - g.lat_off;
+        if (li < int64_t(g.own_lo) * g.cols || li >= int64_t(g.own_hi) * g.cols) continue;
+        if (!isfinite(P.lat_g[i])) atomicAnd(&P.lat_ok[gi], 0);
+    }
+}
+void launch_band_own_finite(const LaunchCtx& L) {
+    k_ok_reset<<<1, 32, 0, L.stream>>>(L.plan);
+    k_band_own_finite<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
 }
 void launch_adam_latents(const LaunchCtx& L) {
     k_adam_latents<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);

@@ -45,6 +45,10 @@ struct GridGeom {
     int64_t lat_off;     // offset inside the flat latent layout
     int64_t dctx_off;    // offset of this grid's S planes inside dctx
     int64_t dfeat_off;   // equipped grids: offset of dF level 0 inside dfeat
+    // row bands (cfg5): this grid holds global rows [row0, row0 + rows) of a
+    // grid with `grows` rows; local rows [own_lo, own_hi) are owned (rate terms,
+    // Adam); the rest is halo.  Whole-image runs: row0 = 0, own = all rows.
+    int row0, grows, own_lo, own_hi;
 };
 
 // One upsampling stage j for one main grid k (k > j).
@@ -82,6 +86,14 @@ struct Plan {
     int n_params, n_tensors;
     float rate_upstream;      // float(lambda / npix), encoder.hpp:64
     double lambda;
+    // row bands: pixel rows of the image held here are global rows
+    // [pix_row0, pix_row0 + H) of an image with npix_global pixels; rows
+    // [pix_own_lo, pix_own_hi) (local) are owned (MSE terms).
+    int band, pix_row0, pix_own_lo, pix_own_hi;
+    int64_t npix_global;
+    int64_t zpix[kMaxLevels];    // z / dz plane k: offset of local pixel (0,0)
+    int zvec;                    // npix and all zpix are multiples of 4 (16-byte loads)
+    int slot_pyr_a[kMaxSlots];   // global row of the dF pyramid origin (aligned)
     uint64_t seed;
 
     int ctx_dy[kMaxCtx], ctx_dx[kMaxCtx];
@@ -144,6 +156,7 @@ struct Plan {
     float* syn_dtmp;
     float* params;
     float* grads;
+    double* grads_d;          // the same gradients before rounding (band reduction)
     float* nn_m;
     float* nn_v;
     double* partials;

@@ -62,6 +62,24 @@ void context_offsets(int count, std::vector<int>& dy, std::vector<int>& dx, int&
 Trainer::Trainer(const float* image, int h, int w, const cc_encoder_config& enc,
                  const cc_decoder_config& dec, int device)
     : enc_(enc), dec_(dec), device_(device) {
+    init(image, h, w);
+}
+
+Trainer::Trainer(const float* image_window, int hg, int w, int r0, int r1, int halo,
+                 const cc_encoder_config& enc, const cc_decoder_config& dec, int device)
+    : enc_(enc), dec_(dec), device_(device) {
+    int w0 = 0, w1 = 0;
+    band_window(hg, w, r0, r1, halo, &w0, &w1);
+    band_.on = true;
+    band_.hg = hg;
+    band_.r0 = r0;
+    band_.r1 = r1;
+    band_.halo = halo;
+    init(image_window, w1 - w0, w);
+}
+
+void Trainer::init(const float* image, int h, int w) {
+    const cc_encoder_config& enc = enc_;
     if (h < 1 || w < 1) throw ConfigError("image dimensions must be positive");
     log_path_ = enc.log_path ? enc.log_path : "";
     enc_.log_path = nullptr;
@@ -119,10 +137,29 @@ void* Trainer::dalloc(size_t bytes) {
     return p;
 }
 
+// Row bands: own full-resolution rows [r0, r1) of an image
+// of hg rows; every grid holds its own rows plus `halo` rows on each side
+// (clipped at the image border).  band_window gives the pixel rows to upload.
+void Trainer::band_window(int hg, int w, int r0, int r1, int halo, int* w0, int* w1) {
+    const int L = int64_t(hg) * int64_t(w) < 1000000 ? 7 : 8;
+    const int align = 1 << (L - 1);
+    if (hg < 1 || w < 1 || r0 < 0 || r1 > hg || r0 >= r1)
+        throw ConfigError("band rows must satisfy 0 <= r0 < r1 <= H");
+    if (r0 % align != 0 || (r1 != hg && r1 % align != 0))
+        throw ConfigError("band edges must be multiples of 2^(L-1) (or the image height)");
+    // 6 rows per level keep every own row exact: the ARM context reaches 3 rows
+    // up, an upsampling cascade loses < 6 rows per level to the window edge
+    // and the synthesis posts reach 4 pixel rows
+    if (halo < 6) throw ConfigError("band halo must be >= 6 rows");
+    *w0 = std::max(0, r0 - halo);
+    *w1 = std::min(hg, r1 + halo);
+}
+
 void Trainer::build_plan() {
     Plan& P = H_;
     const int h = P.H, w = P.W;
-    P.L = int64_t(h) * int64_t(w) < 1000000 ? 7 : 8;  // latent_levels, config.hpp:271
+    const int hg = band_.on ? band_.hg : h;           // global image rows
+    P.L = int64_t(hg) * int64_t(w) < 1000000 ? 7 : 8;  // latent_levels, config.hpp:271
     P.hyper = dec_.use_hyperlatents ? P.L - 4 : 0;     // kHyperCoarsestLevel = 4
     P.S = dec_.spatial_ctx;
     P.F = dec_.ifce_dim;
@@ -139,12 +176,16 @@ void Trainer::build_plan() {
     if (P.D < 1) throw ConfigError("ARM input dimension must be positive");
     arm_padded_dims(P.D, P.Wd, &P.Dp, &P.Wp);
     if (P.Dp < 0) throw ConfigError("ARM dims (input <= 40, width <= 40) exceeded");
+    if (band_.on && !arm_uses_v2(P.Dp, P.Wp))
+        throw ConfigError("row bands need the register-tiled ARM kernel (ARM input/width <= 32/28)");
     if (syn_padded_hidden(P.syn_F) < 0) throw ConfigError("synth_hidden > 64 is not supported");
     if (P.posts < 0 || P.posts > 2) throw ConfigError("synth_posts must be 0, 1 or 2");
     P.npix = int64_t(h) * w;
+    P.npix_global = int64_t(hg) * w;
+    P.band = band_.on ? 1 : 0;
     P.lambda = enc_.lambda;
     P.seed = enc_.seed;
-    P.rate_upstream = float(enc_.lambda / double(P.npix));  // encoder.hpp:64
+    P.rate_upstream = float(enc_.lambda / double(P.npix_global));  // encoder.hpp:64
 
     std::vector<int> dy, dx;
     int cpad = 0;
@@ -170,8 +211,21 @@ void Trainer::build_plan() {
         GridGeom& g = P.g[gi];
         g.level = order[gi].level;
         g.hyper = order[gi].hyper;
-        g.rows = ceil_div(h, 1 << g.level);
+        g.grows = ceil_div(hg, 1 << g.level);
         g.cols = ceil_div(w, 1 << g.level);
+        {
+            int o0 = 0, o1 = g.grows, w0 = 0, w1 = g.grows;
+            if (band_.on) {
+                o0 = band_.r0 >> g.level;
+                o1 = band_.r1 == hg ? g.grows : band_.r1 >> g.level;
+                w0 = std::max(0, o0 - band_.halo);
+                w1 = std::min(g.grows, o1 + band_.halo);
+            }
+            g.row0 = w0;
+            g.rows = w1 - w0;
+            g.own_lo = o0 - w0;
+            g.own_hi = o1 - w0;
+        }
         g.stride = g.cols + 2 * P.P;
         g.pad_base = pad_cur + int64_t(P.P) * g.stride + P.P;
         pad_cur += int64_t(g.rows + 2 * P.P) * g.stride;
@@ -187,6 +241,13 @@ void Trainer::build_plan() {
         grids_.push_back({g.level, g.hyper, g.rows, g.cols, g.lat_off, -1});
     }
     P.n_latents = lat_cur;
+    {
+        const GridGeom& g0 = P.g[P.main_gi[0]];
+        if (g0.rows != h) throw ConfigError("internal: band pixel window does not match grid 0");
+        P.pix_row0 = g0.row0;
+        P.pix_own_lo = g0.own_lo;
+        P.pix_own_hi = g0.own_hi;
+    }
 
     // ---- IFCE slots (model.hpp:244-251): main levels 0..min(3,L)-1 ----
     P.n_slots = 0;
@@ -203,12 +264,13 @@ void Trainer::build_plan() {
             grids_[gi].ifce_slot = s;
             P.slot_gi[s] = gi;
             P.slot_smax[s] = (P.L - 1) - k;
-            int rr = g.rows, cc = g.cols;
+            // pyramid blocks are aligned to global rows: origin A (multiple of 2^smax)
+            const int A = (g.row0 >> P.slot_smax[s]) << P.slot_smax[s];
+            P.slot_pyr_a[s] = A;
+            int cc = g.cols;
             for (int l = 0; l <= P.slot_smax[s]; ++l) {
-                if (l > 0) {
-                    rr = ceil_div(rr, 2);
-                    cc = ceil_div(cc, 2);
-                }
+                if (l > 0) cc = ceil_div(cc, 2);
+                const int rr = l == 0 ? g.rows : ceil_div(g.row0 + g.rows - A, 1 << l);
                 P.slot_pyr_rows[s][l] = rr;
                 P.slot_pyr_cols[s][l] = cc;
                 P.slot_pyr_off[s][l] = df_cur;
@@ -259,17 +321,29 @@ void Trainer::build_plan() {
     }
 
     // ---- upsampling stages (synthesis.hpp:66-92) ----
+    // Cascade k runs on rows aligned to its latent window: level j holds
+    // global rows [row0_k << (k-j), end_j) (the image end at the bottom band),
+    // so every stage is a plain 2x upsampling of a sub-image; its level-0
+    // output (z plane k) is taller than the pixel window, which it contains.
     int64_t ub = 0;
     int64_t stage_out_off[kMaxLevels][kMaxLevels];  // [k][j]
+    int64_t zcur = int64_t(h) * w;                  // z plane 0 = grid 0 copy
+    P.zpix[0] = 0;
     for (int j = 0; j < kMaxLevels; ++j) P.ups_n[j] = 0;
     for (int k = 1; k < P.L; ++k) {
+        const GridGeom& gk = P.g[P.main_gi[k]];
+        const bool bottom = gk.row0 + gk.rows == gk.grows;
+        auto lvl_start = [&](int j) { return gk.row0 << (k - j); };
+        auto lvl_end = [&](int j) { return bottom ? ceil_div(hg, 1 << j) : (gk.row0 + gk.rows) << (k - j); };
         for (int j = k - 1; j >= 0; --j) {
             UpsStage& st = P.ups[j][P.ups_n[j]++];
             st.k = k;
-            st.rows_in = ceil_div(h, 1 << (j + 1));
+            st.rows_in = lvl_end(j + 1) - lvl_start(j + 1);
             st.cols_in = ceil_div(w, 1 << (j + 1));
-            st.rows_out = ceil_div(h, 1 << j);
+            st.rows_out = lvl_end(j) - lvl_start(j);
             st.cols_out = ceil_div(w, 1 << j);
+            if (st.rows_out > 2 * st.rows_in || st.rows_out < 1)
+                throw ConfigError("internal: inconsistent upsampling window");
             if (j == k - 1) {
                 const GridGeom& g = P.g[P.main_gi[k]];
                 st.in_is_pad = 1;
@@ -286,7 +360,12 @@ void Trainer::build_plan() {
             ub += int64_t(st.rows_out) * st.cols_out;
             if (j == 0) {
                 st.out_is_z = 1;
-                st.out_off = int64_t(k) * P.npix;
+                st.out_off = zcur;
+                const int zoff = P.pix_row0 - lvl_start(0);
+                if (zoff < 0 || zoff + h > st.rows_out)
+                    throw ConfigError("internal: z plane does not cover the pixel window");
+                P.zpix[k] = zcur + int64_t(zoff) * w;
+                zcur += int64_t(st.rows_out) * st.cols_out;
             } else {
                 st.out_is_z = 0;
                 st.out_off = ub;
@@ -303,6 +382,10 @@ void Trainer::build_plan() {
     // stage (k, j+1)'s output offset is known before stage (k, j) is built
     // because stages are created from j = k-1 downward.
     const int64_t ups_total = ub;
+    sizes_.z = zcur;
+    P.zvec = (P.npix % 4 == 0) ? 1 : 0;
+    for (int k = 0; k < P.L; ++k)
+        if (P.zpix[k] % 4 != 0) P.zvec = 0;
 
     // ---- launch geometry ----
     L_.num_sms = num_sms_;
@@ -384,8 +467,8 @@ void Trainer::allocate() {
     P.q = static_cast<int32_t*>(dalloc(sizeof(int32_t) * size_t(nl)));
     P.dctx = f32(std::max<int64_t>(sizes_.dctx, 1));
     P.dfeat = f32(sizes_.dfeat);
-    P.z = f32(int64_t(P.L) * np);
-    P.dz = f32(int64_t(P.L) * np);
+    P.z = f32(sizes_.z);
+    P.dz = f32(sizes_.z);  // rows outside the pixel window stay zero
     P.ups_buf = f32(sizes_.ups);
     P.ups_grad = f32(sizes_.ups);
     P.ups_grad2 = nullptr;
@@ -399,6 +482,7 @@ void Trainer::allocate() {
     P.syn_dtmp = f32(3 * np);
     P.params = f32(P.n_params);
     P.grads = f32(P.n_params);
+    P.grads_d = static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_params)));
     P.nn_m = f32(P.n_params);
     P.nn_v = f32(P.n_params);
     P.partials = static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.partials)));
@@ -608,6 +692,116 @@ double Trainer::proxy_iteration(double lr, double temp, double noise_std) {
     last_mse_ = h_scal_->mse;
     last_bits_ = h_scal_->bits;
     return h_scal_->cost;
+}
+
+// ---------------------------------------------------------------- row bands
+// One proxy iteration of a band is split around the exchange steps the band
+// driver performs between ranks: (A) forward + backward up to
+// local partial gradients; exchange halo-row latent gradients, NN-gradient
+// partial sums and the bits / squared-error sums; (B) finish the gradients
+// and the cost; AND the per-grid finiteness over ranks; (C) the Adam steps.
+void Trainer::band_forward_backward(double lr, double temp, double noise_std, double* bits,
+                                    double* se) {
+    require_loaded();
+    if (!band_.on) throw StateError("not a band trainer");
+    CCB_CUDA(cudaSetDevice(device_));
+    h_scal_->lr = lr;
+    h_scal_->temp = temp;
+    h_scal_->noise = noise_std;
+    CCB_CUDA(cudaMemcpyAsync(&H_.scal->lr, &h_scal_->lr, 3 * sizeof(double),
+                             cudaMemcpyHostToDevice, stream_));
+    launch_softq_fwd(L_);
+    launch_arm(L_, kArmProxy);
+    launch_pyramid(L_);
+    launch_ups_forward(L_);
+    launch_syn_forward(L_, true);
+    launch_syn_backward(L_);
+    launch_ups_backward(L_, true);
+    launch_finalize(L_, kArmProxy, -1);  // local sums; latent grads are kept even if
+    launch_latent_grad_partial(L_);      // this band's partial cost is not finite
+    launch_nn_reduce(L_);
+    read_scalars();
+    *bits = h_scal_->bits;
+    *se = h_scal_->mse * double(3 * H_.npix_global);
+}
+
+void Trainer::band_nn_partial(double* out) {
+    CCB_CUDA(cudaMemcpyAsync(out, H_.grads_d, sizeof(double) * size_t(H_.n_params),
+                             cudaMemcpyDeviceToHost, stream_));
+    synchronize();
+}
+
+double Trainer::band_finish(const double* nn_sums, double bits, double se, int* lat_ok_own) {
+    const int np = H_.n_params;
+    std::vector<float> g(static_cast<size_t>(np));
+    std::vector<int> ok(static_cast<size_t>(H_.n_tensors), 1);
+    for (int p = 0; p < np; ++p) g[size_t(p)] = float(nn_sums[p]);
+    for (int t = 0; t < H_.n_tensors; ++t)
+        for (int e = 0; e < H_.tensor_size[t]; ++e)
+            if (!std::isfinite(g[size_t(H_.tensor_off[t] + e)])) ok[size_t(t)] = 0;
+    CCB_CUDA(cudaMemcpyAsync(H_.grads, g.data(), sizeof(float) * g.size(), cudaMemcpyHostToDevice,
+                             stream_));
+    CCB_CUDA(cudaMemcpyAsync(H_.tensor_ok, ok.data(), sizeof(int) * ok.size(),
+                             cudaMemcpyHostToDevice, stream_));
+    const double mse = se / double(3 * H_.npix_global);
+    const double cost = mse + H_.lambda * (bits / double(H_.npix_global));  // encoder.hpp:115
+    h_scal_->bits = bits;
+    h_scal_->mse = mse;
+    h_scal_->cost = cost;
+    h_scal_->cost_ok = std::isfinite(cost) ? 1 : 0;
+    CCB_CUDA(cudaMemcpyAsync(&H_.scal->cost, &h_scal_->cost, 3 * sizeof(double),
+                             cudaMemcpyHostToDevice, stream_));
+    CCB_CUDA(cudaMemcpyAsync(&H_.scal->cost_ok, &h_scal_->cost_ok, sizeof(int),
+                             cudaMemcpyHostToDevice, stream_));
+    launch_band_own_finite(L_);
+    std::vector<int> lo(kMaxGrids);
+    CCB_CUDA(cudaMemcpyAsync(lo.data(), H_.lat_ok, sizeof(int) * kMaxGrids, cudaMemcpyDeviceToHost,
+                             stream_));
+    synchronize();
+    for (int gi = 0; gi < H_.n_grids; ++gi) lat_ok_own[gi] = lo[size_t(gi)];
+    last_mse_ = mse;
+    last_bits_ = bits;
+    return cost;
+}
+
+void Trainer::band_step(const int* lat_ok) {
+    CCB_CUDA(cudaMemcpyAsync(H_.lat_ok, lat_ok, sizeof(int) * size_t(H_.n_grids),
+                             cudaMemcpyHostToDevice, stream_));
+    launch_adam_latents(L_);
+    launch_nn_apply(L_, true, true, nullptr);
+    read_scalars();
+}
+
+// Global rows [rb, re) of grid gi, flat (rows x cols): mode 0 get, 1 set, 2 add.
+void Trainer::band_rows(int which, int gi, int rb, int re, float* buf, int mode) {
+    if (gi < 0 || gi >= H_.n_grids) throw ConfigError("grid index out of range");
+    const GridGeom& g = H_.g[gi];
+    if (rb < g.row0 || re > g.row0 + g.rows || rb > re) throw ConfigError("rows outside the band window");
+    float* base = (which == 0 ? H_.y : which == 1 ? H_.lat_g : nullptr);
+    if (!base) throw ConfigError("band_rows: which must be 0 (latents) or 1 (latent grads)");
+    float* d = base + g.lat_off + int64_t(rb - g.row0) * g.cols;
+    const size_t n = size_t(re - rb) * size_t(g.cols);
+    if (n == 0) return;
+    if (mode == 0) {
+        CCB_CUDA(cudaMemcpyAsync(buf, d, sizeof(float) * n, cudaMemcpyDeviceToHost, stream_));
+    } else if (mode == 1) {
+        CCB_CUDA(cudaMemcpyAsync(d, buf, sizeof(float) * n, cudaMemcpyHostToDevice, stream_));
+    } else {
+        std::vector<float> cur(n);
+        CCB_CUDA(cudaMemcpyAsync(cur.data(), d, sizeof(float) * n, cudaMemcpyDeviceToHost, stream_));
+        synchronize();
+        for (size_t i = 0; i < n; ++i) cur[i] += buf[i];
+        CCB_CUDA(cudaMemcpyAsync(d, cur.data(), sizeof(float) * n, cudaMemcpyHostToDevice, stream_));
+    }
+    synchronize();
+}
+
+void Trainer::band_grid_rows(int gi, int* out4) const {
+    const GridGeom& g = H_.g[gi];
+    out4[0] = g.row0;
+    out4[1] = g.row0 + g.own_lo;
+    out4[2] = g.row0 + g.own_hi;
+    out4[3] = g.row0 + g.rows;
 }
 
 void Trainer::proxy_iterations(int n, const double* lr, const double* temp, const double* noise,

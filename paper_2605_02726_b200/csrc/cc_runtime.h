@@ -58,6 +58,11 @@ class Trainer {
 public:
     Trainer(const float* image, int h, int w, const cc_encoder_config& enc,
             const cc_decoder_config& dec, int device);
+    // one row band [r0, r1) of an hg x w image (cfg5); image_window holds the
+    // pixel rows band_window() returns
+    Trainer(const float* image_window, int hg, int w, int r0, int r1, int halo,
+            const cc_encoder_config& enc, const cc_decoder_config& dec, int device);
+    static void band_window(int hg, int w, int r0, int r1, int halo, int* w0, int* w1);
     ~Trainer();
     Trainer(const Trainer&) = delete;
     Trainer& operator=(const Trainer&) = delete;
@@ -95,6 +100,15 @@ public:
     double current_cost() const { return cur_cost_; }
     void set_current_cost(double c) { cur_cost_ = c; }
 
+    // row bands (cfg5): see cc_runtime.cu
+    bool is_band() const { return band_.on; }
+    void band_forward_backward(double lr, double temp, double noise, double* bits, double* se);
+    void band_nn_partial(double* out);
+    double band_finish(const double* nn_sums, double bits, double se, int* lat_ok_own);
+    void band_step(const int* lat_ok);
+    void band_rows(int which, int gi, int rb, int re, float* buf, int mode);
+    void band_grid_rows(int gi, int* out4) const;
+
     // state transfer
     void set_state(const float* lat, const float* par, const float* lm, const float* lv,
                    const int64_t* lt, const float* nm, const float* nv, const int64_t* nt);
@@ -114,6 +128,7 @@ public:
     void synchronize();
 
 private:
+    void init(const float* image, int h, int w);
     void build_plan();
     void allocate();
     void require_loaded() const;
@@ -158,8 +173,12 @@ private:
     // captured graphs: 0 proxy(single), 1 proxy(batched), 2 true_cost, 100+slot hardround
     std::map<int, cudaGraphExec_t> graphs_;
     struct Sizes {
-        int64_t pad = 0, dctx = 0, dfeat = 0, ups = 0, partials = 0;
+        int64_t pad = 0, dctx = 0, dfeat = 0, ups = 0, partials = 0, z = 0;
     } sizes_;
+    struct BandSpec {
+        bool on = false;
+        int hg = 0, r0 = 0, r1 = 0, halo = 0;
+    } band_;
     std::vector<int2> tiles_host_;
 };
 

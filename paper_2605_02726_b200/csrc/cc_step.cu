@@ -40,8 +40,8 @@ __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, i
     }
     if (threadIdx.x != 0) return;
     const double bits = bits_all, se = se_all;
-    const double mse = se / double(3 * P.npix);
-    const double cost = mse + P.lambda * (bits / double(P.npix));
+    const double mse = se / double(3 * P.npix_global);
+    const double cost = mse + P.lambda * (bits / double(P.npix_global));
     DevScalars* s = P.scal;
     s->bits = bits;
     s->mse = mse;
@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(256) k_nn_reduce(const Plan* __restrict__ pp,
         if (lane == 0) {
             const float g = float(sum);
             P.grads[p] = g;
+            P.grads_d[p] = sum;
             if (!isfinite(g)) {
                 int ti = 0;
                 while (ti + 1 < P.n_tensors && P.tensor_off[ti + 1] <= p) ++ti;

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(256) k_syn_trunk_fwd(const Plan* __restrict__ 
          p += int64_t(gridDim.x) * blockDim.x) {
         float zv[kLZ];
 #pragma unroll
-        for (int k = 0; k < kLZ; ++k) zv[k] = k < L ? P.z[int64_t(k) * np + p] : 0.0f;
+        for (int k = 0; k < kLZ; ++k) zv[k] = k < L ? P.z[P.zpix[k] + p] : 0.0f;
         float t0 = c2b[0], t1 = c2b[1], t2 = c2b[2];
         for (int f = 0; f < F; ++f) {
             float acc = c1b[f];

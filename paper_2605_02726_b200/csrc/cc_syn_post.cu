@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
         }
         if (tid < 4) sm.bias[i][tid] = tid < 3 ? P.params[P.off_pb[i] + tid] : 0.0f;
     }
-    const float s = float(2.0 / double(3 * np));
+    const float s = float(2.0 / double(3 * P.npix_global));  // layers.hpp:655 (whole image)
+    const int own_lo = P.pix_own_lo, own_hi = P.pix_own_hi;  // row bands: loss rows
     // post weight-gradient accumulators: thread (column wc, slot ws) owns the
     // (post, co, ci) pairs ws, ws+8, ws+16: 9 taps + the bias sum (ci == 0)
     const int wc = tid % TW, ws = tid / TW;
@@ -191,17 +192,18 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
                     continue;
                 }
                 const bool inimg = gr >= 0 && gr < H && gc >= 0 && gc < W;
+                const bool loss = inimg && gr >= own_lo && gr < own_hi;  // band-owned pixel
                 const bool own = gr >= y0 && gr < y0 + TH && gc >= x0 && gc < x0 + TW && inimg;
 #pragma unroll
                 for (int co = 0; co < 3; ++co) {
                     float xh = sm.p[NP][co][v] + sm.sz[co][v];
                     xh = std_min(1.0f, std_max(0.0f, xh));
                     const float tgt = sm.img[co][v];
-                    if (own) {
+                    if (own && loss) {
                         const double dd = double(xh) - double(tgt);
                         mse += dd * dd;
                     }
-                    const float g = inimg ? s * (xh - tgt) : 0.0f;
+                    const float g = loss ? s * (xh - tgt) : 0.0f;
                     sm.d[NP][co][v] = g;
                     if (own && with_grad) P.syn_dx[co * np + int64_t(gr) * W + gc] = g;
                 }

@@ -78,12 +78,12 @@ __device__ __forceinline__ void cp_async4_zfill(float* smem, const float* gmem, 
 
 // Asynchronous load of tile t's inputs into feature-major rows: z planes
 // 0..7 (zero past L), dt 0..2, dx̂ 0..2; zero past the last pixel.  16-byte
-// copies when every plane is 16-byte aligned (npix % 4 == 0).  Always commits
+// copies when every plane is 16-byte aligned (Plan::zvec).  Always commits
 // one cp.async group.
 __device__ __forceinline__ void issue_tile(const Plan& P, const float* __restrict__ dt_in, int64_t t,
                                            float* bZ, float* bDT, float* bDX, int tid) {
     const int64_t np = P.npix, p0 = t * T;
-    const bool vec = (np & 3) == 0;
+    const bool vec = P.zvec != 0;  // npix and every z-plane offset are multiples of 4
     for (int c = tid; c < 14 * (T / 4); c += NT) {
         const int row = c / (T / 4), q = c % (T / 4);
         const int64_t p = p0 + 4 * q;
@@ -91,7 +91,7 @@ __device__ __forceinline__ void issue_tile(const Plan& P, const float* __restric
         float* dst;
         bool ok;
         if (row < kLZ) {
-            src = P.z + int64_t(row) * np + p;
+            src = P.z + (row < P.L ? P.zpix[row] : 0) + p;
             dst = bZ + row * LT + 4 * q;
             ok = row < P.L;
         } else if (row < kLZ + 3) {
@@ -237,8 +237,8 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
         if (half == 0 && valid) {
 #pragma unroll
             for (int kp = 0; kp < kLZ / 2; ++kp) {
-                if (2 * kp < L) P.dz[int64_t(2 * kp) * np + p] = dzp[kp].x + sDZ[(2 * kp) * LT + px];
-                if (2 * kp + 1 < L) P.dz[int64_t(2 * kp + 1) * np + p] = dzp[kp].y + sDZ[(2 * kp + 1) * LT + px];
+                if (2 * kp < L) P.dz[P.zpix[2 * kp] + p] = dzp[kp].x + sDZ[(2 * kp) * LT + px];
+                if (2 * kp + 1 < L) P.dz[P.zpix[2 * kp + 1] + p] = dzp[kp].y + sDZ[(2 * kp + 1) * LT + px];
             }
         }
         // ---- phase B: weight gradients ----

@@ -191,7 +191,7 @@ __global__ void k_copy_z0(const Plan* __restrict__ pp) {
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < P.npix;
          e += int64_t(gridDim.x) * blockDim.x) {
         const int r = int(e / P.W), c = int(e - int64_t(r) * P.W);
-        P.z[e] = P.yhat_pad[g.pad_base + int64_t(r) * g.stride + c];
+        P.z[P.zpix[0] + e] = P.yhat_pad[g.pad_base + int64_t(r) * g.stride + c];
     }
 }
 

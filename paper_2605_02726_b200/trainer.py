@@ -254,7 +254,7 @@ class Trainer:
     """
 
     def __init__(self, image: np.ndarray, enc: EncoderConfig, dcfg: DecoderConfig, lib=None,
-                 device: int = 0):
+                 device: int = 0, band: tuple[int, int, int, int] | None = None):
         self.lib = lib or capi.load_product()
         img = np.ascontiguousarray(image, dtype=np.float32)
         if img.ndim != 3 or img.shape[0] != 3:
@@ -264,9 +264,16 @@ class Trainer:
         self._h = C.c_void_p()
         self._enc_c = enc.to_c()
         self._dec_c = dcfg.to_c()
-        _check(self.lib, self.lib.cc_trainer_create(_fp(img), img.shape[1], img.shape[2],
-                                                    C.byref(self._enc_c), C.byref(self._dec_c),
-                                                    device, C.byref(self._h)))
+        self.band = band
+        if band is None:
+            _check(self.lib, self.lib.cc_trainer_create(_fp(img), img.shape[1], img.shape[2],
+                                                        C.byref(self._enc_c), C.byref(self._dec_c),
+                                                        device, C.byref(self._h)))
+        else:  # one row band (H, r0, r1, halo) of a larger image; img = the band window
+            hg, r0, r1, halo = band
+            _check(self.lib, self.lib.cc_band_trainer_create(
+                _fp(img), hg, img.shape[2], r0, r1, halo, C.byref(self._enc_c),
+                C.byref(self._dec_c), device, C.byref(self._h)))
         lay = capi.LayoutC()
         _check(self.lib, self.lib.cc_trainer_layout(self._h, C.byref(lay)))
         self.layout = lay
