@@ -289,7 +289,7 @@ def run_b200(args, rank, world, local_rank):
             traffic = json.loads(tf.read_text()).get("bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "fp32", "kernel": "k_arm (fused ARM+IFCE fwd/bwd)",
+    roofline = {"bound": "fp32", "kernel": "k_arm2 (fused ARM+IFCE fwd/bwd, register-tiled)",
                 "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                 "frac": achieved / peak.value, "traffic": traffic,
                 "flops_per_launch": arm_flops,
