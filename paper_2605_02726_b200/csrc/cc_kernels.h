@@ -49,6 +49,7 @@ void pyramid_configure(const Plan& H);
 void launch_ups_forward(const LaunchCtx& L);
 void launch_ups_backward(const LaunchCtx& L, bool latent_grads);
 int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward);
+int ups_coarse_from(const Plan& H);
 void ups_configure();
 
 // synthesis (cc_syn.cu, cc_syn_trunk.cu)

@@ -127,6 +127,7 @@ struct Plan {
 
     // ---- upsampling stages: stage j -> list of (grid) stages ----
     int ups_n[kMaxLevels];
+    int ups_jc;               // stages j >= ups_jc run fused, one CTA per cascade
     UpsStage ups[kMaxLevels][kMaxUpsGrids];
 
     // ---- device buffers ----

@@ -18,6 +18,9 @@
 // partial rows).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "cc_kernels.h"
 #include "cc_math.cuh"
 #include "cc_reduce.cuh"
@@ -78,22 +81,29 @@ __device__ __forceinline__ float* stage_din(const Plan& P, const UpsStage& s) {
 // One CTA = one kFT x kFT output tile of stage j for grid blockIdx.y.
 constexpr int kFC = kFT + 2;              // coltmp window (tile + refine halo)
 constexpr int kFR = kFC / 2 + 6;          // rowtmp rows / input rows
-__global__ void __launch_bounds__(kThreadsWide) k_ups_fwd(const Plan* __restrict__ pp, int j) {
-    const Plan& P = *pp;
-    const UpsStage& s = P.ups[j][blockIdx.y];
+struct FwdSmem {
+    float s_in[kFR * kFR];
+    float s_row[kFR * kFC];
+    float s_col[kFC * kFC];
+};
+
+// Tiles t_begin, t_begin + t_step, ... of stage j for grid entry si.
+__device__ __forceinline__ void ups_fwd_stage(const Plan& P, int j, int si, int t_begin, int t_step,
+                                              FwdSmem& fs) {
+    const UpsStage& s = P.ups[j][si];
     const int ro = s.rows_out, co = s.cols_out, ri = s.rows_in, ci = s.cols_in;
     const int tiles_x = (co + kFT - 1) / kFT;
     const int ntiles = tiles_x * ((ro + kFT - 1) / kFT);
-    __shared__ float s_in[kFR * kFR];
-    __shared__ float s_row[kFR * kFC];
-    __shared__ float s_col[kFC * kFC];
+    float* s_in = fs.s_in;
+    float* s_row = fs.s_row;
+    float* s_col = fs.s_col;
     const float* k4 = P.params + P.off_tconv[j];
     const float* r3 = P.params + P.off_refine[j];
     const float t0 = k4[0], t1 = k4[1], t2 = k4[2], t3 = k4[3];
     const float kc = r3[0], ke = r3[1], ko = r3[2];
     const float* in = stage_in(P, s);
     float* out = stage_out(P, s);
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int tile = t_begin; tile < ntiles; tile += t_step) {
         const int y0 = (tile / tiles_x) * kFT, x0 = (tile % tiles_x) * kFT;
         if (y0 >= kFT && x0 >= kFT && y0 / 2 + 18 <= ri - 1 && x0 / 2 + 18 <= ci - 1 && y0 + kFT <= ro - 1 &&
             x0 + kFT <= co - 1) {
@@ -181,6 +191,26 @@ __global__ void __launch_bounds__(kThreadsWide) k_ups_fwd(const Plan* __restrict
             out[int64_t(r) * co + c] = kc * x1r[c0] + ke * (x0r[c0] + x2r[c0] + x1r[cm] + x1r[cp]) +
                                        ko * (x0r[cm] + x0r[cp] + x2r[cm] + x2r[cp]);
         }
+    }
+}
+
+__global__ void __launch_bounds__(kThreadsWide) k_ups_fwd(const Plan* __restrict__ pp, int j) {
+    __shared__ FwdSmem fs;
+    ups_fwd_stage(*pp, j, blockIdx.y, blockIdx.x, gridDim.x, fs);
+}
+
+// Coarse stages j >= jc of every cascade k > jc in ONE launch: CTA b runs
+// cascade k = jc + 1 + b through its stages k-1 .. jc in order (a stage's
+// output is the next one's input; __syncthreads orders them in the CTA).
+// The coarse stages have a handful of tiles each, so this trades k - jc
+// latency-bound launches for one.
+__global__ void __launch_bounds__(kThreadsWide) k_ups_fwd_coarse(const Plan* __restrict__ pp, int jc) {
+    __shared__ FwdSmem fs;
+    const Plan& P = *pp;
+    const int k = jc + 1 + blockIdx.x;
+    for (int j = k - 1; j >= jc; --j) {
+        ups_fwd_stage(P, j, k - j - 1, 0, 1, fs);
+        __syncthreads();
     }
 }
 
@@ -367,14 +397,13 @@ __device__ __forceinline__ void bwd_tile_fast(const float* __restrict__ in, int 
     for (int k = 0; k < 7; ++k) acc[k] += double(fa[k]);
 }
 
-__global__ void __launch_bounds__(kThreadsWide) k_ups_bwd(const Plan* __restrict__ pp, int j,
-                                                      int write_lat) {
-    const Plan& P = *pp;
-    const UpsStage& s = P.ups[j][blockIdx.y];
+__device__ __forceinline__ void ups_bwd_stage(const Plan& P, int j, int si, int t_begin, int t_step,
+                                              int write_lat, unsigned char* smem_raw,
+                                              double (&acc)[7]) {
+    const UpsStage& s = P.ups[j][si];
     const int ro = s.rows_out, co = s.cols_out, ri = s.rows_in, ci = s.cols_in;
     const int tiles_x = (ci + kBT - 1) / kBT;
     const int ntiles = tiles_x * ((ri + kBT - 1) / kBT);
-    extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
     const float* k4 = P.params + P.off_tconv[j];
     const float* r3 = P.params + P.off_refine[j];
@@ -384,8 +413,7 @@ __global__ void __launch_bounds__(kThreadsWide) k_ups_bwd(const Plan* __restrict
     const float* dout = stage_dout(P, s);
     float* din = stage_din(P, s);
     const bool wd = write_lat || !s.din_is_lat;
-    double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // dk4[0..3] (rows+cols passes), dr3[0..2]
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (int tile = t_begin; tile < ntiles; tile += t_step) {
         const int U0 = (tile / tiles_x) * kBT, V0 = (tile % tiles_x) * kBT;
         if (bwd_interior(U0, V0, ri, ci, ro, co)) {
             bwd_tile_fast(in, s.in_stride, dout, co, din, ci, wd, U0, V0, kk, kc, ke, ko,
@@ -553,15 +581,45 @@ __global__ void __launch_bounds__(kThreadsWide) k_ups_bwd(const Plan* __restrict
             for (int q = 0; q < 4; ++q) acc[tap[q]] += g * double(x[idx[q]]);
         }
     }
+}
+
+// tap gradients of this CTA for stage j -> partial row `row`
+__device__ __forceinline__ void ups_bwd_write(const Plan& P, int j, int row, unsigned char* smem_raw,
+                                              double (&acc)[7]) {
+    BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
     block_sum_vec<7>(acc, sm.red, sm.tot);
     __syncthreads();
-    const int row = blockIdx.y * gridDim.x + blockIdx.x;
     if (threadIdx.x < 4) {
         const PartialRegion& R = P.region[P.reg_ups_rows[j]];
         P.partials[R.base + int64_t(row) * R.count + threadIdx.x] = sm.tot[threadIdx.x];
     } else if (threadIdx.x < 7) {
         const PartialRegion& R = P.region[P.reg_ups_ref[j]];
         P.partials[R.base + int64_t(row) * R.count + (threadIdx.x - 4)] = sm.tot[threadIdx.x];
+    }
+}
+
+__global__ void __launch_bounds__(kThreadsWide) k_ups_bwd(const Plan* __restrict__ pp, int j,
+                                                      int write_lat) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Plan& P = *pp;
+    double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // dk4[0..3] (rows+cols passes), dr3[0..2]
+    ups_bwd_stage(P, j, blockIdx.y, blockIdx.x, gridDim.x, write_lat, smem_raw, acc);
+    ups_bwd_write(P, j, blockIdx.y * gridDim.x + blockIdx.x, smem_raw, acc);
+}
+
+// Coarse stages j >= jc in one launch (see k_ups_fwd_coarse): CTA b runs
+// cascade k = jc + 1 + b through stages jc .. k-1; one partial row per
+// (stage, cascade).
+__global__ void __launch_bounds__(kThreadsWide) k_ups_bwd_coarse(const Plan* __restrict__ pp, int jc,
+                                                             int write_lat) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Plan& P = *pp;
+    const int k = jc + 1 + blockIdx.x;
+    for (int j = jc; j < k; ++j) {
+        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+        ups_bwd_stage(P, j, k - j - 1, 0, 1, write_lat, smem_raw, acc);
+        ups_bwd_write(P, j, k - j - 1, smem_raw, acc);
+        __syncthreads();
     }
 }
 
@@ -580,16 +638,42 @@ int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward) {
     return best < cap ? best : cap;
 }
 
+// First stage of the fused coarse launch: the smallest j such that every
+// stage j' >= j has at most 8 tiles per grid in either direction.  Off by
+// default (CCB_UPS_FUSE=1 enables it): measured at 512x768 the per-cascade
+// CTA serialises ~9 tiles of the clamp-aware path (~4 us each), which is
+// slower than the 3-4 latency-bound launches it replaces (146 -> 178 us).
+int ups_coarse_from(const Plan& H) {
+    const char* e = std::getenv("CCB_UPS_FUSE");
+    if (!e || e[0] != '1') return H.L - 1;
+    int jc = H.L - 1;
+    for (int j = H.L - 2; j >= 0; --j) {
+        int mt = 0;
+        for (int i = 0; i < H.ups_n[j]; ++i) {
+            const UpsStage& s = H.ups[j][i];
+            const int tf = ((s.rows_out + kFT - 1) / kFT) * ((s.cols_out + kFT - 1) / kFT);
+            const int tb = ((s.rows_in + kBT - 1) / kBT) * ((s.cols_in + kBT - 1) / kBT);
+            mt = std::max(mt, std::max(tf, tb));
+        }
+        if (mt > 8) break;
+        jc = j;
+    }
+    return jc;
+}
+
 size_t ups_bwd_smem() { return sizeof(BwdSmem); }
 
 void ups_configure() {
     cudaFuncSetAttribute(k_ups_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
+    cudaFuncSetAttribute(k_ups_bwd_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
 }
 
 void launch_ups_forward(const LaunchCtx& L) {
     const Plan& H = *L.host;
     k_copy_z0<<<L.pix_blocks, 256, 0, L.stream>>>(L.plan);
-    for (int j = H.L - 2; j >= 0; --j) {
+    const int jc = H.ups_jc;
+    if (jc <= H.L - 2) k_ups_fwd_coarse<<<H.L - 1 - jc, kThreadsWide, 0, L.stream>>>(L.plan, jc);
+    for (int j = jc - 1; j >= 0; --j) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, true), H.ups_n[j]);
         const int nt = int(grid.x * grid.y) < 2 * L.num_sms ? kThreadsWide : kThreads;
@@ -599,12 +683,16 @@ void launch_ups_forward(const LaunchCtx& L) {
 
 void launch_ups_backward(const LaunchCtx& L, bool latent_grads) {
     const Plan& H = *L.host;
-    for (int j = 0; j <= H.L - 2; ++j) {
+    const int jc = H.ups_jc;
+    for (int j = 0; j < jc && j <= H.L - 2; ++j) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, false), H.ups_n[j]);
         const int nt = int(grid.x * grid.y) < 2 * L.num_sms ? kThreadsWide : kThreads;
         k_ups_bwd<<<grid, nt, sizeof(BwdSmem), L.stream>>>(L.plan, j, latent_grads ? 1 : 0);
     }
+    if (jc <= H.L - 2)
+        k_ups_bwd_coarse<<<H.L - 1 - jc, kThreadsWide, sizeof(BwdSmem), L.stream>>>(L.plan, jc,
+                                                                                   latent_grads ? 1 : 0);
 }
 
 }  // namespace ccb
