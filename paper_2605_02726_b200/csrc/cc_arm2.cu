@@ -114,7 +114,7 @@ __device__ __forceinline__ void dw_tile(const float* __restrict__ A, const float
 template <int N, int K>
 __device__ __forceinline__ void tile_gemm(const float* __restrict__ X, const float (*W)[32], int p, int g,
                                           float2 (&acc)[N]) {
-#pragma unroll 4
+#pragma unroll
     for (int k = 0; k < K; ++k) {
         const float2 x = *reinterpret_cast<const float2*>(X + k * LT + 2 * p);
         const float* w = &W[k][g * 8];
