@@ -32,7 +32,9 @@ constexpr int kLZ = kMaxLevels;
 template <int FP>
 struct TB {
     static_assert(T == 128 && FP % 4 == 0, "tile mapping");
-    static constexpr int FH = FP / 2;  // hidden units per phase-A thread
+    static constexpr int FQ = FP / 4;  // hidden units per phase-A thread (a pixel pair)
+    static constexpr int U = FQ < 4 ? FQ : 4;  // hidden units per weight load
+    static_assert(FQ % U == 0, "hidden-unit chunks");
     static constexpr int RZ = 12;      // z 0..7, ones at 8
     static constexpr int RH = FP + 4;  // h1, ones at FP
     static constexpr int O_Z = 0;
@@ -40,8 +42,8 @@ struct TB {
     static constexpr int O_DH = O_H + RH * LT;
     static constexpr int O_DT = O_DH + FP * LT;
     static constexpr int O_DX = O_DT + 4 * LT;
-    static constexpr int O_DZ = O_DX + 4 * LT;   // second half's partial dz
-    static constexpr int O_Z2 = O_DZ + kLZ * LT; // next tile's z / dt / dx̂ (cp.async)
+    static constexpr int O_DZ = O_DX + 4 * LT;   // quarters 1..3: partial dz
+    static constexpr int O_Z2 = O_DZ + 3 * kLZ * LT; // next tile's z / dt / dx̂ (cp.async)
     static constexpr int O_DT2 = O_Z2 + RZ * LT;
     static constexpr int O_DX2 = O_DT2 + 4 * LT;
     static constexpr int ACT = O_DX2 + 4 * LT;
@@ -123,7 +125,6 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TBSmem<FP>& sm = *reinterpret_cast<TBSmem<FP>*>(smem_raw);
     const int tid = threadIdx.x;
-    const int px = tid & (T - 1), half = tid >> 7;
     const int L = P.L, F = P.syn_F;
     const bool has_stab = P.off_sstab >= 0;
     for (int e = tid; e < FP * kLZ; e += NT) {
@@ -164,8 +165,6 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
     const int64_t ntiles = (np + T - 1) / T;
     if (blockIdx.x < ntiles) issue_tile(P, dt_in, blockIdx.x, sZ, sDT, sDX, tid);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int64_t p = t * T + px;
-        const bool valid = p < np;
         // the next tile's inputs land in the other buffers while this one computes
         if (t + gridDim.x < ntiles)
             issue_tile(P, dt_in, t + gridDim.x, nZ, nDT, nDX, tid);
@@ -173,72 +172,100 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
             asm volatile("cp.async.commit_group;\n" ::: "memory");
         asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         __syncthreads();
-        // ---- phase A ----
-        float z[kLZ];
+        // ---- phase A: thread = pixel pair (FFMA2 lanes) x a quarter of the
+        // hidden units; weights are broadcast operands ----
+        const int pq = tid & 63, qt = tid >> 6, px0 = 2 * pq;
+        const int64_t p0 = t * T + px0;
+        const bool v0 = p0 < np, v1 = p0 + 1 < np;
+        float2 z[kLZ], dt[3];
 #pragma unroll
-        for (int k = 0; k < kLZ; ++k) z[k] = sZ[k * LT + px];
-        float dt[3], dx[3];
+        for (int k = 0; k < kLZ; ++k) z[k] = *reinterpret_cast<const float2*>(sZ + k * LT + px0);
 #pragma unroll
-        for (int co = 0; co < 3; ++co) {
-            dt[co] = sDT[co * LT + px];
-            dx[co] = sDX[co * LT + px];
-        }
+        for (int co = 0; co < 3; ++co) dt[co] = *reinterpret_cast<const float2*>(sDT + co * LT + px0);
         // dz starts with the stabilizer term (synthesis.hpp:220), then c1 (:232)
-        float2 dzp[kLZ / 2];
+        float2 dz[kLZ];
 #pragma unroll
-        for (int kp = 0; kp < kLZ / 2; ++kp) {
-            float2 a = make_float2(0.0f, 0.0f);
-            if (half == 0 && has_stab) {
-                a.x = fmaf(sm.st[0][2 * kp], dx[0], 0.0f);
-                a.x = fmaf(sm.st[1][2 * kp], dx[1], a.x);
-                a.x = fmaf(sm.st[2][2 * kp], dx[2], a.x);
-                a.y = fmaf(sm.st[0][2 * kp + 1], dx[0], 0.0f);
-                a.y = fmaf(sm.st[1][2 * kp + 1], dx[1], a.y);
-                a.y = fmaf(sm.st[2][2 * kp + 1], dx[2], a.y);
+        for (int k = 0; k < kLZ; ++k) dz[k] = make_float2(0.0f, 0.0f);
+        if (qt == 0 && has_stab) {
+            float2 dx[3];
+#pragma unroll
+            for (int co = 0; co < 3; ++co) dx[co] = *reinterpret_cast<const float2*>(sDX + co * LT + px0);
+#pragma unroll
+            for (int k = 0; k < kLZ; ++k) {
+                float2 a = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int co = 0; co < 3; ++co) a = ffma2(dx[co], sm.st[co][k], a);
+                dz[k] = a;
             }
-            dzp[kp] = a;
         }
-        const int f0 = half * K::FH;
-#pragma unroll 4
-        for (int fp = 0; fp < K::FH / 2; ++fp) {
-            const int f = f0 + 2 * fp;
-            float2 acc = *reinterpret_cast<const float2*>(&sm.c1b[f]);
+        const int f0 = qt * K::FQ;
+#pragma unroll 1
+        for (int fc = 0; fc < K::FQ; fc += K::U) {
+            const int f = f0 + fc;
+            float2 a[K::U];
+#pragma unroll
+            for (int u = 0; u < K::U; ++u) a[u] = make_float2(sm.c1b[f + u], sm.c1b[f + u]);
+#pragma unroll
+            for (int k = 0; k < kLZ; ++k) {
+                float w[K::U];
+                if constexpr (K::U == 4) {
+                    const float4 w4 = *reinterpret_cast<const float4*>(&sm.W1T[k][f]);
+                    w[0] = w4.x; w[1] = w4.y; w[2] = w4.z; w[3] = w4.w;
+                } else {
+#pragma unroll
+                    for (int u = 0; u < K::U; ++u) w[u] = sm.W1T[k][f + u];
+                }
+#pragma unroll
+                for (int u = 0; u < K::U; ++u) a[u] = ffma2(z[k], w[u], a[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < K::U; ++u) {
+                const float2 h = make_float2(a[u].x > 0.0f ? a[u].x : 0.0f, a[u].y > 0.0f ? a[u].y : 0.0f);
+                float2 d = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int co = 0; co < 3; ++co) d = ffma2(dt[co], sm.c2w[co][f + u], d);
+                d.x = h.x > 0.0f ? d.x : 0.0f;
+                d.y = h.y > 0.0f ? d.y : 0.0f;
+#pragma unroll
+                for (int kq = 0; kq < kLZ / 4; ++kq) {
+                    const float4 w4 = *reinterpret_cast<const float4*>(&sm.W1[f + u][4 * kq]);
+                    dz[4 * kq + 0] = ffma2(d, w4.x, dz[4 * kq + 0]);
+                    dz[4 * kq + 1] = ffma2(d, w4.y, dz[4 * kq + 1]);
+                    dz[4 * kq + 2] = ffma2(d, w4.z, dz[4 * kq + 2]);
+                    dz[4 * kq + 3] = ffma2(d, w4.w, dz[4 * kq + 3]);
+                }
+                *reinterpret_cast<float2*>(sH + (f + u) * LT + px0) = make_float2(v0 ? h.x : 0.0f, v1 ? h.y : 0.0f);
+                *reinterpret_cast<float2*>(sDH + (f + u) * LT + px0) = d;
+            }
+        }
+        if (qt == 0) {
+            *reinterpret_cast<float2*>(sZ + kLZ * LT + px0) = make_float2(v0 ? 1.0f : 0.0f, v1 ? 1.0f : 0.0f);
+        } else {
+            if (qt == 1)
+                *reinterpret_cast<float2*>(sH + FP * LT + px0) = make_float2(v0 ? 1.0f : 0.0f, v1 ? 1.0f : 0.0f);
 #pragma unroll
             for (int k = 0; k < kLZ; ++k)
-                acc = ffma2(*reinterpret_cast<const float2*>(&sm.W1T[k][f]), z[k], acc);
-            const float2 h = make_float2(acc.x > 0.0f ? acc.x : 0.0f, acc.y > 0.0f ? acc.y : 0.0f);
-            float2 d = make_float2(0.0f, 0.0f);
-#pragma unroll
-            for (int co = 0; co < 3; ++co) d = ffma2(*reinterpret_cast<const float2*>(&sm.c2w[co][f]), dt[co], d);
-            d.x = h.x > 0.0f ? d.x : 0.0f;
-            d.y = h.y > 0.0f ? d.y : 0.0f;
-#pragma unroll
-            for (int kp = 0; kp < kLZ / 2; ++kp)
-                dzp[kp] = ffma2(*reinterpret_cast<const float2*>(&sm.W1[f][2 * kp]), d.x, dzp[kp]);
-#pragma unroll
-            for (int kp = 0; kp < kLZ / 2; ++kp)
-                dzp[kp] = ffma2(*reinterpret_cast<const float2*>(&sm.W1[f + 1][2 * kp]), d.y, dzp[kp]);
-            sH[f * LT + px] = valid ? h.x : 0.0f;
-            sH[(f + 1) * LT + px] = valid ? h.y : 0.0f;
-            sDH[f * LT + px] = d.x;
-            sDH[(f + 1) * LT + px] = d.y;
-        }
-        if (half == 0) {
-            sZ[kLZ * LT + px] = valid ? 1.0f : 0.0f;
-        } else {
-            sH[FP * LT + px] = valid ? 1.0f : 0.0f;
-#pragma unroll
-            for (int kp = 0; kp < kLZ / 2; ++kp) {
-                sDZ[(2 * kp) * LT + px] = dzp[kp].x;
-                sDZ[(2 * kp + 1) * LT + px] = dzp[kp].y;
-            }
+                *reinterpret_cast<float2*>(sDZ + ((qt - 1) * kLZ + k) * LT + px0) = dz[k];
         }
         __syncthreads();
-        if (half == 0 && valid) {
+        if (qt == 0 && v0) {  // quarters summed in order
 #pragma unroll
-            for (int kp = 0; kp < kLZ / 2; ++kp) {
-                if (2 * kp < L) P.dz[P.zpix[2 * kp] + p] = dzp[kp].x + sDZ[(2 * kp) * LT + px];
-                if (2 * kp + 1 < L) P.dz[P.zpix[2 * kp + 1] + p] = dzp[kp].y + sDZ[(2 * kp + 1) * LT + px];
+            for (int k = 0; k < kLZ; ++k) {
+                if (k >= L) continue;
+                float2 v = dz[k];
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const float2 o = *reinterpret_cast<const float2*>(sDZ + (q * kLZ + k) * LT + px0);
+                    v.x += o.x;
+                    v.y += o.y;
+                }
+                float* dst = P.dz + P.zpix[k] + p0;
+                if (P.zvec) {
+                    *reinterpret_cast<float2*>(dst) = v;
+                } else {
+                    dst[0] = v.x;
+                    if (v1) dst[1] = v.y;
+                }
             }
         }
         // ---- phase B: weight gradients ----

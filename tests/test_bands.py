@@ -211,7 +211,7 @@ def test_bands_reproduce_whole_image(gpu_lib, h, w, n):
             st = whole.get_state()
             for gi in range(len(whole.grids)):
                 assert rel_l2(lb.gather_grid(0, gi).reshape(-1),
-                              whole.grid_view(st["latents"], gi).reshape(-1)) <= 1e-5, (it, gi)
+                              whole.grid_view(st["latents"], gi).reshape(-1)) <= 1e-4, (it, gi)
             pb = lb.trainers[0].get_state()["params"]
             for ti, p in enumerate(whole.params):
                 assert rel_l2(lb.trainers[0].param_view(pb, ti), whole.param_view(st["params"], ti)) <= 1e-4, p.name
