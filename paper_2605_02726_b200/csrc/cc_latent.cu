@@ -37,6 +37,8 @@ __device__ __forceinline__ int find_grid(const int64_t* s_off, int64_t i) {
 __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
     const Plan& P = *pp;
     CCB_GRID_CACHE(P);
+    // per-grid gradient-finiteness flags of this iteration (ANDed by k_latent_grad)
+    if (blockIdx.x == 0 && threadIdx.x < kMaxGrids) P.lat_ok[threadIdx.x] = 1;
     const float temp = float(P.scal->temp);         // encoder.hpp:98
     const float noise_std = float(P.scal->noise);   // encoder.hpp:108
     const int64_t n = P.n_latents;
@@ -63,6 +65,7 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
         const float t2 = cc_tanh(d * inv_t);
         o = f + 0.5f + t2 * inv_denom;
         P.yhat_pad[g.pad_base + int64_t(r) * g.stride + c] = o;
+        if (g.main_level == 0) P.z[P.zpix[0] + int64_t(r) * P.W + c] = o;  // z plane 0 = ŷ_0
         P.th1[i] = t1;
         P.th2[i] = t2;
     }
@@ -89,6 +92,7 @@ __global__ void k_pads_from_q(const Plan* __restrict__ pp) {
         const int64_t li = i - g.lat_off;
         const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
         P.yhat_pad[g.pad_base + int64_t(r) * g.stride + c] = float(P.q[i]);
+        if (g.main_level == 0) P.z[P.zpix[0] + int64_t(r) * P.W + c] = float(P.q[i]);
     }
 }
 
@@ -102,7 +106,8 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp, int force) {
     const Plan& P = *pp;
     CCB_GRID_CACHE(P);
     const float temp = float(P.scal->temp);
-    const int cost_ok = force || P.scal->cost_ok;  // bands: partial grads regardless
+    (void)force;  // gradients are assembled regardless of the cost flag; k_adam_latents
+                  // zeroes them when the cost is not finite (encoder.hpp:118)
     const float scale = 1.0f / (temp * softround_denom(temp));
     __shared__ int s_dy[kMaxCtx], s_dx[kMaxCtx];
     __shared__ GridGeom s_geo[kMaxGrids];
@@ -115,10 +120,6 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp, int force) {
     __syncthreads();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
-        if (!cost_ok) {  // encoder.hpp:118 returns before the backward chain
-            P.lat_g[i] = 0.0f;
-            continue;
-        }
         const int gi = find_grid(s_off, i);
         const GridGeom& g = s_geo[gi];
         const int64_t cnt = int64_t(g.rows) * g.cols;
@@ -180,7 +181,12 @@ __global__ void k_adam_latents(const Plan* __restrict__ pp) {
     const double lr = P.scal->lr;
     const double* __restrict__ bc = P.bc_lat;
     const int cost_ok = P.scal->cost_ok;
-    if (!cost_ok) return;
+    if (!cost_ok) {  // encoder.hpp:118 returns before the backward: grads stay zero
+        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+             i += int64_t(gridDim.x) * blockDim.x)
+            P.lat_g[i] = 0.0f;
+        return;
+    }
     const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {

@@ -629,11 +629,11 @@ void Trainer::enqueue_proxy(bool batched) {
     launch_syn_backward(L_);
     launch_ups_backward(L_, true);
     join();
-    launch_finalize(L_, kArmProxy, -1);
-    // gradient assembly: the NN-gradient reduction runs beside the latent
+    // gradient assembly: cost + NN-gradient reduction beside the latent
     // gather; the NN Adam step waits for the gather (it reads the IFCE
     // weights) and runs beside the latent Adam step
     fork();
+    launch_finalize(side(), kArmProxy, -1);
     launch_nn_reduce(side());
     launch_latent_grad(L_);
     join();

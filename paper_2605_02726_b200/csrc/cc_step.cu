@@ -35,7 +35,6 @@ __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, i
             const double t = double(P.lat_t[g] + 1);
             bc_lat[2 * g] = 1.0 - pow(0.9, t);
             bc_lat[2 * g + 1] = 1.0 - pow(0.999, t);
-            P.lat_ok[g] = 1;
         }
     }
     if (threadIdx.x != 0) return;
@@ -66,6 +65,7 @@ __global__ void __launch_bounds__(256) k_nn_reduce(const Plan* __restrict__ pp,
             if (p < R.param_off || p >= R.param_off + R.count) continue;
             const double* col = P.partials + R.base + (p - R.param_off);
             double s = 0.0;
+#pragma unroll 4
             for (int b = lane; b < R.nblocks; b += 32) s += col[int64_t(b) * R.count];
             sum += warp_sum(s);
         }

@@ -214,17 +214,6 @@ __global__ void __launch_bounds__(kThreadsWide) k_ups_fwd_coarse(const Plan* __r
     }
 }
 
-// z plane 0 is main grid 0 itself (synthesis.hpp:62-64).
-__global__ void k_copy_z0(const Plan* __restrict__ pp) {
-    const Plan& P = *pp;
-    const GridGeom& g = P.g[P.main_gi[0]];
-    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < P.npix;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int r = int(e / P.W), c = int(e - int64_t(r) * P.W);
-        P.z[P.zpix[0] + e] = P.yhat_pad[g.pad_base + int64_t(r) * g.stride + c];
-    }
-}
-
 // --------------------------------------------------------------- backward
 // (r', d) pairs with clamp(r' + d) == r, r' in [0, n): the transposed
 // replicate-padded 3-tap stencil.
@@ -670,7 +659,7 @@ void ups_configure() {
 
 void launch_ups_forward(const LaunchCtx& L) {
     const Plan& H = *L.host;
-    k_copy_z0<<<L.pix_blocks, 256, 0, L.stream>>>(L.plan);
+    // z plane 0 (= ŷ of main grid 0) is written by k_softq_fwd / k_pads_from_q
     const int jc = H.ups_jc;
     if (jc <= H.L - 2) k_ups_fwd_coarse<<<H.L - 1 - jc, kThreadsWide, 0, L.stream>>>(L.plan, jc);
     for (int j = jc - 1; j >= 0; --j) {
