@@ -78,7 +78,7 @@ cc_encoder_config default_enc() {
     c.hardround_lr = 1e-4;
     c.lambda = 0.001;
     c.seed = 0;
-    c.use_soap = 0;  // SURVEY D4 (the reference default is SOAP)
+    c.use_soap = 1;  // EncoderConfig{} (config.hpp:107); the benchmarks set 0
     c.true_cost_interval = 1000;
     c.log_path = nullptr;
     return c;

@@ -69,6 +69,12 @@ void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, double* c
 void launch_nn_reduce(const LaunchCtx& L);
 void launch_nn_apply(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log);
 void launch_sched_load(const LaunchCtx& L, const double* sched);
+
+// SOAP for the NN parameters (cc_soap.cu)
+size_t soap_smem(const Plan& H);
+void soap_configure(const Plan& H);
+void launch_soap_apply(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log);
+void launch_soap_reset(const LaunchCtx& L);
 void launch_snapshot_if_better(const LaunchCtx& L, int slot, float* snap_y, float* snap_p);
 
 }  // namespace ccb

@@ -114,6 +114,10 @@ struct Plan {
     int off_pw[2], off_pb[2];
     int off_sstab;  // -1 if none
     int tensor_off[kMaxTensors], tensor_size[kMaxTensors];
+    int tensor_rows[kMaxTensors], tensor_cols[kMaxTensors];  // MatView::of shape
+    // SOAP (use_soap): per tensor L (r x r), R (c x c), QL, QR in fp64
+    int use_soap, soap_dmax, soap_nmax;
+    int64_t soap_off[kMaxTensors];
 
     // ---- partial regions ----
     int n_regions;
@@ -158,6 +162,7 @@ struct Plan {
     float* params;
     float* grads;
     double* grads_d;          // the same gradients before rounding (band reduction)
+    double* soap;             // SOAP preconditioners / eigenbases (use_soap)
     float* nn_m;
     float* nn_v;
     double* partials;

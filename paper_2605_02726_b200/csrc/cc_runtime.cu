@@ -83,10 +83,7 @@ void Trainer::init(const float* image, int h, int w) {
     if (h < 1 || w < 1) throw ConfigError("image dimensions must be positive");
     log_path_ = enc.log_path ? enc.log_path : "";
     enc_.log_path = nullptr;
-    if (enc.use_soap)
-        throw ConfigError(
-            "use_soap = true is not implemented by the B200 trainer (NN params use Adam, "
-            "EncoderConfig::use_soap = false)");
+
     H_.H = h;
     H_.W = w;
     CCB_CUDA(cudaSetDevice(device_));
@@ -121,6 +118,7 @@ Trainer::~Trainer() {
     for (auto& kv : cands_) {
         for (float* p : {kv.second.y, kv.second.m, kv.second.v, kv.second.p, kv.second.nm, kv.second.nv})
             cudaFree(p);
+        if (kv.second.soap) cudaFree(kv.second.soap);
     }
     for (auto& kv : snaps_) {
         cudaFree(kv.second.y);
@@ -323,10 +321,24 @@ void Trainer::build_plan() {
     P.n_params = off;
     P.n_tensors = int(tensors_.size());
     if (P.n_tensors > kMaxTensors) throw ConfigError("too many tensors");
+    P.use_soap = enc_.use_soap ? 1 : 0;
+    P.soap_dmax = 1;
+    P.soap_nmax = 1;
+    int64_t soap_cur = 0;
     for (int t = 0; t < P.n_tensors; ++t) {
         P.tensor_off[t] = tensors_[t].offset;
         P.tensor_size[t] = tensors_[t].size;
+        P.tensor_rows[t] = tensors_[t].rows;
+        P.tensor_cols[t] = tensors_[t].cols;
+        P.soap_off[t] = soap_cur;
+        const int r = tensors_[t].rows, c = tensors_[t].cols;
+        soap_cur += 2 * int64_t(r) * r + 2 * int64_t(c) * c;
+        P.soap_dmax = std::max(P.soap_dmax, std::max(r, c));
+        P.soap_nmax = std::max(P.soap_nmax, r * c);
     }
+    sizes_.soap = P.use_soap ? soap_cur : 0;
+    if (P.use_soap && soap_smem(P) > 227 * 1024)
+        throw ConfigError("SOAP: a parameter matrix is too large for the on-chip step");
 
     // ---- upsampling stages (synthesis.hpp:66-92) ----
     // Cascade k runs on rows aligned to its latent window: level j holds
@@ -498,6 +510,7 @@ void Trainer::allocate() {
     P.params = f32(P.n_params);
     P.grads = f32(P.n_params);
     P.grads_d = static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_params)));
+    P.soap = P.use_soap ? static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.soap))) : nullptr;
     P.nn_m = f32(P.n_params);
     P.nn_v = f32(P.n_params);
     P.partials = static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.partials)));
@@ -528,6 +541,7 @@ void Trainer::allocate() {
     ups_configure();
     syn_post_configure();
     pyramid_configure(H_);
+    if (P.use_soap) soap_configure(H_);
 }
 
 void Trainer::synchronize() { CCB_CUDA(cudaStreamSynchronize(stream_)); }
@@ -596,6 +610,16 @@ void Trainer::reset_optimizers() {
     CCB_CUDA(cudaMemsetAsync(H_.nn_v, 0, sizeof(float) * np, stream_));
     CCB_CUDA(cudaMemsetAsync(H_.lat_t, 0, sizeof(int64_t) * kMaxGrids, stream_));
     CCB_CUDA(cudaMemsetAsync(H_.nn_t, 0, sizeof(int64_t) * kMaxTensors, stream_));
+    if (H_.use_soap) launch_soap_reset(L_);  // SoapState::init (optim.hpp:130-143)
+}
+
+// NN-parameter optimizer step: Adam, or SOAP when EncoderConfig::use_soap
+// (NnOptimizer::step, optim.hpp:277-286).
+void Trainer::nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, double* cost_log) {
+    if (H_.use_soap)
+        launch_soap_apply(ctx, do_step, count_iter, cost_log);
+    else
+        launch_nn_apply(ctx, do_step, count_iter, cost_log);
 }
 
 // ---------------------------------------------------------------- sequences
@@ -638,7 +662,7 @@ void Trainer::enqueue_proxy(bool batched) {
     launch_latent_grad(L_);
     join();
     fork();
-    launch_nn_apply(side(), true, true, batched ? d_rec_ : nullptr);
+    nn_apply(side(), true, true, batched ? d_rec_ : nullptr);
     launch_adam_latents(L_);
     join();
 }
@@ -655,7 +679,8 @@ void Trainer::enqueue_hardround(int slot) {
     launch_finalize(L_, kArmHard, slot);
     CCB_CUDA(cudaMemsetAsync(H_.lat_g, 0, sizeof(float) * size_t(H_.n_latents), stream_));
     if (slot >= 0) launch_snapshot_if_better(L_, slot, snaps_.at(slot).y, snaps_.at(slot).p);
-    launch_nn_step(L_, true, true, nullptr);
+    launch_nn_reduce(L_);
+    nn_apply(L_, true, true, nullptr);
 }
 
 // Trainer::true_cost (encoder.hpp:158-168)
@@ -783,7 +808,7 @@ void Trainer::band_step(const int* lat_ok) {
     CCB_CUDA(cudaMemcpyAsync(H_.lat_ok, lat_ok, sizeof(int) * size_t(H_.n_grids),
                              cudaMemcpyHostToDevice, stream_));
     launch_adam_latents(L_);
-    launch_nn_apply(L_, true, true, nullptr);
+    nn_apply(L_, true, true, nullptr);
     read_scalars();
 }
 
@@ -907,7 +932,8 @@ void Trainer::profile_stages(int n, double lr, double temp, double noise, double
         launch_finalize(L_, kArmProxy, -1);
         launch_latent_grad(L_);
         launch_adam_latents(L_);
-        launch_nn_step(L_, true, true, nullptr);
+        launch_nn_reduce(L_);
+        nn_apply(L_, true, true, nullptr);
         CCB_CUDA(cudaEventRecord(ev[8], stream_));
         CCB_CUDA(cudaEventSynchronize(ev[8]));
         for (int s = 0; s < NS; ++s) {
@@ -1035,6 +1061,7 @@ void Trainer::take_candidate(int slot, double cost) {
         CCB_CUDA(cudaMalloc(&c.p, sizeof(float) * np));
         CCB_CUDA(cudaMalloc(&c.nm, sizeof(float) * np));
         CCB_CUDA(cudaMalloc(&c.nv, sizeof(float) * np));
+        if (H_.use_soap) CCB_CUDA(cudaMalloc(&c.soap, sizeof(double) * size_t(sizes_.soap)));
     }
     auto cp = [&](void* d, const void* s, size_t b) {
         CCB_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToDevice, stream_));
@@ -1045,6 +1072,7 @@ void Trainer::take_candidate(int slot, double cost) {
     cp(c.p, H_.params, sizeof(float) * np);
     cp(c.nm, H_.nn_m, sizeof(float) * np);
     cp(c.nv, H_.nn_v, sizeof(float) * np);
+    if (H_.use_soap) cp(c.soap, H_.soap, sizeof(double) * size_t(sizes_.soap));
     c.lat_t.resize(kMaxGrids);
     c.nn_t.resize(kMaxTensors);
     CCB_CUDA(cudaMemcpyAsync(c.lat_t.data(), H_.lat_t, sizeof(int64_t) * kMaxGrids,
@@ -1070,6 +1098,7 @@ void Trainer::load_candidate(int slot) {
     cp(H_.params, c.p, sizeof(float) * np);
     cp(H_.nn_m, c.nm, sizeof(float) * np);
     cp(H_.nn_v, c.nv, sizeof(float) * np);
+    if (H_.use_soap) cp(H_.soap, c.soap, sizeof(double) * size_t(sizes_.soap));
     CCB_CUDA(cudaMemcpyAsync(H_.lat_t, c.lat_t.data(), sizeof(int64_t) * kMaxGrids,
                              cudaMemcpyHostToDevice, stream_));
     CCB_CUDA(cudaMemcpyAsync(H_.nn_t, c.nn_t.data(), sizeof(int64_t) * kMaxTensors,
@@ -1078,6 +1107,7 @@ void Trainer::load_candidate(int slot) {
     synchronize();
     cur_cost_ = c.cost;
     for (float* p : {c.y, c.m, c.v, c.p, c.nm, c.nv}) cudaFree(p);
+    if (c.soap) cudaFree(c.soap);
     cands_.erase(it);
     loaded_ = true;
 }
@@ -1088,6 +1118,7 @@ void Trainer::discard_candidate(int slot) {
     CandSlot& c = it->second;
     synchronize();
     for (float* p : {c.y, c.m, c.v, c.p, c.nm, c.nv}) cudaFree(p);
+    if (c.soap) cudaFree(c.soap);
     cands_.erase(it);
 }
 
@@ -1118,6 +1149,8 @@ void Trainer::set_counters(int64_t gi, int skipped) {
 void Trainer::set_state(const float* lat, const float* par, const float* lm, const float* lv,
                         const int64_t* lt, const float* nm, const float* nv, const int64_t* nt) {
     require_loaded();
+    if (H_.use_soap && (nm || nv || nt))  // as the reference ABI (oracle/ref_capi.cpp)
+        throw ConfigError("optimizer state transfer needs use_soap = false");
     const size_t nl = size_t(H_.n_latents), np = size_t(H_.n_params);
     auto up = [&](void* d, const void* s, size_t b) {
         if (s) CCB_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyHostToDevice, stream_));
@@ -1136,6 +1169,8 @@ void Trainer::set_state(const float* lat, const float* par, const float* lm, con
 void Trainer::get_state(float* lat, float* par, float* lm, float* lv, int64_t* lt, float* nm,
                         float* nv, int64_t* nt) {
     require_loaded();
+    if (H_.use_soap && (nm || nv || nt))
+        throw ConfigError("optimizer state transfer needs use_soap = false");
     const size_t nl = size_t(H_.n_latents), np = size_t(H_.n_params);
     auto dn = [&](void* d, const void* s, size_t b) {
         if (d) CCB_CUDA(cudaMemcpyAsync(d, s, b, cudaMemcpyDeviceToHost, stream_));

@@ -45,6 +45,7 @@ struct GridInfo {
 // Device buffers of one CandidateState (encoder.hpp:42-48).
 struct CandSlot {
     float *y = nullptr, *m = nullptr, *v = nullptr, *p = nullptr, *nm = nullptr, *nv = nullptr;
+    double* soap = nullptr;
     std::vector<int64_t> lat_t, nn_t;
     double cost = 0.0;
 };
@@ -129,6 +130,7 @@ public:
 
 private:
     void init(const float* image, int h, int w);
+    void nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, double* cost_log);
     void build_plan();
     void allocate();
     void require_loaded() const;
@@ -173,7 +175,7 @@ private:
     // captured graphs: 0 proxy(single), 1 proxy(batched), 2 true_cost, 100+slot hardround
     std::map<int, cudaGraphExec_t> graphs_;
     struct Sizes {
-        int64_t pad = 0, dctx = 0, dfeat = 0, ups = 0, partials = 0, z = 0;
+        int64_t pad = 0, dctx = 0, dfeat = 0, ups = 0, partials = 0, z = 0, soap = 0;
     } sizes_;
     struct BandSpec {
         bool on = false;

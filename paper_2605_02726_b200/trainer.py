@@ -439,9 +439,13 @@ class Trainer:
                   lat_t=np.empty(len(self.grids), np.int64),
                   nn_m=np.empty(npar, np.float32), nn_v=np.empty(npar, np.float32),
                   nn_t=np.empty(len(self.params), np.int64))
+        if self.enc.use_soap:  # SOAP state does not transfer (as the reference ABI)
+            st["nn_m"] = st["nn_v"] = st["nn_t"] = None
         _check(self.lib, self.lib.cc_trainer_get_state(
             self._h, _fp(st["latents"]), _fp(st["params"]), _fp(st["lat_m"]), _fp(st["lat_v"]),
-            _ip(st["lat_t"]), _fp(st["nn_m"]), _fp(st["nn_v"]), _ip(st["nn_t"])))
+            _ip(st["lat_t"]), None if st["nn_m"] is None else _fp(st["nn_m"]),
+            None if st["nn_v"] is None else _fp(st["nn_v"]),
+            None if st["nn_t"] is None else _ip(st["nn_t"])))
         st["global_iter"], st["skipped_steps"] = self.counters()
         return st
 

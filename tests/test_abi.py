@@ -69,7 +69,7 @@ def test_with_total_matches_reference(product_lib, ref_lib, total):
     assert product_lib.cc_encoder_config_with_total(total, C.byref(a)) == 0
     assert ref_lib.cc_encoder_config_with_total(total, C.byref(b)) == 0
     keys = ["warmup_candidates", "warmup_keep", "warmup_iters", "main_iters", "hardround_iters"]
-    assert [getattr(a, k) for k in keys] == [getattr(b, k) for k in keys]
+    assert [getattr(a, k) for k in keys + ["use_soap"]] == [getattr(b, k) for k in keys + ["use_soap"]]
     py = EncoderConfig.with_total(total)
     assert [getattr(py, k) for k in keys] == [getattr(b, k) for k in keys]
 

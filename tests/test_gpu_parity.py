@@ -270,3 +270,37 @@ def test_cfg2_size_properties(gpu_lib):
         assert np.isfinite(tc) and bpp > 0
         q = tr.get_q()
         assert np.abs(q).max() <= 255
+
+
+def test_soap_free_running_matches_reference(gpu_lib, ref_lib):
+    """use_soap = true (the reference default, config.hpp:107): soap_step with
+    the Jacobi eigenbasis refresh every 10 steps (optim.hpp:60-250), same
+    initial state on both sides, free-running: RD cost per iteration and the
+    parameters after 12 iterations (two eigenbasis refreshes)."""
+    img = make_image(ref_lib, 64, 96, seed=7)
+    enc = EncoderConfig(lmbda=1e-3, seed=5, use_soap=True)
+    dcfg = DecoderConfig.hop()
+    with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
+        tr_r.fresh_candidate(0)
+        tr_g.fresh_candidate(0)
+        for it in range(12):
+            cr = tr_r.proxy_iteration(1e-2, 0.35, 0.22)
+            cg = tr_g.proxy_iteration(1e-2, 0.35, 0.22)
+            assert abs(cr - cg) <= 1e-4 * abs(cr), (it, cr, cg)
+        pr = tr_r.get_state()["params"]
+        pg = tr_g.get_state()["params"]
+        for ti, p in enumerate(tr_r.params):
+            assert rel_l2(tr_g.param_view(pg, ti), tr_r.param_view(pr, ti)) <= 1e-3, p.name
+        assert tr_g.counters() == tr_r.counters()
+
+
+def test_soap_full_train_final_rd_within_half_percent(gpu_lib, ref_lib):
+    img = make_image(ref_lib, 40, 48, seed=3)
+    enc = EncoderConfig.with_total(600)
+    enc.lmbda, enc.seed, enc.use_soap, enc.true_cost_interval = 1e-3, 4, True, 50
+    with Trainer(img, enc, DecoderConfig.lop(), lib=ref_lib) as tr_r:
+        rr = tr_r.train()
+    with Trainer(img, enc, DecoderConfig.lop(), lib=gpu_lib) as tr_g:
+        rg = tr_g.train()
+    assert rg.stats.iterations == rr.stats.iterations == enc.total_iters()
+    assert abs(rg.stats.true_cost - rr.stats.true_cost) / rr.stats.true_cost <= 5e-3
