@@ -40,6 +40,11 @@ int ccb_fp32_peak(int device, double* tflops, double* ms);
 int ccb_eval_math(int fn, int n, const float* a, const float* b, const float* c, float* out);
 /* counter_gauss(stream, idx0 + i) for i < n, on the device. */
 int ccb_counter_gauss(uint64_t stream, uint64_t idx0, int n, float* out);
+/* SOAP state of a use_soap trainer (tests): *n_arena doubles of per-tensor
+ * L, R, QL, QR (for_each_param order, row-major, L r x r, R c x c) into arena,
+ * the moments m1 / v2 (fp32, n_params) and the step counters (n_tensors).
+ * Any output may be NULL. */
+int ccb_soap_state(cc_trainer* tr, double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena);
 
 #ifdef __cplusplus
 }

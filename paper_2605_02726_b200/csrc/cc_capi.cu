@@ -643,6 +643,13 @@ int ccb_counter_gauss(uint64_t stream, uint64_t idx0, int n, float* out) {
     });
 }
 
+int ccb_soap_state(cc_trainer* t, double* arena, float* m1, float* v2, int64_t* steps, int64_t* n_arena) {
+    return guarded([&] {
+        t->tr->soap_state(arena, m1, v2, steps, n_arena);
+        return CC_OK;
+    });
+}
+
 int cc_trainer_warmup(cc_trainer* t) {
     return guarded([&] {
         ccb::warmup(*t->tr);

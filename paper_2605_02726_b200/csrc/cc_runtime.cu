@@ -1186,6 +1186,22 @@ void Trainer::get_state(float* lat, float* par, float* lm, float* lv, int64_t* l
     synchronize();
 }
 
+void Trainer::soap_state(double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena) {
+    require_loaded();
+    if (!H_.use_soap) throw ConfigError("not a SOAP trainer (use_soap = false)");
+    if (n_arena) *n_arena = sizes_.soap;
+    const size_t np = size_t(H_.n_params);
+    if (arena)
+        CCB_CUDA(cudaMemcpyAsync(arena, H_.soap, sizeof(double) * size_t(sizes_.soap),
+                                 cudaMemcpyDeviceToHost, stream_));
+    if (m1) CCB_CUDA(cudaMemcpyAsync(m1, H_.nn_m, sizeof(float) * np, cudaMemcpyDeviceToHost, stream_));
+    if (v2) CCB_CUDA(cudaMemcpyAsync(v2, H_.nn_v, sizeof(float) * np, cudaMemcpyDeviceToHost, stream_));
+    if (t)
+        CCB_CUDA(cudaMemcpyAsync(t, H_.nn_t, sizeof(int64_t) * size_t(H_.n_tensors),
+                                 cudaMemcpyDeviceToHost, stream_));
+    synchronize();
+}
+
 void Trainer::get_grads(float* lg, float* pg) {
     require_loaded();
     if (lg)

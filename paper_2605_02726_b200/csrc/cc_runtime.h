@@ -116,6 +116,7 @@ public:
     void get_state(float* lat, float* par, float* lm, float* lv, int64_t* lt, float* nm,
                    float* nv, int64_t* nt);
     void get_grads(float* lg, float* pg);
+    void soap_state(double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena);
     void get_q(int32_t* q);
     void get_params(float* p);
 
