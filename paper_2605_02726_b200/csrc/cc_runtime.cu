@@ -105,6 +105,7 @@ void Trainer::init(const float* image, int h, int w) {
     }
     CCB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     CCB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+    CCB_CUDA(cudaEventCreateWithFlags(&ev_sched_, cudaEventDisableTiming));
     stream_ = own_stream_;
     build_plan();
     allocate();
@@ -128,9 +129,12 @@ Trainer::~Trainer() {
     if (h_scal_) cudaFreeHost(h_scal_);
     if (d_sched_) cudaFree(d_sched_);
     if (d_rec_) cudaFree(d_rec_);
+    if (h_rec_) cudaFreeHost(h_rec_);
+    if (h_sched_) cudaFreeHost(h_sched_);
     if (side_stream_) cudaStreamSynchronize(side_stream_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
+    if (ev_sched_) cudaEventDestroy(ev_sched_);
     if (side_stream_) cudaStreamDestroy(side_stream_);
     if (own_stream_) cudaStreamDestroy(own_stream_);
 }
@@ -856,9 +860,8 @@ void Trainer::proxy_iterations(int n, const double* lr, const double* temp, cons
 void Trainer::last_records(int n, double* rec) {
     if (n <= 0) return;
     if (n > sched_cap_) throw ConfigError("more records requested than the last batch holds");
-    CCB_CUDA(cudaMemcpyAsync(rec, d_rec_, sizeof(double) * 4 * size_t(n), cudaMemcpyDeviceToHost,
-                             stream_));
-    read_scalars();
+    read_scalars();  // synchronises the stream: the per-iteration copies have landed
+    std::memcpy(rec, h_rec_, sizeof(double) * 4 * size_t(n));
     last_mse_ = rec[4 * size_t(n - 1) + 1];
     last_bits_ = rec[4 * size_t(n - 1) + 2];
 }
@@ -880,6 +883,10 @@ void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* te
         if (d_rec_) cudaFree(d_rec_);
         CCB_CUDA(cudaMalloc(&d_sched_, sizeof(double) * 3 * size_t(n)));
         CCB_CUDA(cudaMalloc(&d_rec_, sizeof(double) * 4 * size_t(n)));
+        if (h_rec_) cudaFreeHost(h_rec_);
+        CCB_CUDA(cudaMallocHost(&h_rec_, sizeof(double) * 4 * size_t(n)));
+        if (h_sched_) cudaFreeHost(h_sched_);
+        CCB_CUDA(cudaMallocHost(&h_sched_, sizeof(double) * 3 * size_t(n)));
         sched_cap_ = n;
         auto it = graphs_.find(1);
         if (it != graphs_.end()) {
@@ -887,16 +894,23 @@ void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* te
             graphs_.erase(it);
         }
     }
-    std::vector<double> s(3 * size_t(n));
-    for (int i = 0; i < n; ++i) {
-        s[3 * i] = lr[i];
-        s[3 * i + 1] = temp[i];
-        s[3 * i + 2] = noise[i];
+    CCB_CUDA(cudaEventSynchronize(ev_sched_));  // the previous batch's upload has left h_sched_
+    for (int i = 0; i < n; ++i) {  // the schedule goes up from pinned memory
+        h_sched_[3 * i] = lr[i];
+        h_sched_[3 * i + 1] = temp[i];
+        h_sched_[3 * i + 2] = noise[i];
     }
-    CCB_CUDA(cudaMemcpyAsync(d_sched_, s.data(), sizeof(double) * s.size(), cudaMemcpyHostToDevice,
+    CCB_CUDA(cudaMemcpyAsync(d_sched_, h_sched_, sizeof(double) * 3 * size_t(n), cudaMemcpyHostToDevice,
                              stream_));
+    CCB_CUDA(cudaEventRecord(ev_sched_, stream_));
     CCB_CUDA(cudaMemsetAsync(&H_.scal->sched_pos, 0, sizeof(int64_t), stream_));
-    for (int i = 0; i < n; ++i) run_graph(1);
+    // every iteration's record (cost, mse, bits, global_iter) goes to pinned
+    // host memory right after the iteration, without a host synchronisation
+    for (int i = 0; i < n; ++i) {
+        run_graph(1);
+        CCB_CUDA(cudaMemcpyAsync(h_rec_ + 4 * size_t(i), d_rec_ + 4 * size_t(i), 4 * sizeof(double),
+                                 cudaMemcpyDeviceToHost, stream_));
+    }
 }
 
 // Stage-by-stage replay of one proxy iteration with events in between

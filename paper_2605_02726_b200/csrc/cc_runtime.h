@@ -157,6 +157,7 @@ private:
     cudaStream_t own_stream_ = nullptr;
     cudaStream_t side_stream_ = nullptr;  // concurrent rate branch
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    cudaEvent_t ev_sched_ = nullptr;  // the pinned schedule upload of the last batch
     Plan H_{};
     Plan* d_plan_ = nullptr;
     LaunchCtx L_{};
@@ -166,6 +167,8 @@ private:
     int2* d_tiles_ = nullptr;
     double* d_sched_ = nullptr;     // 3 doubles per iteration (batched)
     double* d_rec_ = nullptr;       // 4 doubles per iteration (batched)
+    double* h_rec_ = nullptr;       // pinned mirror, filled after every iteration
+    double* h_sched_ = nullptr;     // pinned schedule staging
     int sched_cap_ = 0;
     DevScalars* h_scal_ = nullptr;  // pinned mirror
     bool loaded_ = false;
