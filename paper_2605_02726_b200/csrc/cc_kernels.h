@@ -34,6 +34,7 @@ void launch_latent_grad_partial(const LaunchCtx& L);  // row bands: ignore the l
 void launch_band_own_finite(const LaunchCtx& L);
 void launch_adam_latents(const LaunchCtx& L);
 void launch_init_latents(const LaunchCtx& L, uint64_t stream, float amp);
+void launch_noise_ahead(const LaunchCtx& L);
 
 // entropy model (cc_arm.cu)
 bool arm_dims_supported(int D, int W);

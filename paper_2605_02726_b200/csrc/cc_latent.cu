@@ -43,6 +43,9 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
     const float noise_std = float(P.scal->noise);   // encoder.hpp:108
     const int64_t n = P.n_latents;
     const uint64_t giter = uint64_t(P.scal->global_iter);
+    // the unit Gaussians of this iteration, if the previous iteration drew them
+    // ahead (k_noise_ahead) for the counter value it ended with
+    const bool pre = P.noise_buf != nullptr && P.scal->noise_iter == P.scal->global_iter;
     const float inv_denom = 1.0f / softround_denom(temp);
     const float inv_t = 1.0f / temp;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
@@ -57,8 +60,14 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
         const float t1 = cc_tanh(d * inv_t);
         float o = f + 0.5f + t1 * inv_denom;
         if (noise_std > 0.0f) {
-            const uint64_t stream = hash_combine(hash_combine(P.seed, giter), uint64_t(gi));
-            o += noise_std * counter_gauss(stream, uint64_t(li + int64_t(g.row0) * g.cols));  // global raster index
+            float gz;
+            if (pre) {
+                gz = P.noise_buf[i];
+            } else {
+                const uint64_t stream = hash_combine(hash_combine(P.seed, giter), uint64_t(gi));
+                gz = counter_gauss(stream, uint64_t(li + int64_t(g.row0) * g.cols));  // global raster index
+            }
+            o += noise_std * gz;
         }
         f = floorf(o);
         d = o - f - 0.5f;
@@ -69,6 +78,25 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
         P.th1[i] = t1;
         P.th2[i] = t2;
     }
+}
+
+// The noise of the NEXT iteration (noise_stream(seed, global_iter + 1),
+// encoder.hpp:213-215): it depends only on the counter, so it is drawn on the
+// rate branch while the distortion branch of this iteration runs.  If this
+// iteration's cost turns out non-finite the counter does not advance and
+// k_softq_fwd draws inline instead.
+__global__ void k_noise_ahead(const Plan* __restrict__ pp) {
+    const Plan& P = *pp;
+    CCB_GRID_CACHE(P);
+    const uint64_t giter = uint64_t(P.scal->global_iter) + 1;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int gi = find_grid(s_off, i);
+        const GridGeom& g = P.g[gi];
+        const uint64_t stream = hash_combine(hash_combine(P.seed, giter), uint64_t(gi));
+        P.noise_buf[i] = counter_gauss(stream, uint64_t(i - g.lat_off + int64_t(g.row0) * g.cols));
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.scal->noise_iter = int64_t(giter);
 }
 
 __global__ void k_quantize(const Plan* __restrict__ pp, int amp) {
@@ -261,6 +289,9 @@ void launch_band_own_finite(const LaunchCtx& L) {
 }
 void launch_adam_latents(const LaunchCtx& L) {
     k_adam_latents<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+}
+void launch_noise_ahead(const LaunchCtx& L) {
+    k_noise_ahead<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
 }
 void launch_init_latents(const LaunchCtx& L, uint64_t stream, float amp) {
     k_init_latents<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, stream, amp);

@@ -163,6 +163,7 @@ struct Plan {
     float* grads;
     double* grads_d;          // the same gradients before rounding (band reduction)
     double* soap;             // SOAP preconditioners / eigenbases (use_soap)
+    float* noise_buf;         // unit Gaussians drawn ahead for scal->noise_iter
     float* nn_m;
     float* nn_v;
     double* partials;
@@ -187,6 +188,7 @@ struct DevScalars {
     int pad0;
     int64_t global_iter;      // encoder.hpp:71; keys the noise stream
     int64_t sched_pos;        // batched runs: index into the schedule arrays
+    int64_t noise_iter;       // global_iter the noise_buf values belong to (-1: none)
     double snap_cost[8];      // per snapshot slot
 };
 

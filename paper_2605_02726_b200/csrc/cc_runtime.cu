@@ -515,6 +515,7 @@ void Trainer::allocate() {
     P.grads = f32(P.n_params);
     P.grads_d = static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_params)));
     P.soap = P.use_soap ? static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.soap))) : nullptr;
+    P.noise_buf = f32(nl);
     P.nn_m = f32(P.n_params);
     P.nn_v = f32(P.n_params);
     P.partials = static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.partials)));
@@ -534,6 +535,7 @@ void Trainer::allocate() {
     CCB_CUDA(cudaMallocHost(&h_scal_, sizeof(DevScalars)));
     std::memset(h_scal_, 0, sizeof(DevScalars));
     for (int s = 0; s < kSnapSlots; ++s) h_scal_->snap_cost[s] = std::numeric_limits<double>::infinity();
+    h_scal_->noise_iter = -1;  // nothing drawn ahead yet
     CCB_CUDA(cudaMemcpy(P.scal, h_scal_, sizeof(DevScalars), cudaMemcpyHostToDevice));
 
     L_.plan = d_plan_;
@@ -652,6 +654,7 @@ void Trainer::enqueue_proxy(bool batched) {
     fork();
     launch_arm(side(), kArmProxy);
     launch_pyramid(side());
+    launch_noise_ahead(side());  // next iteration's noise, off the critical path
     launch_ups_forward(L_);
     launch_syn_forward(L_, true);
     launch_syn_backward(L_);
