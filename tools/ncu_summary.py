@@ -6,7 +6,7 @@ import subprocess
 import sys
 
 KEYS = {
-    "gpu__time_duration.sum": "duration_ns",
+    "gpu__time_duration.sum": "duration_us",
     "dram__bytes_read.sum": "dram_read_bytes",
     "dram__bytes_write.sum": "dram_write_bytes",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_throughput_pct",
@@ -37,12 +37,19 @@ for rep in sys.argv[1:]:
     if len(rows) < 3:
         continue
     hdr = rows[0]
+    units = dict(zip(hdr, rows[1]))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0,
+             "msecond": 1e3}
     for r in rows[2:]:
         d = dict(zip(hdr, r))
         k = {"report": rep.split("/")[-1], "kernel": d.get("Kernel Name", "")[:80]}
         for m, name in KEYS.items():
             if m in d:
-                k[name] = num(d[m])
+                v = num(d[m])
+                u = units.get(m, "")
+                if isinstance(v, float) and u in scale:
+                    v *= scale[u]  # bytes in bytes, durations in microseconds
+                k[name] = v
         if "dram_read_bytes" in k and "dram_write_bytes" in k:
             k["dram_bytes"] = k["dram_read_bytes"] + k["dram_write_bytes"]
         out.append(k)
