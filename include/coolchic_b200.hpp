@@ -6,17 +6,23 @@
 // libcoolchic_b200.so.  Names and signatures mirror
 //   coolcodec::detail::Trainer   (encoder.hpp:59-306)
 //   coolcodec::warmup / train    (encoder.hpp:315-413)
+//   coolcodec::select_nn_coding  (nn_coding.hpp:146-224), its decode passes on the GPU
+//   coolcodec::encode_image      (bitstream.hpp:187-228)
 // so switching an encoder to the GPU is a namespace change:
 //   coolcodec::TrainResult r = coolcodec::gpu::train(img, enc, dcfg);
 // Errors come back as the reference's exception types (tensor.hpp:11-25).
 #pragma once
 
+#include <algorithm>
+#include <chrono>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <string>
 #include <vector>
 
 #include "coolchic_b200.h"
+#include "coolchic_b200_codec.h"
 
 namespace coolcodec {
 namespace gpu {
@@ -152,6 +158,21 @@ public:
         });
     }
 
+    // forward-only decode passes (decode_core.hpp:38-63) on the device
+    void set_q(const LatentSet& lat) {
+        std::vector<int32_t> q;
+        q.reserve(size_t(layout_.n_latents));
+        for (const auto& g : lat.grids) q.insert(q.end(), g.q.begin(), g.q.end());
+        check(cc_trainer_set_q(t_, q.data()));
+    }
+    // which: 1 = latent_rate_estimate, 2 = mse_rgb(reconstruct_image), 3 = both
+    void decode_terms(DecoderModel& m, int which, double* rate_bits, double* mse) {
+        std::vector<float> p;
+        p.reserve(size_t(layout_.n_params));
+        for_each_param(m, [&](ParamTensor& t) { p.insert(p.end(), t.v.begin(), t.v.end()); });
+        check(cc_trainer_decode_terms(t_, p.data(), which, rate_bits, mse));
+    }
+
     cc_trainer* handle() { return t_; }
 
 private:
@@ -179,6 +200,123 @@ inline TrainResult train(const Image& img, const EncoderConfig& enc, const Decod
     r.stats.skipped_steps = st.skipped_steps;
     r.stats.seconds = st.seconds;
     return r;
+}
+
+// select_nn_coding (nn_coding.hpp:146-224) with every candidate evaluation —
+// a latent-rate estimate for ARM / IFCE candidates, a reconstruction MSE for
+// synthesis / upsampling candidates — done by the trainer's device decode
+// passes on its quantised latents (set with Trainer::set_q).  The search
+// order, tie rule (strict improvement, coarse-to-fine) and the bit accounting
+// are the reference's, through its own helpers.
+inline NnCodingResult select_nn_coding(Trainer& tr, const LatentSet& lat, DecoderModel& m,
+                                       double lambda) {
+    const double npix = double(lat.image_h) * double(lat.image_w);
+    NnCodingResult res;
+    double cur_rate = 0.0, cur_mse = 0.0, nn_bits = 0.0;
+    tr.decode_terms(m, 3, &cur_rate, &cur_mse);
+    for (int s = 0; s < kSubmoduleCount; ++s) {
+        const Submodule sub = Submodule(s);
+        const int which = (sub == Submodule::Arm || sub == Submodule::Ifce) ? 1 : 2;
+        auto sp = submodule_params(m, sub);
+        std::vector<std::vector<float>> keep_w, keep_b;
+        for (auto* t : sp.weights) keep_w.push_back(t->v);
+        for (auto* t : sp.biases) keep_b.push_back(t->v);
+        auto put_back = [&]() {
+            for (size_t i = 0; i < sp.weights.size(); ++i) sp.weights[i]->v = keep_w[i];
+            for (size_t i = 0; i < sp.biases.size(); ++i) sp.biases[i]->v = keep_b[i];
+        };
+        double best = std::numeric_limits<double>::infinity();
+        NnPartSpec bw, bb;
+        double b_rate = cur_rate, b_mse = cur_mse, b_bits = 0.0;
+        for (int iw = 0; iw < kNnDeltaCount; ++iw) {
+            const double dw = nn_delta_from_index(iw);
+            const auto qw = nn_detail::quantize_part(sp.weights, dw);
+            size_t wbits = 0;
+            const int kw = nn_detail::best_kappa(qw, &wbits);
+            for (int ib = 0; ib < kNnDeltaCount; ++ib) {
+                const double db = nn_delta_from_index(ib);
+                const auto qb = nn_detail::quantize_part(sp.biases, db);
+                size_t bbits = 0;
+                const int kb = nn_detail::best_kappa(qb, &bbits);
+                nn_detail::apply_dequant(sp.weights, qw, dw);
+                nn_detail::apply_dequant(sp.biases, qb, db);
+                double rate = cur_rate, mse = cur_mse;
+                tr.decode_terms(m, which, &rate, &mse);
+                const double bits = double(wbits + bbits) + 2.0 * double(nn_detail::kPartHeaderBits);
+                const double cost = mse + lambda * (rate + nn_bits + bits) / npix;
+                if (cost < best) {
+                    best = cost;
+                    bw = {iw, kw};
+                    bb = {ib, kb};
+                    b_rate = rate;
+                    b_mse = mse;
+                    b_bits = bits;
+                }
+                put_back();
+            }
+        }
+        nn_detail::apply_dequant(sp.weights,
+                                 nn_detail::quantize_part(sp.weights, nn_delta_from_index(bw.delta_idx)),
+                                 nn_delta_from_index(bw.delta_idx));
+        nn_detail::apply_dequant(sp.biases,
+                                 nn_detail::quantize_part(sp.biases, nn_delta_from_index(bb.delta_idx)),
+                                 nn_delta_from_index(bb.delta_idx));
+        res.spec.parts[size_t(s)][0] = bw;
+        res.spec.parts[size_t(s)][1] = bb;
+        nn_bits += b_bits;
+        cur_rate = b_rate;
+        cur_mse = b_mse;
+    }
+    res.payload = write_nn_payload(m, res.spec);
+    res.rate_bits = cur_rate;
+    res.mse = cur_mse;
+    res.cost = cur_mse + lambda * (cur_rate + 8.0 * double(res.payload.size())) / npix;
+    return res;
+}
+
+// encode_image (bitstream.hpp:187-228): training and the NN-coding search on
+// the GPU; the latent entropy coding and the bitstream assembly are the
+// reference's (not on the iteration path).
+inline EncodeResult encode_image(const Image& img, const EncoderConfig& enc,
+                                 const DecoderConfig& dcfg, int device = 0) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (img.h > 0xFFFF || img.w > 0xFFFF) throw ConfigError("image too large for header");
+    Trainer gt(img, enc, dcfg, device);
+    cc_train_stats st{};
+    check(cc_trainer_train(gt.handle(), &st, nullptr, nullptr, nullptr));
+    TrainResult tr;
+    gt.export_state(tr.latents, tr.model);
+    const ContextOffsets ctx = make_context_offsets(dcfg.spatial_ctx);
+    for (auto& g : tr.latents.grids) {
+        g.amp = measure_amplitude(g);
+        for (auto& q : g.q) q = std::min(std::max(q, -g.amp), g.amp);
+    }
+    gt.set_q(tr.latents);
+    NnCodingResult nn = select_nn_coding(gt, tr.latents, tr.model, enc.lambda);
+    const std::vector<uint8_t> latent_payload = encode_latents(tr.latents, tr.model, ctx);
+    BitstreamHeader h;
+    h.height = uint16_t(img.h);
+    h.width = uint16_t(img.w);
+    h.config_id = uint8_t(dcfg.preset);
+    for (const auto& g : tr.latents.grids) h.amps.push_back(uint8_t(g.amp));
+    h.nn_bytes = uint32_t(nn.payload.size());
+    h.latent_bytes = uint32_t(latent_payload.size());
+    EncodeResult res;
+    res.bytes = write_header(h);
+    res.bytes.insert(res.bytes.end(), nn.payload.begin(), nn.payload.end());
+    res.bytes.insert(res.bytes.end(), latent_payload.begin(), latent_payload.end());
+    res.recon = reconstruct_image(tr.latents, tr.model);
+    res.stats.file_bytes = res.bytes.size();
+    res.stats.nn_bytes = nn.payload.size();
+    res.stats.latent_bytes = latent_payload.size();
+    res.stats.bpp = 8.0 * double(res.bytes.size()) / (double(img.h) * double(img.w));
+    res.stats.psnr = psnr_rgb(img, res.recon);
+    res.stats.latent_rate_estimate_bits = total_rate_bits(tr.latents, tr.model, ctx);
+    res.stats.iterations = st.iterations;
+    res.stats.restarts = st.restarts;
+    res.stats.macs_per_pixel = count_macs_per_pixel(dcfg, img.h, img.w);
+    res.stats.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return res;
 }
 
 }  // namespace gpu

@@ -630,3 +630,44 @@ int ccref_parallel_proxy(const float* image, int h, int w, const cc_encoder_conf
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- decode passes
+#include "coolchic_b200_codec.h"
+
+extern "C" {
+
+int cc_trainer_set_q(cc_trainer* t, const int32_t* q) {
+    return guarded([&] {
+        auto& c = t->cur();
+        size_t o = 0;
+        for (auto& g : c.lat.grids) {
+            std::copy(q + o, q + o + g.count(), g.q.begin());
+            o += g.count();
+        }
+        return CC_OK;
+    });
+}
+
+int cc_trainer_decode_terms(cc_trainer* t, const float* params, int which, double* rate_bits,
+                            double* mse) {
+    return guarded([&] {
+        if (which < 1 || which > 3) throw ConfigError("which must be 1 (rate), 2 (mse) or 3");
+        auto& c = t->cur();
+        DecoderModel m = c.model;
+        if (params) {
+            size_t o = 0;
+            for_each_param(m, [&](ParamTensor& p) {
+                std::copy(params + o, params + o + p.size(), p.v.begin());
+                o += p.size();
+            });
+        }
+        if (which & 1) {
+            const ContextOffsets ctx = make_context_offsets(t->dec.spatial_ctx);
+            *rate_bits = latent_rate_estimate(c.lat, m, ctx);
+        }
+        if (which & 2) *mse = mse_rgb(reconstruct_image(c.lat, m), t->img);
+        return CC_OK;
+    });
+}
+
+}  // extern "C"

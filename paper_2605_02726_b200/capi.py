@@ -171,6 +171,12 @@ BAND_SIGNATURES = {
     "cc_band_step": (C.c_int, [_P, _I]),
 }
 
+# include/coolchic_b200_codec.h (product and reference checker): decode passes
+CODEC_SIGNATURES = {
+    "cc_trainer_set_q": (C.c_int, [_P, C.POINTER(C.c_int32)]),
+    "cc_trainer_decode_terms": (C.c_int, [_P, _F, C.c_int, _D, _D]),
+}
+
 DIAG_SIGNATURES = {
     "ccb_stage_name": (C.c_char_p, [C.c_int]),
     "ccb_profile_stages": (C.c_int, [_P, C.c_int, C.c_double, C.c_double, C.c_double, _D]),
@@ -203,6 +209,11 @@ def load_library(path: os.PathLike | str, diag: bool = False) -> C.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    for name, (res, args) in CODEC_SIGNATURES.items():  # absent from the plain-C port
+        if hasattr(lib, name):
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
     return lib
 
 

@@ -761,3 +761,26 @@ int cc_band_step(cc_trainer* t, const int* lat_ok) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- decode passes
+#include "../../include/coolchic_b200_codec.h"
+
+extern "C" {
+
+int cc_trainer_set_q(cc_trainer* t, const int32_t* q) {
+    return guarded([&] {
+        t->tr->set_q(q);
+        return CC_OK;
+    });
+}
+
+int cc_trainer_decode_terms(cc_trainer* t, const float* params, int which, double* rate_bits,
+                            double* mse) {
+    return guarded([&] {
+        if (which < 1 || which > 3) throw ccb::ConfigError("which must be 1 (rate), 2 (mse) or 3");
+        t->tr->decode_terms(params, which, rate_bits, mse);
+        return CC_OK;
+    });
+}
+
+}  // extern "C"

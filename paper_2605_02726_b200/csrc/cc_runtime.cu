@@ -1203,6 +1203,42 @@ void Trainer::get_state(float* lat, float* par, float* lm, float* lv, int64_t* l
     synchronize();
 }
 
+// ---------------------------------------------------------------- decode passes
+// encode_image's amplitude-clamped q (bitstream.hpp:194-197) -> device.
+void Trainer::set_q(const int32_t* q) {
+    require_loaded();
+    CCB_CUDA(cudaMemcpyAsync(H_.q, q, sizeof(int32_t) * size_t(H_.n_latents), cudaMemcpyHostToDevice,
+                             stream_));
+    launch_pads_from_q(L_);
+    synchronize();
+}
+
+// latent_rate_estimate / mse_rgb(reconstruct_image) (decode_core.hpp:38-63) on
+// the current q with `params` substituted for the call.
+void Trainer::decode_terms(const float* params, int which, double* bits, double* mse) {
+    require_loaded();
+    const size_t np = size_t(H_.n_params);
+    if (params) {
+        if (!d_param_save_) d_param_save_ = static_cast<float*>(dalloc(sizeof(float) * np));
+        CCB_CUDA(cudaMemcpyAsync(d_param_save_, H_.params, sizeof(float) * np, cudaMemcpyDeviceToDevice,
+                                 stream_));
+        CCB_CUDA(cudaMemcpyAsync(H_.params, params, sizeof(float) * np, cudaMemcpyHostToDevice, stream_));
+    }
+    launch_pads_from_q(L_);
+    if (which & 1) launch_arm(L_, kArmForward);
+    if (which & 2) {
+        launch_ups_forward(L_);
+        launch_syn_forward(L_, false);
+    }
+    launch_finalize(L_, kArmForward, -1);
+    if (params)
+        CCB_CUDA(cudaMemcpyAsync(H_.params, d_param_save_, sizeof(float) * np, cudaMemcpyDeviceToDevice,
+                                 stream_));
+    read_scalars();
+    if (bits && (which & 1)) *bits = h_scal_->bits;
+    if (mse && (which & 2)) *mse = h_scal_->mse;
+}
+
 void Trainer::soap_state(double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena) {
     require_loaded();
     if (!H_.use_soap) throw ConfigError("not a SOAP trainer (use_soap = false)");

@@ -117,6 +117,8 @@ public:
                    float* nv, int64_t* nt);
     void get_grads(float* lg, float* pg);
     void soap_state(double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena);
+    void set_q(const int32_t* q);
+    void decode_terms(const float* params, int which, double* bits, double* mse);
     void get_q(int32_t* q);
     void get_params(float* p);
 
@@ -169,6 +171,7 @@ private:
     double* d_rec_ = nullptr;       // 4 doubles per iteration (batched)
     double* h_rec_ = nullptr;       // pinned mirror, filled after every iteration
     double* h_sched_ = nullptr;     // pinned schedule staging
+    float* d_param_save_ = nullptr; // decode_terms: the trainer's own parameters
     int sched_cap_ = 0;
     DevScalars* h_scal_ = nullptr;  // pinned mirror
     bool loaded_ = false;

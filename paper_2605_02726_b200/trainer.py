@@ -464,6 +464,21 @@ class Trainer:
             _check(self.lib, self.lib.cc_trainer_set_counters(
                 self._h, int(st["global_iter"]), int(st.get("skipped_steps", 0))))
 
+    def set_q(self, q: np.ndarray) -> None:
+        """Quantised latents (flat layout) for the decode passes."""
+        qa = np.ascontiguousarray(q, dtype=np.int32)
+        _check(self.lib, self.lib.cc_trainer_set_q(self._h, qa.ctypes.data_as(C.POINTER(C.c_int32))))
+
+    def decode_terms(self, params: np.ndarray | None = None, which: int = 3):
+        """latent_rate_estimate / mse_rgb(reconstruct_image) (decode_core.hpp:38-63)
+        on the current q with `params` substituted: (rate_bits, mse); None for
+        a term not requested."""
+        b, m = C.c_double(np.nan), C.c_double(np.nan)
+        pa = None if params is None else np.ascontiguousarray(params, dtype=np.float32)
+        _check(self.lib, self.lib.cc_trainer_decode_terms(self._h, None if pa is None else _fp(pa), which,
+                                                          C.byref(b), C.byref(m)))
+        return (b.value if which & 1 else None), (m.value if which & 2 else None)
+
     def get_grads(self):
         lg = np.empty(self.n_latents, np.float32)
         pg = np.empty(self.n_params, np.float32)

@@ -26,7 +26,7 @@ def _exports(lib, names):
 
 def test_product_exports_every_declared_symbol(product_lib):
     names = (capi.header_symbols("coolchic_b200.h") + capi.header_symbols("coolchic_b200_diag.h")
-             + capi.header_symbols("coolchic_b200_band.h"))
+             + capi.header_symbols("coolchic_b200_band.h") + capi.header_symbols("coolchic_b200_codec.h"))
     assert len(names) >= 48
     assert _exports(product_lib, names) == []
     assert product_lib.cc_impl_name() == b"b200"
@@ -36,11 +36,13 @@ def test_signature_table_covers_header():
     assert sorted(capi.SIGNATURES) == capi.header_symbols("coolchic_b200.h")
     assert sorted(capi.DIAG_SIGNATURES) == capi.header_symbols("coolchic_b200_diag.h")
     assert sorted(capi.BAND_SIGNATURES) == capi.header_symbols("coolchic_b200_band.h")
+    assert sorted(capi.CODEC_SIGNATURES) == capi.header_symbols("coolchic_b200_codec.h")
 
 
 def test_checkers_export_the_same_abi(ref_lib, port_lib):
     names = capi.header_symbols("coolchic_b200.h")
     assert _exports(ref_lib, names) == []
+    assert _exports(ref_lib, capi.header_symbols("coolchic_b200_codec.h")) == []
     assert _exports(port_lib, names) == []
     assert ref_lib.cc_impl_name() == b"reference"
     assert port_lib.cc_impl_name() == b"port"

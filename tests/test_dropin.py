@@ -24,3 +24,19 @@ def test_cpp_dropin_train_matches_reference(gpu_lib):
     r = json.loads(out.strip().splitlines()[-1])
     assert r["gpu_iters"] == r["ref_iters"] == 600
     assert abs(r["gpu_cost"] - r["ref_cost"]) / r["ref_cost"] <= 5e-3
+
+
+def test_cpp_nn_coding_search_on_gpu_matches_reference(gpu_lib):
+    """gpu::select_nn_coding (decode passes on the device) picks the reference's
+    quantisation spec on the same trained state; gpu::encode_image runs end to end."""
+    exe = REF_DIR / "dropin_nncoding"
+    if not exe.exists():
+        pytest.skip("oracle/_ref/dropin_nncoding not built (needs /root/reference once)")
+    out = subprocess.run([str(exe), "48", "64", "600"], capture_output=True, text=True,
+                         timeout=900, check=True).stdout
+    r = json.loads(out.strip().splitlines()[-1])
+    assert abs(r["gpu_cost"] - r["ref_cost"]) <= 1e-5 * r["ref_cost"]
+    assert abs(r["gpu_rate"] - r["ref_rate"]) <= 1e-5 * r["ref_rate"]
+    assert abs(r["gpu_mse"] - r["ref_mse"]) <= 1e-5 * r["ref_mse"]
+    assert r["same_spec"] == 1 and r["same_payload"] == 1
+    assert r["encode_bytes"] > 0 and r["encode_psnr"] > 15

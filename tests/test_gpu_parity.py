@@ -363,3 +363,34 @@ def test_soap_full_train_final_rd(gpu_lib, ref_lib):
         rg = tr_g.train()
     assert rg.stats.iterations == rr.stats.iterations == enc.total_iters()
     assert abs(rg.stats.true_cost - rr.stats.true_cost) / rr.stats.true_cost <= 2e-2
+
+
+def test_decode_terms_match_reference(gpu_lib, ref_lib):
+    """latent_rate_estimate and mse_rgb(reconstruct_image) (decode_core.hpp:38-63)
+    on identical quantised latents and substituted parameters, as the
+    NN-quantisation search evaluates them (nn_coding.hpp:146-224)."""
+    img = make_image(ref_lib, 64, 96, seed=11)
+    enc, dcfg = EncoderConfig(lmbda=1e-3, seed=2), DecoderConfig.hop()
+    with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
+        tr_r.fresh_candidate(0)
+        for _ in range(20):
+            tr_r.proxy_iteration(1e-2, 0.35, 0.22)
+        tr_r.true_cost()
+        st = tr_r.get_state()
+        tr_g.fresh_candidate(0)
+        tr_g.set_state(st)
+        q = np.empty(tr_r.n_latents, np.int32)
+        assert ref_lib.cc_trainer_get_q(tr_r._h, q.ctypes.data_as(C.POINTER(C.c_int32))) == 0
+        q = np.clip(q, -3, 3)  # an amplitude clamp, as encode_image applies
+        tr_r.set_q(q)
+        tr_g.set_q(q)
+        rng = np.random.default_rng(0)
+        for k in range(3):
+            p = None if k == 0 else st["params"] * (1 + 0.05 * rng.standard_normal(st["params"].size)).astype(np.float32)
+            br, mr = tr_r.decode_terms(p)
+            bg, mg = tr_g.decode_terms(p)
+            assert abs(bg - br) <= 1e-5 * br, (k, br, bg)
+            assert abs(mg - mr) <= 1e-5 * mr, (k, mr, mg)
+            bg1, mg1 = tr_g.decode_terms(p, which=1)
+            assert mg1 is None and abs(bg1 - bg) <= 1e-12 * bg
+        assert np.array_equal(tr_g.get_state()["params"], st["params"])  # substitution is per call
