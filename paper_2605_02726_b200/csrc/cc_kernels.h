@@ -33,6 +33,8 @@ void launch_latent_grad(const LaunchCtx& L);
 void launch_latent_grad_partial(const LaunchCtx& L);  // row bands: ignore the local cost flag
 void launch_band_own_finite(const LaunchCtx& L);
 void launch_adam_latents(const LaunchCtx& L);
+void launch_latent_grad_grids(const LaunchCtx& L, int g_begin, int g_end);
+void launch_adam_latents_grids(const LaunchCtx& L, int g_begin, int g_end);
 void launch_init_latents(const LaunchCtx& L, uint64_t stream, float amp);
 void launch_noise_ahead(const LaunchCtx& L);
 
@@ -48,7 +50,7 @@ void pyramid_configure(const Plan& H);
 
 // upsampling (cc_ups.cu)
 void launch_ups_forward(const LaunchCtx& L);
-void launch_ups_backward(const LaunchCtx& L, bool latent_grads);
+void launch_ups_backward(const LaunchCtx& L, bool latent_grads, int j_begin = 0, int j_end = 1 << 30);
 int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward);
 int ups_coarse_from(const Plan& H);
 void ups_configure();

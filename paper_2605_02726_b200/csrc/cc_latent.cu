@@ -12,6 +12,7 @@
 //   k_init_latents init_latents_uniform                      latent.hpp:73-80
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "cc_kernels.h"
@@ -39,6 +40,7 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
     CCB_GRID_CACHE(P);
     // per-grid gradient-finiteness flags of this iteration (ANDed by k_latent_grad)
     if (blockIdx.x == 0 && threadIdx.x < kMaxGrids) P.lat_ok[threadIdx.x] = 1;
+    if (blockIdx.x == 0 && threadIdx.x < kMaxTensors) P.tensor_ok[threadIdx.x] = 1;  // ANDed by k_nn_reduce
     const float temp = float(P.scal->temp);         // encoder.hpp:98
     const float noise_std = float(P.scal->noise);   // encoder.hpp:108
     const int64_t n = P.n_latents;
@@ -130,7 +132,7 @@ __global__ void k_pads_from_q(const Plan* __restrict__ pp) {
 // successors, the IFCE terms W_f^T * (block sum of dF) from every equipped
 // finer grid, and the upsampling gradient for main grids.  Then the
 // soft-quantize backward chain rule and the per-grid finiteness flag.
-__global__ void k_latent_grad(const Plan* __restrict__ pp, int force) {
+__global__ void k_latent_grad(const Plan* __restrict__ pp, int force, int64_t i_begin, int64_t i_end) {
     const Plan& P = *pp;
     CCB_GRID_CACHE(P);
     const float temp = float(P.scal->temp);
@@ -146,7 +148,7 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp, int force) {
     }
     for (int k = threadIdx.x; k < P.n_grids; k += blockDim.x) s_geo[k] = P.g[k];
     __syncthreads();
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+    for (int64_t i = i_begin + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < i_end;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int gi = find_grid(s_off, i);
         const GridGeom& g = s_geo[gi];
@@ -203,20 +205,22 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp, int force) {
 // whose gradient has a non-finite element is left untouched.  bc1/bc2 were
 // computed per grid by k_finalize from lat_t + 1.  Block 0 / thread 0 also
 // advances the step counters (encoder.hpp:129-133).
-__global__ void k_adam_latents(const Plan* __restrict__ pp) {
+__global__ void k_adam_latents(const Plan* __restrict__ pp, int g_begin, int g_end) {
     const Plan& P = *pp;
     CCB_GRID_CACHE(P);
     const double lr = P.scal->lr;
     const double* __restrict__ bc = P.bc_lat;
     const int cost_ok = P.scal->cost_ok;
+    const int64_t i_begin = P.g[g_begin].lat_off;
+    const int64_t i_end = g_end < P.n_grids ? P.g[g_end].lat_off : P.n_latents;
     if (!cost_ok) {  // encoder.hpp:118 returns before the backward: grads stay zero
-        for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+        for (int64_t i = i_begin + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < i_end;
              i += int64_t(gridDim.x) * blockDim.x)
             P.lat_g[i] = 0.0f;
         return;
     }
     const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
+    for (int64_t i = i_begin + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < i_end;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int gi = find_grid(s_off, i);
         if (!P.lat_ok[gi]) continue;
@@ -229,7 +233,7 @@ __global__ void k_adam_latents(const Plan* __restrict__ pp) {
         P.y[i] = float(double(P.y[i]) - lr * (mt / bc1) / (sqrt(vt / bc2) + eps));
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        for (int gi = 0; gi < P.n_grids; ++gi) {
+        for (int gi = g_begin; gi < g_end; ++gi) {
             if (P.lat_ok[gi])
                 P.lat_t[gi] += 1;
             else
@@ -260,10 +264,23 @@ void launch_pads_from_q(const LaunchCtx& L) {
     k_pads_from_q<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
 }
 void launch_latent_grad(const LaunchCtx& L) {
-    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 0);
+    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 0, 0, L.host->n_latents);
 }
 void launch_latent_grad_partial(const LaunchCtx& L) {
-    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 1);
+    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 1, 0, L.host->n_latents);
+}
+// grids [g_begin, g_end) only (their latents are contiguous in decode order)
+void launch_latent_grad_grids(const LaunchCtx& L, int g_begin, int g_end) {
+    const Plan& H = *L.host;
+    const int64_t a = H.g[g_begin].lat_off, b = g_end < H.n_grids ? H.g[g_end].lat_off : H.n_latents;
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((b - a + 255) / 256, L.elem_blocks)));
+    k_latent_grad<<<blocks, 256, 0, L.stream>>>(L.plan, 0, a, b);
+}
+void launch_adam_latents_grids(const LaunchCtx& L, int g_begin, int g_end) {
+    const Plan& H = *L.host;
+    const int64_t a = H.g[g_begin].lat_off, b = g_end < H.n_grids ? H.g[g_end].lat_off : H.n_latents;
+    const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((b - a + 255) / 256, L.elem_blocks)));
+    k_adam_latents<<<blocks, 256, 0, L.stream>>>(L.plan, g_begin, g_end);
 }
 
 // Row bands: per-grid finiteness of the OWN rows' (complete) latent gradients,
@@ -288,7 +305,7 @@ void launch_band_own_finite(const LaunchCtx& L) {
     k_band_own_finite<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
 }
 void launch_adam_latents(const LaunchCtx& L) {
-    k_adam_latents<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+    k_adam_latents<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 0, L.host->n_grids);
 }
 void launch_noise_ahead(const LaunchCtx& L) {
     k_noise_ahead<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);

@@ -658,20 +658,24 @@ void Trainer::enqueue_proxy(bool batched) {
     launch_ups_forward(L_);
     launch_syn_forward(L_, true);
     launch_syn_backward(L_);
-    launch_ups_backward(L_, true);
+    launch_ups_backward(L_, true, 0, 1);
     join();
-    // gradient assembly: cost + NN-gradient reduction beside the latent
-    // gather; the NN Adam step waits for the gather (it reads the IFCE
-    // weights) and runs beside the latent Adam step
+    // The two finest grids (main levels 1, 0: ~93 % of the latents) have all
+    // their gradient terms once the first upsampling-backward stage is done:
+    // their gather and Adam step run beside the remaining (latency-bound)
+    // coarse upsampling-backward stages.  The NN Adam step waits for every
+    // gather (they read the IFCE weights).
+    const int fine = H_.L >= 2 ? H_.main_gi[1] : 0;
     fork();
     launch_finalize(side(), kArmProxy, -1);
-    launch_nn_reduce(side());
-    launch_latent_grad(L_);
+    launch_latent_grad_grids(side(), fine, H_.n_grids);
+    launch_adam_latents_grids(side(), fine, H_.n_grids);
+    launch_ups_backward(L_, true, 1);
+    launch_latent_grad_grids(L_, 0, fine);
+    launch_nn_reduce(L_);
     join();
-    fork();
-    nn_apply(side(), true, true, batched ? d_rec_ : nullptr);
-    launch_adam_latents(L_);
-    join();
+    if (fine > 0) launch_adam_latents_grids(L_, 0, fine);
+    nn_apply(L_, true, true, batched ? d_rec_ : nullptr);
 }
 
 // Trainer::hardround_iteration (encoder.hpp:141-155)

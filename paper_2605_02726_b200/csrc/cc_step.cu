@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, i
     for (int b = threadIdx.x; b < P.n_mse_part; b += blockDim.x) s_loc += P.mse_part[b];
     const double bits_all = block_sum(b_loc, red);
     const double se_all = block_sum(s_loc, red);
-    for (int t = threadIdx.x; t < P.n_tensors; t += blockDim.x) P.tensor_ok[t] = 1;
+    if (mode != kArmProxy)  // proxy iterations reset the flags in k_softq_fwd
+        for (int t = threadIdx.x; t < P.n_tensors; t += blockDim.x) P.tensor_ok[t] = 1;
     if (mode == kArmProxy) {  // Adam bias corrections of every latent grid, one thread each
         for (int g = threadIdx.x; g < P.n_grids; g += blockDim.x) {
             const double t = double(P.lat_t[g] + 1);

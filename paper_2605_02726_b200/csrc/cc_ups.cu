@@ -670,16 +670,16 @@ void launch_ups_forward(const LaunchCtx& L) {
     }
 }
 
-void launch_ups_backward(const LaunchCtx& L, bool latent_grads) {
+void launch_ups_backward(const LaunchCtx& L, bool latent_grads, int j_begin, int j_end) {
     const Plan& H = *L.host;
     const int jc = H.ups_jc;
-    for (int j = 0; j < jc && j <= H.L - 2; ++j) {
+    for (int j = j_begin; j < jc && j <= H.L - 2 && j < j_end; ++j) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, false), H.ups_n[j]);
         const int nt = int(grid.x * grid.y) < 2 * L.num_sms ? kThreadsWide : kThreads;
         k_ups_bwd<<<grid, nt, sizeof(BwdSmem), L.stream>>>(L.plan, j, latent_grads ? 1 : 0);
     }
-    if (jc <= H.L - 2)
+    if (jc <= H.L - 2 && j_end > H.L - 2)
         k_ups_bwd_coarse<<<H.L - 1 - jc, kThreadsWide, sizeof(BwdSmem), L.stream>>>(L.plan, jc,
                                                                                    latent_grads ? 1 : 0);
 }
