@@ -44,6 +44,10 @@ int ccb_counter_gauss(uint64_t stream, uint64_t idx0, int n, float* out);
  * L, R, QL, QR (for_each_param order, row-major, L r x r, R c x c) into arena,
  * the moments m1 / v2 (fp32, n_params) and the step counters (n_tensors).
  * Any output may be NULL. */
+/* Event timeline of one proxy iteration (graph with event marks, mean over n
+ * replays): ms[13] = time after the start of mark k (see cc_runtime.cu
+ * Trainer::enqueue_proxy; 0 = start). */
+int ccb_timeline(cc_trainer* tr, int n, double lr, double temp, double noise, double* ms);
 int ccb_soap_state(cc_trainer* tr, double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena);
 
 #ifdef __cplusplus

@@ -185,6 +185,7 @@ DIAG_SIGNATURES = {
     "ccb_fp32_peak": (C.c_int, [C.c_int, _D, _D]),
     "ccb_eval_math": (C.c_int, [C.c_int, C.c_int, _F, _F, _F, _F]),
     "ccb_counter_gauss": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, _F]),
+    "ccb_timeline": (C.c_int, [_P, C.c_int, C.c_double, C.c_double, C.c_double, _D]),
     "ccb_soap_state": (C.c_int, [_P, _D, _F, _F, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
 }
 

@@ -643,6 +643,13 @@ int ccb_counter_gauss(uint64_t stream, uint64_t idx0, int n, float* out) {
     });
 }
 
+int ccb_timeline(cc_trainer* t, int n, double lr, double temp, double noise, double* ms) {
+    return guarded([&] {
+        t->tr->timeline(n, lr, temp, noise, ms);
+        return CC_OK;
+    });
+}
+
 int ccb_soap_state(cc_trainer* t, double* arena, float* m1, float* v2, int64_t* steps, int64_t* n_arena) {
     return guarded([&] {
         t->tr->soap_state(arena, m1, v2, steps, n_arena);

@@ -69,7 +69,7 @@ int syn_post_tiles(int H, int W);
 // optimizer / bookkeeping (cc_step.cu)
 void launch_finalize(const LaunchCtx& L, int mode, int snap_slot);
 void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log);
-void launch_nn_reduce(const LaunchCtx& L);
+void launch_nn_reduce(const LaunchCtx& L, int p_begin = 0, int p_end = -1);
 void launch_nn_apply(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log);
 void launch_sched_load(const LaunchCtx& L, const double* sched);
 

@@ -648,17 +648,31 @@ LaunchCtx Trainer::side() const {
     return s;
 }
 
+// timeline diagnostics (ccb_timeline): event marks inside the captured sequence
+void Trainer::mark(int id, bool on_side) {
+    if (tl_ev_)  // an event-record node of the graph (timing), not a capture dependency
+        CCB_CUDA(cudaEventRecordWithFlags(tl_ev_[id], on_side ? side_stream_ : stream_, cudaEventRecordExternal));
+}
+
 void Trainer::enqueue_proxy(bool batched) {
+    mark(0, false);
     if (batched) launch_sched_load(L_, d_sched_);
     launch_softq_fwd(L_);
+    mark(1, false);
     fork();
     launch_arm(side(), kArmProxy);
+    mark(2, true);
     launch_pyramid(side());
     launch_noise_ahead(side());  // next iteration's noise, off the critical path
+    mark(3, true);
     launch_ups_forward(L_);
+    mark(4, false);
     launch_syn_forward(L_, true);
+    mark(5, false);
     launch_syn_backward(L_);
+    mark(6, false);
     launch_ups_backward(L_, true, 0, 1);
+    mark(7, false);
     join();
     // The two finest grids (main levels 1, 0: ~93 % of the latents) have all
     // their gradient terms once the first upsampling-backward stage is done:
@@ -666,16 +680,62 @@ void Trainer::enqueue_proxy(bool batched) {
     // coarse upsampling-backward stages.  The NN Adam step waits for every
     // gather (they read the IFCE weights).
     const int fine = H_.L >= 2 ? H_.main_gi[1] : 0;
+    // NN gradients: every region but the upsampling taps is complete here
+    // (ARM, synthesis); the taps ([off_tconv[0], off_c1w)) after the last stage
+    const int ups_lo = H_.off_tconv[0], ups_hi = H_.off_c1w;
     fork();
     launch_finalize(side(), kArmProxy, -1);
     launch_latent_grad_grids(side(), fine, H_.n_grids);
+    mark(8, true);
     launch_adam_latents_grids(side(), fine, H_.n_grids);
+    launch_nn_reduce(side(), 0, ups_lo);
+    launch_nn_reduce(side(), ups_hi, H_.n_params);
+    mark(9, true);
     launch_ups_backward(L_, true, 1);
+    mark(10, false);
     launch_latent_grad_grids(L_, 0, fine);
-    launch_nn_reduce(L_);
+    launch_nn_reduce(L_, ups_lo, ups_hi);
+    mark(11, false);
     join();
     if (fine > 0) launch_adam_latents_grids(L_, 0, fine);
     nn_apply(L_, true, true, batched ? d_rec_ : nullptr);
+    mark(12, false);
+}
+
+// Mean event times (ms after the iteration start) of the marks above over n
+// graph replays of an instrumented proxy iteration.
+void Trainer::timeline(int n, double lr, double temp, double noise, double* ms) {
+    require_loaded();
+    CCB_CUDA(cudaSetDevice(device_));
+    h_scal_->lr = lr;
+    h_scal_->temp = temp;
+    h_scal_->noise = noise;
+    CCB_CUDA(cudaMemcpyAsync(&H_.scal->lr, &h_scal_->lr, 3 * sizeof(double), cudaMemcpyHostToDevice,
+                             stream_));
+    std::vector<cudaEvent_t> ev(kTimelineMarks);
+    for (auto& e : ev) CCB_CUDA(cudaEventCreate(&e));
+    tl_ev_ = ev.data();
+    cudaGraph_t g;
+    CCB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    enqueue_proxy(false);
+    CCB_CUDA(cudaStreamEndCapture(stream_, &g));
+    tl_ev_ = nullptr;
+    cudaGraphExec_t ex;
+    CCB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    cudaGraphDestroy(g);
+    std::vector<double> acc(kTimelineMarks, 0.0);
+    for (int it = 0; it < n; ++it) {
+        CCB_CUDA(cudaGraphLaunch(ex, stream_));
+        synchronize();
+        for (int k = 1; k < kTimelineMarks; ++k) {
+            float t = 0.0f;
+            CCB_CUDA(cudaEventElapsedTime(&t, ev[0], ev[size_t(k)]));
+            acc[size_t(k)] += t;
+        }
+    }
+    cudaGraphExecDestroy(ex);
+    for (auto& e : ev) cudaEventDestroy(e);
+    for (int k = 0; k < kTimelineMarks; ++k) ms[k] = n > 0 ? acc[size_t(k)] / n : 0.0;
 }
 
 // Trainer::hardround_iteration (encoder.hpp:141-155)

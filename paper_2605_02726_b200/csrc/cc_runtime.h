@@ -80,6 +80,8 @@ public:
     void last_records(int n, double* rec);
     void set_stream(cudaStream_t s);
     void profile_stages(int n, double lr, double temp, double noise, double* ms);
+    static constexpr int kTimelineMarks = 13;
+    void timeline(int n, double lr, double temp, double noise, double* ms);
     int kernels_per_iteration();
     double hardround_iteration(double lr, int best_slot);
     double true_cost(double* psnr, double* bpp);
@@ -133,6 +135,7 @@ public:
 
 private:
     void init(const float* image, int h, int w);
+    void mark(int id, bool on_side);
     void nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, double* cost_log);
     void build_plan();
     void allocate();
@@ -172,6 +175,7 @@ private:
     double* h_rec_ = nullptr;       // pinned mirror, filled after every iteration
     double* h_sched_ = nullptr;     // pinned schedule staging
     float* d_param_save_ = nullptr; // decode_terms: the trainer's own parameters
+    cudaEvent_t* tl_ev_ = nullptr;  // timeline marks while capturing ccb_timeline
     int sched_cap_ = 0;
     DevScalars* h_scal_ = nullptr;  // pinned mirror
     bool loaded_ = false;

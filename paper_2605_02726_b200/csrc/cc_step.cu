@@ -54,12 +54,12 @@ __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, i
 // per-CTA partial rows, fixed shuffle tree, regions in index order.  Writes
 // ParamTensor::g and clears the tensor's finiteness flag on a non-finite grad.
 __global__ void __launch_bounds__(256) k_nn_reduce(const Plan* __restrict__ pp,
-                                                   int* __restrict__ tensor_ok) {
+                                                   int* __restrict__ tensor_ok, int p_begin, int p_end) {
     const Plan& P = *pp;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
-    for (int p = gw; p < P.n_params; p += nw) {
+    for (int p = p_begin + gw; p < p_end; p += nw) {
         double sum = 0.0;
         for (int r = 0; r < P.n_regions; ++r) {
             const PartialRegion& R = P.region[r];
@@ -152,10 +152,12 @@ void launch_finalize(const LaunchCtx& L, int mode, int snap_slot) {
     k_finalize<<<1, 256, 0, L.stream>>>(L.plan, mode, snap_slot);
 }
 
-void launch_nn_reduce(const LaunchCtx& L) {
-    const int warps = L.host->n_params;
-    const int blocks = (warps + 7) / 8;
-    k_nn_reduce<<<blocks, 256, 0, L.stream>>>(L.plan, L.host->tensor_ok);
+void launch_nn_reduce(const LaunchCtx& L, int p_begin, int p_end) {
+    const Plan& H = *L.host;
+    if (p_end < 0 || p_end > H.n_params) p_end = H.n_params;
+    if (p_end <= p_begin) return;
+    const int blocks = (p_end - p_begin + 7) / 8;
+    k_nn_reduce<<<blocks, 256, 0, L.stream>>>(L.plan, H.tensor_ok, p_begin, p_end);
 }
 
 void launch_nn_apply(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log) {

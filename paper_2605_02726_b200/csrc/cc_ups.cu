@@ -623,7 +623,11 @@ int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward) {
                               : ((s.rows_in + kBT - 1) / kBT) * ((s.cols_in + kBT - 1) / kBT);
         best = t > best ? t : best;
     }
-    const int cap = (2 * num_sms * 8 + H.ups_n[j] - 1) / (H.ups_n[j] > 0 ? H.ups_n[j] : 1);
+    // forward: up to ~2 waves; backward: persistent CTAs (~3 per SM over all
+    // grids of the stage) — every backward CTA writes a partial row of tap
+    // gradients that k_nn_reduce sums, so fewer, longer-lived CTAs
+    const int n = H.ups_n[j] > 0 ? H.ups_n[j] : 1;
+    const int cap = forward ? (2 * num_sms * 8 + n - 1) / n : (3 * num_sms + n - 1) / n;
     return best < cap ? best : cap;
 }
 
