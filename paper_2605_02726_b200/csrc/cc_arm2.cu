@@ -104,8 +104,9 @@ struct alignas(16) A2Smem {
     double red[NT / 32];
 };
 
+template <typename AccT>
 __device__ __forceinline__ void dw_tile(const float* __restrict__ A, const float* __restrict__ B,
-                                        int i0, int i1, float (&acc)[16]) {
+                                        int i0, int i1, AccT (&acc)[16]) {
     dw_tile4x4<LT>(A, B, i0, i1, acc);
 }
 
@@ -265,11 +266,11 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
     if (blockIdx.x < ntiles) issue_gather<DP>(P, sm.geo, cur, sm.ctx_dy, sm.ctx_dx, sC, sR, half, lt);
 
     // persistent weight-gradient accumulators of this thread's units
-    float uacc[K::MAXU][16];
+    double uacc[K::MAXU][16];  // fp64 across tiles: large images sum millions of terms
 #pragma unroll
     for (int m = 0; m < K::MAXU; ++m)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) uacc[m][e] = 0.0f;
+        for (int e = 0; e < 16; ++e) uacc[m][e] = 0.0;
     double bits_thr = 0.0;
     const float upstream = P.rate_upstream;
 
@@ -522,7 +523,8 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
     // stage the register units in (now dead) activation memory, then every
     // parameter of the region is written exactly once: the three latent
     // thirds of its job summed in order
-    float* stage = sm.act;
+    static_assert(K::NU * 16 * 2 <= K::ACT, "fp64 staging fits in the activation buffers");
+    double* stage = reinterpret_cast<double*>(sm.act);
 #pragma unroll
     for (int m = 0; m < K::MAXU; ++m) {
         const int u = tid + m * NT;
@@ -533,8 +535,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
     __syncthreads();
     for (int x = tid; x < K::NJ * 16; x += NT) {
         const int j = x / 16, q = x % 16;
-        const double v = (double(stage[(3 * j) * 16 + q]) + double(stage[(3 * j + 1) * 16 + q])) +
-                         double(stage[(3 * j + 2) * 16 + q]);
+        const double v = (stage[(3 * j) * 16 + q] + stage[(3 * j + 1) * 16 + q]) + stage[(3 * j + 2) * 16 + q];
         int o = -1;
         if (j < K::J1) {
             constexpr int nq = DP / 4 + 1;

@@ -155,11 +155,11 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
     float* const sDH = sm.act + K::O_DH;
     float* const sDZ = sm.act + K::O_DZ;
 
-    float uacc[K::MAXU][16];
+    double uacc[K::MAXU][16];  // fp64 across tiles (large images: millions of pixels)
 #pragma unroll
     for (int m = 0; m < K::MAXU; ++m)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) uacc[m][e] = 0.0f;
+        for (int e = 0; e < 16; ++e) uacc[m][e] = 0.0;
 
     const int64_t np = P.npix;
     const int64_t ntiles = (np + T - 1) / T;
@@ -299,7 +299,8 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
     __syncthreads();
 
     // ---- epilogue: stage the units, sum ranges in order, one row per CTA ----
-    float* stage = sm.act;
+    static_assert(K::NU * 16 * 2 <= K::ACT, "fp64 staging fits in the activation buffers");
+    double* stage = reinterpret_cast<double*>(sm.act);
 #pragma unroll
     for (int m = 0; m < K::MAXU; ++m) {
         const int u = tid + m * NT;
@@ -335,7 +336,7 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
         }
         double v = 0.0;
         if (job >= 0)
-            for (int s = 0; s < K::NPART; ++s) v += double(stage[(job * K::NPART + s) * 16 + q]);
+            for (int s = 0; s < K::NPART; ++s) v += stage[(job * K::NPART + s) * 16 + q];
         row[e] = v;
     }
 }

@@ -10,9 +10,12 @@ namespace ccb {
 // of two feature-major arrays (row stride LD floats, i0/i1 multiples of 4).
 // FFMA2 lanes carry the even / odd columns; they are folded (even + odd)
 // into acc once at the end.
-template <int LD>
+// AccT = double for accumulators that live across many tiles (the per-tile
+// partial is an fp32 sum over <= 64 columns; the cross-tile sum is fp64, so
+// the error does not grow with the image).
+template <int LD, typename AccT>
 __device__ __forceinline__ void dw_tile4x4(const float* __restrict__ A, const float* __restrict__ B,
-                                           int i0, int i1, float (&acc)[16]) {
+                                           int i0, int i1, AccT (&acc)[16]) {
     float2 p[16];
 #pragma unroll
     for (int e = 0; e < 16; ++e) p[e] = make_float2(0.0f, 0.0f);
@@ -35,7 +38,7 @@ __device__ __forceinline__ void dw_tile4x4(const float* __restrict__ A, const fl
             }
     }
 #pragma unroll
-    for (int e = 0; e < 16; ++e) acc[e] += p[e].x + p[e].y;
+    for (int e = 0; e < 16; ++e) acc[e] += AccT(p[e].x + p[e].y);
 }
 
 }  // namespace ccb

@@ -92,10 +92,16 @@ class DecoderConfig:
         return DecoderConfig(3, 20, 6, 26, 2, 64, 2, True, True)
 
     @staticmethod
+    def cfg4():
+        """BASELINE config 4's higher-complexity decoder: ARM context
+        26 + IFCE 6 (d = 32), width 20, synthesis hidden 64."""
+        return DecoderConfig(2, 26, 6, 20, 2, 64, 2, True, True)
+
+    @staticmethod
     def from_name(name: str):
         try:
             return {"lop": DecoderConfig.lop, "mop": DecoderConfig.mop, "hop": DecoderConfig.hop,
-                    "vhop": DecoderConfig.vhop}[name]()
+                    "vhop": DecoderConfig.vhop, "cfg4": DecoderConfig.cfg4}[name]()
         except KeyError:
             raise ConfigError(f"unknown decoder config: {name}") from None
 

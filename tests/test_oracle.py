@@ -194,3 +194,17 @@ def test_port_matches_reference_cfg1_prefix(port_lib):
             ref = g["scalars"][i]
             assert abs(c - ref[0]) / ref[0] <= 1e-5
             assert abs(b - ref[2]) / ref[2] <= 1e-5
+
+
+def test_fp32_sequential_sum_drift():
+    """Why the large-image lock-step test bounds NN gradients at 1e-2: a
+    sequential fp32 sum of millions of same-sign terms (how the reference
+    accumulates weight gradients, layers.hpp:131-145) drifts by O(n * eps)
+    from the exact sum, while pairwise / fp64 partial sums do not."""
+    rng = np.random.default_rng(0)
+    x = (rng.random(3_700_000) * 1e-9).astype(np.float32)
+    exact = float(np.sum(x.astype(np.float64)))
+    seq = np.cumsum(x, dtype=np.float32)[-1]  # cumsum is sequential (np.sum is pairwise)
+    assert abs(float(seq) - exact) / exact > 1e-3
+    tiles = x.reshape(-1, 100).sum(axis=1, dtype=np.float32).astype(np.float64).sum()
+    assert abs(tiles - exact) / exact < 1e-6
