@@ -164,6 +164,7 @@ struct Plan {
     double* grads_d;          // the same gradients before rounding (band reduction)
     double* soap;             // SOAP preconditioners / eigenbases (use_soap)
     float* noise_buf;         // unit Gaussians drawn ahead for scal->noise_iter
+    double* post_scratch;     // k_syn_post2 fp64 dW slots (large images), zeroed per iteration
     float* nn_m;
     float* nn_v;
     double* partials;

@@ -516,6 +516,10 @@ void Trainer::allocate() {
     P.grads_d = static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_params)));
     P.soap = P.use_soap ? static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.soap))) : nullptr;
     P.noise_buf = f32(nl);
+    // k_syn_post2's fp64 flush slots, only when a CTA walks >= 16 tiles
+    P.post_scratch = syn_post_tiles(P.H, P.W) >= 16 * P.n_mse_part
+                         ? static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_mse_part) * 256 * 30))
+                         : nullptr;
     P.nn_m = f32(P.n_params);
     P.nn_v = f32(P.n_params);
     P.partials = static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.partials)));
@@ -822,12 +826,14 @@ void Trainer::band_forward_backward(double lr, double temp, double noise_std, do
     CCB_CUDA(cudaMemcpyAsync(&H_.scal->lr, &h_scal_->lr, 3 * sizeof(double),
                              cudaMemcpyHostToDevice, stream_));
     launch_softq_fwd(L_);
-    launch_arm(L_, kArmProxy);
-    launch_pyramid(L_);
+    fork();  // rate branch beside the distortion branch, as in enqueue_proxy
+    launch_arm(side(), kArmProxy);
+    launch_pyramid(side());
     launch_ups_forward(L_);
     launch_syn_forward(L_, true);
     launch_syn_backward(L_);
     launch_ups_backward(L_, true);
+    join();
     launch_finalize(L_, kArmProxy, -1);  // local sums; latent grads are kept even if
     launch_latent_grad_partial(L_);      // this band's partial cost is not finite
     launch_nn_reduce(L_);

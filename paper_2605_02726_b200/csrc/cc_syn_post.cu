@@ -135,7 +135,20 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
     double mse = 0.0;
     const int tiles_x = (W + TW - 1) / TW;
     const int ntiles = tiles_x * ((H + TH - 1) / TH);
+    // large images: every 16 tiles the fp32 per-thread dW sums move into an
+    // fp64 per-thread slot (their fp32 chains stay <= 256 terms long)
+    double* flush = P.post_scratch ? P.post_scratch + (int64_t(blockIdx.x) * NT + tid) * 30 : nullptr;
+    int tcount = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (flush && NP > 0 && with_grad && ++tcount % 16 == 0) {
+#pragma unroll
+            for (int hq = 0; hq < 3; ++hq)
+#pragma unroll
+                for (int k = 0; k < 10; ++k) {
+                    flush[hq * 10 + k] += double(wacc[hq][k]);
+                    wacc[hq][k] = 0.0f;
+                }
+        }
         const int y0 = (tile / tiles_x) * TH, x0 = (tile % tiles_x) * TW;
         const int gy0 = y0 - C::H4, gx0 = x0 - C::H4;  // global coords of virtual (0,0)
         const bool border = gy0 < 0 || gx0 < 0 || gy0 + C::PH > H || gx0 + C::PW > W;
@@ -329,13 +342,17 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
     if constexpr (NP > 0) {
         if (!with_grad) return;
         __syncthreads();
-        float* scratch = &sm.p[0][0][0];  // [pair][column][10]
+        static_assert(sizeof(double) * NP * 9 * TW * 10 <= sizeof(float) * 2 * (NP + 1) * 3 * C::PL,
+                      "fp64 scratch fits in the p / d planes");
+        double* scratch = reinterpret_cast<double*>(&sm.p[0][0][0]);  // [pair][column][10]
 #pragma unroll
         for (int hq = 0; hq < 3; ++hq) {
             const int pair = ws + 8 * hq;
             if (pair < NP * 9)
 #pragma unroll
-                for (int k = 0; k < 10; ++k) scratch[(pair * TW + wc) * 10 + k] = wacc[hq][k];
+                for (int k = 0; k < 10; ++k)
+                    scratch[(pair * TW + wc) * 10 + k] =
+                        double(wacc[hq][k]) + (flush ? flush[hq * 10 + k] : 0.0);
         }
         __syncthreads();
         for (int i = 0; i < NP; ++i) {
@@ -354,7 +371,7 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
                 }
                 double v = 0.0;
                 if (pair >= 0)
-                    for (int c = 0; c < TW; ++c) v += double(scratch[(pair * TW + c) * 10 + k]);
+                    for (int c = 0; c < TW; ++c) v += scratch[(pair * TW + c) * 10 + k];
                 row[e] = v;
             }
         }
@@ -373,6 +390,8 @@ int syn_post_tiles(int H, int W) { return ((H + TH - 1) / TH) * ((W + TW - 1) / 
 
 void launch_syn_post(const LaunchCtx& L, bool backward) {
     const Plan& H = *L.host;
+    if (H.post_scratch && backward)
+        cudaMemsetAsync(H.post_scratch, 0, sizeof(double) * size_t(H.n_mse_part) * NT * 30, L.stream);
     const int g = H.n_mse_part;
     const int wg = backward ? 1 : 0;
     switch (H.posts) {
