@@ -47,6 +47,14 @@ int cc_band_grid_rows(cc_trainer* tr, int gi, int* out4);
  * 2 = add buf. */
 int cc_band_rows(cc_trainer* tr, int which, int gi, int rb, int re, float* buf, int mode);
 
+/* Device views for a collective library (NCCL): the device address of global
+ * rows [rb, re) of grid gi (which 0 = latents, 1 = latent gradients; fp32,
+ * contiguous) and of the fp64 NN-gradient partial sums.  Valid until the
+ * trainer is destroyed; the trainer's own work is complete when
+ * cc_band_forward_backward / cc_band_step return. */
+int cc_band_device_rows(cc_trainer* tr, int which, int gi, int rb, int re, void** dptr, int64_t* count);
+int cc_band_device_nn_partial(cc_trainer* tr, void** dptr, int64_t* count);
+
 int cc_band_forward_backward(cc_trainer* tr, double lr, double temp, double noise_std,
                              double* bits, double* sq_err);
 /* this band's NN-gradient partial sums (fp64, for_each_param order) */

@@ -113,6 +113,7 @@ class BandTrainer(Trainer):
         _check(lib, lib.cc_band_window(h, w, r0, r1, halo, C.byref(w0), C.byref(w1)))
         self.H, self.W, self.r0, self.r1, self.halo = h, w, r0, r1, halo
         self.window = (w0.value, w1.value)
+        self._device = device
         super().__init__(np.ascontiguousarray(image[:, w0.value:w1.value]), enc, dcfg, lib=lib,
                          device=device, band=(h, r0, r1, halo))
 
@@ -131,6 +132,17 @@ class BandTrainer(Trainer):
         _check(self.lib, self.lib.cc_band_rows(self._h, which, gi, rb, re,
                                                buf.ctypes.data_as(C.POINTER(C.c_float)), mode))
         return buf
+
+    def device_rows(self, which: int, gi: int, rb: int, re: int):
+        """Zero-copy torch CUDA view of global rows [rb, re) of grid gi."""
+        ptr, n = C.c_void_p(), C.c_int64()
+        _check(self.lib, self.lib.cc_band_device_rows(self._h, which, gi, rb, re, C.byref(ptr), C.byref(n)))
+        return _device_view(ptr.value, n.value, "<f4", self._device)
+
+    def device_nn_partial(self):
+        ptr, n = C.c_void_p(), C.c_int64()
+        _check(self.lib, self.lib.cc_band_device_nn_partial(self._h, C.byref(ptr), C.byref(n)))
+        return _device_view(ptr.value, n.value, "<f8", self._device)
 
     def forward_backward(self, lr, temp, noise):
         b, s = C.c_double(), C.c_double()
@@ -155,6 +167,23 @@ class BandTrainer(Trainer):
     def step(self, lat_ok: np.ndarray) -> None:
         ok = (C.c_int * len(self.grids))(*[int(v) for v in lat_ok])
         _check(self.lib, self.lib.cc_band_step(self._h, ok))
+
+
+class _CudaArray:
+    """__cuda_array_interface__ around a device address owned by the library."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def _device_view(ptr: int, n: int, typestr: str, device: int):
+    import torch
+
+    if n == 0:
+        return torch.empty(0, dtype=torch.float32 if typestr == "<f4" else torch.float64,
+                           device=f"cuda:{device}")
+    return torch.as_tensor(_CudaArray(ptr, n, typestr), device=f"cuda:{device}")
 
 
 # ---------------------------------------------------------------- one iteration
@@ -301,7 +330,52 @@ class DistBand:
         self.dist.all_gather(bufs, t)
         return [self._np(x) for x in bufs]
 
+    # ---- device-direct path (NCCL on the library's own buffers, no host staging)
+    def _device_ok(self) -> bool:
+        return self.device is not None and hasattr(self.tr, "device_rows")
+
+    def _p2p(self, sends, recvs):
+        ops = [self.dist.P2POp(self.dist.isend, t, peer) for t, peer in sends if t.numel()]
+        ops += [self.dist.P2POp(self.dist.irecv, t, peer) for t, peer in recvs if t.numel()]
+        if ops:
+            for r in self.dist.batch_isend_irecv(ops):
+                r.wait()
+
+    def _refresh_halos_device(self) -> None:
+        sends, recvs = [], []
+        for gi, d in enumerate(self.plan):  # one message per grid and direction
+            if self.rank > 0:
+                sends.append((self.tr.device_rows(0, gi, *d["send_up"]), self.rank - 1))
+                recvs.append((self.tr.device_rows(0, gi, *d["halo_up"]), self.rank - 1))
+            if self.rank + 1 < self.world:
+                sends.append((self.tr.device_rows(0, gi, *d["send_down"]), self.rank + 1))
+                recvs.append((self.tr.device_rows(0, gi, *d["halo_down"]), self.rank + 1))
+        self._p2p(sends, recvs)
+
+    def _return_grads_device(self) -> None:
+        import torch
+
+        sends, recvs, adds = [], [], []
+        for gi, d in enumerate(self.plan):
+            if self.rank > 0:
+                sends.append((self.tr.device_rows(1, gi, *d["halo_up"]), self.rank - 1))
+                own = self.tr.device_rows(1, gi, *d["send_up"])
+                tmp = torch.empty_like(own)
+                recvs.append((tmp, self.rank - 1))
+                adds.append((own, tmp))
+            if self.rank + 1 < self.world:
+                sends.append((self.tr.device_rows(1, gi, *d["halo_down"]), self.rank + 1))
+                own = self.tr.device_rows(1, gi, *d["send_down"])
+                tmp = torch.empty_like(own)
+                recvs.append((tmp, self.rank + 1))
+                adds.append((own, tmp))
+        self._p2p(sends, recvs)
+        for own, tmp in adds:
+            own.add_(tmp)
+
     def proxy_iteration(self, lr: float, temp: float, noise: float) -> float:
+        if self._device_ok():
+            return self._proxy_iteration_device(lr, temp, noise)
         self.refresh_halos()
         bits, se = self.tr.forward_backward(lr, temp, noise)
         up, dn = self._swap(_pack(self.tr, 1, self.plan, "halo_up"),
@@ -318,4 +392,25 @@ class DistBand:
         cost, ok = self.tr.finish(tot[:-2], float(tot[-2]), float(tot[-1]))
         oks = self._gather(ok.astype(np.int32))
         self.tr.step(np.minimum.reduce(oks))
+        return cost
+
+    def _proxy_iteration_device(self, lr: float, temp: float, noise: float) -> float:
+        import torch
+
+        self._refresh_halos_device()
+        torch.cuda.synchronize(self.device)
+        bits, se = self.tr.forward_backward(lr, temp, noise)  # returns with the band's work done
+        self._return_grads_device()
+        nn = self.tr.device_nn_partial()
+        mine = torch.cat([nn, torch.tensor([bits, se], dtype=torch.float64, device=nn.device)])
+        parts = [torch.empty_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(parts, mine)
+        tot = parts[0].clone()
+        for p in parts[1:]:  # rank order: identical sums on every rank
+            tot += p
+        oks = [torch.empty(len(self.plan), dtype=torch.int32, device=nn.device) for _ in range(self.world)]
+        tot_h = tot.cpu().numpy()  # synchronises the NCCL stream
+        cost, ok = self.tr.finish(tot_h[:-2], float(tot_h[-2]), float(tot_h[-1]))
+        self.dist.all_gather(oks, torch.from_numpy(ok.astype(np.int32)).to(nn.device))
+        self.tr.step(np.minimum.reduce([o.cpu().numpy() for o in oks]))
         return cost

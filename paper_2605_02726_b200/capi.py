@@ -165,6 +165,9 @@ BAND_SIGNATURES = {
                                          C.c_int, C.POINTER(C.c_void_p)]),
     "cc_band_grid_rows": (C.c_int, [_P, C.c_int, _I]),
     "cc_band_rows": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _F, C.c_int]),
+    "cc_band_device_rows": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                                      C.POINTER(C.c_int64)]),
+    "cc_band_device_nn_partial": (C.c_int, [_P, C.POINTER(C.c_void_p), C.POINTER(C.c_int64)]),
     "cc_band_forward_backward": (C.c_int, [_P, C.c_double, C.c_double, C.c_double, _D, _D]),
     "cc_band_nn_partial": (C.c_int, [_P, _D]),
     "cc_band_finish": (C.c_int, [_P, _D, C.c_double, C.c_double, _D, _I]),

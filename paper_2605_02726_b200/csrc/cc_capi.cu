@@ -733,6 +733,23 @@ int cc_band_rows(cc_trainer* t, int which, int gi, int rb, int re, float* buf, i
     });
 }
 
+int cc_band_device_rows(cc_trainer* t, int which, int gi, int rb, int re, void** dptr, int64_t* count) {
+    return guarded([&] {
+        int64_t n = 0;
+        *dptr = t->tr->band_device_rows(which, gi, rb, re, &n);
+        if (count) *count = n;
+        return CC_OK;
+    });
+}
+
+int cc_band_device_nn_partial(cc_trainer* t, void** dptr, int64_t* count) {
+    return guarded([&] {
+        *dptr = t->tr->nn_partial_device();
+        if (count) *count = t->tr->plan().n_params;
+        return CC_OK;
+    });
+}
+
 int cc_band_forward_backward(cc_trainer* t, double lr, double temp, double noise_std, double* bits,
                              double* sq_err) {
     return guarded([&] {

@@ -913,6 +913,16 @@ void Trainer::band_rows(int which, int gi, int rb, int re, float* buf, int mode)
     synchronize();
 }
 
+void* Trainer::band_device_rows(int which, int gi, int rb, int re, int64_t* count) {
+    if (gi < 0 || gi >= H_.n_grids) throw ConfigError("grid index out of range");
+    const GridGeom& g = H_.g[gi];
+    if (rb < g.row0 || re > g.row0 + g.rows || rb > re) throw ConfigError("rows outside the band window");
+    float* base = (which == 0 ? H_.y : which == 1 ? H_.lat_g : nullptr);
+    if (!base) throw ConfigError("which must be 0 (latents) or 1 (latent grads)");
+    *count = int64_t(re - rb) * g.cols;
+    return base + g.lat_off + int64_t(rb - g.row0) * g.cols;
+}
+
 void Trainer::band_grid_rows(int gi, int* out4) const {
     const GridGeom& g = H_.g[gi];
     out4[0] = g.row0;

@@ -111,6 +111,8 @@ public:
     void band_step(const int* lat_ok);
     void band_rows(int which, int gi, int rb, int re, float* buf, int mode);
     void band_grid_rows(int gi, int* out4) const;
+    void* band_device_rows(int which, int gi, int rb, int re, int64_t* count);
+    double* nn_partial_device() { return H_.grads_d; }
 
     // state transfer
     void set_state(const float* lat, const float* par, const float* lm, const float* lv,

@@ -221,3 +221,26 @@ def test_bands_reproduce_whole_image(gpu_lib, h, w, n):
     finally:
         lb.close()
         whole.close()
+
+
+@pytest.mark.gpu
+def test_band_device_views_are_the_library_buffers(gpu_lib):
+    """The zero-copy CUDA views DistBand hands to NCCL (cc_band_device_rows /
+    cc_band_device_nn_partial) alias the band trainer's own buffers."""
+    import torch
+
+    img = make_image(gpu_lib, 256, 192, seed=2)
+    r0, r1 = B.split_rows(256, 192, 2)[1]
+    with B.BandTrainer(img, r0, r1, 6, EncoderConfig(), DecoderConfig.hop(), lib=gpu_lib) as t:
+        t.fresh_candidate(0)
+        gi = len(t.grids) - 1
+        gr = t.grid_rows(gi)
+        v = t.device_rows(0, gi, gr.w0, gr.o0)
+        assert v.is_cuda and v.numel() == (gr.o0 - gr.w0) * t.grids[gi].cols
+        assert np.array_equal(v.cpu().numpy(), t.rows(0, gi, gr.w0, gr.o0))
+        v.fill_(1.5)
+        torch.cuda.synchronize()
+        assert np.all(t.rows(0, gi, gr.w0, gr.o0) == 1.5)
+        t.forward_backward(1e-2, 0.35, 0.22)
+        nn = t.device_nn_partial()
+        assert nn.dtype == torch.float64 and np.array_equal(nn.cpu().numpy(), t.nn_partial())
