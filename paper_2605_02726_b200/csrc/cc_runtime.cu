@@ -1043,10 +1043,12 @@ void Trainer::profile_stages(int n, double lr, double temp, double noise, double
     for (auto& e : ev) cudaEventDestroy(e);
 }
 
+// Kernel nodes of one batched proxy iteration (the graph the benchmark and
+// cc_trainer_train replay; the schedule-load kernel included).
 int Trainer::kernels_per_iteration() {
     cudaGraph_t g;
     CCB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-    enqueue_proxy(false);
+    enqueue_proxy(true);
     CCB_CUDA(cudaStreamEndCapture(stream_, &g));
     size_t n = 0;
     CCB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
