@@ -30,7 +30,6 @@ namespace ccb {
 namespace {
 
 constexpr int kFT = 32;   // forward output tile (level j), square
-constexpr int kBT = 16;   // backward input tile (level j+1), square
 constexpr int kThreads = 256;     // big stages
 constexpr int kThreadsWide = 512; // stages with few tiles: shorter per-CTA phase chains
 
@@ -199,201 +198,307 @@ __global__ void __launch_bounds__(kThreadsWide) k_ups_fwd(const Plan* __restrict
     ups_fwd_stage(*pp, j, blockIdx.y, blockIdx.x, gridDim.x, fs);
 }
 
-// Coarse stages j >= jc of every cascade k > jc in ONE launch: CTA b runs
-// cascade k = jc + 1 + b through its stages k-1 .. jc in order (a stage's
-// output is the next one's input; __syncthreads orders them in the CTA).
-// The coarse stages have a handful of tiles each, so this trades k - jc
-// latency-bound launches for one.
-__global__ void __launch_bounds__(kThreadsWide) k_ups_fwd_coarse(const Plan* __restrict__ pp, int jc) {
-    __shared__ FwdSmem fs;
-    const Plan& P = *pp;
-    const int k = jc + 1 + blockIdx.x;
-    for (int j = k - 1; j >= jc; --j) {
-        ups_fwd_stage(P, j, k - j - 1, 0, 1, fs);
-        __syncthreads();
-    }
-}
-
 // --------------------------------------------------------------- backward
-// (r', d) pairs with clamp(r' + d) == r, r' in [0, n): the transposed
-// replicate-padded 3-tap stencil.
-__device__ __forceinline__ int nbr_pairs(int r, int n, int (&rr)[3], int (&dd)[3]) {
-    int k = 0;
-    for (int q = r - 1; q <= r + 1; ++q) {
-        if (q < 0 || q >= n) continue;
-        for (int d = -1; d <= 1; ++d)
-            if (clampi(q + d, 0, n - 1) == r && k < 3) {
-                rr[k] = q;
-                dd[k] = d;
-                ++k;
-            }
-    }
-    return k;
-}
+// A CTA owns input tile [U0,U0+TB) x [V0,V0+TB) of stage j+1 and the level-j
+// outputs [a,a+2TB) x [b,b+2TB) (a = 2U0, b = 2V0) it parents.  Every phase is
+// a flat loop over a compile-time window; each thread produces a short
+// register strip (4 rows of a stencil, a polyphase pair), so operands loaded
+// from shared memory are reused across the strip.
+//
+// Border tiles (touching the image edge or the crop of an odd-sized level)
+// run the same stencils over a virtual, unclamped window and restore the
+// replicate-padding semantics of the reference around them:
+//   * input X is clamp-loaded, so rowtmp / coltmp recomputed on the window
+//     equal R[clamp(u)] / C[clamp(t)] (tconv_map's clamped indices,
+//     layers.hpp:353-429);
+//   * coltmp one position outside [0,ro) x [0,co) is re-clamped to its edge
+//     value (the replicate padding of conv3x3_sym_forward, layers.hpp:467-483);
+//   * dOut is zero outside the image; the transposed refine stencil then
+//     gives dC at virtual positions (nonzero only at distance 1), which are
+//     folded onto the edge positions they clamp to, rows then columns
+//     (conv3x3_sym_backward, layers.hpp:486-515);
+//   * drow (virtual input rows, distance <= 2) and din (virtual input
+//     columns) are folded the same way (tconv2x_{cols,rows}_backward).
+// The border windows are 3 (dOut, dcol) / 2 (drow, din) positions wider per
+// side.  a - 7 is odd, never 0, so every edge position a later phase reads
+// has its fold sources inside the window.
+template <int TB, bool BORDER>
+struct BwdGeo {
+    static constexpr int M = BORDER ? 3 : 0, MR = BORDER ? 2 : 0;
+    static constexpr int FO = 2 * TB;           // owned level-j span
+    static constexpr int DO = FO + 10 + 2 * M;  // dOut, origin a-5-M (both axes)
+    static constexpr int DC = FO + 8 + 2 * M;   // dcol, origin a-4-M
+    static constexpr int DR = TB + 2 * MR;      // drow rows, origin U0-MR (cols: dcol's)
+    static constexpr int DI = TB + 2 * MR;      // din cols, origin V0-MR
+    static constexpr int XW = TB + 6;           // input window, origin U0-3 / V0-3
+    static constexpr int RC = FO + 4;           // rowtmp cols, origin b-2 (rows: XW)
+    static constexpr int CR = FO + 4;           // coltmp rows, origin a-2 (pairs u = U0-1 .. U0+TB)
+    static constexpr int CC = FO + 2;           // coltmp cols, origin b-1
+    static constexpr int OFF = 4 + M - 2 * MR;  // dcol row of 2u for drow row 0 (same for cols)
+};
 
-// windows of the backward tile (input tile [U0,U0+kBT) x [V0,V0+kBT))
-constexpr int kBO = 2 * kBT;              // owned level-j span
-constexpr int kBD = kBO + 10;             // dcol / drow-column window
-constexpr int kBG = kBD + 2;              // dOut window
-constexpr int kBC = kBO + 2;              // coltmp window (owned + refine halo)
-constexpr int kBR = kBC / 2 + 6;          // rowtmp rows / input rows
-constexpr int kBI = kBD / 2 + 8;          // input cols window
-
+template <int TB>
 struct BwdSmem {
-    float dout[kBG * kBG];
-    float dcol[kBD * kBD];
-    float drow[kBT * kBD];
-    float in[kBR * kBI];
-    float row[kBR * kBC];
-    float col[kBC * kBC];
-    double red[7 * (kThreadsWide / 32)];
+    using G = BwdGeo<TB, true>;
+    float dout[G::DO * G::DO];
+    float dcol[G::DC * G::DC];
+    float x[G::XW * G::XW];
+    float r[G::XW * G::RC];
+    float c[G::CR * G::CC];
+    float drow[G::DR * G::DC];
+    float din[TB * G::DI];
+    double red[7 * (kThreads / 32)];
     double tot[7];
 };
 
-// ---- interior fast path of the backward tile --------------------------
-// For tiles whose every window is in range (no replicate clamp, no crop, no
-// tconv index clamp) the stencils have fixed taps and fixed geometry, so each
-// phase is a flat loop over a compile-time window.  a = 2·U0, b = 2·V0.
-constexpr int FO = 2 * kBT;    // owned level-j span (32)
-constexpr int FDO = FO + 10;   // dOut window: a-5 .. a+36
-constexpr int FDC = FO + 8;    // dcol window: a-4 .. a+35
-constexpr int FX = kBT + 6;    // input window: U0-3 .. U0+18
-constexpr int FRC = FO + 4;    // rowtmp columns: b-2 .. b+33 (rows = input rows)
-constexpr int FC = FO + 2;     // coltmp window: a-1 .. a+32
-struct FastSmem {
-    float dout[FDO * FDO];
-    float dcol[FDC * FDC];
-    float x[FX * FX];
-    float r[FX * FRC];
-    float c[FC * FC];
-    float drow[kBT * FDC];
-};
-static_assert(sizeof(FastSmem) <= sizeof(BwdSmem) - sizeof(double) * 7 * (kThreadsWide / 32 + 1),
-              "fast-path windows overlay the generic ones");
-
+template <int TB>
 __device__ __forceinline__ bool bwd_interior(int U0, int V0, int ri, int ci, int ro, int co) {
-    return U0 >= kBT && V0 >= kBT && U0 + kBT + 2 <= ri - 1 && V0 + kBT + 2 <= ci - 1 &&
-           2 * U0 + FO + 4 <= ro - 1 && 2 * V0 + FO + 4 <= co - 1;
+    return U0 >= 3 && V0 >= 3 && U0 + TB + 2 <= ri - 1 && V0 + TB + 2 <= ci - 1 &&
+           2 * U0 + 2 * TB + 5 <= ro && 2 * V0 + 2 * TB + 5 <= co;
 }
 
-__device__ __forceinline__ void bwd_tile_fast(const float* __restrict__ in, int in_stride,
-                                              const float* __restrict__ dout, int co,
-                                              float* __restrict__ din, int ci, bool wd, int U0, int V0,
-                                              const float (&kk)[4], float kc, float ke, float ko,
-                                              FastSmem& f, double (&acc)[7]) {
+template <int TB, bool BORDER>
+__device__ __forceinline__ void bwd_tile(const float* __restrict__ in, int in_stride,
+                                         const float* __restrict__ dout, int ro, int co,
+                                         float* __restrict__ din, int ri, int ci, bool wd, int U0, int V0,
+                                         const float (&kk)[4], float kc, float ke, float ko,
+                                         BwdSmem<TB>& f, double (&acc)[7]) {
+    using G = BwdGeo<TB, BORDER>;
+    constexpr int M = G::M, MR = G::MR, FO = G::FO, DO = G::DO, DC = G::DC, DR = G::DR, DI = G::DI;
+    constexpr int XW = G::XW, RC = G::RC, CR = G::CR, CC = G::CC, OFF = G::OFF;
     const int a = 2 * U0, b = 2 * V0;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
-    __syncthreads();
-    for (int i = ty; i < FDO; i += ny)
-    for (int j = tx; j < FDO; j += 32) {
-        const int e = i * FDO + j;
-        cp_async4(&f.dout[e], dout + int64_t(a - 5 + i) * co + (b - 5 + j));
+    const int tid = threadIdx.x, nt = blockDim.x;
+    __syncthreads();  // the previous tile's readers are done with the windows
+    // ---- P0: dOut window (zero outside the image), input window (clamped)
+    for (int e = tid; e < DO * DO; e += nt) {
+        const int i = e / DO, j = e - i * DO;
+        const int t = a - 5 - M + i, tc = b - 5 - M + j;
+        if (!BORDER || (t >= 0 && t < ro && tc >= 0 && tc < co))
+            cp_async4(&f.dout[e], dout + int64_t(t) * co + tc);
+        else
+            f.dout[e] = 0.0f;
     }
-    for (int i = ty; i < FX; i += ny)
-    for (int j = tx; j < FX; j += 32) {
-        const int e = i * FX + j;
-        cp_async4(&f.x[e], in + int64_t(U0 - 3 + i) * in_stride + (V0 - 3 + j));
+    for (int e = tid; e < XW * XW; e += nt) {
+        const int i = e / XW, j = e - i * XW;
+        int u = U0 - 3 + i, v = V0 - 3 + j;
+        if (BORDER) {
+            u = clampi(u, 0, ri - 1);
+            v = clampi(v, 0, ci - 1);
+        }
+        cp_async4(&f.x[e], in + int64_t(u) * in_stride + v);
     }
     cp_async_wait_all();
     __syncthreads();
-    // dcol = refineᵀ(dOut) (symmetric interior stencil), rowtmp recompute
-    for (int i = ty; i < FDC; i += ny)
-    for (int j = tx; j < FDC; j += 32) {
-        const int e = i * FDC + j;
-        const float* g = &f.dout[(i + 1) * FDO + (j + 1)];
-        f.dcol[e] = kc * g[0] + ke * (g[-FDO] + g[FDO] + g[-1] + g[1]) +
-                    ko * (g[-FDO - 1] + g[-FDO + 1] + g[FDO - 1] + g[FDO + 1]);
+    // ---- P1: dcol = refineᵀ(dOut) in 4-row strips; rowtmp in polyphase pairs
+    {
+        constexpr int NB = (DC + 3) / 4;
+        for (int e = tid; e < NB * DC; e += nt) {
+            const int rb = e / DC, j = e - rb * DC, i0 = 4 * rb;
+            float m[6], h[6];
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                if (DC % 4 == 0 || i0 + q < DO) {
+                    const float* g = &f.dout[(i0 + q) * DO + j];
+                    m[q] = g[1];
+                    h[q] = g[0] + g[2];
+                } else {
+                    m[q] = h[q] = 0.0f;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (DC % 4 == 0 || i0 + q < DC)
+                    f.dcol[(i0 + q) * DC + j] = kc * m[q + 1] + ke * (m[q] + m[q + 2] + h[q + 1]) + ko * (h[q] + h[q + 2]);
+        }
     }
-    for (int i = ty; i < FX; i += ny)
-    for (int j = tx; j < FRC; j += 32) {
-        const int e = i * FRC + j;
-        const float* x = &f.x[i * FX + (j >> 1) + 2];
-        f.r[e] = (j & 1) == 0 ? kk[0] * x[-2] + kk[2] * x[-1] + kk[3] * x[0] + kk[1] * x[1]
-                              : kk[1] * x[-1] + kk[3] * x[0] + kk[2] * x[1] + kk[0] * x[2];
-    }
-    __syncthreads();
-    // coltmp recompute; drow = colᵀ(dcol) on the tile's input rows
-    for (int i = ty; i < FC; i += ny)
-    for (int j = tx; j < FC; j += 32) {
-        const int e = i * FC + j;
-        const int tr = i - 1;                 // output row a + tr
-        const int v = (tr >> 1) + 3;          // R row (local) of v = U0 + floor(tr/2)
-        const float* rr = &f.r[v * FRC + j + 1];
-        f.c[e] = (tr & 1) == 0 ? kk[0] * rr[-2 * FRC] + kk[2] * rr[-FRC] + kk[3] * rr[0] + kk[1] * rr[FRC]
-                               : kk[1] * rr[-FRC] + kk[3] * rr[0] + kk[2] * rr[FRC] + kk[0] * rr[2 * FRC];
-    }
-    for (int i = ty; i < kBT; i += ny)
-    for (int j = tx; j < FDC; j += 32) {
-        const int e = i * FDC + j;
-        const float* g = &f.dcol[(2 * i + 4) * FDC + j];
-        f.drow[e] = kk[0] * (g[4 * FDC] + g[-3 * FDC]) + kk[1] * (g[-2 * FDC] + g[3 * FDC]) +
-                    kk[2] * (g[2 * FDC] + g[-FDC]) + kk[3] * (g[0] + g[FDC]);
+    for (int e = tid; e < XW * (TB + 2); e += nt) {
+        const int i = e / (TB + 2), m = e - i * (TB + 2);  // t' = b - 2 + 2m, +1
+        const float* x = &f.x[i * XW + m];
+        float* r = &f.r[i * RC + 2 * m];
+        r[0] = kk[0] * x[0] + kk[2] * x[1] + kk[3] * x[2] + kk[1] * x[3];
+        r[1] = kk[1] * x[1] + kk[3] * x[2] + kk[2] * x[3] + kk[0] * x[4];
     }
     __syncthreads();
+    // ---- P2: coltmp in polyphase pairs; fold of dcol rows -1 -> 0, ro -> ro-1
+    for (int e = tid; e < (TB + 2) * CC; e += nt) {
+        const int p = e / CC, j = e - p * CC;  // t = a - 2 + 2p, +1
+        const float* r = &f.r[p * RC + j + 1];
+        const float r0 = r[0], r1 = r[RC], r2 = r[2 * RC], r3 = r[3 * RC], r4 = r[4 * RC];
+        f.c[(2 * p) * CC + j] = kk[0] * r0 + kk[2] * r1 + kk[3] * r2 + kk[1] * r3;
+        f.c[(2 * p + 1) * CC + j] = kk[1] * r1 + kk[3] * r2 + kk[2] * r3 + kk[0] * r4;
+    }
+    if (BORDER && tid < DC) {
+        const int j = tid;
+        const int i0 = 4 + M - a;           // local row of t = 0
+        const int i1 = ro - 1 - (a - 4 - M);  // local row of t = ro - 1
+        if (i0 >= 1 && i0 < DC) {
+            f.dcol[i0 * DC + j] += f.dcol[(i0 - 1) * DC + j];
+            f.dcol[(i0 - 1) * DC + j] = 0.0f;
+        }
+        if (i1 >= 0 && i1 + 1 < DC) {
+            f.dcol[i1 * DC + j] += f.dcol[(i1 + 1) * DC + j];
+            f.dcol[(i1 + 1) * DC + j] = 0.0f;
+        }
+    }
+    __syncthreads();
+    if (BORDER) {
+        // fold of dcol columns; coltmp rows -1 / ro re-clamped
+        if (tid < DC) {
+            float* d = &f.dcol[tid * DC];
+            const int j0 = 4 + M - b, j1 = co - 1 - (b - 4 - M);
+            if (j0 >= 1 && j0 < DC) {
+                d[j0] += d[j0 - 1];
+                d[j0 - 1] = 0.0f;
+            }
+            if (j1 >= 0 && j1 + 1 < DC) {
+                d[j1] += d[j1 + 1];
+                d[j1 + 1] = 0.0f;
+            }
+        }
+        if (tid >= nt - CC) {
+            const int j = tid - (nt - CC);
+            const int im = 1 - a, ip = ro - (a - 2);  // local rows of t = -1, t = ro
+            if (im >= 0) f.c[im * CC + j] = f.c[(im + 1) * CC + j];
+            if (ip < CR) f.c[ip * CC + j] = f.c[(ip - 1) * CC + j];
+        }
+        __syncthreads();
+        if (tid >= nt - CR) {  // coltmp columns -1 / co (after the rows: corners)
+            float* c = &f.c[(tid - (nt - CR)) * CC];
+            const int jm = -b, jp = co - (b - 1);
+            if (jm >= 0) c[jm] = c[jm + 1];
+            if (jp < CC) c[jp] = c[jp - 1];
+        }
+    }
+    // ---- P3: drow = colᵀ(dcol), two input rows per thread
+    for (int e = tid; e < (DR / 2) * DC; e += nt) {
+        const int pb = e / DC, j = e - pb * DC;
+        const float* g = &f.dcol[(4 * pb + OFF - 3) * DC + j];
+        float v[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) v[k] = g[k * DC];
+        f.drow[(2 * pb) * DC + j] = kk[0] * (v[7] + v[0]) + kk[1] * (v[1] + v[6]) + kk[2] * (v[5] + v[2]) + kk[3] * (v[3] + v[4]);
+        f.drow[(2 * pb + 1) * DC + j] = kk[0] * (v[9] + v[2]) + kk[1] * (v[3] + v[8]) + kk[2] * (v[7] + v[4]) + kk[3] * (v[5] + v[6]);
+    }
+    __syncthreads();
+    if (BORDER) {
+        // fold of drow rows -2,-1 -> 0 and ri, ri+1 -> ri-1 (only own rows are read)
+        if (tid < DC) {
+            const int j = tid;
+            if (U0 == 0) {
+                float* d = &f.drow[MR * DC + j];
+                float s = d[-DC] + d[-2 * DC];
+                if (ri == 1) s += d[DC] + d[2 * DC];
+                d[0] += s;
+            }
+            const int i1 = ri - 1 - (U0 - MR);
+            if (ri > 1 && ri - 1 >= U0 && ri - 1 < U0 + TB) {
+                float* d = &f.drow[i1 * DC + j];
+                d[0] += d[DC] + d[2 * DC];
+            }
+        }
+        __syncthreads();
+    }
+    // ---- P4: din = rowᵀ(drow); tap gradients
     float fa[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    // din = rowᵀ(drow)
     if (wd) {
-        for (int i = ty; i < kBT; i += ny)
-        for (int j = tx; j < kBT; j += 32) {
-            const float* g = &f.drow[i * FDC + 2 * j + 4];
-            din[int64_t(U0 + i) * ci + V0 + j] = kk[0] * (g[4] + g[-3]) + kk[1] * (g[-2] + g[3]) +
-                                                 kk[2] * (g[2] + g[-1]) + kk[3] * (g[0] + g[1]);
+        constexpr int NI = BORDER ? DI : TB;
+        for (int e = tid; e < TB * NI; e += nt) {
+            const int i = e / NI, jj = e - i * NI;
+            if (BORDER && U0 + i >= ri) continue;
+            const float* g = &f.drow[(i + MR) * DC + 2 * jj + OFF];
+            const float s = kk[0] * (g[4] + g[-3]) + kk[1] * (g[-2] + g[3]) + kk[2] * (g[2] + g[-1]) + kk[3] * (g[0] + g[1]);
+            if (BORDER) f.din[i * DI + jj] = s;
+            else din[int64_t(U0 + i) * ci + V0 + jj] = s;
         }
     }
-    // refine taps over the owned outputs: dOut x coltmp neighbourhoods
-    for (int i = ty; i < FO; i += ny)
-    for (int j = tx; j < FO; j += 32) {
-        const float g = f.dout[(i + 5) * FDO + j + 5];
-        const float* x0 = &f.c[i * FC + j];
-        const float* x1 = x0 + FC;
-        const float* x2 = x1 + FC;
-        fa[4] = fmaf(g, x1[1], fa[4]);
-        fa[5] = fmaf(g, x0[1] + x2[1] + x1[0] + x1[2], fa[5]);
-        fa[6] = fmaf(g, x0[0] + x0[2] + x2[0] + x2[2], fa[6]);
-        // column pass: dcol x rowtmp (owned output (a+i, b+j))
-        const float gc = f.dcol[(i + 4) * FDC + j + 4];
-        const float* rr = &f.r[((i >> 1) + 3) * FRC + j + 2];
-        if ((i & 1) == 0) {
-            fa[0] = fmaf(gc, rr[-2 * FRC], fa[0]);
-            fa[2] = fmaf(gc, rr[-FRC], fa[2]);
-            fa[3] = fmaf(gc, rr[0], fa[3]);
-            fa[1] = fmaf(gc, rr[FRC], fa[1]);
-        } else {
-            fa[1] = fmaf(gc, rr[-FRC], fa[1]);
-            fa[3] = fmaf(gc, rr[0], fa[3]);
-            fa[2] = fmaf(gc, rr[FRC], fa[2]);
-            fa[0] = fmaf(gc, rr[2 * FRC], fa[0]);
+    // refine taps (dOut x coltmp neighbourhood) and column pass (dcol x
+    // rowtmp) over 4-row strips of owned outputs
+    for (int e = tid; e < (FO / 4) * FO; e += nt) {
+        const int sb = e / FO, j = e - sb * FO;
+        const int t0 = a + 4 * sb;
+        if (BORDER && (t0 >= ro || b + j >= co)) continue;
+        float cm[6], ch[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const float* c = &f.c[(4 * sb + 1 + q) * CC + j];
+            cm[q] = c[1];
+            ch[q] = c[0] + c[2];
+        }
+        float rr[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) rr[q] = f.r[(2 * sb + 1 + q) * RC + j + 2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (BORDER && t0 + q >= ro) break;
+            const float g = f.dout[(4 * sb + q + 5 + M) * DO + j + 5 + M];
+            fa[4] = fmaf(g, cm[q + 1], fa[4]);
+            fa[5] = fmaf(g, cm[q] + cm[q + 2] + ch[q + 1], fa[5]);
+            fa[6] = fmaf(g, ch[q] + ch[q + 2], fa[6]);
+            const float gc = f.dcol[(4 * sb + q + 4 + M) * DC + j + 4 + M];
+            const int u = q >> 1;  // rr[u + k] = R row (t>>1) - 2 + k
+            if ((q & 1) == 0) {
+                fa[0] = fmaf(gc, rr[u + 0], fa[0]);
+                fa[2] = fmaf(gc, rr[u + 1], fa[2]);
+                fa[3] = fmaf(gc, rr[u + 2], fa[3]);
+                fa[1] = fmaf(gc, rr[u + 3], fa[1]);
+            } else {
+                fa[1] = fmaf(gc, rr[u + 1], fa[1]);
+                fa[3] = fmaf(gc, rr[u + 2], fa[3]);
+                fa[2] = fmaf(gc, rr[u + 3], fa[2]);
+                fa[0] = fmaf(gc, rr[u + 4], fa[0]);
+            }
         }
     }
-    // row pass: drow x input (input rows of the tile, owned output columns)
-    for (int i = ty; i < kBT; i += ny)
-    for (int j = tx; j < FO; j += 32) {
-        const float g = f.drow[i * FDC + j + 4];
-        const float* x = &f.x[(i + 3) * FX + (j >> 1) + 3];
-        if ((j & 1) == 0) {
-            fa[0] = fmaf(g, x[-2], fa[0]);
-            fa[2] = fmaf(g, x[-1], fa[2]);
-            fa[3] = fmaf(g, x[0], fa[3]);
-            fa[1] = fmaf(g, x[1], fa[1]);
-        } else {
-            fa[1] = fmaf(g, x[-1], fa[1]);
-            fa[3] = fmaf(g, x[0], fa[3]);
-            fa[2] = fmaf(g, x[1], fa[2]);
-            fa[0] = fmaf(g, x[2], fa[0]);
+    // row pass: drow x input over own input rows and owned output column pairs
+    for (int e = tid; e < TB * TB; e += nt) {
+        const int i = e / TB, m = e - i * TB;
+        if (BORDER && (U0 + i >= ri || b + 2 * m >= co)) continue;
+        const float* x = &f.x[(i + 3) * XW + m + 1];  // x[k] = X col V0 + m - 2 + k
+        const float* g = &f.drow[(i + MR) * DC + 2 * m + 4 + M];
+        const float ge = g[0];
+        fa[0] = fmaf(ge, x[0], fa[0]);
+        fa[2] = fmaf(ge, x[1], fa[2]);
+        fa[3] = fmaf(ge, x[2], fa[3]);
+        fa[1] = fmaf(ge, x[3], fa[1]);
+        if (!BORDER || b + 2 * m + 1 < co) {
+            const float go = g[1];
+            fa[1] = fmaf(go, x[1], fa[1]);
+            fa[3] = fmaf(go, x[2], fa[3]);
+            fa[2] = fmaf(go, x[3], fa[2]);
+            fa[0] = fmaf(go, x[4], fa[0]);
         }
     }
 #pragma unroll
     for (int k = 0; k < 7; ++k) acc[k] += double(fa[k]);
+    if (!BORDER || !wd) return;
+    __syncthreads();
+    // din: fold virtual cols -2,-1 -> 0 and ci, ci+1 -> ci-1; own in-image writes
+    for (int e = tid; e < TB * TB; e += nt) {
+        const int i = e / TB, jj = e - i * TB;
+        const int v = V0 + jj;
+        if (U0 + i >= ri || v >= ci) continue;
+        const float* d = &f.din[i * DI + MR];  // d[k] = column V0 + k
+        float s = d[jj];
+        if (v == 0) s += d[-1] + d[-2];
+        if (v == ci - 1) s += d[jj + 1] + d[jj + 2];
+        din[int64_t(U0 + i) * ci + v] = s;
+    }
 }
 
+// Backward tile edge per stage: the largest of 16 / 8 / 4 that still gives
+// every resident CTA slot work (2 per SM); coarse stages take small tiles so
+// their latency-bound phase chain is short.
+__host__ __device__ inline int bwd_tiles(const UpsStage& s, int tb) {
+    return ((s.rows_in + tb - 1) / tb) * ((s.cols_in + tb - 1) / tb);
+}
+
+template <int TB>
 __device__ __forceinline__ void ups_bwd_stage(const Plan& P, int j, int si, int t_begin, int t_step,
-                                              int write_lat, unsigned char* smem_raw,
-                                              double (&acc)[7]) {
+                                              int write_lat, BwdSmem<TB>& f, double (&acc)[7]) {
     const UpsStage& s = P.ups[j][si];
     const int ro = s.rows_out, co = s.cols_out, ri = s.rows_in, ci = s.cols_in;
-    const int tiles_x = (ci + kBT - 1) / kBT;
-    const int ntiles = tiles_x * ((ri + kBT - 1) / kBT);
-    BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
+    const int tiles_x = (ci + TB - 1) / TB;
+    const int ntiles = tiles_x * ((ri + TB - 1) / TB);
     const float* k4 = P.params + P.off_tconv[j];
     const float* r3 = P.params + P.off_refine[j];
     const float kk[4] = {k4[0], k4[1], k4[2], k4[3]};
@@ -403,224 +508,52 @@ __device__ __forceinline__ void ups_bwd_stage(const Plan& P, int j, int si, int 
     float* din = stage_din(P, s);
     const bool wd = write_lat || !s.din_is_lat;
     for (int tile = t_begin; tile < ntiles; tile += t_step) {
-        const int U0 = (tile / tiles_x) * kBT, V0 = (tile % tiles_x) * kBT;
-        if (bwd_interior(U0, V0, ri, ci, ro, co)) {
-            bwd_tile_fast(in, s.in_stride, dout, co, din, ci, wd, U0, V0, kk, kc, ke, ko,
-                          *reinterpret_cast<FastSmem*>(smem_raw), acc);
-            continue;
-        }
-        const int U1 = min(U0 + kBT, ri) - 1, V1 = min(V0 + kBT, ci) - 1;  // inclusive
-        // owned level-j positions: parents in the tile
-        const Win own_r{2 * U0, min(2 * U1 + 1, ro - 1)};
-        const Win own_c{2 * V0, min(2 * V1 + 1, co - 1)};
-        // level-j rows/cols whose transposed-tconv reaches the tile: t with
-        // any idx(t, q) in [U0, U1]  ->  t in [2U0 - 4, 2U1 + 5]
-        const Win dr{clampi(2 * U0 - 4, 0, ro - 1), clampi(2 * U1 + 5, 0, ro - 1)};
-        const Win dc{clampi(2 * V0 - 4, 0, co - 1), clampi(2 * V1 + 5, 0, co - 1)};
-        const Win gr{clampi(dr.lo - 1, 0, ro - 1), clampi(dr.hi + 1, 0, ro - 1)};
-        const Win gc{clampi(dc.lo - 1, 0, co - 1), clampi(dc.hi + 1, 0, co - 1)};
-        // recomputed forward intermediates over the owned region + refine halo
-        const Win cr{clampi(own_r.lo - 1, 0, ro - 1), clampi(own_r.hi + 1, 0, ro - 1)};
-        const Win cc{clampi(own_c.lo - 1, 0, co - 1), clampi(own_c.hi + 1, 0, co - 1)};
-        const Win rr = tconv_src(cr, ri - 1);  // rowtmp rows (also covers rows U0..U1)
-        const Win rw{min(rr.lo, U0), max(rr.hi, U1)};
-        // input columns: for rowtmp over cc, and for the row-pass dk4 over own_c
-        const Win ic = tconv_src(Win{min(cc.lo, own_c.lo), max(cc.hi, own_c.hi)}, ci - 1);
-        __syncthreads();
-        for (int e = threadIdx.x; e < gr.n() * gc.n(); e += blockDim.x) {
-            const int a = FDiv(gc.n()).div(e), b = e - a * gc.n();
-            cp_async4(&sm.dout[a * kBG + b], dout + int64_t(gr.lo + a) * co + (gc.lo + b));
-        }
-        for (int e = threadIdx.x; e < rw.n() * ic.n(); e += blockDim.x) {
-            const int a = FDiv(ic.n()).div(e), b = e - a * ic.n();
-            cp_async4(&sm.in[a * kBI + b], in + int64_t(rw.lo + a) * s.in_stride + (ic.lo + b));
-        }
-        cp_async_wait_all();
-        __syncthreads();
-        // rowtmp over rows rw, cols cc (recompute of tconv2x_rows_forward)
-        for (int e = threadIdx.x; e < rw.n() * cc.n(); e += blockDim.x) {
-            const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
-            int idx[4], tap[4];
-            tconv_map(cc.lo + b, ci - 1, idx, tap);
-            const float* x = sm.in + a * kBI - ic.lo;
-            sm.row[a * kBC + b] = kk[tap[0]] * x[idx[0]] + kk[tap[1]] * x[idx[1]] +
-                                  kk[tap[2]] * x[idx[2]] + kk[tap[3]] * x[idx[3]];
-        }
-        // dcol over (dr, dc): transposed refine (conv3x3_sym_backward, layers.hpp:486-515)
-        for (int e = threadIdx.x; e < dr.n() * dc.n(); e += blockDim.x) {
-            const int a = FDiv(dc.n()).div(e), b = e - a * dc.n();
-            const int r = dr.lo + a, c = dc.lo + b;
-            if (r >= 1 && r <= ro - 2 && c >= 1 && c <= co - 2) {
-                // interior: the symmetric stencil is its own transpose
-                const float* g = sm.dout + (r - gr.lo) * kBG + (c - gc.lo);
-                sm.dcol[a * kBD + b] = kc * g[0] + ke * (g[-kBG] + g[kBG] + g[-1] + g[1]) +
-                                       ko * (g[-kBG - 1] + g[-kBG + 1] + g[kBG - 1] + g[kBG + 1]);
-                continue;
-            }
-            int rp[3], rd[3], cp[3], cd[3];
-            const int nr = nbr_pairs(r, ro, rp, rd), nc = nbr_pairs(c, co, cp, cd);
-            float sum = 0.0f;
-            for (int x = 0; x < nr; ++x)
-                for (int y = 0; y < nc; ++y) {
-                    const int cls = (rd[x] != 0) + (cd[y] != 0);
-                    const float w = cls == 0 ? kc : (cls == 1 ? ke : ko);
-                    sum += w * sm.dout[(rp[x] - gr.lo) * kBG + (cp[y] - gc.lo)];
-                }
-            sm.dcol[a * kBD + b] = sum;
-        }
-        __syncthreads();
-        // coltmp over (cr, cc) (recompute of tconv2x_cols_forward)
-        for (int e = threadIdx.x; e < cr.n() * cc.n(); e += blockDim.x) {
-            const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
-            int idx[4], tap[4];
-            tconv_map(cr.lo + a, ri - 1, idx, tap);
-            const float* xr = sm.row + b - rw.lo * kBC;
-            sm.col[a * kBC + b] = kk[tap[0]] * xr[idx[0] * kBC] + kk[tap[1]] * xr[idx[1] * kBC] +
-                                  kk[tap[2]] * xr[idx[2] * kBC] + kk[tap[3]] * xr[idx[3] * kBC];
-        }
-        // drow[u][t'] for u in tile rows, t' in dc: transposed column pass
-        const int vmax_r = (ro - 1) >> 1;
-        const int ufast_hi = min(ri - 2, (ro - 5) / 2);
-        for (int e = threadIdx.x; e < (U1 - U0 + 1) * dc.n(); e += blockDim.x) {
-            const int a = FDiv(dc.n()).div(e), b = e - a * dc.n();
-            const int u = U0 + a;
-            if (u >= 2 && u <= ufast_hi) {
-                // interior: outputs 2u-3 .. 2u+4 reach u with fixed taps
-                const float* g = sm.dcol + (2 * u - dr.lo) * kBD + b;
-                sm.drow[a * kBD + b] = kk[0] * (g[4 * kBD] + g[-3 * kBD]) + kk[1] * (g[-2 * kBD] + g[3 * kBD]) +
-                                       kk[2] * (g[2 * kBD] + g[-kBD]) + kk[3] * (g[0] + g[kBD]);
-                continue;
-            }
-            float sum = 0.0f;
-            const int v0 = max(u - 2, 0), v1 = min(u + 2, vmax_r);
-            for (int v = v0; v <= v1; ++v)
-                for (int par = 0; par < 2; ++par) {
-                    const int t = 2 * v + par;
-                    if (t >= ro) continue;
-                    int idx[4], tap[4];
-                    tconv_map(t, ri - 1, idx, tap);
-                    const float g = sm.dcol[(t - dr.lo) * kBD + b];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (idx[q] == u) sum += kk[tap[q]] * g;
-                }
-            sm.drow[a * kBD + b] = sum;
-        }
-        __syncthreads();
-        // din[u][v]: transposed row pass (tconv2x_rows_backward, layers.hpp:378-405)
-        if (wd) {
-            const int vmax_c = (co - 1) >> 1;
-            const int vfast_hi = min(ci - 2, (co - 5) / 2);
-            for (int e = threadIdx.x; e < (U1 - U0 + 1) * (V1 - V0 + 1); e += blockDim.x) {
-                const int a = FDiv(V1 - V0 + 1).div(e), b = e - a * (V1 - V0 + 1);
-                const int u = V0 + b;
-                if (u >= 2 && u <= vfast_hi) {
-                    const float* g = sm.drow + a * kBD + (2 * u - dc.lo);
-                    din[int64_t(U0 + a) * ci + u] = kk[0] * (g[4] + g[-3]) + kk[1] * (g[-2] + g[3]) +
-                                                    kk[2] * (g[2] + g[-1]) + kk[3] * (g[0] + g[1]);
-                    continue;
-                }
-                float sum = 0.0f;
-                const int w0 = max(u - 2, 0), w1 = min(u + 2, vmax_c);
-                for (int w = w0; w <= w1; ++w)
-                    for (int par = 0; par < 2; ++par) {
-                        const int t = 2 * w + par;
-                        if (t >= co) continue;
-                        int idx[4], tap[4];
-                        tconv_map(t, ci - 1, idx, tap);
-                        const float g = sm.drow[a * kBD + (t - dc.lo)];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            if (idx[q] == u) sum += kk[tap[q]] * g;
-                    }
-                din[int64_t(U0 + a) * ci + u] = sum;
-            }
-        }
-        // tap gradients over owned positions
-        for (int e = threadIdx.x; e < own_r.n() * own_c.n(); e += blockDim.x) {
-            const int a = FDiv(own_c.n()).div(e), b = e - a * own_c.n();
-            const int r = own_r.lo + a, c = own_c.lo + b;
-            // refine: dOut x coltmp neighbourhood (layers.hpp:504-506)
-            const float g = sm.dout[(r - gr.lo) * kBG + (c - gc.lo)];
-            const int rm = (r > 0 ? r - 1 : 0) - cr.lo, r0 = r - cr.lo, rp = (r < ro - 1 ? r + 1 : ro - 1) - cr.lo;
-            const int cm = (c > 0 ? c - 1 : 0) - cc.lo, c0 = c - cc.lo, cp = (c < co - 1 ? c + 1 : co - 1) - cc.lo;
-            const float* x0 = sm.col + rm * kBC;
-            const float* x1 = sm.col + r0 * kBC;
-            const float* x2 = sm.col + rp * kBC;
-            acc[4] += double(g) * double(x1[c0]);
-            acc[5] += double(g) * double(x0[c0] + x2[c0] + x1[cm] + x1[cp]);
-            acc[6] += double(g) * double(x0[cm] + x0[cp] + x2[cm] + x2[cp]);
-            // column pass: dcol x rowtmp (layers.hpp:452-457)
-            int idx[4], tap[4];
-            tconv_map(r, ri - 1, idx, tap);
-            const double gc2 = double(sm.dcol[(r - dr.lo) * kBD + (c - dc.lo)]);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-                acc[tap[q]] += gc2 * double(sm.row[(idx[q] - rw.lo) * kBC + (c - cc.lo)]);
-        }
-        // row pass: drow x input over (u in tile, t' owned) (layers.hpp:395,401)
-        for (int e = threadIdx.x; e < (U1 - U0 + 1) * own_c.n(); e += blockDim.x) {
-            const int a = FDiv(own_c.n()).div(e), b = e - a * own_c.n();
-            const int t = own_c.lo + b;
-            int idx[4], tap[4];
-            tconv_map(t, ci - 1, idx, tap);
-            const double g = double(sm.drow[a * kBD + (t - dc.lo)]);
-            const float* x = sm.in + (U0 + a - rw.lo) * kBI - ic.lo;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) acc[tap[q]] += g * double(x[idx[q]]);
-        }
+        const int U0 = (tile / tiles_x) * TB, V0 = (tile % tiles_x) * TB;
+        if (bwd_interior<TB>(U0, V0, ri, ci, ro, co))
+            bwd_tile<TB, false>(in, s.in_stride, dout, ro, co, din, ri, ci, wd, U0, V0, kk, kc, ke, ko, f, acc);
+        else
+            bwd_tile<TB, true>(in, s.in_stride, dout, ro, co, din, ri, ci, wd, U0, V0, kk, kc, ke, ko, f, acc);
     }
 }
 
-// tap gradients of this CTA for stage j -> partial row `row`
-__device__ __forceinline__ void ups_bwd_write(const Plan& P, int j, int row, unsigned char* smem_raw,
-                                              double (&acc)[7]) {
-    BwdSmem& sm = *reinterpret_cast<BwdSmem*>(smem_raw);
-    block_sum_vec<7>(acc, sm.red, sm.tot);
-    __syncthreads();
-    if (threadIdx.x < 4) {
-        const PartialRegion& R = P.region[P.reg_ups_rows[j]];
-        P.partials[R.base + int64_t(row) * R.count + threadIdx.x] = sm.tot[threadIdx.x];
-    } else if (threadIdx.x < 7) {
-        const PartialRegion& R = P.region[P.reg_ups_ref[j]];
-        P.partials[R.base + int64_t(row) * R.count + (threadIdx.x - 4)] = sm.tot[threadIdx.x];
-    }
-}
-
-__global__ void __launch_bounds__(kThreadsWide) k_ups_bwd(const Plan* __restrict__ pp, int j,
-                                                      int write_lat) {
+template <int TB>
+__global__ void __launch_bounds__(kThreads, 3) k_ups_bwd(const Plan* __restrict__ pp, int j, int write_lat) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    BwdSmem<TB>& f = *reinterpret_cast<BwdSmem<TB>*>(smem_raw);
     const Plan& P = *pp;
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // dk4[0..3] (rows+cols passes), dr3[0..2]
-    ups_bwd_stage(P, j, blockIdx.y, blockIdx.x, gridDim.x, write_lat, smem_raw, acc);
-    ups_bwd_write(P, j, blockIdx.y * gridDim.x + blockIdx.x, smem_raw, acc);
-}
-
-// Coarse stages j >= jc in one launch (see k_ups_fwd_coarse): CTA b runs
-// cascade k = jc + 1 + b through stages jc .. k-1; one partial row per
-// (stage, cascade).
-__global__ void __launch_bounds__(kThreadsWide) k_ups_bwd_coarse(const Plan* __restrict__ pp, int jc,
-                                                             int write_lat) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Plan& P = *pp;
-    const int k = jc + 1 + blockIdx.x;
-    for (int j = jc; j < k; ++j) {
-        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-        ups_bwd_stage(P, j, k - j - 1, 0, 1, write_lat, smem_raw, acc);
-        ups_bwd_write(P, j, k - j - 1, smem_raw, acc);
-        __syncthreads();
+    ups_bwd_stage<TB>(P, j, blockIdx.y, blockIdx.x, gridDim.x, write_lat, f, acc);
+    // tap gradients of this CTA -> partial row (blockIdx.y, blockIdx.x)
+    block_sum_vec<7>(acc, f.red, f.tot);
+    __syncthreads();
+    const int row = blockIdx.y * gridDim.x + blockIdx.x;
+    if (threadIdx.x < 4) {
+        const PartialRegion& R = P.region[P.reg_ups_rows[j]];
+        P.partials[R.base + int64_t(row) * R.count + threadIdx.x] = f.tot[threadIdx.x];
+    } else if (threadIdx.x < 7) {
+        const PartialRegion& R = P.region[P.reg_ups_ref[j]];
+        P.partials[R.base + int64_t(row) * R.count + (threadIdx.x - 4)] = f.tot[threadIdx.x];
     }
 }
 
 }  // namespace
 
+int ups_bwd_tile(const Plan& H, int j, int num_sms) {
+    for (int tb : {16, 8}) {
+        int t = 0;
+        for (int i = 0; i < H.ups_n[j]; ++i) t += bwd_tiles(H.ups[j][i], tb);
+        if (t >= 2 * num_sms) return tb;
+    }
+    return 4;
+}
+
 int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward) {
-    // enough CTAs to cover the largest grid of the stage, capped at ~2 waves
+    // enough CTAs to cover the largest grid of the stage, capped
+    const int tb = forward ? kFT : ups_bwd_tile(H, j, num_sms);
     int best = 1;
     for (int i = 0; i < H.ups_n[j]; ++i) {
         const UpsStage& s = H.ups[j][i];
-        const int t = forward ? ((s.rows_out + kFT - 1) / kFT) * ((s.cols_out + kFT - 1) / kFT)
-                              : ((s.rows_in + kBT - 1) / kBT) * ((s.cols_in + kBT - 1) / kBT);
+        const int t = forward ? ((s.rows_out + kFT - 1) / kFT) * ((s.cols_out + kFT - 1) / kFT) : bwd_tiles(s, tb);
         best = t > best ? t : best;
     }
     // forward: up to ~2 waves; backward: persistent CTAs (~3 per SM over all
@@ -631,42 +564,19 @@ int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward) {
     return best < cap ? best : cap;
 }
 
-// First stage of the fused coarse launch: the smallest j such that every
-// stage j' >= j has at most 8 tiles per grid in either direction.  Off by
-// default (CCB_UPS_FUSE=1 enables it): measured at 512x768 the per-cascade
-// CTA serialises ~9 tiles of the clamp-aware path (~4 us each), which is
-// slower than the 3-4 latency-bound launches it replaces (146 -> 178 us).
-int ups_coarse_from(const Plan& H) {
-    const char* e = std::getenv("CCB_UPS_FUSE");
-    if (!e || e[0] != '1') return H.L - 1;
-    int jc = H.L - 1;
-    for (int j = H.L - 2; j >= 0; --j) {
-        int mt = 0;
-        for (int i = 0; i < H.ups_n[j]; ++i) {
-            const UpsStage& s = H.ups[j][i];
-            const int tf = ((s.rows_out + kFT - 1) / kFT) * ((s.cols_out + kFT - 1) / kFT);
-            const int tb = ((s.rows_in + kBT - 1) / kBT) * ((s.cols_in + kBT - 1) / kBT);
-            mt = std::max(mt, std::max(tf, tb));
-        }
-        if (mt > 8) break;
-        jc = j;
-    }
-    return jc;
-}
-
-size_t ups_bwd_smem() { return sizeof(BwdSmem); }
+// no fused coarse launch: every stage has its own (small-tile) launch
+int ups_coarse_from(const Plan& H) { return H.L - 1; }
 
 void ups_configure() {
-    cudaFuncSetAttribute(k_ups_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
-    cudaFuncSetAttribute(k_ups_bwd_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem)));
+    cudaFuncSetAttribute(k_ups_bwd<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<16>)));
+    cudaFuncSetAttribute(k_ups_bwd<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<8>)));
+    cudaFuncSetAttribute(k_ups_bwd<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<4>)));
 }
 
 void launch_ups_forward(const LaunchCtx& L) {
     const Plan& H = *L.host;
     // z plane 0 (= ŷ of main grid 0) is written by k_softq_fwd / k_pads_from_q
-    const int jc = H.ups_jc;
-    if (jc <= H.L - 2) k_ups_fwd_coarse<<<H.L - 1 - jc, kThreadsWide, 0, L.stream>>>(L.plan, jc);
-    for (int j = jc - 1; j >= 0; --j) {
+    for (int j = H.L - 2; j >= 0; --j) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, true), H.ups_n[j]);
         const int nt = int(grid.x * grid.y) < 2 * L.num_sms ? kThreadsWide : kThreads;
@@ -676,16 +586,16 @@ void launch_ups_forward(const LaunchCtx& L) {
 
 void launch_ups_backward(const LaunchCtx& L, bool latent_grads, int j_begin, int j_end) {
     const Plan& H = *L.host;
-    const int jc = H.ups_jc;
-    for (int j = j_begin; j < jc && j <= H.L - 2 && j < j_end; ++j) {
+    for (int j = j_begin; j <= H.L - 2 && j < j_end; ++j) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, false), H.ups_n[j]);
-        const int nt = int(grid.x * grid.y) < 2 * L.num_sms ? kThreadsWide : kThreads;
-        k_ups_bwd<<<grid, nt, sizeof(BwdSmem), L.stream>>>(L.plan, j, latent_grads ? 1 : 0);
+        const int wl = latent_grads ? 1 : 0;
+        switch (ups_bwd_tile(H, j, L.num_sms)) {
+            case 16: k_ups_bwd<16><<<grid, kThreads, sizeof(BwdSmem<16>), L.stream>>>(L.plan, j, wl); break;
+            case 8: k_ups_bwd<8><<<grid, kThreads, sizeof(BwdSmem<8>), L.stream>>>(L.plan, j, wl); break;
+            default: k_ups_bwd<4><<<grid, kThreads, sizeof(BwdSmem<4>), L.stream>>>(L.plan, j, wl); break;
+        }
     }
-    if (jc <= H.L - 2 && j_end > H.L - 2)
-        k_ups_bwd_coarse<<<H.L - 1 - jc, kThreadsWide, sizeof(BwdSmem), L.stream>>>(L.plan, jc,
-                                                                                   latent_grads ? 1 : 0);
 }
 
 }  // namespace ccb
