@@ -23,6 +23,25 @@ struct LaunchCtx {
     int red_blocks;        // per-CTA partial rows of the small reduction kernels
 };
 
+// Launch with programmatic stream serialization (see pdl_wait in
+// cc_math.cuh); CCB_PDL=0 falls back to plain stream order (A/B).
+bool pdl_enabled(char which = 'a');  // which: 'f' upsampling forward, 'b' backward
+template <typename... P, typename... A>
+inline void launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, char which,
+                       A... args) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled(which) ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, static_cast<P>(args)...);
+}
+
 enum ArmMode { kArmForward = 0, kArmHard = 1, kArmProxy = 2 };
 
 // latent side (cc_latent.cu)

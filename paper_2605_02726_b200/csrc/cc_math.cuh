@@ -132,6 +132,16 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 }
 __device__ __forceinline__ float2 ffma2(float2 a, float b, float2 c) { return ffma2(a, make_float2(b, b), c); }
 
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor in
+// the stream drains; it reads only long-settled data (plan, parameters,
+// forward activations) before pdl_wait(), which blocks until the
+// predecessor grid has completed and its writes are visible.  pdl_trigger()
+// then lets the successor's CTAs be scheduled.  Both are no-ops for a
+// kernel launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.wait_all;\n" ::: "memory");
 }

@@ -14,6 +14,17 @@
 
 namespace ccb {
 
+bool pdl_enabled(char which) {
+    // Default: the upsampling forward chain only.  PDL on the backward chain
+    // makes each stage faster alone but its early-resident CTAs crowd out the
+    // concurrent fine-grid gradient / Adam tail (512x768: +12 us per step).
+    static const char* e = std::getenv("CCB_PDL");  // A/B: 0 off, 1 both, f / b one direction
+    if (!e) return which == 'f';
+    if (e[0] == '0') return false;
+    if (e[0] == 'f' || e[0] == 'b') return which == e[0];
+    return true;
+}
+
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
         throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
@@ -102,6 +113,9 @@ void Trainer::init(const float* image, int h, int w) {
         const char* e = std::getenv("CCB_SIDE_PRIO");
         const int prio = (e && e[0] == '0') ? 0 : lo;
         CCB_CUDA(cudaStreamCreateWithPriority(&side_stream_, cudaStreamNonBlocking, prio));
+        const char* t = std::getenv("CCB_TAIL_PRIO");  // A/B: l(ow, default) / n(ormal) / h(igh)
+        const int tprio = (t && t[0] == 'n') ? 0 : (t && t[0] == 'h') ? hi : lo;
+        CCB_CUDA(cudaStreamCreateWithPriority(&tail_stream_, cudaStreamNonBlocking, tprio));
     }
     CCB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     CCB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
@@ -132,10 +146,12 @@ Trainer::~Trainer() {
     if (h_rec_) cudaFreeHost(h_rec_);
     if (h_sched_) cudaFreeHost(h_sched_);
     if (side_stream_) cudaStreamSynchronize(side_stream_);
+    if (tail_stream_) cudaStreamSynchronize(tail_stream_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (ev_sched_) cudaEventDestroy(ev_sched_);
     if (side_stream_) cudaStreamDestroy(side_stream_);
+    if (tail_stream_) cudaStreamDestroy(tail_stream_);
     if (own_stream_) cudaStreamDestroy(own_stream_);
 }
 
@@ -638,24 +654,25 @@ void Trainer::nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, doub
 // (upsampling, synthesis, their backward) only share ŷ as input, so they run
 // as two concurrent branches of the graph and join before the gradient
 // assembly.
-void Trainer::fork() {
+void Trainer::fork(bool tail) {
     CCB_CUDA(cudaEventRecord(ev_fork_, stream_));
-    CCB_CUDA(cudaStreamWaitEvent(side_stream_, ev_fork_, 0));
+    CCB_CUDA(cudaStreamWaitEvent(tail ? tail_stream_ : side_stream_, ev_fork_, 0));
 }
-void Trainer::join() {
-    CCB_CUDA(cudaEventRecord(ev_join_, side_stream_));
+void Trainer::join(bool tail) {
+    CCB_CUDA(cudaEventRecord(ev_join_, tail ? tail_stream_ : side_stream_));
     CCB_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
 }
-LaunchCtx Trainer::side() const {
+LaunchCtx Trainer::side(bool tail) const {
     LaunchCtx s = L_;
-    s.stream = side_stream_;
+    s.stream = tail ? tail_stream_ : side_stream_;
     return s;
 }
 
 // timeline diagnostics (ccb_timeline): event marks inside the captured sequence
-void Trainer::mark(int id, bool on_side) {
+void Trainer::mark(int id, int on) {
     if (tl_ev_)  // an event-record node of the graph (timing), not a capture dependency
-        CCB_CUDA(cudaEventRecordWithFlags(tl_ev_[id], on_side ? side_stream_ : stream_, cudaEventRecordExternal));
+        CCB_CUDA(cudaEventRecordWithFlags(tl_ev_[id], on == 2 ? tail_stream_ : on ? side_stream_ : stream_,
+                                          cudaEventRecordExternal));
 }
 
 void Trainer::enqueue_proxy(bool batched) {
@@ -687,20 +704,20 @@ void Trainer::enqueue_proxy(bool batched) {
     // NN gradients: every region but the upsampling taps is complete here
     // (ARM, synthesis); the taps ([off_tconv[0], off_c1w)) after the last stage
     const int ups_lo = H_.off_tconv[0], ups_hi = H_.off_c1w;
-    fork();
-    launch_finalize(side(), kArmProxy, -1);
-    launch_latent_grad_grids(side(), fine, H_.n_grids);
-    mark(8, true);
-    launch_adam_latents_grids(side(), fine, H_.n_grids);
-    launch_nn_reduce(side(), 0, ups_lo);
-    launch_nn_reduce(side(), ups_hi, H_.n_params);
-    mark(9, true);
+    fork(true);
+    launch_finalize(side(true), kArmProxy, -1);
+    launch_latent_grad_grids(side(true), fine, H_.n_grids);
+    mark(8, 2);
+    launch_adam_latents_grids(side(true), fine, H_.n_grids);
+    launch_nn_reduce(side(true), 0, ups_lo);
+    launch_nn_reduce(side(true), ups_hi, H_.n_params);
+    mark(9, 2);
     launch_ups_backward(L_, true, 1);
     mark(10, false);
     launch_latent_grad_grids(L_, 0, fine);
     launch_nn_reduce(L_, ups_lo, ups_hi);
     mark(11, false);
-    join();
+    join(true);
     if (fine > 0) launch_adam_latents_grids(L_, 0, fine);
     nn_apply(L_, true, true, batched ? d_rec_ : nullptr);
     mark(12, false);

@@ -137,16 +137,16 @@ public:
 
 private:
     void init(const float* image, int h, int w);
-    void mark(int id, bool on_side);
+    void mark(int id, int on);  // 0 main, 1 side, 2 tail stream
     void nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, double* cost_log);
     void build_plan();
     void allocate();
     void require_loaded() const;
     void init_params_host(uint64_t stream, std::vector<float>& out) const;
     void enqueue_proxy(bool batched);
-    void fork();
-    void join();
-    LaunchCtx side() const;
+    void fork(bool tail = false);
+    void join(bool tail = false);
+    LaunchCtx side(bool tail = false) const;
     void enqueue_hardround(int slot);
     void enqueue_true_cost();
     void run_graph(int which, int slot = -1);
@@ -163,6 +163,7 @@ private:
     cudaStream_t stream_ = nullptr;
     cudaStream_t own_stream_ = nullptr;
     cudaStream_t side_stream_ = nullptr;  // concurrent rate branch
+    cudaStream_t tail_stream_ = nullptr;  // concurrent fine-grid gradient tail
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     cudaEvent_t ev_sched_ = nullptr;  // the pinned schedule upload of the last batch
     Plan H_{};

@@ -102,6 +102,8 @@ __device__ __forceinline__ void ups_fwd_stage(const Plan& P, int j, int si, int 
     const float kc = r3[0], ke = r3[1], ko = r3[2];
     const float* in = stage_in(P, s);
     float* out = stage_out(P, s);
+    pdl_wait();  // the stage input is the previous stage's output
+    pdl_trigger();
     for (int tile = t_begin; tile < ntiles; tile += t_step) {
         const int y0 = (tile / tiles_x) * kFT, x0 = (tile % tiles_x) * kFT;
         if (y0 >= kFT && x0 >= kFT && y0 / 2 + 18 <= ri - 1 && x0 / 2 + 18 <= ci - 1 && y0 + kFT <= ro - 1 &&
@@ -262,22 +264,15 @@ __device__ __forceinline__ void bwd_tile(const float* __restrict__ in, int in_st
                                          const float* __restrict__ dout, int ro, int co,
                                          float* __restrict__ din, int ri, int ci, bool wd, int U0, int V0,
                                          const float (&kk)[4], float kc, float ke, float ko,
-                                         BwdSmem<TB>& f, double (&acc)[7]) {
+                                         BwdSmem<TB>& f, double (&acc)[7], bool first) {
     using G = BwdGeo<TB, BORDER>;
     constexpr int M = G::M, MR = G::MR, FO = G::FO, DO = G::DO, DC = G::DC, DR = G::DR, DI = G::DI;
     constexpr int XW = G::XW, RC = G::RC, CR = G::CR, CC = G::CC, OFF = G::OFF;
     const int a = 2 * U0, b = 2 * V0;
     const int tid = threadIdx.x, nt = blockDim.x;
     __syncthreads();  // the previous tile's readers are done with the windows
-    // ---- P0: dOut window (zero outside the image), input window (clamped)
-    for (int e = tid; e < DO * DO; e += nt) {
-        const int i = e / DO, j = e - i * DO;
-        const int t = a - 5 - M + i, tc = b - 5 - M + j;
-        if (!BORDER || (t >= 0 && t < ro && tc >= 0 && tc < co))
-            cp_async4(&f.dout[e], dout + int64_t(t) * co + tc);
-        else
-            f.dout[e] = 0.0f;
-    }
+    // ---- P0: input window (clamped; forward data), then — once the
+    // predecessor grid is done — the dOut window (zero outside the image)
     for (int e = tid; e < XW * XW; e += nt) {
         const int i = e / XW, j = e - i * XW;
         int u = U0 - 3 + i, v = V0 - 3 + j;
@@ -286,6 +281,18 @@ __device__ __forceinline__ void bwd_tile(const float* __restrict__ in, int in_st
             v = clampi(v, 0, ci - 1);
         }
         cp_async4(&f.x[e], in + int64_t(u) * in_stride + v);
+    }
+    if (first) {
+        pdl_wait();
+        pdl_trigger();
+    }
+    for (int e = tid; e < DO * DO; e += nt) {
+        const int i = e / DO, j = e - i * DO;
+        const int t = a - 5 - M + i, tc = b - 5 - M + j;
+        if (!BORDER || (t >= 0 && t < ro && tc >= 0 && tc < co))
+            cp_async4(&f.dout[e], dout + int64_t(t) * co + tc);
+        else
+            f.dout[e] = 0.0f;
     }
     cp_async_wait_all();
     __syncthreads();
@@ -509,10 +516,11 @@ __device__ __forceinline__ void ups_bwd_stage(const Plan& P, int j, int si, int 
     const bool wd = write_lat || !s.din_is_lat;
     for (int tile = t_begin; tile < ntiles; tile += t_step) {
         const int U0 = (tile / tiles_x) * TB, V0 = (tile % tiles_x) * TB;
+        const bool first = tile == t_begin;
         if (bwd_interior<TB>(U0, V0, ri, ci, ro, co))
-            bwd_tile<TB, false>(in, s.in_stride, dout, ro, co, din, ri, ci, wd, U0, V0, kk, kc, ke, ko, f, acc);
+            bwd_tile<TB, false>(in, s.in_stride, dout, ro, co, din, ri, ci, wd, U0, V0, kk, kc, ke, ko, f, acc, first);
         else
-            bwd_tile<TB, true>(in, s.in_stride, dout, ro, co, din, ri, ci, wd, U0, V0, kk, kc, ke, ko, f, acc);
+            bwd_tile<TB, true>(in, s.in_stride, dout, ro, co, din, ri, ci, wd, U0, V0, kk, kc, ke, ko, f, acc, first);
     }
 }
 
@@ -580,7 +588,7 @@ void launch_ups_forward(const LaunchCtx& L) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, true), H.ups_n[j]);
         const int nt = int(grid.x * grid.y) < 2 * L.num_sms ? kThreadsWide : kThreads;
-        k_ups_fwd<<<grid, nt, 0, L.stream>>>(L.plan, j);
+        launch_pdl(k_ups_fwd, grid, dim3(nt), 0, L.stream, 'f', L.plan, j);
     }
 }
 
@@ -591,9 +599,9 @@ void launch_ups_backward(const LaunchCtx& L, bool latent_grads, int j_begin, int
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, false), H.ups_n[j]);
         const int wl = latent_grads ? 1 : 0;
         switch (ups_bwd_tile(H, j, L.num_sms)) {
-            case 16: k_ups_bwd<16><<<grid, kThreads, sizeof(BwdSmem<16>), L.stream>>>(L.plan, j, wl); break;
-            case 8: k_ups_bwd<8><<<grid, kThreads, sizeof(BwdSmem<8>), L.stream>>>(L.plan, j, wl); break;
-            default: k_ups_bwd<4><<<grid, kThreads, sizeof(BwdSmem<4>), L.stream>>>(L.plan, j, wl); break;
+            case 16: launch_pdl(k_ups_bwd<16>, grid, kThreads, sizeof(BwdSmem<16>), L.stream, 'b', L.plan, j, wl); break;
+            case 8: launch_pdl(k_ups_bwd<8>, grid, kThreads, sizeof(BwdSmem<8>), L.stream, 'b', L.plan, j, wl); break;
+            default: launch_pdl(k_ups_bwd<4>, grid, kThreads, sizeof(BwdSmem<4>), L.stream, 'b', L.plan, j, wl); break;
         }
     }
 }
