@@ -30,15 +30,19 @@ template <typename... P, typename... A>
 inline void launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, char which,
                        A... args) {
     cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    int na = 0;
+    if (pdl_enabled(which)) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled(which) ? 1 : 0;
+    cfg.numAttrs = na;
     cudaLaunchKernelEx(&cfg, k, static_cast<P>(args)...);
 }
 

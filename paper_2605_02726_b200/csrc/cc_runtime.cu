@@ -15,11 +15,8 @@
 namespace ccb {
 
 bool pdl_enabled(char which) {
-    // Default: the upsampling forward chain only.  PDL on the backward chain
-    // makes each stage faster alone but its early-resident CTAs crowd out the
-    // concurrent fine-grid gradient / Adam tail (512x768: +12 us per step).
-    static const char* e = std::getenv("CCB_PDL");  // A/B: 0 off, 1 both, f / b one direction
-    if (!e) return which == 'f';
+    static const char* e = std::getenv("CCB_PDL");  // A/B: 0 off, f / b one direction only
+    if (!e) return true;
     if (e[0] == '0') return false;
     if (e[0] == 'f' || e[0] == 'b') return which == e[0];
     return true;
@@ -104,12 +101,15 @@ void Trainer::init(const float* image, int h, int w) {
         throw CudaError("libcoolchic_b200 is built for sm_100a; device " + std::string(prop.name) +
                         " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
     num_sms_ = prop.multiProcessorCount;
-    CCB_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
     {
-        // the rate branch (persistent ARM) yields CTA slots to the critical
-        // distortion branch: side stream at the lowest priority
+        // The critical chain (softq -> upsampling -> synthesis -> backward ->
+        // upsampling backward) runs on the main stream at the greatest
+        // priority: its CTAs are scheduled ahead of the concurrent branches
+        // (persistent ARM, gradient gathers, reductions) whenever SM slots free.
         int lo = 0, hi = 0;
         CCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        const char* m = std::getenv("CCB_MAIN_PRIO");  // A/B: n = default priority
+        CCB_CUDA(cudaStreamCreateWithPriority(&own_stream_, cudaStreamNonBlocking, (m && m[0] == 'n') ? lo : hi));
         const char* e = std::getenv("CCB_SIDE_PRIO");
         const int prio = (e && e[0] == '0') ? 0 : lo;
         CCB_CUDA(cudaStreamCreateWithPriority(&side_stream_, cudaStreamNonBlocking, prio));
@@ -120,6 +120,7 @@ void Trainer::init(const float* image, int h, int w) {
     CCB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     CCB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     CCB_CUDA(cudaEventCreateWithFlags(&ev_sched_, cudaEventDisableTiming));
+    CCB_CUDA(cudaEventCreateWithFlags(&ev_fin_, cudaEventDisableTiming));
     stream_ = own_stream_;
     build_plan();
     allocate();
@@ -150,6 +151,7 @@ Trainer::~Trainer() {
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (ev_sched_) cudaEventDestroy(ev_sched_);
+    if (ev_fin_) cudaEventDestroy(ev_fin_);
     if (side_stream_) cudaStreamDestroy(side_stream_);
     if (tail_stream_) cudaStreamDestroy(tail_stream_);
     if (own_stream_) cudaStreamDestroy(own_stream_);
@@ -704,19 +706,26 @@ void Trainer::enqueue_proxy(bool batched) {
     // NN gradients: every region but the upsampling taps is complete here
     // (ARM, synthesis); the taps ([off_tconv[0], off_c1w)) after the last stage
     const int ups_lo = H_.off_tconv[0], ups_hi = H_.off_c1w;
+    // side: cost / bias corrections, then the NN-gradient reductions that
+    // are already complete; tail: the fine-grid gather and (once the cost
+    // flag is known) their Adam step
+    fork();
+    launch_finalize(side(), kArmProxy, -1);
+    CCB_CUDA(cudaEventRecord(ev_fin_, side_stream_));
+    launch_nn_reduce(side(), 0, ups_lo);
+    launch_nn_reduce(side(), ups_hi, H_.n_params);
     fork(true);
-    launch_finalize(side(true), kArmProxy, -1);
     launch_latent_grad_grids(side(true), fine, H_.n_grids);
     mark(8, 2);
+    CCB_CUDA(cudaStreamWaitEvent(tail_stream_, ev_fin_, 0));
     launch_adam_latents_grids(side(true), fine, H_.n_grids);
-    launch_nn_reduce(side(true), 0, ups_lo);
-    launch_nn_reduce(side(true), ups_hi, H_.n_params);
     mark(9, 2);
     launch_ups_backward(L_, true, 1);
     mark(10, false);
     launch_latent_grad_grids(L_, 0, fine);
     launch_nn_reduce(L_, ups_lo, ups_hi);
     mark(11, false);
+    join();
     join(true);
     if (fine > 0) launch_adam_latents_grids(L_, 0, fine);
     nn_apply(L_, true, true, batched ? d_rec_ : nullptr);

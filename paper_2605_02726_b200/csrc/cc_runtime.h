@@ -165,6 +165,7 @@ private:
     cudaStream_t side_stream_ = nullptr;  // concurrent rate branch
     cudaStream_t tail_stream_ = nullptr;  // concurrent fine-grid gradient tail
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    cudaEvent_t ev_fin_ = nullptr;    // k_finalize done (the cost flag the latent Adam step reads)
     cudaEvent_t ev_sched_ = nullptr;  // the pinned schedule upload of the last batch
     Plan H_{};
     Plan* d_plan_ = nullptr;
