@@ -129,7 +129,7 @@ struct OutMap {
 
 template <int DP, int WP, int MODE>
 __global__ void __launch_bounds__(kArmTile) k_arm(const Plan* __restrict__ pp,
-                                                  const int2* __restrict__ tiles, int ntiles) {
+                                                  const int4* __restrict__ tiles, int ntiles) {
     using K = ArmCfg<DP, WP>;
     const Plan& P = *pp;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -186,11 +186,11 @@ __global__ void __launch_bounds__(kArmTile) k_arm(const Plan* __restrict__ pp,
     double bits_cta = 0.0;  // thread 0
 
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int2 tile = tiles[t];
+        const int4 tile = tiles[t];
         const GridGeom& g = P.g[tile.x];
         const int64_t count = int64_t(g.rows) * g.cols;
         const int64_t li = int64_t(tile.y) + tid;
-        const bool valid = li < count;
+        const bool valid = tid < tile.w;  // row segment of tile.w latents
         const int r = valid ? int(li / g.cols) : 0;
         const int c = valid ? int(li - int64_t(r) * g.cols) : 0;
         const int slot = g.ifce_slot;

@@ -41,6 +41,10 @@ constexpr int NT = 2 * T;     // threads per CTA
 constexpr int LT = T + 4;     // shared-memory row length (floats)
 constexpr int kRM = 12;       // max IFCE source grids
 constexpr int kFM = 8;        // max IFCE width
+constexpr int kMaxPad = 4;    // context window halo (yhat_pad border P)
+constexpr int WS = T + 2 * kMaxPad;  // context window row: columns c0-P .. c0+len-1+P
+constexpr int WC = (kMaxPad + 1) * WS;  // context part of a window
+constexpr int WIN = WC + (kRM + 4) * LT;  // + R rows [j][latent]: sources, ones at kRM, zeros
 
 template <int DP, int WP>
 struct A2 {
@@ -53,7 +57,6 @@ struct A2 {
     static constexpr int RH = WP + 4;   // H1 / H2: ones at WP
     static constexpr int RDH = WP;      // dH1 / dH2
     static constexpr int RDR = 4;       // dmu, dsr, 0, 0
-    static constexpr int RR = kRM + 4;  // R: ones at kRM
     static constexpr int RF = kFM;      // dF
     static constexpr int O_C = 0;
     static constexpr int O_H1 = O_C + RC * LT;
@@ -61,12 +64,9 @@ struct A2 {
     static constexpr int O_DH1 = O_H2 + RH * LT;
     static constexpr int O_DH2 = O_DH1 + RDH * LT;
     static constexpr int O_DR = O_DH2 + RDH * LT;
-    static constexpr int O_R = O_DR + RDR * LT;
-    static constexpr int O_DF = O_R + RR * LT;
-    static constexpr int O_RAW = O_DF + RF * LT;   // head outputs (mu, sigma-raw)
-    static constexpr int O_C2 = O_RAW + 2 * LT;    // second C / R buffers: the
-    static constexpr int O_R2 = O_C2 + RC * LT;    // next tile's gather lands here
-    static constexpr int ACT = O_R2 + RR * LT;
+    static constexpr int O_DF = O_DR + RDR * LT;
+    static constexpr int O_HP = O_DF + RF * LT;    // head partials [group][mu|sigma-raw]
+    static constexpr int ACT = O_HP + 8 * LT;
     // weight-gradient jobs (4x4 micro-tiles) and units (job x latent third)
     static constexpr int J1 = (WP / 4) * (DP / 4 + 1);   // dH1 x [C|1]
     static constexpr int J2 = (WP / 4) * (WP / 4 + 1);   // dH2 x [H1|1]
@@ -97,10 +97,11 @@ struct alignas(16) A2Smem {
     alignas(16) float Wf[kMaxSlots][kFM][kRM];
     alignas(16) float bf[kMaxSlots][kFM];
     alignas(16) float act[K::ACT];
+    alignas(16) float win[2][WIN];   // gather windows: this tile's, the next tile's
+    int woff[kMaxCtx];               // context offset o -> window position
     alignas(16) float stage5[K::NU5][16];
     double acc5[K::NACC5];  // IFCE dW (+db), per slot, fp64
     GridGeom geo[kMaxGrids];
-    int ctx_dy[kMaxCtx], ctx_dx[kMaxCtx];
     double red[NT / 32];
 };
 
@@ -136,53 +137,42 @@ __device__ __forceinline__ void cp_async4_zfill(float* smem, const float* gmem, 
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 
-// Asynchronous gather of one tile.  Threads [0,128) (latent lt): the S causal
-// context values and the latent's own value (row DP+1); threads [128,256): on
-// IFCE grids, the kRM co-located coarser-grid values (zero past rdim / past
-// the grid).  Always commits one cp.async group.
-template <int DP>
-__device__ __forceinline__ void issue_gather(const Plan& P, const GridGeom* geo, int2 tile,
-                                             const int* cdy, const int* cdx, float* sCb, float* sRb,
-                                             int half, int lt) {
+// Asynchronous gather of one row-segment tile (grid tile.x, latents
+// tile.y .. tile.y+len-1 = row r, columns c0 .. c0+len-1) into a window
+// buffer: the P+1 padded rows r-P .. r over columns c0-P .. c0+len-1+P (the
+// causal context of every latent of the tile, zero border included), and on
+// IFCE grids the R rows [j][latent] = ŷ of coarser grid j < rdim at
+// (r >> sh, c >> sh) (global rows, clamped to the band) — one warp per
+// source grid.  All 256 threads; always commits one cp.async group.
+__device__ __forceinline__ void issue_gather(const Plan& P, const GridGeom* geo, int4 tile, float* win,
+                                             int tid) {
     const GridGeom& g = geo[tile.x];
-    const int64_t count = int64_t(g.rows) * g.cols;
-    const int64_t li = int64_t(tile.y) + lt;
-    const bool valid = li < count;
-    const int r = valid ? int(li / g.cols) : 0;
-    const int c = valid ? int(li - int64_t(r) * g.cols) : 0;
-    if (half == 0) {
-        const float* base = P.yhat_pad + g.pad_base + int64_t(r) * g.stride + c;
-        const int S = P.S;
-#pragma unroll 4
-        for (int o = 0; o < S; ++o)
-            cp_async4_zfill(sCb + o * LT + lt, base + cdy[o] * g.stride + cdx[o], valid);
-        cp_async4_zfill(sCb + (DP + 1) * LT + lt, base, valid);
-    } else if (g.ifce_slot >= 0) {
-        const int rd = g.rdim;
-#pragma unroll
-        for (int j = 0; j < kRM; ++j) {
-            const bool on = valid && j < rd;
-            const float* src = P.yhat_pad;
-            if (on) {  // co-located coarser latent, in global rows (row bands)
-                const GridGeom& sg = geo[j];
-                const int sh = sg.level - g.level;
-                const int rs = min(max(((g.row0 + r) >> sh) - sg.row0, 0), sg.rows - 1);
-                src = P.yhat_pad + sg.pad_base + int64_t(rs) * sg.stride + (c >> sh);
-            }
-            cp_async4_zfill(sRb + j * LT + lt, src, on);
+    const int r = tile.z, len = tile.w, c0 = tile.y - r * g.cols;
+    const int pad = P.P;
+    const float* base = P.yhat_pad + g.pad_base + int64_t(r - pad) * g.stride + (c0 - pad);
+    const int lenw = len + 2 * pad;
+    for (int e = tid; e < (pad + 1) * WS; e += NT) {
+        const int i = e / WS, x = e - i * WS;
+        const bool full = x < lenw;
+        cp_async4_zfill(win + e, full ? base + int64_t(i) * g.stride + x : base, full);
+    }
+    if (g.ifce_slot >= 0) {
+        float* wr = win + WC;
+        const int warp = tid >> 5, lane = tid & 31;
+        for (int j = warp; j < g.rdim; j += NT / 32) {
+            const GridGeom& sg = geo[j];
+            const int sh = sg.level - g.level;
+            const int rs = min(max(((g.row0 + r) >> sh) - sg.row0, 0), sg.rows - 1);
+            const float* src = P.yhat_pad + sg.pad_base + int64_t(rs) * sg.stride;
+            for (int x = lane; x < len; x += 32) cp_async4(wr + j * LT + x, src + ((c0 + x) >> sh));
         }
     }
     cp_async_commit();
 }
 
-__device__ __forceinline__ void swap_bufs(float*& a, float*& b, float*& c, float*& d) {
-    float* x = a; a = b; b = x;
-    x = c; c = d; d = x;
-}
-
 template <int DP, int WP, int MODE>
 __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
-                                                const int2* __restrict__ tiles, int ntiles) {
+                                                const int4* __restrict__ tiles, int ntiles) {
     using K = A2<DP, WP>;
     const Plan& P = *pp;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -238,32 +228,30 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
         const int s = e / kFM, f = e % kFM;
         sm.bf[s][f] = (s < P.n_slots && f < F) ? prm[P.off_ifb[s] + f] : 0.0f;
     }
-    for (int e = tid; e < kMaxCtx; e += NT) {
-        sm.ctx_dy[e] = e < S ? P.ctx_dy[e] : 0;
-        sm.ctx_dx[e] = e < S ? P.ctx_dx[e] : 0;
-    }
+    for (int e = tid; e < kMaxCtx; e += NT)  // context offset o -> window position
+        sm.woff[e] = e < S ? (P.P + P.ctx_dy[e]) * WS + P.P + P.ctx_dx[e] : 0;
     for (int e = tid; e < K::NACC5; e += NT) sm.acc5[e] = 0.0;
     for (int e = tid; e < P.n_grids; e += NT) sm.geo[e] = P.g[e];
-    // constant rows: zero padding of every activation array (written once)
+    // constant rows: zero padding of every activation array (written once);
+    // windows zeroed so R rows past a grid's rdim are always finite
     for (int e = tid; e < K::ACT; e += NT) sm.act[e] = 0.0f;
+    for (int e = tid; e < 2 * WIN; e += NT) (&sm.win[0][0])[e] = 0.0f;
     __syncthreads();
 
-    float* sC = sm.act + K::O_C;
-    float* sR = sm.act + K::O_R;
-    float* sCn = sm.act + K::O_C2;
-    float* sRn = sm.act + K::O_R2;
+    float* const sC = sm.act + K::O_C;
     float* const sH1 = sm.act + K::O_H1;
     float* const sH2 = sm.act + K::O_H2;
     float* const sDH1 = sm.act + K::O_DH1;
     float* const sDH2 = sm.act + K::O_DH2;
     float* const sDR = sm.act + K::O_DR;
     float* const sDF = sm.act + K::O_DF;
-    float* const sRaw = sm.act + K::O_RAW;
+    float* const sHP = sm.act + K::O_HP;
     // tile records run two ahead of the tile being computed (register
     // prefetch); the gather of tile t+grid is issued while tile t computes
-    int2 cur = blockIdx.x < ntiles ? tiles[blockIdx.x] : make_int2(0, 0);
-    int2 nxt = blockIdx.x + gridDim.x < ntiles ? tiles[blockIdx.x + gridDim.x] : make_int2(0, 0);
-    if (blockIdx.x < ntiles) issue_gather<DP>(P, sm.geo, cur, sm.ctx_dy, sm.ctx_dx, sC, sR, half, lt);
+    int4 cur = blockIdx.x < ntiles ? tiles[blockIdx.x] : make_int4(0, 0, 0, 0);
+    int4 nxt = blockIdx.x + gridDim.x < ntiles ? tiles[blockIdx.x + gridDim.x] : make_int4(0, 0, 0, 0);
+    int wb = 0;  // window buffer of the current tile
+    if (blockIdx.x < ntiles) issue_gather(P, sm.geo, cur, sm.win[0], tid);
 
     // persistent weight-gradient accumulators of this thread's units
     double uacc[K::MAXU][16];  // fp64 across tiles: large images sum millions of terms
@@ -275,27 +263,33 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
     const float upstream = P.rate_upstream;
 
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int2 tile = cur;
-        const int2 nxt2 = t + 2 * int(gridDim.x) < ntiles ? tiles[t + 2 * gridDim.x] : make_int2(0, 0);
+        const int4 tile = cur;
+        const int4 nxt2 = t + 2 * int(gridDim.x) < ntiles ? tiles[t + 2 * gridDim.x] : make_int4(0, 0, 0, 0);
         const GridGeom& g = sm.geo[tile.x];
         const int64_t count = int64_t(g.rows) * g.cols;
         const int slot = g.ifce_slot;
+        const int len = tile.w;
         const int64_t li = int64_t(tile.y) + lt;
-        const bool valid = li < count;
+        const bool valid = lt < len;
         // rate terms only for owned rows (row bands; whole images own all rows)
-        const bool own = valid && li >= int64_t(g.own_lo) * g.cols && li < int64_t(g.own_hi) * g.cols;
+        const bool own = valid && tile.z >= g.own_lo && tile.z < g.own_hi;
 
         // ---- P0: prefetch the next tile (its buffers' last readers finished
         // at the previous tile's closing barrier), land the current one ----
         if (t + int(gridDim.x) < ntiles)
-            issue_gather<DP>(P, sm.geo, nxt, sm.ctx_dy, sm.ctx_dx, sCn, sRn, half, lt);
+            issue_gather(P, sm.geo, nxt, sm.win[wb ^ 1], tid);
         else
             cp_async_commit();
         asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         __syncthreads();
 
-        // ---- P1: IFCE forward (two threads per latent) + constant rows ----
+        // ---- P1: context rows from the window, IFCE forward (two threads
+        // per latent), constant rows ----
+        float* const sR = sm.win[wb] + WC;  // this tile's R rows
         {
+            const float* win = sm.win[wb];
+            for (int o = half; o < S; o += 2)  // C[o] = ŷ(r + dy_o, c + dx_o)
+                sC[o * LT + lt] = valid ? win[sm.woff[o] + lt] : 0.0f;
             constexpr int FH = kFM / 2;
             if (slot >= 0) {
                 float rv[kRM];
@@ -320,6 +314,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
                 }
             }
             if (half == 0) {
+                sC[(DP + 1) * LT + lt] = valid ? win[P.P * WS + P.P + lt] : 0.0f;  // own value
                 sC[DP * LT + lt] = valid ? 1.0f : 0.0f;
                 sH1[WP * LT + lt] = valid ? 1.0f : 0.0f;
             } else {
@@ -353,28 +348,35 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
                 acc[n] = make_float2(b, b);
             }
             tile_gemm<K::NW, WP>(sH1, sm.W2T, pr, grp, acc);
+            // the two head outputs, this group's share: W3 over its H2
+            // outputs plus the stabiliser over its quarter of the C rows
+            float2 p0 = make_float2(0.0f, 0.0f), p1 = make_float2(0.0f, 0.0f);
 #pragma unroll
             for (int n = 0; n < K::NW; ++n) {
+                const int a = grp * K::NW + n;
                 const float2 h = make_float2(acc[n].x > 0.0f ? acc[n].x : 0.0f, acc[n].y > 0.0f ? acc[n].y : 0.0f);
-                *reinterpret_cast<float2*>(sH2 + (grp * K::NW + n) * LT + 2 * pr) = h;
+                *reinterpret_cast<float2*>(sH2 + a * LT + 2 * pr) = h;
+                p0 = ffma2(h, sm.W3[0][a], p0);
+                p1 = ffma2(h, sm.W3[1][a], p1);
             }
-        }
-        __syncthreads();
-        // ---- P4a: head output `half` (mu / sigma-raw) of latent lt ----
-        {
-            float a = sm.b3[half];
 #pragma unroll
-            for (int k = 0; k < WP; ++k) a = fmaf(sH2[k * LT + lt], sm.W3[half][k], a);
-#pragma unroll
-            for (int k = 0; k < DP; ++k) a = fmaf(sC[k * LT + lt], sm.stab[half][k], a);
-            sRaw[half * LT + lt] = a;
+            for (int n = 0; n < K::ND; ++n) {
+                const int k = grp * K::ND + n;
+                const float2 c = *reinterpret_cast<const float2*>(sC + k * LT + 2 * pr);
+                p0 = ffma2(c, sm.stab[0][k], p0);
+                p1 = ffma2(c, sm.stab[1][k], p1);
+            }
+            *reinterpret_cast<float2*>(sHP + (2 * grp) * LT + 2 * pr) = p0;
+            *reinterpret_cast<float2*>(sHP + (2 * grp + 1) * LT + 2 * pr) = p1;
         }
         __syncthreads();
         // ---- P4b: Laplace rate + its backward, dH2 (threads [0,128)) ----
         if (half == 0) {
             const float v = sC[(DP + 1) * LT + lt];
-            const float mu = sRaw[lt];
-            const float sg = sigma_from_raw(sRaw[LT + lt]);
+            // raw = b3 + sum of the four group partials (fixed order)
+            const float mu = sm.b3[0] + (((sHP[lt] + sHP[2 * LT + lt]) + sHP[4 * LT + lt]) + sHP[6 * LT + lt]);
+            const float sr = sm.b3[1] + (((sHP[LT + lt] + sHP[3 * LT + lt]) + sHP[5 * LT + lt]) + sHP[7 * LT + lt]);
+            const float sg = sigma_from_raw(sr);
             const float bsc = sg * kInvSqrt2F;
             const float u = fabsf(v - mu);
             const float e1 = cc_exp(-(u + 0.5f) / bsc);
@@ -407,7 +409,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
         }
         __syncthreads();
         if (MODE == kArmForward) {
-            swap_bufs(sC, sCn, sR, sRn);
+            wb ^= 1;
             cur = nxt;
             nxt = nxt2;
             continue;
@@ -435,7 +437,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
             tile_gemm<K::ND, WP>(sDH1, sm.W1, pr, grp, acc);
             tile_gemm<K::ND, 2>(sDR, sm.ST, pr, grp, acc);
             const int64_t l0 = int64_t(tile.y) + 2 * pr;
-            const bool v0 = l0 < count, v1 = l0 + 1 < count;
+            const bool v0 = 2 * pr < len, v1 = 2 * pr + 1 < len;
 #pragma unroll
             for (int n = 0; n < K::ND; ++n) {
                 const int k = grp * K::ND + n;
@@ -508,7 +510,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
             }
             // stage5 is rewritten only after the next tile's five barriers
         }
-        swap_bufs(sC, sCn, sR, sRn);
+        wb ^= 1;
         cur = nxt;
         nxt = nxt2;
     }

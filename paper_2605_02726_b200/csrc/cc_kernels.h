@@ -15,7 +15,7 @@ struct LaunchCtx {
     int elem_blocks;       // grid for elementwise kernels over the latents
     int pix_blocks;        // grid for per-pixel kernels
     // ARM work table
-    const int2* arm_tiles; // (grid index, first latent) per 128-latent tile
+    const int4* arm_tiles; // (grid, first latent, row, length) per <=128-latent row segment
     int arm_ntiles;
     int arm_blocks;
     int syn_ntiles;        // 128-pixel tiles of the trunk-backward kernel

@@ -223,6 +223,10 @@ void Trainer::build_plan() {
         P.ctx_dx[o] = dx[o];
     }
     P.P = std::max(1, cpad);  // encoder.hpp:218
+    // the register-tiled ARM stages a (P+1)-row context window of <= 4-wide
+    // halo; every context that fits its input width (<= 32) has P <= 4
+    if (arm_uses_v2(P.Dp, P.Wp) && P.P > 4)
+        throw ConfigError("spatial context halo > 4 exceeds the register-tiled ARM window");
 
     // ---- grids in decode order (latent.hpp:66-68) ----
     struct G {
@@ -439,11 +443,14 @@ void Trainer::build_plan() {
     L_.elem_blocks = cap(P.n_latents, 256);
     L_.pix_blocks = cap(P.npix, 256);
     L_.red_blocks = num_sms_;
-    std::vector<int2> tiles;
-    for (int gi = 0; gi < P.n_grids; ++gi) {
-        const int64_t cnt = int64_t(P.g[gi].rows) * P.g[gi].cols;
-        for (int64_t s = 0; s < cnt; s += kArmTileHost) tiles.push_back(make_int2(gi, int(s)));
-    }
+    // ARM tiles: row segments of <= 128 latents (grid, first latent, row,
+    // length), so a tile's causal context is one (P+1)-row window and its
+    // IFCE sources are one segment per coarser grid
+    std::vector<int4> tiles;
+    for (int gi = 0; gi < P.n_grids; ++gi)
+        for (int r = 0; r < P.g[gi].rows; ++r)
+            for (int c0 = 0; c0 < P.g[gi].cols; c0 += kArmTileHost)
+                tiles.push_back(make_int4(gi, r * P.g[gi].cols + c0, r, std::min(kArmTileHost, P.g[gi].cols - c0)));
     L_.arm_ntiles = int(tiles.size());
     int arm_occ = arm_blocks_per_sm(P.Dp, P.Wp);
     if (const char* e = std::getenv("CCB_ARM_OCC")) arm_occ = std::max(1, std::min(arm_occ, std::atoi(e)));
@@ -549,8 +556,8 @@ void Trainer::allocate() {
     P.lat_ok = static_cast<int*>(dalloc(sizeof(int) * kMaxGrids));
     P.tensor_ok = static_cast<int*>(dalloc(sizeof(int) * kMaxTensors));
     P.scal = static_cast<DevScalars*>(dalloc(sizeof(DevScalars)));
-    d_tiles_ = static_cast<int2*>(dalloc(sizeof(int2) * tiles_host_.size()));
-    CCB_CUDA(cudaMemcpy(d_tiles_, tiles_host_.data(), sizeof(int2) * tiles_host_.size(),
+    d_tiles_ = static_cast<int4*>(dalloc(sizeof(int4) * tiles_host_.size()));
+    CCB_CUDA(cudaMemcpy(d_tiles_, tiles_host_.data(), sizeof(int4) * tiles_host_.size(),
                         cudaMemcpyHostToDevice));
     d_plan_ = static_cast<Plan*>(dalloc(sizeof(Plan)));
     CCB_CUDA(cudaMemcpy(d_plan_, &H_, sizeof(Plan), cudaMemcpyHostToDevice));

@@ -173,7 +173,7 @@ private:
     std::vector<TensorInfo> tensors_;
     std::vector<GridInfo> grids_;
     std::vector<void*> allocs_;
-    int2* d_tiles_ = nullptr;
+    int4* d_tiles_ = nullptr;
     double* d_sched_ = nullptr;     // 3 doubles per iteration (batched)
     double* d_rec_ = nullptr;       // 4 doubles per iteration (batched)
     double* h_rec_ = nullptr;       // pinned mirror, filled after every iteration
@@ -196,7 +196,7 @@ private:
         bool on = false;
         int hg = 0, r0 = 0, r1 = 0, halo = 0;
     } band_;
-    std::vector<int2> tiles_host_;
+    std::vector<int4> tiles_host_;
 };
 
 void fp32_peak(int device, double* tflops, double* ms);
