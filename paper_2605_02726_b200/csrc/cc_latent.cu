@@ -153,25 +153,35 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp, int force, int64_t i_
         const int gi = find_grid(s_off, i);
         const GridGeom& g = s_geo[gi];
         const int64_t cnt = int64_t(g.rows) * g.cols;
-        const int64_t li = i - g.lat_off;
-        const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
+        const int li = int(i - g.lat_off);  // < 2^31 latents per grid
+        const int r = li / g.cols, c = li - r * g.cols;
+        // every load of the latent is issued before the ordered sums: own
+        // rate gradient, the per-latent terms below, and the causal
+        // successors' context gradients (chunks of 8 offsets)
         float acc = P.gown[i];
-        const float* dc = P.dctx + g.dctx_off;
-        // causal successors' context gradients, fixed offset order; the loads
-        // of a chunk of 8 offsets are all in flight before the ordered sum
+        const float t2 = P.th2[i], t1 = P.th1[i];
+        float zterm = 0.0f;
+        if (g.main_level == 0)
+            zterm = P.dz[P.zpix[0] + int64_t(r) * P.W + c];
+        else if (g.main_level > 0)
+            zterm = P.dups[i];
+        const float* dc = P.dctx + g.dctx_off + li;
         for (int o0 = 0; o0 < S; o0 += 8) {
             float v[8];
-            bool in[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int o = o0 + k;
-                const int rs = r - (o < S ? s_dy[o] : 0), cs = c - (o < S ? s_dx[o] : 0);
-                in[k] = o < S && rs >= 0 && rs < g.rows && cs >= 0 && cs < g.cols;
-                v[k] = in[k] ? __ldg(dc + int64_t(o) * cnt + int64_t(rs) * g.cols + cs) : 0.0f;
+                v[k] = 0.0f;
+                if (o < S) {
+                    const int dy = s_dy[o], dx = s_dx[o];
+                    const int rs = r - dy, cs = c - dx;
+                    if (rs >= 0 && rs < g.rows && cs >= 0 && cs < g.cols)
+                        v[k] = __ldg(dc + (int64_t(o) * cnt - (dy * g.cols + dx)));
+                }
             }
 #pragma unroll
             for (int k = 0; k < 8; ++k)
-                if (in[k]) acc += v[k];
+                if (o0 + k < S) acc += v[k];  // out-of-grid terms are +0
         }
         for (int s = 0; s < P.n_slots; ++s) {
             const GridGeom& e = s_geo[P.slot_gi[s]];
@@ -188,11 +198,7 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp, int force, int64_t i_
                 dr += wf[f * e.rdim + gi] * pyr[int64_t(f) * pc + int64_t(R) * g.cols + c];
             acc += dr;
         }
-        if (g.main_level == 0)
-            acc += P.dz[P.zpix[0] + int64_t(r) * P.W + c];
-        else if (g.main_level > 0)
-            acc += P.dups[i];
-        const float t2 = P.th2[i], t1 = P.th1[i];
+        if (g.main_level >= 0) acc += zterm;
         const float d2 = fmaf(-t2, t2, 1.0f) * scale;
         const float d1 = fmaf(-t1, t1, 1.0f) * scale;
         const float dy = acc * d2 * d1;
