@@ -693,7 +693,6 @@ void Trainer::enqueue_proxy(bool batched) {
     launch_arm(side(), kArmProxy);
     mark(2, true);
     launch_pyramid(side());
-    launch_noise_ahead(side());  // next iteration's noise, off the critical path
     mark(3, true);
     launch_ups_forward(L_);
     mark(4, false);
@@ -726,11 +725,13 @@ void Trainer::enqueue_proxy(bool batched) {
     mark(8, 2);
     CCB_CUDA(cudaStreamWaitEvent(tail_stream_, ev_fin_, 0));
     launch_adam_latents_grids(side(true), fine, H_.n_grids);
+    launch_noise_ahead(side(true));  // next iteration's noise, in the tail's slack
     mark(9, 2);
     launch_ups_backward(L_, true, 1);
     mark(10, false);
+    fork();  // the upsampling-tap reduction beside the coarse-grid gather
+    launch_nn_reduce(side(), ups_lo, ups_hi);
     launch_latent_grad_grids(L_, 0, fine);
-    launch_nn_reduce(L_, ups_lo, ups_hi);
     mark(11, false);
     join();
     join(true);

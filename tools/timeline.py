@@ -10,7 +10,7 @@ from paper_2605_02726_b200 import capi  # noqa: E402
 from paper_2605_02726_b200.trainer import DecoderConfig, EncoderConfig, Trainer, make_synthetic_image  # noqa: E402
 
 NAMES = ["start", "softq", "ARM (side)", "pyramid+noise (side)", "ups fwd", "syn fwd", "syn bwd",
-         "ups bwd stage 0", "fine grad (tail)", "fine adam (tail)", "ups bwd rest", "coarse grad + nn_reduce",
+         "ups bwd stage 0", "fine grad (tail)", "fine adam (tail)", "ups bwd rest", "coarse grad",
          "end"]
 lib = capi.load_product()
 h, w = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (512, 768)
