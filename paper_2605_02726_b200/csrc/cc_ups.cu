@@ -29,39 +29,14 @@ namespace ccb {
 
 namespace {
 
-constexpr int kFT = 32;   // forward output tile (level j), square
-constexpr int kThreads = 256;     // big stages
-constexpr int kThreadsWide = 512; // stages with few tiles: shorter per-CTA phase chains
+constexpr int kThreads = 256;
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-// Polyphase tap table (layers.hpp:346-351): output t reads idx[q] with tap[q].
-__device__ __forceinline__ void tconv_map(int t, int last, int (&idx)[4], int (&tap)[4]) {
-    const int u = t >> 1;
-    if ((t & 1) == 0) {
-        idx[0] = u >= 2 ? u - 2 : 0;
-        idx[1] = u >= 1 ? u - 1 : 0;
-        idx[2] = u;
-        idx[3] = u < last ? u + 1 : last;
-        tap[0] = 0; tap[1] = 2; tap[2] = 3; tap[3] = 1;
-    } else {
-        idx[0] = u >= 1 ? u - 1 : 0;
-        idx[1] = u;
-        idx[2] = u < last ? u + 1 : last;
-        idx[3] = u + 2 < last ? u + 2 : last;
-        tap[0] = 1; tap[1] = 3; tap[2] = 2; tap[3] = 0;
-    }
-}
-
-// A clamped index window [lo, hi] of one axis, stored densely in smem.
-struct Win {
-    int lo, hi;
-    __device__ __forceinline__ int n() const { return hi - lo + 1; }
-};
-// window of the tconv inputs read by outputs in [a, b] (clamped to [0, last])
-__device__ __forceinline__ Win tconv_src(Win out, int last) {
-    return Win{clampi((out.lo >> 1) - 2, 0, last), clampi((out.hi >> 1) + 2, 0, last)};
-}
+// Polyphase taps (layers.hpp:346-351): with u = t >> 1, an even output t
+// reads inputs (u-2, u-1, u, u+1) with taps (k0, k2, k3, k1), an odd output
+// reads (u-1, u, u+1, u+2) with taps (k1, k3, k2, k0); indices clamp to the
+// input (replicate).  Every phase below hard-codes this table on a window.
 
 __device__ __forceinline__ const float* stage_in(const Plan& P, const UpsStage& s) {
     return s.in_is_pad ? P.yhat_pad + s.in_off : P.ups_buf + s.in_off;
@@ -77,127 +52,133 @@ __device__ __forceinline__ float* stage_din(const Plan& P, const UpsStage& s) {
 }
 
 // ---------------------------------------------------------------- forward
-// One CTA = one kFT x kFT output tile of stage j for grid blockIdx.y.
-constexpr int kFC = kFT + 2;              // coltmp window (tile + refine halo)
-constexpr int kFR = kFC / 2 + 6;          // rowtmp rows / input rows
+// A CTA owns output tile [a,a+2TB) x [b,b+2TB) of stage j (a = 2U0, b = 2V0),
+// computed from the input window [U0-3,U0+TB+3) x [V0-3,V0+TB+3): rowtmp
+// and coltmp in polyphase pairs, the refinement in 4-row register strips.
+// Border tiles clamp-load the input (replicate padding of the tconv,
+// layers.hpp:353-429) and re-clamp coltmp one position outside the cropped
+// level (replicate padding of conv3x3_sym_forward, layers.hpp:467-483).
+template <int TB>
+struct FwdGeo {
+    static constexpr int FO = 2 * TB;  // owned outputs per side
+    static constexpr int XW = TB + 6;  // input window, origin U0-3 / V0-3
+    static constexpr int RC = FO + 4;  // rowtmp cols, origin b-2 (rows: XW)
+    static constexpr int CR = FO + 4;  // coltmp rows, origin a-2
+    static constexpr int CC = FO + 2;  // coltmp cols, origin b-1
+};
+template <int TB>
 struct FwdSmem {
-    float s_in[kFR * kFR];
-    float s_row[kFR * kFC];
-    float s_col[kFC * kFC];
+    using G = FwdGeo<TB>;
+    float x[G::XW * G::XW];
+    float r[G::XW * G::RC];
+    float c[G::CR * G::CC];
 };
 
-// Tiles t_begin, t_begin + t_step, ... of stage j for grid entry si.
-__device__ __forceinline__ void ups_fwd_stage(const Plan& P, int j, int si, int t_begin, int t_step,
-                                              FwdSmem& fs) {
-    const UpsStage& s = P.ups[j][si];
+template <int TB>
+__device__ __forceinline__ bool fwd_interior(int U0, int V0, int ri, int ci, int ro, int co) {
+    return U0 >= 3 && V0 >= 3 && U0 + TB + 2 <= ri - 1 && V0 + TB + 2 <= ci - 1 &&
+           2 * U0 + 2 * TB + 1 <= ro - 1 && 2 * V0 + 2 * TB + 1 <= co - 1;
+}
+
+template <int TB, bool BORDER>
+__device__ __forceinline__ void fwd_tile(const float* __restrict__ in, int in_stride, float* __restrict__ out,
+                                         int ro, int co, int ri, int ci, int U0, int V0, const float (&kk)[4],
+                                         float kc, float ke, float ko, FwdSmem<TB>& f) {
+    using G = FwdGeo<TB>;
+    constexpr int FO = G::FO, XW = G::XW, RC = G::RC, CR = G::CR, CC = G::CC;
+    const int a = 2 * U0, b = 2 * V0;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    __syncthreads();  // the previous tile's readers are done with the windows
+    for (int e = tid; e < XW * XW; e += nt) {
+        const int i = e / XW, j = e - i * XW;
+        int u = U0 - 3 + i, v = V0 - 3 + j;
+        if (BORDER) {
+            u = clampi(u, 0, ri - 1);
+            v = clampi(v, 0, ci - 1);
+        }
+        cp_async4(&f.x[e], in + int64_t(u) * in_stride + v);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // rowtmp (tconv2x_rows_forward, layers.hpp:353-376): column pairs
+    for (int e = tid; e < XW * (TB + 2); e += nt) {
+        const int i = e / (TB + 2), m = e - i * (TB + 2);  // t' = b - 2 + 2m, +1
+        const float* x = &f.x[i * XW + m];
+        float* r = &f.r[i * RC + 2 * m];
+        r[0] = kk[0] * x[0] + kk[2] * x[1] + kk[3] * x[2] + kk[1] * x[3];
+        r[1] = kk[1] * x[1] + kk[3] * x[2] + kk[2] * x[3] + kk[0] * x[4];
+    }
+    __syncthreads();
+    // coltmp (tconv2x_cols_forward, layers.hpp:407-429): row pairs
+    for (int e = tid; e < (TB + 2) * CC; e += nt) {
+        const int p = e / CC, j = e - p * CC;  // t = a - 2 + 2p, +1
+        const float* r = &f.r[p * RC + j + 1];
+        const float r0 = r[0], r1 = r[RC], r2 = r[2 * RC], r3 = r[3 * RC], r4 = r[4 * RC];
+        f.c[(2 * p) * CC + j] = kk[0] * r0 + kk[2] * r1 + kk[3] * r2 + kk[1] * r3;
+        f.c[(2 * p + 1) * CC + j] = kk[1] * r1 + kk[3] * r2 + kk[2] * r3 + kk[0] * r4;
+    }
+    __syncthreads();
+    if (BORDER) {  // replicate padding of the cropped level: rows -1 / ro, then columns
+        if (tid < CC) {
+            const int im = 1 - a, ip = ro - (a - 2);
+            if (im >= 0) f.c[im * CC + tid] = f.c[(im + 1) * CC + tid];
+            if (ip < CR) f.c[ip * CC + tid] = f.c[(ip - 1) * CC + tid];
+        }
+        __syncthreads();
+        if (tid < CR) {
+            float* c = &f.c[tid * CC];
+            const int jm = -b, jp = co - (b - 1);
+            if (jm >= 0) c[jm] = c[jm + 1];
+            if (jp < CC) c[jp] = c[jp - 1];
+        }
+        __syncthreads();
+    }
+    // conv3x3_sym_forward (layers.hpp:467-483) in 4-row strips
+    for (int e = tid; e < (FO / 4) * FO; e += nt) {
+        const int sb = e / FO, j = e - sb * FO;
+        const int t0 = a + 4 * sb, tc = b + j;
+        if (BORDER && (t0 >= ro || tc >= co)) continue;
+        float cl[6], cm[6], cr[6];
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const float* c = &f.c[(4 * sb + 1 + q) * CC + j];
+            cl[q] = c[0];
+            cm[q] = c[1];
+            cr[q] = c[2];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (BORDER && t0 + q >= ro) break;
+            out[int64_t(t0 + q) * co + tc] = kc * cm[q + 1] + ke * (cm[q] + cm[q + 2] + cl[q + 1] + cr[q + 1]) +
+                                             ko * (cl[q] + cr[q] + cl[q + 2] + cr[q + 2]);
+        }
+    }
+}
+
+template <int TB>
+__global__ void __launch_bounds__(kThreads) k_ups_fwd(const Plan* __restrict__ pp, int j) {
+    __shared__ FwdSmem<TB> f;
+    const Plan& P = *pp;
+    const UpsStage& s = P.ups[j][blockIdx.y];
     const int ro = s.rows_out, co = s.cols_out, ri = s.rows_in, ci = s.cols_in;
-    const int tiles_x = (co + kFT - 1) / kFT;
-    const int ntiles = tiles_x * ((ro + kFT - 1) / kFT);
-    float* s_in = fs.s_in;
-    float* s_row = fs.s_row;
-    float* s_col = fs.s_col;
+    constexpr int FO = 2 * TB;
+    const int tiles_x = (co + FO - 1) / FO;
+    const int ntiles = tiles_x * ((ro + FO - 1) / FO);
     const float* k4 = P.params + P.off_tconv[j];
     const float* r3 = P.params + P.off_refine[j];
-    const float t0 = k4[0], t1 = k4[1], t2 = k4[2], t3 = k4[3];
+    const float kk[4] = {k4[0], k4[1], k4[2], k4[3]};
     const float kc = r3[0], ke = r3[1], ko = r3[2];
     const float* in = stage_in(P, s);
     float* out = stage_out(P, s);
     pdl_wait();  // the stage input is the previous stage's output
     pdl_trigger();
-    for (int tile = t_begin; tile < ntiles; tile += t_step) {
-        const int y0 = (tile / tiles_x) * kFT, x0 = (tile % tiles_x) * kFT;
-        if (y0 >= kFT && x0 >= kFT && y0 / 2 + 18 <= ri - 1 && x0 / 2 + 18 <= ci - 1 && y0 + kFT <= ro - 1 &&
-            x0 + kFT <= co - 1) {
-            // interior tile: fixed taps and geometry, 2D thread mapping
-            constexpr int XW = 22, RW = kFT + 2, CW = kFT + 2;
-            const int U = y0 / 2, V = x0 / 2;
-            const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
-            const float kk[4] = {t0, t1, t2, t3};
-            __syncthreads();
-            for (int i = ty; i < XW; i += ny)
-                for (int j = tx; j < XW; j += 32)
-                    cp_async4(&s_in[i * XW + j], in + int64_t(U - 3 + i) * s.in_stride + (V - 3 + j));
-            cp_async_wait_all();
-            __syncthreads();
-            for (int i = ty; i < XW; i += ny)
-                for (int j = tx; j < RW; j += 32) {
-                    const float* x = &s_in[i * XW + ((j - 1) >> 1) + 3];
-                    s_row[i * RW + j] = ((j - 1) & 1) == 0
-                                            ? kk[0] * x[-2] + kk[2] * x[-1] + kk[3] * x[0] + kk[1] * x[1]
-                                            : kk[1] * x[-1] + kk[3] * x[0] + kk[2] * x[1] + kk[0] * x[2];
-                }
-            __syncthreads();
-            for (int i = ty; i < CW; i += ny)
-                for (int j = tx; j < CW; j += 32) {
-                    const float* rr = &s_row[(((i - 1) >> 1) + 3) * RW + j];
-                    s_col[i * CW + j] = ((i - 1) & 1) == 0
-                                            ? kk[0] * rr[-2 * RW] + kk[2] * rr[-RW] + kk[3] * rr[0] + kk[1] * rr[RW]
-                                            : kk[1] * rr[-RW] + kk[3] * rr[0] + kk[2] * rr[RW] + kk[0] * rr[2 * RW];
-                }
-            __syncthreads();
-            for (int i = ty; i < kFT; i += ny) {
-                const float* x0r = &s_col[i * CW + 1];
-                const float* x1r = x0r + CW;
-                const float* x2r = x1r + CW;
-                const int j = tx;
-                out[int64_t(y0 + i) * co + x0 + j] = kc * x1r[j] + ke * (x0r[j] + x2r[j] + x1r[j - 1] + x1r[j + 1]) +
-                                                     ko * (x0r[j - 1] + x0r[j + 1] + x2r[j - 1] + x2r[j + 1]);
-            }
-            continue;
-        }
-        const Win cr{clampi(y0 - 1, 0, ro - 1), clampi(y0 + kFT, 0, ro - 1)};   // coltmp rows
-        const Win cc{clampi(x0 - 1, 0, co - 1), clampi(x0 + kFT, 0, co - 1)};   // coltmp cols
-        const Win rr = tconv_src(cr, ri - 1);                                  // rowtmp/input rows
-        const Win ic = tconv_src(cc, ci - 1);                                  // input cols
-        __syncthreads();
-        for (int e = threadIdx.x; e < rr.n() * ic.n(); e += blockDim.x) {
-            const int a = FDiv(ic.n()).div(e), b = e - a * ic.n();
-            cp_async4(&s_in[a * kFR + b], in + int64_t(rr.lo + a) * s.in_stride + (ic.lo + b));
-        }
-        cp_async_wait_all();
-        __syncthreads();
-        // tconv2x_rows_forward (layers.hpp:353-376)
-        for (int e = threadIdx.x; e < rr.n() * cc.n(); e += blockDim.x) {
-            const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
-            const int t = cc.lo + b;
-            int idx[4], tap[4];
-            tconv_map(t, ci - 1, idx, tap);
-            const float* x = s_in + a * kFR - ic.lo;
-            const float kk[4] = {t0, t1, t2, t3};
-            s_row[a * kFC + b] = kk[tap[0]] * x[idx[0]] + kk[tap[1]] * x[idx[1]] +
-                                 kk[tap[2]] * x[idx[2]] + kk[tap[3]] * x[idx[3]];
-        }
-        __syncthreads();
-        // tconv2x_cols_forward (layers.hpp:407-429)
-        for (int e = threadIdx.x; e < cr.n() * cc.n(); e += blockDim.x) {
-            const int a = FDiv(cc.n()).div(e), b = e - a * cc.n();
-            const int t = cr.lo + a;
-            int idx[4], tap[4];
-            tconv_map(t, ri - 1, idx, tap);
-            const float kk[4] = {t0, t1, t2, t3};
-            const float* xr = s_row + b - rr.lo * kFC;
-            s_col[a * kFC + b] = kk[tap[0]] * xr[idx[0] * kFC] + kk[tap[1]] * xr[idx[1] * kFC] +
-                                 kk[tap[2]] * xr[idx[2] * kFC] + kk[tap[3]] * xr[idx[3] * kFC];
-        }
-        __syncthreads();
-        // conv3x3_sym_forward (layers.hpp:467-483)
-        for (int e = threadIdx.x; e < kFT * kFT; e += blockDim.x) {
-            const int r = y0 + e / kFT, c = x0 + (e % kFT);
-            if (r >= ro || c >= co) continue;
-            const int rm = (r > 0 ? r - 1 : 0) - cr.lo, r0 = r - cr.lo, rp = (r < ro - 1 ? r + 1 : ro - 1) - cr.lo;
-            const int cm = (c > 0 ? c - 1 : 0) - cc.lo, c0 = c - cc.lo, cp = (c < co - 1 ? c + 1 : co - 1) - cc.lo;
-            const float* x0r = s_col + rm * kFC;
-            const float* x1r = s_col + r0 * kFC;
-            const float* x2r = s_col + rp * kFC;
-            out[int64_t(r) * co + c] = kc * x1r[c0] + ke * (x0r[c0] + x2r[c0] + x1r[cm] + x1r[cp]) +
-                                       ko * (x0r[cm] + x0r[cp] + x2r[cm] + x2r[cp]);
-        }
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int U0 = (tile / tiles_x) * TB, V0 = (tile % tiles_x) * TB;
+        if (fwd_interior<TB>(U0, V0, ri, ci, ro, co))
+            fwd_tile<TB, false>(in, s.in_stride, out, ro, co, ri, ci, U0, V0, kk, kc, ke, ko, f);
+        else
+            fwd_tile<TB, true>(in, s.in_stride, out, ro, co, ri, ci, U0, V0, kk, kc, ke, ko, f);
     }
-}
-
-__global__ void __launch_bounds__(kThreadsWide) k_ups_fwd(const Plan* __restrict__ pp, int j) {
-    __shared__ FwdSmem fs;
-    ups_fwd_stage(*pp, j, blockIdx.y, blockIdx.x, gridDim.x, fs);
 }
 
 // --------------------------------------------------------------- backward
@@ -498,6 +479,9 @@ __device__ __forceinline__ void bwd_tile(const float* __restrict__ in, int in_st
 __host__ __device__ inline int bwd_tiles(const UpsStage& s, int tb) {
     return ((s.rows_in + tb - 1) / tb) * ((s.cols_in + tb - 1) / tb);
 }
+__host__ __device__ inline int fwd_tiles(const UpsStage& s, int tb) {
+    return ((s.rows_out + 2 * tb - 1) / (2 * tb)) * ((s.cols_out + 2 * tb - 1) / (2 * tb));
+}
 
 template <int TB>
 __device__ __forceinline__ void ups_bwd_stage(const Plan& P, int j, int si, int t_begin, int t_step,
@@ -555,13 +539,23 @@ int ups_bwd_tile(const Plan& H, int j, int num_sms) {
     return 4;
 }
 
+// Forward tile edge (input units; outputs 2x) per stage, by the same rule.
+int ups_fwd_tile(const Plan& H, int j, int num_sms) {
+    for (int tb : {16, 8}) {
+        int t = 0;
+        for (int i = 0; i < H.ups_n[j]; ++i) t += fwd_tiles(H.ups[j][i], tb);
+        if (t >= 2 * num_sms) return tb;
+    }
+    return 4;
+}
+
 int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward) {
     // enough CTAs to cover the largest grid of the stage, capped
-    const int tb = forward ? kFT : ups_bwd_tile(H, j, num_sms);
+    const int tb = forward ? ups_fwd_tile(H, j, num_sms) : ups_bwd_tile(H, j, num_sms);
     int best = 1;
     for (int i = 0; i < H.ups_n[j]; ++i) {
         const UpsStage& s = H.ups[j][i];
-        const int t = forward ? ((s.rows_out + kFT - 1) / kFT) * ((s.cols_out + kFT - 1) / kFT) : bwd_tiles(s, tb);
+        const int t = forward ? fwd_tiles(s, tb) : bwd_tiles(s, tb);
         best = t > best ? t : best;
     }
     // forward: up to ~2 waves; backward: persistent CTAs (~3 per SM over all
@@ -587,8 +581,11 @@ void launch_ups_forward(const LaunchCtx& L) {
     for (int j = H.L - 2; j >= 0; --j) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, true), H.ups_n[j]);
-        const int nt = int(grid.x * grid.y) < 2 * L.num_sms ? kThreadsWide : kThreads;
-        launch_pdl(k_ups_fwd, grid, dim3(nt), 0, L.stream, 'f', L.plan, j);
+        switch (ups_fwd_tile(H, j, L.num_sms)) {
+            case 16: launch_pdl(k_ups_fwd<16>, grid, kThreads, 0, L.stream, 'f', L.plan, j); break;
+            case 8: launch_pdl(k_ups_fwd<8>, grid, kThreads, 0, L.stream, 'f', L.plan, j); break;
+            default: launch_pdl(k_ups_fwd<4>, grid, kThreads, 0, L.stream, 'f', L.plan, j); break;
+        }
     }
 }
 
