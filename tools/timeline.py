@@ -9,7 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2605_02726_b200 import capi  # noqa: E402
 from paper_2605_02726_b200.trainer import DecoderConfig, EncoderConfig, Trainer, make_synthetic_image  # noqa: E402
 
-NAMES = ["start", "softq", "ARM (side)", "pyramid+noise (side)", "ups fwd", "syn fwd", "syn bwd",
+NAMES = ["start", "softq", "ARM (side)", "pyramid (side)", "ups fwd", "syn fwd", "syn bwd",
          "ups bwd stage 0", "fine grad (tail)", "fine adam (tail)", "ups bwd rest", "coarse grad",
          "end"]
 lib = capi.load_product()
