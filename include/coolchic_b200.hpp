@@ -173,6 +173,17 @@ public:
         check(cc_trainer_decode_terms(t_, p.data(), which, rate_bits, mse));
     }
 
+    // encode_latents' (mu, sigma) of every quantised latent (decode order),
+    // with m's parameters substituted
+    void latent_mu_sigma(DecoderModel& m, std::vector<float>& mu, std::vector<float>& sigma) {
+        std::vector<float> p;
+        p.reserve(size_t(layout_.n_params));
+        for_each_param(m, [&](ParamTensor& t) { p.insert(p.end(), t.v.begin(), t.v.end()); });
+        mu.resize(size_t(layout_.n_latents));
+        sigma.resize(size_t(layout_.n_latents));
+        check(cc_trainer_latent_mu_sigma(t_, p.data(), mu.data(), sigma.data()));
+    }
+
     cc_trainer* handle() { return t_; }
 
 private:
@@ -274,9 +285,29 @@ inline NnCodingResult select_nn_coding(Trainer& tr, const LatentSet& lat, Decode
     return res;
 }
 
-// encode_image (bitstream.hpp:187-228): training and the NN-coding search on
-// the GPU; the latent entropy coding and the bitstream assembly are the
-// reference's (not on the iteration path).
+// encode_latents (bitstream.hpp:145-155) with the per-latent Laplace
+// parameters computed on the device for all latents at once (the trainer's q,
+// set with Trainer::set_q, and m's parameters); the CDF quantisation
+// (quantize_cdf, range_coder.hpp:119-161) and the range coder stay the
+// reference's, in walk_symbols' order, so the payload is byte-identical.
+inline std::vector<uint8_t> encode_latents(Trainer& tr, LatentSet& set, DecoderModel& m) {
+    std::vector<float> mu, sigma;
+    tr.latent_mu_sigma(m, mu, sigma);
+    RangeEncoder enc;
+    std::vector<uint32_t> cum;
+    size_t i = 0;
+    for (auto& g : set.grids)
+        for (size_t k = 0; k < g.q.size(); ++k, ++i) {
+            quantize_cdf(mu[i], sigma[i], g.amp, cum);
+            const int sym = int(g.q[k]) + g.amp;
+            enc.encode(cum[size_t(sym)], cum[size_t(sym) + 1] - cum[size_t(sym)]);
+        }
+    return enc.finish();
+}
+
+// encode_image (bitstream.hpp:187-228): training, the NN-coding search and the
+// latents' (mu, sigma) on the GPU; the CDF quantisation, the range coder and
+// the bitstream assembly are the reference's.
 inline EncodeResult encode_image(const Image& img, const EncoderConfig& enc,
                                  const DecoderConfig& dcfg, int device = 0) {
     const auto t0 = std::chrono::steady_clock::now();
@@ -293,7 +324,7 @@ inline EncodeResult encode_image(const Image& img, const EncoderConfig& enc,
     }
     gt.set_q(tr.latents);
     NnCodingResult nn = select_nn_coding(gt, tr.latents, tr.model, enc.lambda);
-    const std::vector<uint8_t> latent_payload = encode_latents(tr.latents, tr.model, ctx);
+    const std::vector<uint8_t> latent_payload = encode_latents(gt, tr.latents, tr.model);
     BitstreamHeader h;
     h.height = uint16_t(img.h);
     h.width = uint16_t(img.w);

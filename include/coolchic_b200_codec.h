@@ -27,6 +27,14 @@ int cc_trainer_set_q(cc_trainer* tr, const int32_t* q);
 int cc_trainer_decode_terms(cc_trainer* tr, const float* params, int which, double* rate_bits,
                             double* mse);
 
+/* The Laplace parameters of every quantised latent as encode_latents computes
+ * them (bitstream.hpp:106-141: causal context of q, IFCE features,
+ * arm_forward_single, entropy_model.hpp:107-134), flat layout, with params
+ * (for_each_param order; NULL = the trainer's own) substituted.  Bit-identical
+ * to the reference's scalar evaluation, so the reference decoder rebuilds the
+ * same CDFs.  mu / sigma: n_latents floats each. */
+int cc_trainer_latent_mu_sigma(cc_trainer* tr, const float* params, float* mu, float* sigma);
+
 #ifdef __cplusplus
 }
 #endif

@@ -670,4 +670,51 @@ int cc_trainer_decode_terms(cc_trainer* t, const float* params, int which, doubl
     });
 }
 
+// walk_symbols' (mu, sigma) sequence (bitstream.hpp:106-141), in decode order
+int cc_trainer_latent_mu_sigma(cc_trainer* t, const float* params, float* mu, float* sigma) {
+    return guarded([&] {
+        auto& c = t->cur();
+        DecoderModel m = c.model;
+        if (params) {
+            size_t o = 0;
+            for_each_param(m, [&](ParamTensor& p) {
+                std::copy(params + o, params + o + p.size(), p.v.begin());
+                o += p.size();
+            });
+        }
+        const ContextOffsets ctx = make_context_offsets(t->dec.spatial_ctx);
+        const auto arm = make_arm_view(m, false);
+        const auto ifces = make_ifce_views(m, false);
+        std::vector<float> cbuf(size_t(arm.d), 0.0f);
+        size_t i = 0;
+        for (size_t gi = 0; gi < c.lat.grids.size(); ++gi) {
+            auto& g = c.lat.grids[gi];
+            const int slot = g.hyper ? -1 : m.ifce_slot(g.level);
+            const int rdim = slot >= 0 ? ifces[size_t(slot)].rdim : 0;
+            for (int j = int(ctx.off.size()); j < arm.d; ++j) cbuf[size_t(j)] = 0.0f;
+            for (int r = 0; r < g.rows; ++r)
+                for (int cc = 0; cc < g.cols; ++cc, ++i) {
+                    extract_spatial_context(g.q.data(), g.rows, g.cols, r, cc, ctx, cbuf.data());
+                    if (slot >= 0) {
+                        float rvec[kMaxFanOut];
+                        for (int j = 0; j < rdim; ++j) {
+                            const auto& s = c.lat.grids[size_t(j)];
+                            const int sh = s.level - g.level;
+                            rvec[j] = float(s.q[size_t(r >> sh) * s.cols + (cc >> sh)]);
+                        }
+                        const auto& fv = ifces[size_t(slot)];
+                        for (int j = 0; j < fv.fdim; ++j) {
+                            float acc = fv.b[j];
+                            const float* wr = fv.w + size_t(j) * rdim;
+                            for (int k = 0; k < rdim; ++k) acc += wr[k] * rvec[k];
+                            cbuf[ctx.off.size() + size_t(j)] = acc;
+                        }
+                    }
+                    arm_forward_single(arm, cbuf.data(), mu[i], sigma[i]);
+                }
+        }
+        return CC_OK;
+    });
+}
+
 }  // extern "C"

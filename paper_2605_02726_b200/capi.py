@@ -178,6 +178,7 @@ BAND_SIGNATURES = {
 CODEC_SIGNATURES = {
     "cc_trainer_set_q": (C.c_int, [_P, C.POINTER(C.c_int32)]),
     "cc_trainer_decode_terms": (C.c_int, [_P, _F, C.c_int, _D, _D]),
+    "cc_trainer_latent_mu_sigma": (C.c_int, [_P, _F, _F, _F]),
 }
 
 DIAG_SIGNATURES = {

@@ -807,4 +807,11 @@ int cc_trainer_decode_terms(cc_trainer* t, const float* params, int which, doubl
     });
 }
 
+int cc_trainer_latent_mu_sigma(cc_trainer* t, const float* params, float* mu, float* sigma) {
+    return guarded([&] {
+        t->tr->latent_mu_sigma(params, mu, sigma);
+        return CC_OK;
+    });
+}
+
 }  // extern "C"

@@ -79,6 +79,9 @@ int ups_coarse_from(const Plan& H);
 int ups_bwd_tile(const Plan& H, int j, int num_sms);  // backward tile edge of stage j
 void ups_configure();
 
+// latent entropy-coding parameters (cc_cdf.cu)
+void launch_latent_mu_sigma(const LaunchCtx& L, float* mu, float* sigma);
+
 // synthesis (cc_syn.cu, cc_syn_trunk.cu)
 void launch_syn_forward(const LaunchCtx& L, bool backward);
 void launch_syn_backward(const LaunchCtx& L);

@@ -1355,6 +1355,28 @@ void Trainer::decode_terms(const float* params, int which, double* bits, double*
     if (mse && (which & 2)) *mse = h_scal_->mse;
 }
 
+// encode_latents' per-latent (mu, sigma) (bitstream.hpp:106-141) on the device
+void Trainer::latent_mu_sigma(const float* params, float* mu, float* sigma) {
+    require_loaded();
+    if (band_.on) throw ConfigError("latent entropy coding needs the whole image (not a row band)");
+    const size_t np = size_t(H_.n_params), nl = size_t(H_.n_latents);
+    if (params) {
+        if (!d_param_save_) d_param_save_ = static_cast<float*>(dalloc(sizeof(float) * np));
+        CCB_CUDA(cudaMemcpyAsync(d_param_save_, H_.params, sizeof(float) * np, cudaMemcpyDeviceToDevice,
+                                 stream_));
+        CCB_CUDA(cudaMemcpyAsync(H_.params, params, sizeof(float) * np, cudaMemcpyHostToDevice, stream_));
+    }
+    if (!d_mu_sigma_) d_mu_sigma_ = static_cast<float*>(dalloc(sizeof(float) * 2 * nl));
+    launch_latent_mu_sigma(L_, d_mu_sigma_, d_mu_sigma_ + nl);
+    if (params)
+        CCB_CUDA(cudaMemcpyAsync(H_.params, d_param_save_, sizeof(float) * np, cudaMemcpyDeviceToDevice,
+                                 stream_));
+    if (mu) CCB_CUDA(cudaMemcpyAsync(mu, d_mu_sigma_, sizeof(float) * nl, cudaMemcpyDeviceToHost, stream_));
+    if (sigma)
+        CCB_CUDA(cudaMemcpyAsync(sigma, d_mu_sigma_ + nl, sizeof(float) * nl, cudaMemcpyDeviceToHost, stream_));
+    synchronize();
+}
+
 void Trainer::soap_state(double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena) {
     require_loaded();
     if (!H_.use_soap) throw ConfigError("not a SOAP trainer (use_soap = false)");

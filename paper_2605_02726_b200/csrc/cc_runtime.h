@@ -123,6 +123,8 @@ public:
     void soap_state(double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena);
     void set_q(const int32_t* q);
     void decode_terms(const float* params, int which, double* bits, double* mse);
+    // (mu, sigma) of every quantised latent, params substituted (NULL: own)
+    void latent_mu_sigma(const float* params, float* mu, float* sigma);
     void get_q(int32_t* q);
     void get_params(float* p);
 
@@ -179,6 +181,7 @@ private:
     double* h_rec_ = nullptr;       // pinned mirror, filled after every iteration
     double* h_sched_ = nullptr;     // pinned schedule staging
     float* d_param_save_ = nullptr; // decode_terms: the trainer's own parameters
+    float* d_mu_sigma_ = nullptr;   // latent_mu_sigma output (mu | sigma)
     cudaEvent_t* tl_ev_ = nullptr;  // timeline marks while capturing ccb_timeline
     int sched_cap_ = 0;
     DevScalars* h_scal_ = nullptr;  // pinned mirror

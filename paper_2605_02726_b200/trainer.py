@@ -485,6 +485,16 @@ class Trainer:
                                                           C.byref(b), C.byref(m)))
         return (b.value if which & 1 else None), (m.value if which & 2 else None)
 
+    def latent_mu_sigma(self, params: np.ndarray | None = None):
+        """(mu, sigma) of every quantised latent as the entropy coder computes
+        them (bitstream.hpp:106-141), flat layout, `params` substituted."""
+        mu = np.empty(self.n_latents, np.float32)
+        sg = np.empty(self.n_latents, np.float32)
+        pa = None if params is None else np.ascontiguousarray(params, dtype=np.float32)
+        _check(self.lib, self.lib.cc_trainer_latent_mu_sigma(self._h, None if pa is None else _fp(pa),
+                                                             _fp(mu), _fp(sg)))
+        return mu, sg
+
     def get_grads(self):
         lg = np.empty(self.n_latents, np.float32)
         pg = np.empty(self.n_params, np.float32)

@@ -43,12 +43,28 @@ int main(int argc, char** argv) {
             same &= r.spec.parts[s][p].delta_idx == g.spec.parts[s][p].delta_idx &&
                     r.spec.parts[s][p].kappa == g.spec.parts[s][p].kappa;
     const int same_payload = r.payload == g.payload;
+    // latent entropy coding with the device's (mu, sigma): byte-identical
+    // payload, and the reference decoder recovers every q from it
+    const std::vector<uint8_t> lat_ref = encode_latents(tr.latents, m_ref, ctx);
+    const std::vector<uint8_t> lat_gpu = gpu::encode_latents(gt, tr.latents, m_gpu);
+    LatentSet back = tr.latents;
+    for (auto& gq : back.grids) std::fill(gq.q.begin(), gq.q.end(), 0);
+    decode_latents(back, m_ref, ctx, lat_gpu.data(), lat_gpu.size());
+    int decodes = 1;
+    for (size_t k = 0; k < back.grids.size(); ++k) decodes &= back.grids[k].q == tr.latents.grids[k].q;
+    const int same_latent_payload = lat_ref == lat_gpu;
     const EncodeResult e = gpu::encode_image(img, enc, dcfg);
+    const int encode_decodes = [&] {
+        const DecodeResult d = decode_image(e.bytes);
+        return int(d.img.h == img.h && d.img.w == img.w && psnr_rgb(img, d.img) == e.stats.psnr);
+    }();
     std::printf(
         "{\"same_spec\": %d, \"same_payload\": %d, \"ref_cost\": %.12g, \"gpu_cost\": %.12g, "
         "\"ref_rate\": %.12g, \"gpu_rate\": %.12g, \"ref_mse\": %.12g, \"gpu_mse\": %.12g, "
-        "\"encode_bytes\": %zu, \"encode_psnr\": %.6g, \"encode_bpp\": %.6g}\n",
+        "\"encode_bytes\": %zu, \"encode_psnr\": %.6g, \"encode_bpp\": %.6g, "
+        "\"same_latent_payload\": %d, \"latent_decodes\": %d, \"latent_bytes\": %zu, "
+        "\"encode_decodes\": %d}\n",
         same, same_payload, r.cost, g.cost, r.rate_bits, g.rate_bits, r.mse, g.mse, e.bytes.size(),
-        e.stats.psnr, e.stats.bpp);
+        e.stats.psnr, e.stats.bpp, same_latent_payload, decodes, lat_gpu.size(), encode_decodes);
     return 0;
 }

@@ -40,3 +40,7 @@ def test_cpp_nn_coding_search_on_gpu_matches_reference(gpu_lib):
     assert abs(r["gpu_mse"] - r["ref_mse"]) <= 1e-5 * r["ref_mse"]
     assert r["same_spec"] == 1 and r["same_payload"] == 1
     assert r["encode_bytes"] > 0 and r["encode_psnr"] > 15
+    # latent entropy coding from the device's (mu, sigma) (§8f row 4): the
+    # reference's bytes, and the reference decoder reads the image back
+    assert r["same_latent_payload"] == 1 and r["latent_decodes"] == 1 and r["latent_bytes"] > 0
+    assert r["encode_decodes"] == 1

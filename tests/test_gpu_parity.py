@@ -424,3 +424,45 @@ def test_decode_terms_match_reference(gpu_lib, ref_lib):
             bg1, mg1 = tr_g.decode_terms(p, which=1)
             assert mg1 is None and abs(bg1 - bg) <= 1e-12 * bg
         assert np.array_equal(tr_g.get_state()["params"], st["params"])  # substitution is per call
+
+
+@pytest.mark.parametrize("h,w,preset", [(64, 96, "hop"), (45, 71, "lop"), (96, 128, "cfg4")])
+def test_latent_mu_sigma_bit_exact(gpu_lib, h, w, preset):
+    """encode_latents' per-latent Laplace parameters (bitstream.hpp:106-141,
+    arm_forward_single entropy_model.hpp:107-134) computed on the device for
+    all latents at once must be BIT-identical to the reference's sequential
+    scalar evaluation: the reference decoder rebuilds every CDF from them
+    (SURVEY §8f row 4).  The reference's codegen is ISA-specific: its own
+    x86-64-v3 (AVX2+FMA) and x86-64-v4 (AVX-512) builds disagree on ~80 % of
+    the mu values (tools/mu_sigma_isa.py), so a coolcodec bitstream only
+    decodes on the build that wrote it.  The device reproduces the v3 build
+    (FMA-contracted sequential chains) — the one the C++ drop-in binary is
+    built as, whose decoder reads the device-encoded payload back
+    (tests/test_dropin.py)."""
+    from tests.oracle_util import REF_DIR
+
+    v3 = REF_DIR / "libccref_v3.so"
+    if not v3.exists():
+        pytest.skip("oracle/_ref/libccref_v3.so not built")
+    ref_lib = capi.load_library(v3)
+    img = make_image(ref_lib, h, w, seed=7)
+    enc, dcfg = EncoderConfig(lmbda=1e-3, seed=3), DecoderConfig.from_name(preset)
+    with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
+        tr_g.fresh_candidate(0)
+        for _ in range(30):
+            tr_g.proxy_iteration(1e-2, 0.35, 0.22)
+        st = tr_g.get_state()
+        tr_r.fresh_candidate(0)
+        tr_r.set_state(st)
+        tr_g.quantize_all()
+        q = np.clip(tr_g.get_q(), -7, 7)
+        tr_r.set_q(q)
+        tr_g.set_q(q)
+        rng = np.random.default_rng(1)
+        for k in range(3):
+            p = None if k == 0 else st["params"] * (1 + 0.3 * rng.standard_normal(st["params"].size)).astype(np.float32)
+            mr, sr = tr_r.latent_mu_sigma(p)
+            mg, sg = tr_g.latent_mu_sigma(p)
+            assert np.array_equal(mg, mr), (k, np.mean(mg != mr), np.abs(mg - mr).max())
+            assert np.array_equal(sg, sr), (k, np.mean(sg != sr), np.abs(sg - sr).max())
+            assert np.all(np.isfinite(mg)) and np.all((sg >= 0.06) & (sg <= 256.0))
