@@ -84,7 +84,7 @@ void launch_latent_mu_sigma(const LaunchCtx& L, float* mu, float* sigma);
 
 // synthesis (cc_syn.cu, cc_syn_trunk.cu)
 void launch_syn_forward(const LaunchCtx& L, bool backward);
-void launch_syn_backward(const LaunchCtx& L);
+void launch_syn_backward(const LaunchCtx& L, int part = 0);  // 0 all, 1 dz, 2 weight grads
 int syn_padded_hidden(int F);
 size_t syn_trunk_smem(int FP);
 int syn_trunk_blocks_per_sm(int FP);

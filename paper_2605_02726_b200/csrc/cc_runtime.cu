@@ -121,6 +121,8 @@ void Trainer::init(const float* image, int h, int w) {
     CCB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
     CCB_CUDA(cudaEventCreateWithFlags(&ev_sched_, cudaEventDisableTiming));
     CCB_CUDA(cudaEventCreateWithFlags(&ev_fin_, cudaEventDisableTiming));
+    CCB_CUDA(cudaEventCreateWithFlags(&ev_rate_, cudaEventDisableTiming));
+    CCB_CUDA(cudaEventCreateWithFlags(&ev_synfwd_, cudaEventDisableTiming));
     stream_ = own_stream_;
     build_plan();
     allocate();
@@ -152,6 +154,8 @@ Trainer::~Trainer() {
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (ev_sched_) cudaEventDestroy(ev_sched_);
     if (ev_fin_) cudaEventDestroy(ev_fin_);
+    if (ev_rate_) cudaEventDestroy(ev_rate_);
+    if (ev_synfwd_) cudaEventDestroy(ev_synfwd_);
     if (side_stream_) cudaStreamDestroy(side_stream_);
     if (tail_stream_) cudaStreamDestroy(tail_stream_);
     if (own_stream_) cudaStreamDestroy(own_stream_);
@@ -689,20 +693,44 @@ void Trainer::enqueue_proxy(bool batched) {
     if (batched) launch_sched_load(L_, d_sched_);
     launch_softq_fwd(L_);
     mark(1, false);
+    // A/B: the synthesis trunk's weight gradients as a separate launch on the
+    // rate branch (1: after the dF pyramid, 2: before it) instead of fused
+    // into the critical-chain backward (0).  Measured at 512x768: 0.483 ms
+    // fused, 0.496 / 0.499 split — the recomputed hidden layer costs more than
+    // the shorter critical chain saves.
+    static const int mode = [] {
+        const char* e = std::getenv("CCB_TRUNKW");
+        return e ? std::atoi(e) : 0;
+    }();
     fork();
     launch_arm(side(), kArmProxy);
     mark(2, true);
-    launch_pyramid(side());
-    mark(3, true);
+    if (mode != 2) {
+        launch_pyramid(side());
+        mark(3, true);
+        CCB_CUDA(cudaEventRecord(ev_rate_, side_stream_));
+    }
     launch_ups_forward(L_);
     mark(4, false);
     launch_syn_forward(L_, true);
     mark(5, false);
-    launch_syn_backward(L_);
+    if (mode == 0) {
+        launch_syn_backward(L_, 0);
+    } else {
+        CCB_CUDA(cudaEventRecord(ev_synfwd_, stream_));
+        CCB_CUDA(cudaStreamWaitEvent(side_stream_, ev_synfwd_, 0));
+        launch_syn_backward(side(), 2);
+        launch_syn_backward(L_, 1);
+    }
+    if (mode == 2) {
+        launch_pyramid(side());
+        mark(3, true);
+        CCB_CUDA(cudaEventRecord(ev_rate_, side_stream_));
+    }
     mark(6, false);
     launch_ups_backward(L_, true, 0, 1);
     mark(7, false);
-    join();
+    CCB_CUDA(cudaStreamWaitEvent(stream_, ev_rate_, 0));
     // The two finest grids (main levels 1, 0: ~93 % of the latents) have all
     // their gradient terms once the first upsampling-backward stage is done:
     // their gather and Adam step run beside the remaining (latency-bound)
@@ -712,18 +740,15 @@ void Trainer::enqueue_proxy(bool batched) {
     // NN gradients: every region but the upsampling taps is complete here
     // (ARM, synthesis); the taps ([off_tconv[0], off_c1w)) after the last stage
     const int ups_lo = H_.off_tconv[0], ups_hi = H_.off_c1w;
-    // side: cost / bias corrections, then the NN-gradient reductions that
-    // are already complete; tail: the fine-grid gather and (once the cost
-    // flag is known) their Adam step
-    fork();
-    launch_finalize(side(), kArmProxy, -1);
-    CCB_CUDA(cudaEventRecord(ev_fin_, side_stream_));
+    // side (after the trunk weight gradients): the NN-gradient reductions that
+    // are complete; tail: cost / bias corrections, the fine-grid gather and
+    // their Adam step
     launch_nn_reduce(side(), 0, ups_lo);
     launch_nn_reduce(side(), ups_hi, H_.n_params);
     fork(true);
+    launch_finalize(side(true), kArmProxy, -1);
     launch_latent_grad_grids(side(true), fine, H_.n_grids);
     mark(8, 2);
-    CCB_CUDA(cudaStreamWaitEvent(tail_stream_, ev_fin_, 0));
     launch_adam_latents_grids(side(true), fine, H_.n_grids);
     launch_noise_ahead(side(true));  // next iteration's noise, in the tail's slack
     mark(9, 2);

@@ -168,6 +168,8 @@ private:
     cudaStream_t tail_stream_ = nullptr;  // concurrent fine-grid gradient tail
     cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     cudaEvent_t ev_fin_ = nullptr;    // k_finalize done (the cost flag the latent Adam step reads)
+    cudaEvent_t ev_rate_ = nullptr;   // rate branch (ARM, dF pyramid) done
+    cudaEvent_t ev_synfwd_ = nullptr; // synthesis forward + posts done (trunk weight grads may start)
     cudaEvent_t ev_sched_ = nullptr;  // the pinned schedule upload of the last batch
     Plan H_{};
     Plan* d_plan_ = nullptr;

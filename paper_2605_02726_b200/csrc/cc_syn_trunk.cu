@@ -14,6 +14,12 @@
 //            accumulators stay in registers across all tiles of the CTA and
 //            are summed (ranges in fixed order, fp64) once at the end.
 // Deterministic: fixed thread->work mapping, no atomics.
+//
+// PART selects the work: 0 both phases (one launch); 1 the data path only
+// (dz, the input of the upsampling backward: on the critical chain); 2 the
+// weight gradients only (h1, dh1 recomputed, phase B, partial rows: an
+// off-critical-path launch beside the upsampling backward).  1 + 2 compute
+// exactly what 0 does.
 #include <cuda_runtime.h>
 
 #include "cc_kernels.h"
@@ -117,9 +123,10 @@ __device__ __forceinline__ void issue_tile(const Plan& P, const float* __restric
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <int FP>
+template <int FP, int PART>
 __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict__ pp,
                                                           const float* __restrict__ dt_in) {
+    constexpr bool kDz = PART != 2, kDw = PART != 1;
     using K = TB<FP>;
     const Plan& P = *pp;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -186,7 +193,7 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
         float2 dz[kLZ];
 #pragma unroll
         for (int k = 0; k < kLZ; ++k) dz[k] = make_float2(0.0f, 0.0f);
-        if (qt == 0 && has_stab) {
+        if (kDz && qt == 0 && has_stab) {
             float2 dx[3];
 #pragma unroll
             for (int co = 0; co < 3; ++co) dx[co] = *reinterpret_cast<const float2*>(sDX + co * LT + px0);
@@ -226,29 +233,34 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
                 for (int co = 0; co < 3; ++co) d = ffma2(dt[co], sm.c2w[co][f + u], d);
                 d.x = h.x > 0.0f ? d.x : 0.0f;
                 d.y = h.y > 0.0f ? d.y : 0.0f;
+                if (kDz) {
 #pragma unroll
-                for (int kq = 0; kq < kLZ / 4; ++kq) {
-                    const float4 w4 = *reinterpret_cast<const float4*>(&sm.W1[f + u][4 * kq]);
-                    dz[4 * kq + 0] = ffma2(d, w4.x, dz[4 * kq + 0]);
-                    dz[4 * kq + 1] = ffma2(d, w4.y, dz[4 * kq + 1]);
-                    dz[4 * kq + 2] = ffma2(d, w4.z, dz[4 * kq + 2]);
-                    dz[4 * kq + 3] = ffma2(d, w4.w, dz[4 * kq + 3]);
+                    for (int kq = 0; kq < kLZ / 4; ++kq) {
+                        const float4 w4 = *reinterpret_cast<const float4*>(&sm.W1[f + u][4 * kq]);
+                        dz[4 * kq + 0] = ffma2(d, w4.x, dz[4 * kq + 0]);
+                        dz[4 * kq + 1] = ffma2(d, w4.y, dz[4 * kq + 1]);
+                        dz[4 * kq + 2] = ffma2(d, w4.z, dz[4 * kq + 2]);
+                        dz[4 * kq + 3] = ffma2(d, w4.w, dz[4 * kq + 3]);
+                    }
                 }
-                *reinterpret_cast<float2*>(sH + (f + u) * LT + px0) = make_float2(v0 ? h.x : 0.0f, v1 ? h.y : 0.0f);
-                *reinterpret_cast<float2*>(sDH + (f + u) * LT + px0) = d;
+                if (kDw) {
+                    *reinterpret_cast<float2*>(sH + (f + u) * LT + px0) = make_float2(v0 ? h.x : 0.0f, v1 ? h.y : 0.0f);
+                    *reinterpret_cast<float2*>(sDH + (f + u) * LT + px0) = d;
+                }
             }
         }
         if (qt == 0) {
-            *reinterpret_cast<float2*>(sZ + kLZ * LT + px0) = make_float2(v0 ? 1.0f : 0.0f, v1 ? 1.0f : 0.0f);
+            if (kDw) *reinterpret_cast<float2*>(sZ + kLZ * LT + px0) = make_float2(v0 ? 1.0f : 0.0f, v1 ? 1.0f : 0.0f);
         } else {
-            if (qt == 1)
+            if (kDw && qt == 1)
                 *reinterpret_cast<float2*>(sH + FP * LT + px0) = make_float2(v0 ? 1.0f : 0.0f, v1 ? 1.0f : 0.0f);
+            if (kDz)
 #pragma unroll
-            for (int k = 0; k < kLZ; ++k)
-                *reinterpret_cast<float2*>(sDZ + ((qt - 1) * kLZ + k) * LT + px0) = dz[k];
+                for (int k = 0; k < kLZ; ++k)
+                    *reinterpret_cast<float2*>(sDZ + ((qt - 1) * kLZ + k) * LT + px0) = dz[k];
         }
         __syncthreads();
-        if (qt == 0 && v0) {  // quarters summed in order
+        if (kDz && qt == 0 && v0) {  // quarters summed in order
 #pragma unroll
             for (int k = 0; k < kLZ; ++k) {
                 if (k >= L) continue;
@@ -270,7 +282,7 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
         }
         // ---- phase B: weight gradients ----
 #pragma unroll
-        for (int m = 0; m < K::MAXU; ++m) {
+        for (int m = 0; m < (kDw ? K::MAXU : 0); ++m) {
             const int u = tid + m * NT;
             if (u < K::NU) {
                 const int j = u / K::NPART, s = u - j * K::NPART;
@@ -296,6 +308,7 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
         x = sDX; sDX = nDX; nDX = x;
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (!kDw) return;
     __syncthreads();
 
     // ---- epilogue: stage the units, sum ranges in order, one row per CTA ----
@@ -347,13 +360,18 @@ size_t tb_smem() {
 }
 
 template <int FP>
-void launch_t(const LaunchCtx& L, const float* dt) {
-    k_syn_trunk_bwd2<FP><<<L.syn_blocks, NT, tb_smem<FP>(), L.stream>>>(L.plan, dt);
+void launch_t(const LaunchCtx& L, const float* dt, int part) {
+    if (part == 1) k_syn_trunk_bwd2<FP, 1><<<L.syn_blocks, NT, tb_smem<FP>(), L.stream>>>(L.plan, dt);
+    else if (part == 2) k_syn_trunk_bwd2<FP, 2><<<L.syn_blocks, NT, tb_smem<FP>(), L.stream>>>(L.plan, dt);
+    else k_syn_trunk_bwd2<FP, 0><<<L.syn_blocks, NT, tb_smem<FP>(), L.stream>>>(L.plan, dt);
 }
 
 template <int FP>
 void configure_t() {
-    cudaFuncSetAttribute(k_syn_trunk_bwd2<FP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(tb_smem<FP>()));
+    const int sm = int(tb_smem<FP>());
+    cudaFuncSetAttribute(k_syn_trunk_bwd2<FP, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_syn_trunk_bwd2<FP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_syn_trunk_bwd2<FP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 }
 
 }  // namespace
@@ -389,14 +407,14 @@ void syn_configure(int FP) {
     }
 }
 
-void launch_syn_backward(const LaunchCtx& L) {
+void launch_syn_backward(const LaunchCtx& L, int part) {
     const Plan& H = *L.host;
     const float* dt = H.syn_dt;
     switch (syn_padded_hidden(H.syn_F)) {
-        case 8: launch_t<8>(L, dt); break;
-        case 16: launch_t<16>(L, dt); break;
-        case 48: launch_t<48>(L, dt); break;
-        default: launch_t<64>(L, dt); break;
+        case 8: launch_t<8>(L, dt, part); break;
+        case 16: launch_t<16>(L, dt, part); break;
+        case 48: launch_t<48>(L, dt, part); break;
+        default: launch_t<64>(L, dt, part); break;
     }
 }
 
