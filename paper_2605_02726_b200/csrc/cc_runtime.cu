@@ -740,9 +740,10 @@ void Trainer::enqueue_proxy(bool batched) {
     // NN gradients: every region but the upsampling taps is complete here
     // (ARM, synthesis); the taps ([off_tconv[0], off_c1w)) after the last stage
     const int ups_lo = H_.off_tconv[0], ups_hi = H_.off_c1w;
-    // side (after the trunk weight gradients): the NN-gradient reductions that
-    // are complete; tail: cost / bias corrections, the fine-grid gather and
-    // their Adam step
+    // side (once the synthesis backward has written its partial rows): the
+    // NN-gradient reductions that are complete; tail: cost / bias
+    // corrections, the fine-grid gather and their Adam step
+    fork();
     launch_nn_reduce(side(), 0, ups_lo);
     launch_nn_reduce(side(), ups_hi, H_.n_params);
     fork(true);
