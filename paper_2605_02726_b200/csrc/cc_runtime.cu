@@ -667,25 +667,38 @@ void Trainer::nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, doub
 // (upsampling, synthesis, their backward) only share ŷ as input, so they run
 // as two concurrent branches of the graph and join before the gradient
 // assembly.
+// CCB_SERIAL=1 runs every branch on the main stream in program order (the
+// race check of tests/test_gpu_parity.py::test_branches_match_serial_order).
+static bool serial_branches() {
+    static const bool on = [] {
+        const char* e = std::getenv("CCB_SERIAL");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+cudaStream_t Trainer::branch(bool tail) const {
+    return serial_branches() ? stream_ : (tail ? tail_stream_ : side_stream_);
+}
 void Trainer::fork(bool tail) {
+    if (serial_branches()) return;
     CCB_CUDA(cudaEventRecord(ev_fork_, stream_));
-    CCB_CUDA(cudaStreamWaitEvent(tail ? tail_stream_ : side_stream_, ev_fork_, 0));
+    CCB_CUDA(cudaStreamWaitEvent(branch(tail), ev_fork_, 0));
 }
 void Trainer::join(bool tail) {
-    CCB_CUDA(cudaEventRecord(ev_join_, tail ? tail_stream_ : side_stream_));
+    if (serial_branches()) return;
+    CCB_CUDA(cudaEventRecord(ev_join_, branch(tail)));
     CCB_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
 }
 LaunchCtx Trainer::side(bool tail) const {
     LaunchCtx s = L_;
-    s.stream = tail ? tail_stream_ : side_stream_;
+    s.stream = branch(tail);
     return s;
 }
 
 // timeline diagnostics (ccb_timeline): event marks inside the captured sequence
 void Trainer::mark(int id, int on) {
     if (tl_ev_)  // an event-record node of the graph (timing), not a capture dependency
-        CCB_CUDA(cudaEventRecordWithFlags(tl_ev_[id], on == 2 ? tail_stream_ : on ? side_stream_ : stream_,
-                                          cudaEventRecordExternal));
+        CCB_CUDA(cudaEventRecordWithFlags(tl_ev_[id], on ? branch(on == 2) : stream_, cudaEventRecordExternal));
 }
 
 void Trainer::enqueue_proxy(bool batched) {
@@ -708,7 +721,7 @@ void Trainer::enqueue_proxy(bool batched) {
     if (mode != 2) {
         launch_pyramid(side());
         mark(3, true);
-        CCB_CUDA(cudaEventRecord(ev_rate_, side_stream_));
+        CCB_CUDA(cudaEventRecord(ev_rate_, branch(false)));
     }
     launch_ups_forward(L_);
     mark(4, false);
@@ -718,14 +731,14 @@ void Trainer::enqueue_proxy(bool batched) {
         launch_syn_backward(L_, 0);
     } else {
         CCB_CUDA(cudaEventRecord(ev_synfwd_, stream_));
-        CCB_CUDA(cudaStreamWaitEvent(side_stream_, ev_synfwd_, 0));
+        CCB_CUDA(cudaStreamWaitEvent(branch(false), ev_synfwd_, 0));
         launch_syn_backward(side(), 2);
         launch_syn_backward(L_, 1);
     }
     if (mode == 2) {
         launch_pyramid(side());
         mark(3, true);
-        CCB_CUDA(cudaEventRecord(ev_rate_, side_stream_));
+        CCB_CUDA(cudaEventRecord(ev_rate_, branch(false)));
     }
     mark(6, false);
     launch_ups_backward(L_, true, 0, 1);

@@ -149,6 +149,7 @@ private:
     void fork(bool tail = false);
     void join(bool tail = false);
     LaunchCtx side(bool tail = false) const;
+    cudaStream_t branch(bool tail) const;  // side / tail stream (the main one under CCB_SERIAL=1)
     void enqueue_hardround(int slot);
     void enqueue_true_cost();
     void run_graph(int which, int slot = -1);

@@ -466,3 +466,23 @@ def test_latent_mu_sigma_bit_exact(gpu_lib, h, w, preset):
             assert np.array_equal(mg, mr), (k, np.mean(mg != mr), np.abs(mg - mr).max())
             assert np.array_equal(sg, sr), (k, np.mean(sg != sr), np.abs(sg - sr).max())
             assert np.all(np.isfinite(mg)) and np.all((sg >= 0.06) & (sg <= 256.0))
+
+
+def test_branches_match_serial_order(gpu_lib, tmp_path):
+    """The concurrent branches of the iteration graph (rate branch, tail and
+    side streams, programmatic dependent launches) compute exactly what the
+    same kernels compute one after another on one stream (CCB_SERIAL=1): a
+    missing dependency shows up as a bitwise difference."""
+    import os
+    import subprocess
+    import sys
+
+    res = {}
+    for mode in ("0", "1"):
+        out = tmp_path / f"run{mode}.npz"
+        env = dict(os.environ, CCB_SERIAL=mode)
+        subprocess.run([sys.executable, "-m", "tests.branch_run", str(out), "256", "384", "6"], env=env,
+                       check=True, timeout=600, cwd=str(golden_util.GOLDEN.parents[1]))
+        res[mode] = dict(np.load(out))
+    for k in res["0"]:
+        assert np.array_equal(res["0"][k], res["1"][k]), k
