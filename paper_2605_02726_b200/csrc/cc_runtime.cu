@@ -772,10 +772,13 @@ void Trainer::enqueue_proxy(bool batched) {
     launch_nn_reduce(side(), ups_lo, ups_hi);
     launch_latent_grad_grids(L_, 0, fine);
     mark(11, false);
-    join();
+    // every gather has read the weights: the NN step (side, after its
+    // reductions) beside the coarse grids' Adam step (main)
     join(true);
+    fork();
+    nn_apply(side(), true, true, batched ? d_rec_ : nullptr);
     if (fine > 0) launch_adam_latents_grids(L_, 0, fine);
-    nn_apply(L_, true, true, batched ? d_rec_ : nullptr);
+    join();
     mark(12, false);
 }
 
