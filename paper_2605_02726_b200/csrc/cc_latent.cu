@@ -50,12 +50,15 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
     const bool pre = P.noise_buf != nullptr && P.scal->noise_iter == P.scal->global_iter;
     const float inv_denom = 1.0f / softround_denom(temp);
     const float inv_t = 1.0f / temp;
+    __shared__ GridGeom s_geo[kMaxGrids];
+    for (int k = threadIdx.x; k < P.n_grids; k += blockDim.x) s_geo[k] = P.g[k];
+    __syncthreads();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x) {
         const int gi = find_grid(s_off, i);
-        const GridGeom& g = P.g[gi];
-        const int64_t li = i - g.lat_off;
-        const int r = int(li / g.cols), c = int(li - int64_t(r) * g.cols);
+        const GridGeom& g = s_geo[gi];
+        const int li = int(i - g.lat_off);  // < 2^31 latents per grid
+        const int r = li / g.cols, c = li - r * g.cols;
         const float x = P.y[i];
         float f = floorf(x);
         float d = x - f - 0.5f;
@@ -67,7 +70,7 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
                 gz = P.noise_buf[i];
             } else {
                 const uint64_t stream = hash_combine(hash_combine(P.seed, giter), uint64_t(gi));
-                gz = counter_gauss(stream, uint64_t(li + int64_t(g.row0) * g.cols));  // global raster index
+                gz = counter_gauss(stream, uint64_t(li) + uint64_t(int64_t(g.row0) * g.cols));  // global raster index
             }
             o += noise_std * gz;
         }
