@@ -28,10 +28,13 @@ namespace ccb {
         s_off[threadIdx.x] = int(threadIdx.x) < (P).n_grids ? (P).g[threadIdx.x].lat_off : INT64_MAX; \
     __syncthreads()
 
+// binary search over the (sorted, INT64_MAX-padded) offsets: s_off[gi] <= i
 __device__ __forceinline__ int find_grid(const int64_t* s_off, int64_t i) {
+    static_assert((kMaxGrids & (kMaxGrids - 1)) == 0, "power-of-two grid table");
     int gi = 0;
 #pragma unroll
-    for (int k = 1; k < kMaxGrids; ++k) gi += i >= s_off[k] ? 1 : 0;
+    for (int step = kMaxGrids / 2; step >= 1; step >>= 1)
+        if (s_off[gi + step] <= i) gi += step;
     return gi;
 }
 
