@@ -154,7 +154,7 @@ def run_reference(args, rank, world):
     # each step = one proxy_iteration on every thread (~0.8 s wall); cap the
     # timed steps so the whole arm ends within a couple of minutes
     steps = max(1, min(args.steps, 60))
-    warm = max(0, min(args.warmup, 1))
+    warm = max(0, min(args.warmup, 3))
     secs = cpu_reference_run(h, w, args.preset, args.seed, threads, warm, steps)
     value = threads * steps * h * w / secs / 1e9
     line = {
