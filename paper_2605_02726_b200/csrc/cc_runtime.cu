@@ -102,20 +102,14 @@ void Trainer::init(const float* image, int h, int w) {
                         " is sm_" + std::to_string(prop.major) + std::to_string(prop.minor));
     num_sms_ = prop.multiProcessorCount;
     {
-        // The critical chain (softq -> upsampling -> synthesis -> backward ->
-        // upsampling backward) runs on the main stream at the greatest
-        // priority: its CTAs are scheduled ahead of the concurrent branches
-        // (persistent ARM, gradient gathers, reductions) whenever SM slots free.
+        // main stream (the critical chain) at the greatest priority, the
+        // concurrent branches at the least: effective for eager launches; a
+        // CUDA graph runs its nodes at the launch stream's priority
         int lo = 0, hi = 0;
         CCB_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        const char* m = std::getenv("CCB_MAIN_PRIO");  // A/B: n = default priority
-        CCB_CUDA(cudaStreamCreateWithPriority(&own_stream_, cudaStreamNonBlocking, (m && m[0] == 'n') ? lo : hi));
-        const char* e = std::getenv("CCB_SIDE_PRIO");
-        const int prio = (e && e[0] == '0') ? 0 : lo;
-        CCB_CUDA(cudaStreamCreateWithPriority(&side_stream_, cudaStreamNonBlocking, prio));
-        const char* t = std::getenv("CCB_TAIL_PRIO");  // A/B: l(ow, default) / n(ormal) / h(igh)
-        const int tprio = (t && t[0] == 'n') ? 0 : (t && t[0] == 'h') ? hi : lo;
-        CCB_CUDA(cudaStreamCreateWithPriority(&tail_stream_, cudaStreamNonBlocking, tprio));
+        CCB_CUDA(cudaStreamCreateWithPriority(&own_stream_, cudaStreamNonBlocking, hi));
+        CCB_CUDA(cudaStreamCreateWithPriority(&side_stream_, cudaStreamNonBlocking, lo));
+        CCB_CUDA(cudaStreamCreateWithPriority(&tail_stream_, cudaStreamNonBlocking, lo));
     }
     CCB_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
     CCB_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
