@@ -168,6 +168,7 @@ struct Plan {
     float* nn_m;
     float* nn_v;
     double* partials;
+    double* arm_qs;           // cc_arm3: latent-quarter rows 1..3 of every ARM CTA (3 x arm CTAs x ARM params)
     double* bc_lat;           // per grid Adam bias corrections (2 per grid)
     double* bits_part;
     double* mse_part;

@@ -486,3 +486,29 @@ def test_branches_match_serial_order(gpu_lib, tmp_path):
         res[mode] = dict(np.load(out))
     for k in res["0"]:
         assert np.array_equal(res["0"][k], res["1"][k]), k
+
+
+def test_tensor_core_arm_matches_default(gpu_lib, tmp_path):
+    """The opt-in tensor-core ARM (cc_arm3.cu, mma.sync TF32 with a 3-term
+    split; CCB_ARM_V3=1) against the default FFMA2 kernel over a few
+    free-running batched iterations: costs within 1e-5, final state and
+    gradients within drift bounds, and its own runs bitwise deterministic."""
+    import os
+    import subprocess
+    import sys
+
+    res = {}
+    for tag, v3 in (("v2", "0"), ("v3a", "1"), ("v3b", "1")):
+        out = tmp_path / f"{tag}.npz"
+        env = dict(os.environ, CCB_ARM_V3=v3)
+        subprocess.run([sys.executable, "-m", "tests.branch_run", str(out), "256", "384", "6"], env=env,
+                       check=True, timeout=600, cwd=str(golden_util.GOLDEN.parents[1]))
+        res[tag] = dict(np.load(out))
+    for k in res["v3a"]:
+        assert np.array_equal(res["v3a"][k], res["v3b"][k]), k
+    a, b = res["v3a"], res["v2"]
+    assert np.max(np.abs(a["costs"] - b["costs"]) / np.abs(b["costs"])) <= 1e-5
+    assert rel_l2(a["latents"], b["latents"]) <= 1e-5
+    assert rel_l2(a["params"], b["params"]) <= 1e-5
+    assert rel_l2(a["pg"], b["pg"]) <= 1e-3
+    assert rel_l2(a["lg"], b["lg"]) <= 1e-3
