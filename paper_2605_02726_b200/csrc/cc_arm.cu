@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kArmTile) k_arm(const Plan* __restrict__ pp,
     if (tid == 0) P.bits_part[blockIdx.x] = bits_cta;
     if (MODE != kArmForward) {
         const PartialRegion& R = P.region[P.reg_arm];
-        double* row = P.partials + R.base + int64_t(blockIdx.x) * R.count;
+        const PartialRow row(P, R, blockIdx.x);
         for (int e = tid; e < R.count; e += kArmTile) row[e] = sm.acc[e];
     }
 }

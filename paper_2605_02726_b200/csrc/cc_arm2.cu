@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
     if (tid == 0) P.bits_part[blockIdx.x] = tb;
     if (MODE == kArmForward) return;
     const PartialRegion& R = P.region[P.reg_arm];
-    double* row = P.partials + R.base + int64_t(blockIdx.x) * R.count;
+    const PartialRow row(P, R, blockIdx.x);
     // stage the register units in (now dead) activation memory, then every
     // parameter of the region is written exactly once: the three latent
     // thirds of its job summed in order

@@ -355,8 +355,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm3(const Plan* __restrict__ pp, con
 #pragma unroll
             for (int r = 0; r < 4; ++r) uacc[i][n][r] = 0.0f;
     auto qrow = [&](int q) -> double* {
-        return q == 0 ? P.partials + R.base + int64_t(blockIdx.x) * R.count - R.param_off
-                      : P.arm_qs + (int64_t(q - 1) * gridDim.x + blockIdx.x) * R.count - R.param_off;
+        return P.arm_qs + (int64_t(q) * gridDim.x + blockIdx.x) * R.count - R.param_off;
     };
     // this warp's units, resolved once: A / B row bases (A, B inside the
     // activation buffer; the IFCE unit's B is the tile window's R rows)
@@ -730,11 +729,13 @@ __global__ void __launch_bounds__(NT, 2) k_arm3(const Plan* __restrict__ pp, con
     }
     __syncthreads();
     // quarters summed in fixed order into the CTA's partial row
-    double* row0 = qrow(0);
+    const double* q0 = qrow(0);
     const double* q1 = qrow(1);
     const double* q2 = qrow(2);
     const double* q3 = qrow(3);
-    for (int o = R.param_off + tid; o < R.param_off + R.count; o += NT) row0[o] = ((row0[o] + q1[o]) + q2[o]) + q3[o];
+    const PartialRow row(P, R, blockIdx.x);
+    for (int o = R.param_off + tid; o < R.param_off + R.count; o += NT)
+        row[o - R.param_off] = ((q0[o] + q1[o]) + q2[o]) + q3[o];
 }
 
 template <int DP, int WP>

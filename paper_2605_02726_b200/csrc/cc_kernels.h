@@ -69,7 +69,7 @@ void launch_pyramid(const LaunchCtx& L);
 int arm_blocks_per_sm(int Dp, int Wp);
 void arm_configure(int Dp, int Wp);
 bool arm_uses_v2(int Dp, int Wp);
-bool arm_uses_v3(int Dp, int Wp);  // the tensor-core kernel (cc_arm3.cu): 3 extra fp64 quarter rows per CTA (Plan::arm_qs)  // the register-tiled kernel (cc_arm2.cu) is selected
+bool arm_uses_v3(int Dp, int Wp);  // the tensor-core kernel (cc_arm3.cu): fp64 quarter rows per CTA (Plan::arm_qs)
 void pyramid_configure(const Plan& H);
 
 // upsampling (cc_ups.cu)

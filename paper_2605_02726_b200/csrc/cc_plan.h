@@ -18,7 +18,8 @@
 //              caches of upsample_forward (synthesis.hpp:40-93).
 //   syn_*    : (3, H, W) planes: trunk output t, posts p_i, stab term, dx̂.
 //   params/grads/nn_m/nn_v : for_each_param order (model.hpp:158-171).
-//   partials : per-CTA weight-gradient partial sums, reduced in a fixed order.
+//   partials : per-CTA weight-gradient partial sums, reduced in a fixed order
+//              (parameter-major: the rows of one parameter are contiguous).
 #pragma once
 
 #include <stdint.h>
@@ -168,7 +169,7 @@ struct Plan {
     float* nn_m;
     float* nn_v;
     double* partials;
-    double* arm_qs;           // cc_arm3: latent-quarter rows 1..3 of every ARM CTA (3 x arm CTAs x ARM params)
+    double* arm_qs;           // cc_arm3: the four latent-quarter rows of every ARM CTA (4 x arm CTAs x ARM params)
     double* bc_lat;           // per grid Adam bias corrections (2 per grid)
     double* bits_part;
     double* mse_part;

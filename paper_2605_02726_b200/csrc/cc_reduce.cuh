@@ -4,6 +4,8 @@
 // (tests/test_encoder.cpp:27-54) and so does this port.
 #pragma once
 
+#include "cc_plan.h"
+
 namespace ccb {
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -14,6 +16,17 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 // Sum of `v` over the block; the result is valid in thread 0 only.
 // `sbuf` needs blockDim.x / 32 doubles.  Must be called by every thread.
+// A CTA's partial row of a PartialRegion.  Storage is PARAMETER-major
+// (row b of parameter e at base + e * nblocks + b), so k_nn_reduce reads the
+// rows of one parameter contiguously; the writers index it like a row.
+struct PartialRow {
+    double* p;
+    int64_t stride;
+    __device__ __forceinline__ PartialRow(const Plan& P, const PartialRegion& R, int64_t b)
+        : p(P.partials + R.base + b), stride(R.nblocks) {}
+    __device__ __forceinline__ double& operator[](int64_t e) const { return p[e * stride]; }
+};
+
 __device__ __forceinline__ double block_sum(double v, double* sbuf) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     v = warp_sum(v);

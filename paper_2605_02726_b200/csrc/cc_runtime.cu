@@ -547,7 +547,7 @@ void Trainer::allocate() {
     P.nn_v = f32(P.n_params);
     P.partials = static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.partials)));
     P.arm_qs = arm_uses_v3(P.Dp, P.Wp)
-                   ? static_cast<double*>(dalloc(sizeof(double) * 3 * size_t(L_.arm_blocks) * size_t(P.arm_nvals)))
+                   ? static_cast<double*>(dalloc(sizeof(double) * 4 * size_t(L_.arm_blocks) * size_t(P.arm_nvals)))
                    : nullptr;
     P.bc_lat = static_cast<double*>(dalloc(sizeof(double) * 2 * kMaxGrids));
     P.bits_part = static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_bits_part)));

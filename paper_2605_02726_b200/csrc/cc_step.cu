@@ -64,10 +64,10 @@ __global__ void __launch_bounds__(256) k_nn_reduce(const Plan* __restrict__ pp,
         for (int r = 0; r < P.n_regions; ++r) {
             const PartialRegion& R = P.region[r];
             if (p < R.param_off || p >= R.param_off + R.count) continue;
-            const double* col = P.partials + R.base + (p - R.param_off);
+            const double* col = P.partials + R.base + int64_t(p - R.param_off) * R.nblocks;  // parameter-major
             double s = 0.0;
 #pragma unroll 4
-            for (int b = lane; b < R.nblocks; b += 32) s += col[int64_t(b) * R.count];
+            for (int b = lane; b < R.nblocks; b += 32) s += col[b];
             sum += warp_sum(s);
         }
         if (lane == 0) {

@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
         __syncthreads();
         for (int i = 0; i < NP; ++i) {
             const PartialRegion& R = P.region[P.reg_post[i]];
-            double* row = P.partials + R.base + int64_t(blockIdx.x) * R.count;
+            const PartialRow row(P, R, blockIdx.x);
             for (int e = tid; e < R.count; e += NT) {
                 const int pidx = R.param_off + e;
                 int pair = -1, k = 0;

@@ -24,6 +24,7 @@
 
 #include "cc_kernels.h"
 #include "cc_math.cuh"
+#include "cc_reduce.cuh"
 #include "cc_tile.cuh"
 
 namespace ccb {
@@ -323,7 +324,7 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
     }
     __syncthreads();
     const PartialRegion& R = P.region[P.reg_syn_trunk];
-    double* row = P.partials + R.base + int64_t(blockIdx.x) * R.count;
+    const PartialRow row(P, R, blockIdx.x);
     for (int e = tid; e < R.count; e += NT) {
         const int pidx = R.param_off + e;
         int job = -1, q = 0;

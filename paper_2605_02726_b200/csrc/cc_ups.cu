@@ -521,10 +521,10 @@ __global__ void __launch_bounds__(kThreads, 3) k_ups_bwd(const Plan* __restrict_
     const int row = blockIdx.y * gridDim.x + blockIdx.x;
     if (threadIdx.x < 4) {
         const PartialRegion& R = P.region[P.reg_ups_rows[j]];
-        P.partials[R.base + int64_t(row) * R.count + threadIdx.x] = f.tot[threadIdx.x];
+        P.partials[R.base + int64_t(threadIdx.x) * R.nblocks + row] = f.tot[threadIdx.x];
     } else if (threadIdx.x < 7) {
         const PartialRegion& R = P.region[P.reg_ups_ref[j]];
-        P.partials[R.base + int64_t(row) * R.count + (threadIdx.x - 4)] = f.tot[threadIdx.x];
+        P.partials[R.base + int64_t(threadIdx.x - 4) * R.nblocks + row] = f.tot[threadIdx.x];
     }
 }
 
