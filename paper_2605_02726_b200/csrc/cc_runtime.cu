@@ -139,8 +139,7 @@ Trainer::~Trainer() {
     for (void* p : allocs_) cudaFree(p);
     if (h_scal_) cudaFreeHost(h_scal_);
     if (d_sched_) cudaFree(d_sched_);
-    if (d_rec_) cudaFree(d_rec_);
-    if (h_rec_) cudaFreeHost(h_rec_);
+    if (h_rec_) cudaFreeHost(h_rec_);  // d_rec_ is its device mapping
     if (h_sched_) cudaFreeHost(h_sched_);
     if (side_stream_) cudaStreamSynchronize(side_stream_);
     if (tail_stream_) cudaStreamSynchronize(tail_stream_);
@@ -1016,7 +1015,7 @@ void Trainer::proxy_iterations(int n, const double* lr, const double* temp, cons
 void Trainer::last_records(int n, double* rec) {
     if (n <= 0) return;
     if (n > sched_cap_) throw ConfigError("more records requested than the last batch holds");
-    read_scalars();  // synchronises the stream: the per-iteration copies have landed
+    read_scalars();  // synchronises the stream: the kernels' host writes have landed
     std::memcpy(rec, h_rec_, sizeof(double) * 4 * size_t(n));
     last_mse_ = rec[4 * size_t(n - 1) + 1];
     last_bits_ = rec[4 * size_t(n - 1) + 2];
@@ -1036,11 +1035,12 @@ void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* te
     if (n > sched_cap_) {
         synchronize();
         if (d_sched_) cudaFree(d_sched_);
-        if (d_rec_) cudaFree(d_rec_);
         CCB_CUDA(cudaMalloc(&d_sched_, sizeof(double) * 3 * size_t(n)));
-        CCB_CUDA(cudaMalloc(&d_rec_, sizeof(double) * 4 * size_t(n)));
+        // the records live in mapped pinned host memory: k_nn_step writes each
+        // iteration's record straight to the host (no copy between graphs)
         if (h_rec_) cudaFreeHost(h_rec_);
-        CCB_CUDA(cudaMallocHost(&h_rec_, sizeof(double) * 4 * size_t(n)));
+        CCB_CUDA(cudaHostAlloc(&h_rec_, sizeof(double) * 4 * size_t(n), cudaHostAllocMapped));
+        CCB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_rec_), h_rec_, 0));
         if (h_sched_) cudaFreeHost(h_sched_);
         CCB_CUDA(cudaMallocHost(&h_sched_, sizeof(double) * 3 * size_t(n)));
         sched_cap_ = n;
@@ -1060,13 +1060,10 @@ void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* te
                              stream_));
     CCB_CUDA(cudaEventRecord(ev_sched_, stream_));
     CCB_CUDA(cudaMemsetAsync(&H_.scal->sched_pos, 0, sizeof(int64_t), stream_));
-    // every iteration's record (cost, mse, bits, global_iter) goes to pinned
-    // host memory right after the iteration, without a host synchronisation
-    for (int i = 0; i < n; ++i) {
-        run_graph(1);
-        CCB_CUDA(cudaMemcpyAsync(h_rec_ + 4 * size_t(i), d_rec_ + 4 * size_t(i), 4 * sizeof(double),
-                                 cudaMemcpyDeviceToHost, stream_));
-    }
+    // every iteration's record (cost, mse, bits, global_iter) is written by
+    // the iteration's last kernel into mapped pinned host memory, without a
+    // host synchronisation or a copy between the graphs
+    for (int i = 0; i < n; ++i) run_graph(1);
 }
 
 // Stage-by-stage replay of one proxy iteration with events in between

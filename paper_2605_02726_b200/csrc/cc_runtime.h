@@ -180,8 +180,8 @@ private:
     std::vector<void*> allocs_;
     int4* d_tiles_ = nullptr;
     double* d_sched_ = nullptr;     // 3 doubles per iteration (batched)
-    double* d_rec_ = nullptr;       // 4 doubles per iteration (batched)
-    double* h_rec_ = nullptr;       // pinned mirror, filled after every iteration
+    double* d_rec_ = nullptr;       // device mapping of h_rec_
+    double* h_rec_ = nullptr;       // 4 doubles per iteration (batched), mapped pinned host memory
     double* h_sched_ = nullptr;     // pinned schedule staging
     float* d_param_save_ = nullptr; // decode_terms: the trainer's own parameters
     float* d_mu_sigma_ = nullptr;   // latent_mu_sigma output (mu | sigma)
