@@ -55,6 +55,10 @@ __global__ void __launch_bounds__(256) k_syn_trunk_fwd(const Plan* __restrict__ 
         st[co][k] = (P.off_sstab >= 0 && k < L) ? P.params[P.off_sstab + co * L + k] : 0.0f;
     }
     __syncthreads();
+    // programmatic dependent launch: the weights (settled since the last NN
+    // step) are staged while the upsampling chain drains; z only after it
+    pdl_wait();
+    pdl_trigger();
     const int64_t np = P.npix;
     const int64_t npairs = (np + 1) / 2;
     const bool vec = P.zvec != 0;
@@ -131,7 +135,7 @@ __global__ void __launch_bounds__(256) k_syn_trunk_fwd(const Plan* __restrict__ 
 }  // namespace
 
 void launch_syn_forward(const LaunchCtx& L, bool backward) {
-    k_syn_trunk_fwd<<<L.pix_blocks, 256, 0, L.stream>>>(L.plan);
+    launch_pdl(k_syn_trunk_fwd, dim3(L.pix_blocks), dim3(256), 0, L.stream, 's', L.plan);
     launch_syn_post(L, backward);
 }
 

@@ -139,6 +139,8 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
     // fp64 per-thread slot (their fp32 chains stay <= 256 terms long)
     double* flush = P.post_scratch ? P.post_scratch + (int64_t(blockIdx.x) * NT + tid) * 30 : nullptr;
     int tcount = 0;
+    pdl_wait();  // t, s of the trunk forward (weights above were staged before)
+    pdl_trigger();
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         if (flush && NP > 0 && with_grad && ++tcount % 16 == 0) {
 #pragma unroll
@@ -395,9 +397,9 @@ void launch_syn_post(const LaunchCtx& L, bool backward) {
     const int g = H.n_mse_part;
     const int wg = backward ? 1 : 0;
     switch (H.posts) {
-        case 0: k_syn_post2<0><<<g, NT, sizeof(PostSmem2<0>), L.stream>>>(L.plan, wg); break;
-        case 1: k_syn_post2<1><<<g, NT, sizeof(PostSmem2<1>), L.stream>>>(L.plan, wg); break;
-        default: k_syn_post2<2><<<g, NT, sizeof(PostSmem2<2>), L.stream>>>(L.plan, wg); break;
+        case 0: launch_pdl(k_syn_post2<0>, dim3(g), dim3(NT), sizeof(PostSmem2<0>), L.stream, 's', L.plan, wg); break;
+        case 1: launch_pdl(k_syn_post2<1>, dim3(g), dim3(NT), sizeof(PostSmem2<1>), L.stream, 's', L.plan, wg); break;
+        default: launch_pdl(k_syn_post2<2>, dim3(g), dim3(NT), sizeof(PostSmem2<2>), L.stream, 's', L.plan, wg); break;
     }
 }
 

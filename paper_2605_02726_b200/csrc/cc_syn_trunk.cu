@@ -171,6 +171,8 @@ __global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict
 
     const int64_t np = P.npix;
     const int64_t ntiles = (np + T - 1) / T;
+    pdl_wait();  // dt / dx of the posts kernel (weights above were staged before)
+    pdl_trigger();
     if (blockIdx.x < ntiles) issue_tile(P, dt_in, blockIdx.x, sZ, sDT, sDX, tid);
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         // the next tile's inputs land in the other buffers while this one computes
@@ -362,9 +364,10 @@ size_t tb_smem() {
 
 template <int FP>
 void launch_t(const LaunchCtx& L, const float* dt, int part) {
-    if (part == 1) k_syn_trunk_bwd2<FP, 1><<<L.syn_blocks, NT, tb_smem<FP>(), L.stream>>>(L.plan, dt);
-    else if (part == 2) k_syn_trunk_bwd2<FP, 2><<<L.syn_blocks, NT, tb_smem<FP>(), L.stream>>>(L.plan, dt);
-    else k_syn_trunk_bwd2<FP, 0><<<L.syn_blocks, NT, tb_smem<FP>(), L.stream>>>(L.plan, dt);
+    const dim3 g(L.syn_blocks), b(NT);
+    if (part == 1) launch_pdl(k_syn_trunk_bwd2<FP, 1>, g, b, tb_smem<FP>(), L.stream, 's', L.plan, dt);
+    else if (part == 2) launch_pdl(k_syn_trunk_bwd2<FP, 2>, g, b, tb_smem<FP>(), L.stream, 's', L.plan, dt);
+    else launch_pdl(k_syn_trunk_bwd2<FP, 0>, g, b, tb_smem<FP>(), L.stream, 's', L.plan, dt);
 }
 
 template <int FP>
