@@ -44,6 +44,9 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
     // per-grid gradient-finiteness flags of this iteration (ANDed by k_latent_grad)
     if (blockIdx.x == 0 && threadIdx.x < kMaxGrids) P.lat_ok[threadIdx.x] = 1;
     if (blockIdx.x == 0 && threadIdx.x < kMaxTensors) P.tensor_ok[threadIdx.x] = 1;  // ANDed by k_nn_reduce
+    // programmatic dependent launch: the schedule scalars come from k_sched_load
+    pdl_wait();
+    pdl_trigger();  // the first upsampling stage may become resident
     const float temp = float(P.scal->temp);         // encoder.hpp:98
     const float noise_std = float(P.scal->noise);   // encoder.hpp:108
     const int64_t n = P.n_latents;
@@ -267,7 +270,7 @@ __global__ void k_init_latents(const Plan* __restrict__ pp, uint64_t stream, flo
 
 // ---------------------------------------------------------------------------
 void launch_softq_fwd(const LaunchCtx& L) {
-    k_softq_fwd<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+    launch_pdl(k_softq_fwd, dim3(L.elem_blocks), dim3(256), 0, L.stream, 's', L.plan);
 }
 void launch_quantize(const LaunchCtx& L, int amp) {
     k_quantize<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, amp);
