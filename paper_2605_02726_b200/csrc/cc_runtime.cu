@@ -739,7 +739,9 @@ void Trainer::enqueue_proxy(bool batched) {
     mark(6, false);
     launch_ups_backward(L_, true, 0, 1);
     mark(7, false);
-    CCB_CUDA(cudaStreamWaitEvent(stream_, ev_rate_, 0));
+    // the remaining upsampling-backward stages do not read the rate branch;
+    // the branches that do wait for it themselves (side: its own stream; tail:
+    // below; main: before the coarse-grid gather)
     // The two finest grids (main levels 1, 0: ~93 % of the latents) have all
     // their gradient terms once the first upsampling-backward stage is done:
     // their gather and Adam step run beside the remaining (latency-bound)
@@ -756,6 +758,7 @@ void Trainer::enqueue_proxy(bool batched) {
     launch_nn_reduce(side(), 0, ups_lo);
     launch_nn_reduce(side(), ups_hi, H_.n_params);
     fork(true);
+    if (!serial_branches()) CCB_CUDA(cudaStreamWaitEvent(branch(true), ev_rate_, 0));
     launch_finalize(side(true), kArmProxy, -1);
     launch_latent_grad_grids(side(true), fine, H_.n_grids);
     mark(8, 2);
@@ -766,6 +769,7 @@ void Trainer::enqueue_proxy(bool batched) {
     mark(10, false);
     fork();  // the upsampling-tap reduction beside the coarse-grid gather
     launch_nn_reduce(side(), ups_lo, ups_hi);
+    CCB_CUDA(cudaStreamWaitEvent(stream_, ev_rate_, 0));
     launch_latent_grad_grids(L_, 0, fine);
     mark(11, false);
     // every gather has read the weights: the NN step (side, after its
