@@ -65,8 +65,12 @@ struct A2 {
     static constexpr int O_DH2 = O_DH1 + RDH * LT;
     static constexpr int O_DR = O_DH2 + RDH * LT;
     static constexpr int O_DF = O_DR + RDR * LT;
-    static constexpr int O_HP = O_DF + RF * LT;    // head partials [group][mu|sigma-raw]
-    static constexpr int ACT = O_HP + 8 * LT;
+    // head partials [group][mu|sigma-raw]: written in P3, read in P4b, so
+    // they share dH1's rows (first written in P6); keeps the (32, 20)
+    // variant (cfg4) at two CTAs per SM
+    static constexpr int O_HP = O_DH1;
+    static_assert(RDH >= 8, "head partials fit in the dH1 rows");
+    static constexpr int ACT = O_DF + RF * LT;
     // weight-gradient jobs (4x4 micro-tiles) and units (job x latent third)
     static constexpr int J1 = (WP / 4) * (DP / 4 + 1);   // dH1 x [C|1]
     static constexpr int J2 = (WP / 4) * (WP / 4 + 1);   // dH2 x [H1|1]
