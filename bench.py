@@ -330,7 +330,8 @@ def run_b200(args, rank, world, local_rank):
                "d2h_bytes_per_step": 32,
                "steps": Ke,
                "api": "cc_trainer_upload_image + cc_trainer_enqueue_proxy_iterations (per step: "
-                      "schedule H2D from pinned memory, record D2H to pinned memory) + "
+                      "schedule H2D from pinned memory, record written by the step's last kernel into "
+                      "mapped pinned host memory) + "
                       "cc_trainer_last_records (the path of cc_trainer_train)"}
         # the synchronous per-iteration call (cost returned to the host each step)
         torch.cuda.synchronize(dev)
