@@ -25,6 +25,8 @@
 //     grid) into a second set of buffers while tile t computes.
 #include <cuda_runtime.h>
 
+#include <cstdint>
+
 #pragma nv_diag_suppress 128  // forward-only instantiations skip the backward phases
 
 #include "cc_kernels.h"
@@ -448,16 +450,24 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
                 if (k < S) {
                     if (MODE == kArmProxy) {
                         float* dcp = P.dctx + g.dctx_off + int64_t(k) * count + l0;
-                        if (v0) dcp[0] = acc[n].x;
-                        if (v1) dcp[1] = acc[n].y;
+                        if (v1 && (reinterpret_cast<uintptr_t>(dcp) & 7) == 0) {
+                            *reinterpret_cast<float2*>(dcp) = acc[n];
+                        } else {
+                            if (v0) dcp[0] = acc[n].x;
+                            if (v1) dcp[1] = acc[n].y;
+                        }
                     }
                 } else if (k < S + F && slot >= 0) {
                     const float2 dv = make_float2(v0 ? acc[n].x : 0.0f, v1 ? acc[n].y : 0.0f);
                     *reinterpret_cast<float2*>(sDF + (k - S) * LT + 2 * pr) = dv;
                     if (MODE == kArmProxy) {
                         float* dfp = P.dfeat + g.dfeat_off + int64_t(k - S) * count + l0;
-                        if (v0) dfp[0] = dv.x;
-                        if (v1) dfp[1] = dv.y;
+                        if (v1 && (reinterpret_cast<uintptr_t>(dfp) & 7) == 0) {
+                            *reinterpret_cast<float2*>(dfp) = dv;
+                        } else {
+                            if (v0) dfp[0] = dv.x;
+                            if (v1) dfp[1] = dv.y;
+                        }
                     }
                 }
             }
