@@ -109,6 +109,7 @@ struct alignas(16) A2Smem {
     double acc5[K::NACC5];  // IFCE dW (+db), per slot, fp64
     GridGeom geo[kMaxGrids];
     double red[NT / 32];
+    alignas(16) int4 trec[4];  // tile records two ahead, landed by cp.async with the gathers
 };
 
 template <typename AccT>
@@ -257,7 +258,10 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
     int4 cur = blockIdx.x < ntiles ? tiles[blockIdx.x] : make_int4(0, 0, 0, 0);
     int4 nxt = blockIdx.x + gridDim.x < ntiles ? tiles[blockIdx.x + gridDim.x] : make_int4(0, 0, 0, 0);
     int wb = 0;  // window buffer of the current tile
+    if (tid == 0)  // ring slot of the first tile's record two ahead; later ones by cp.async
+        sm.trec[0] = blockIdx.x + 2 * gridDim.x < ntiles ? tiles[blockIdx.x + 2 * gridDim.x] : make_int4(0, 0, 0, 0);
     if (blockIdx.x < ntiles) issue_gather(P, sm.geo, cur, sm.win[0], tid);
+    int kt = 0;  // tile count of this CTA (ring index)
 
     // persistent weight-gradient accumulators of this thread's units
     double uacc[K::MAXU][16];  // fp64 across tiles: large images sum millions of terms
@@ -270,7 +274,6 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
 
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int4 tile = cur;
-        const int4 nxt2 = t + 2 * int(gridDim.x) < ntiles ? tiles[t + 2 * gridDim.x] : make_int4(0, 0, 0, 0);
         const GridGeom& g = sm.geo[tile.x];
         const int64_t count = int64_t(g.rows) * g.cols;
         const int slot = g.ifce_slot;
@@ -282,12 +285,21 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
 
         // ---- P0: prefetch the next tile (its buffers' last readers finished
         // at the previous tile's closing barrier), land the current one ----
+        if (tid == 0) {  // the record three ahead joins this group (read two tiles from now)
+            const int64_t t3 = int64_t(t) + 3 * int64_t(gridDim.x);
+            const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(&sm.trec[(kt + 1) & 3]));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
+                         "l"(t3 < ntiles ? tiles + t3 : tiles), "r"(t3 < ntiles ? 16 : 0)
+                         : "memory");
+        }
         if (t + int(gridDim.x) < ntiles)
             issue_gather(P, sm.geo, nxt, sm.win[wb ^ 1], tid);
         else
             cp_async_commit();
         asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         __syncthreads();
+        const int4 nxt2 = sm.trec[kt & 3];
+        ++kt;
 
         // ---- P1: context rows from the window, IFCE forward (two threads
         // per latent), constant rows ----
