@@ -55,7 +55,7 @@ def parse_args():
 
 
 def schedule(enc: EncoderConfig, n: int, start: int = 0):
-    """Main-stage scalars of with_total(10000) (config.hpp:301-309)."""
+    """Main-stage scalars of with_total(10000) (config.hpp:114-122)."""
     lr_s, t_s, n_s = enc.schedules()
     its = range(start, start + n)
     return (np.array([lr_s.value(i) for i in its]), np.array([t_s.value(i) for i in its]),
@@ -155,7 +155,7 @@ def run_reference(args, rank, world):
     # each step = one proxy_iteration on every thread (~0.8 s wall); cap the
     # timed steps so the whole arm ends within a couple of minutes
     steps = max(1, min(args.steps, 60))
-    warm = max(0, min(args.warmup, 3))
+    warm = max(0, min(args.warmup, 10))
     secs = cpu_reference_run(h, w, args.preset, args.seed, threads, warm, steps)
     value = threads * steps * h * w / secs / 1e9
     line = {
@@ -163,8 +163,9 @@ def run_reference(args, rank, world):
         "steps": steps, "warmup": warm, "steps_requested": args.steps,
         "ms_per_step": 1e3 * secs / steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": config_dict(args, threads_cpu=threads),
+        "config": config_dict(args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "cpu_model": cpu_model(),
                          "sample": f"{threads} independent detail::Trainer (oracle/_ref, reference "
                                    f"headers, -O3 -ffp-contract=fast) x {steps} proxy_iteration "
                                    f"each after {warm} warm-up, {h}x{w} {args.preset}"},
@@ -173,7 +174,17 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def config_dict(args, threads_cpu=None):
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_dict(args):
     d = {
         "workload": f"cfg2: one {args.height}x{args.width} RGB synthetic image per GPU, "
                     f"{args.preset.upper()} decoder, proxy_iteration (NN params Adam)",
@@ -184,8 +195,6 @@ def config_dict(args, threads_cpu=None):
         "l2": "back-to-back iterations, per-iteration working set ~150 MB > 126 MB L2; "
               "value_l2_flushed = same steps with a 512 MB L2 flush before each",
     }
-    if threads_cpu:
-        d["cpu_threads"] = threads_cpu
     return d
 
 
@@ -222,6 +231,10 @@ def run_b200(args, rank, world, local_rank):
         if rc != 0:
             raise RuntimeError(lib.cc_last_error().decode())
 
+    # one-off setup (batch buffers sized for the largest batch used below, the
+    # batched iteration graph instantiated) happens here, outside every timed region
+    if lib.cc_trainer_reserve_iterations(tr._h, max(W, K)) != 0:
+        raise RuntimeError(lib.cc_last_error().decode())
     enqueue(0, W)
     torch.cuda.synchronize(dev)
     kpi = C.c_int()
@@ -384,7 +397,7 @@ def run_b200(args, rank, world, local_rank):
         try:
             secs = cpu_reference_run(h, w, args.preset, args.seed, threads, 1, iters)
             cpu = {"value": threads * iters * h * w / secs / 1e9, "unit": UNIT, "cores": threads,
-                   "kind": "reference",
+                   "kind": "reference", "cpu_model": cpu_model(),
                    "sample": f"{threads} independent detail::Trainer x {iters} proxy_iteration "
                              f"after 1 warm-up, {h}x{w} {args.preset}, oracle/_ref"}
         except Exception as e:  # noqa: BLE001

@@ -49,7 +49,7 @@ extern "C" {
 #define CC_ERR_CUDA 4
 #define CC_ERR_STATE 5
 
-/* DecoderConfig (config.hpp:227-268).  Presets: "lop", "mop", "hop", "vhop". */
+/* DecoderConfig (config.hpp:40-81).  Presets: "lop", "mop", "hop", "vhop". */
 typedef struct cc_decoder_config {
     int preset; /* 0 lop, 1 mop, 2 hop, 3 vhop (name only) */
     int spatial_ctx;
@@ -62,7 +62,7 @@ typedef struct cc_decoder_config {
     int use_stabilizer;
 } cc_decoder_config;
 
-/* EncoderConfig (config.hpp:280-329). */
+/* EncoderConfig (config.hpp:93-142). */
 typedef struct cc_encoder_config {
     int warmup_candidates;
     int warmup_keep;
@@ -75,14 +75,14 @@ typedef struct cc_encoder_config {
     double hardround_lr;
     double lambda;
     uint64_t seed;
-    int use_soap;           /* must be 0: Adam on the NN params */
+    int use_soap;           /* 1 (reference default, config.hpp:107): SOAP on the NN params; 0: Adam */
     int true_cost_interval;
     const char* log_path;   /* optional per-iteration CSV, NULL/"" = off */
 } cc_encoder_config;
 
 typedef struct cc_layout {
     int height, width;
-    int levels;        /* L, latent_levels() config.hpp:271 */
+    int levels;        /* L, latent_levels() config.hpp:84 */
     int hyper_count;
     int n_grids;
     int64_t n_latents;
@@ -94,12 +94,12 @@ typedef struct cc_layout {
 typedef struct cc_grid_info {
     int level, hyper, rows, cols;
     int64_t offset;    /* into the flat latent layout */
-    int ifce_slot;     /* model.hpp:221-226 (-1 = none) */
+    int ifce_slot;     /* model.hpp:72-77 (-1 = none) */
 } cc_grid_info;
 
 typedef struct cc_param_info {
     char name[32];
-    int rows, cols;    /* MatView::of (tensor.hpp:179-183) */
+    int rows, cols;    /* MatView::of (tensor.hpp:74-78) */
     int64_t size;
     int64_t offset;    /* into the flat parameter layout */
 } cc_param_info;
@@ -122,11 +122,11 @@ const char* cc_last_error(void);
 /* Implementation tag: "b200", "reference" or "port". */
 const char* cc_impl_name(void);
 
-/* DecoderConfig::from_name (config.hpp:253-259). */
+/* DecoderConfig::from_name (config.hpp:66-72). */
 int cc_decoder_config_preset(const char* name, cc_decoder_config* out);
-/* EncoderConfig{} defaults (config.hpp:280-296). */
+/* EncoderConfig{} defaults (config.hpp:93-109). */
 int cc_encoder_config_default(cc_encoder_config* out);
-/* EncoderConfig::with_total (config.hpp:314-328). */
+/* EncoderConfig::with_total (config.hpp:127-141). */
 int cc_encoder_config_with_total(int total, cc_encoder_config* out);
 /* count_macs_per_pixel (synthesis.hpp:239-277): the FLOP convention. */
 double cc_count_macs_per_pixel(const cc_decoder_config* cfg, int h, int w);
@@ -214,6 +214,9 @@ int cc_trainer_candidate_cost(cc_trainer* tr, int slot, double* cost);
 int cc_trainer_set_stream(cc_trainer* tr, void* cuda_stream);
 int cc_trainer_enqueue_proxy_iterations(cc_trainer* tr, int n, const double* lr,
                                         const double* temp, const double* noise_std);
+/* size the batch buffers for n enqueued iterations and instantiate the batched
+ * iteration graph now, so later enqueues of up to n iterations do no setup. */
+int cc_trainer_reserve_iterations(cc_trainer* tr, int n);
 int cc_trainer_synchronize(cc_trainer* tr);
 /* records of the last batched run: 4 doubles per iteration
  * (cost, mse, bits, global_iter after the iteration). */

@@ -49,6 +49,10 @@ int ccb_counter_gauss(uint64_t stream, uint64_t idx0, int n, float* out);
  * Trainer::enqueue_proxy; 0 = start). */
 int ccb_timeline(cc_trainer* tr, int n, double lr, double temp, double noise, double* ms);
 int ccb_soap_state(cc_trainer* tr, double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena);
+/* Load a SOAP state in the same layout (teacher-forced lock-step against the
+ * reference's soap_step, optim.hpp:189-254).  Any input may be NULL. */
+int ccb_soap_set_state(cc_trainer* tr, const double* arena, const float* m1, const float* v2,
+                       const int64_t* t);
 
 #ifdef __cplusplus
 }

@@ -204,7 +204,7 @@ static int add_tensor(cc_trainer* T, const char* name, int rows, int cols) {
 }
 
 static int build(cc_trainer* T, const cc_decoder_config* dec) {
-    T->L = (int64_t)T->H * T->W < 1000000 ? 7 : 8;  /* config.hpp:271 */
+    T->L = (int64_t)T->H * T->W < 1000000 ? 7 : 8;  /* config.hpp:84 */
     T->use_hyper = dec->use_hyperlatents;
     T->hyper = dec->use_hyperlatents ? T->L - 4 : 0;
     T->S = dec->spatial_ctx;
@@ -266,10 +266,10 @@ static int build(cc_trainer* T, const cc_decoder_config* dec) {
         for (int k = 0; k < 3 && k < T->L; ++k) {
             const int gi = T->main_gi[k];
             T->g[gi].slot = T->n_slots;
-            T->g[gi].rdim = T->hyper + T->L - 1 - k;  /* model.hpp:219 */
+            T->g[gi].rdim = T->hyper + T->L - 1 - k;  /* model.hpp:70-71 */
             T->slot_gi[T->n_slots++] = gi;
         }
-    /* make_model (model.hpp:229-272) + for_each_param order */
+    /* make_model (model.hpp:80-123) + for_each_param order */
     char nm[32];
     T->o_l1w = add_tensor(T, "arm.l1.w", T->Wd, T->D);
     T->o_l1b = add_tensor(T, "arm.l1.b", 1, T->Wd);
@@ -953,7 +953,7 @@ static void fresh_candidate(cc_trainer* T, int index) { /* encoder.hpp:82-93 */
 #define KAIMING(off, n, fan) do { const uint64_t s_ = hash_combine(ms, ctr++); \
         const float a_ = sqrtf(6.0f / (float)(fan)); \
         for (int i_ = 0; i_ < (n); ++i_) T->par[(off) + i_] = counter_uniform(s_, (uint64_t)i_, -a_, a_); } while (0)
-    KAIMING(T->o_l1w, T->Wd * T->D, T->D); /* init_model model.hpp:286-305 */
+    KAIMING(T->o_l1w, T->Wd * T->D, T->D); /* init_model model.hpp:137-156 */
     KAIMING(T->o_l2w, T->Wd * T->Wd, T->Wd);
     KAIMING(T->o_hw, 2 * T->Wd, T->Wd);
     for (int s = 0; s < T->n_slots; ++s) {
@@ -999,7 +999,7 @@ int cc_encoder_config_default(cc_encoder_config* o) {
     return CC_OK;
 }
 
-int cc_encoder_config_with_total(int total, cc_encoder_config* o) { /* config.hpp:314-328 */
+int cc_encoder_config_with_total(int total, cc_encoder_config* o) { /* config.hpp:127-141 */
     cc_encoder_config_default(o);
     if (total == 100000) return CC_OK;
     if (total < 20) return fail(CC_ERR_CONFIG, "iteration budget too small");
@@ -1210,6 +1210,7 @@ int cc_trainer_proxy_iterations(cc_trainer* T, int n, const double* lr, const do
 
 int cc_trainer_set_stream(cc_trainer* T, void* s) { (void)T; (void)s; return CC_OK; }
 int cc_trainer_synchronize(cc_trainer* T) { (void)T; return CC_OK; }
+int cc_trainer_reserve_iterations(cc_trainer* T, int n) { (void)T; (void)n; return CC_OK; }
 int cc_trainer_last_records(cc_trainer* T, int n, double* rec) {
     if (n > T->n_records) return fail(CC_ERR_CONFIG, "no such records");
     memcpy(rec, T->records, sizeof(double) * 4 * (size_t)n);
@@ -1340,7 +1341,7 @@ static void warmup(cc_trainer* T) {
 
 int cc_trainer_warmup(cc_trainer* T) { warmup(T); return CC_OK; }
 
-static double sched(double a, double b, int cosine, int hor, int it) { /* config.hpp:210-216 */
+static double sched(double a, double b, int cosine, int hor, int it) { /* config.hpp:23-29 */
     if (it <= 0) return a;
     if (it >= hor) return b;
     const double t = (double)it / hor;

@@ -416,6 +416,7 @@ int cc_trainer_enqueue_proxy_iterations(cc_trainer* t, int n, const double* lr,
 }
 
 int cc_trainer_synchronize(cc_trainer*) { return CC_OK; }
+int cc_trainer_reserve_iterations(cc_trainer*, int) { return CC_OK; }
 
 int cc_trainer_last_records(cc_trainer* t, int n, double* rec) {
     if (size_t(n) * 4 > t->records.size()) return fail(CC_ERR_CONFIG, "no such records");
@@ -718,3 +719,204 @@ int cc_trainer_latent_mu_sigma(cc_trainer* t, const float* params, float* mu, fl
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// fp64 TRUTH of one proxy iteration's gradients (test infrastructure).
+//
+// The reference's compute kernels are templated on the scalar type so its own
+// tests can run them in double (entropy_model.hpp:48-50, mathutil.hpp:49-52:
+// the double overloads of cc_exp/cc_log/cc_tanh are libm).  This evaluates
+// exactly what Trainer::proxy_iteration (encoder.hpp:97-120) computes before
+// its optimiser step — soft-quantise (latent.hpp:118-139), rate_pass
+// (entropy_model.hpp:180-336), upsample_forward/backward (synthesis.hpp:55-139),
+// synthesize_forward/backward (synthesis.hpp:191-233), mse (layers.hpp:643-657)
+// — on the trainer's current state, with every kernel instantiated for
+// double.  The inputs are the same values the float trainer uses (latents,
+// parameters, image, temp / noise_std / rate upstream rounded to float as
+// encoder.hpp:98,64 do); only the arithmetic is wider.  Outputs: latent
+// gradients (flat layout), parameter gradients (for_each_param order) and
+// {cost, mse, bits}.
+// ---------------------------------------------------------------------------
+extern "C" int ccref_truth_grads(cc_trainer* t, double temp, double noise_std, double* lat_grad,
+                                 double* param_grad, double* scalars) {
+    return guarded([&] {
+        auto& cs = t->cur();
+        LatentSet& lat = cs.lat;
+        DecoderModel& m = cs.model;
+        const int H = t->img.h, W = t->img.w;
+        const size_t npix = size_t(H) * W;
+        const ContextOffsets ctx = make_context_offsets(t->dec.spatial_ctx);
+        const double tf = double(float(temp)), nf = double(float(noise_std));
+        const double upstream = double(float(t->enc.lambda / double(npix)));
+
+        // double copies of every parameter tensor (value + grad), by address
+        std::map<const ParamTensor*, std::pair<std::vector<double>, std::vector<double>>> P;
+        std::vector<const ParamTensor*> order;
+        for_each_param(m, [&](ParamTensor& p) {
+            auto& e = P[&p];
+            e.first.assign(p.v.begin(), p.v.end());
+            e.second.assign(p.v.size(), 0.0);
+            order.push_back(&p);
+        });
+        auto V = [&](const ParamTensor& p) -> const double* { return P.at(&p).first.data(); };
+        auto G = [&](const ParamTensor& p) -> double* { return P.at(&p).second.data(); };
+
+        ArmView<double> arm;
+        arm.d = m.arm.input_dim;
+        arm.w = m.arm.width;
+        arm.w1 = V(m.arm.l1.w); arm.b1 = V(m.arm.l1.b);
+        arm.w2 = V(m.arm.l2.w); arm.b2 = V(m.arm.l2.b);
+        arm.w3 = V(m.arm.head.w); arm.b3 = V(m.arm.head.b);
+        arm.stab = m.arm.use_stab ? V(m.arm.stab) : nullptr;
+        arm.dw1 = G(m.arm.l1.w); arm.db1 = G(m.arm.l1.b);
+        arm.dw2 = G(m.arm.l2.w); arm.db2 = G(m.arm.l2.b);
+        arm.dw3 = G(m.arm.head.w); arm.db3 = G(m.arm.head.b);
+        arm.dstab = m.arm.use_stab ? G(m.arm.stab) : nullptr;
+        std::vector<IfceView<double>> ifces;
+        for (auto& p : m.ifce) {
+            IfceView<double> v;
+            v.rdim = p.map.in;
+            v.fdim = p.map.out;
+            v.w = V(p.map.w); v.b = V(p.map.b);
+            v.dw = G(p.map.w); v.db = G(p.map.b);
+            ifces.push_back(v);
+        }
+        std::vector<UpsampleStageView<double>> ups;
+        for (auto& s : m.ups) {
+            UpsampleStageView<double> v;
+            v.k4 = V(s.tconv); v.r3 = V(s.refine);
+            v.dk4 = G(s.tconv); v.dr3 = G(s.refine);
+            ups.push_back(v);
+        }
+        SynthesisView<double> sv;
+        sv.L = m.syn.in_ch;
+        sv.F = m.syn.hidden;
+        sv.posts = int(m.syn.post_w.size());
+        sv.c1w = V(m.syn.c1.w); sv.c1b = V(m.syn.c1.b);
+        sv.c2w = V(m.syn.c2.w); sv.c2b = V(m.syn.c2.b);
+        sv.dc1w = G(m.syn.c1.w); sv.dc1b = G(m.syn.c1.b);
+        sv.dc2w = G(m.syn.c2.w); sv.dc2b = G(m.syn.c2.b);
+        for (int i = 0; i < sv.posts; ++i) {
+            sv.pw[i] = V(m.syn.post_w[i]); sv.pb[i] = V(m.syn.post_b[i]);
+            sv.dpw[i] = G(m.syn.post_w[i]); sv.dpb[i] = G(m.syn.post_b[i]);
+        }
+        sv.stab = m.syn.use_stab ? V(m.syn.stab) : nullptr;
+        sv.dstab = m.syn.use_stab ? G(m.syn.stab) : nullptr;
+
+        // soft-quantise every grid into its padded double plane
+        const int pad = std::max(1, ctx.pad);
+        const size_t ng = lat.grids.size();
+        std::vector<PaddedGrid<double>> pads(ng);
+        std::vector<std::vector<double>> y(ng), th1(ng), th2(ng);
+        std::vector<int> slots(ng);
+        const uint64_t gi_iter = uint64_t(t->tr->global_iter);
+        for (size_t gi = 0; gi < ng; ++gi) {
+            auto& g = lat.grids[gi];
+            pads[gi].resize(g.rows, g.cols, pad, g.level, g.hyper);
+            y[gi].assign(g.y.v.begin(), g.y.v.end());
+            th1[gi].assign(g.count(), 0.0);
+            th2[gi].assign(g.count(), 0.0);
+            slots[gi] = g.hyper ? -1 : m.ifce_slot(g.level);
+            const uint64_t stream = hash_combine(hash_combine(t->enc.seed, gi_iter), gi);  // encoder.hpp:213-215
+            for (int r = 0; r < g.rows; ++r) {
+                const size_t o = size_t(r) * g.cols;
+                soft_quantize_forward(y[gi].data() + o, pads[gi].v_at(r, 0), th1[gi].data() + o,
+                                      th2[gi].data() + o, size_t(g.cols), tf, nf, stream, o);
+            }
+        }
+        const double bits = rate_pass(pads, ctx, arm, ifces, slots, lat.hyper_count, upstream, true);
+
+        const int L = lat.levels;
+        std::vector<PlaneRef<double>> mains(L);
+        std::vector<PlaneGrad<double>> dmains(L);
+        for (int k = 0; k < L; ++k) {
+            auto& p = pads[lat.main_index(k)];
+            mains[k] = {p.v_at(0, 0), p.stride(), p.rows, p.cols};
+            dmains[k] = {p.g_at(0, 0), p.stride()};
+        }
+        std::vector<double> z(size_t(L) * npix, 0.0), dz(z.size(), 0.0), xhat(3 * npix, 0.0),
+            dx(3 * npix, 0.0), img(t->img.pix.begin(), t->img.pix.end());
+        UpsampleCache<double> ucache;
+        SynthCache<double> scache;
+        upsample_forward(mains, H, W, ups, z.data(), &ucache);
+        synthesize_forward(z.data(), L, H, W, sv, xhat.data(), &scache);
+        const double mse = mse_forward(xhat.data(), img.data(), xhat.size());
+        mse_backward(xhat.data(), img.data(), 1.0, dx.data(), xhat.size());
+        synthesize_backward(z.data(), L, H, W, sv, scache, dx.data(), dz.data());
+        upsample_backward(mains, H, W, ups, ucache, dz.data(), dmains);
+
+        size_t off = 0;
+        for (size_t gi = 0; gi < ng; ++gi) {
+            auto& g = lat.grids[gi];
+            std::vector<double> dy(g.count(), 0.0);
+            for (int r = 0; r < g.rows; ++r) {
+                const size_t o = size_t(r) * g.cols;
+                soft_quantize_backward(pads[gi].g_at(r, 0), th1[gi].data() + o, th2[gi].data() + o,
+                                       dy.data() + o, size_t(g.cols), tf);
+            }
+            if (lat_grad) std::copy(dy.begin(), dy.end(), lat_grad + off);
+            off += g.count();
+        }
+        size_t po = 0;
+        for (const ParamTensor* p : order) {
+            const auto& gr = P.at(p).second;
+            if (param_grad) std::copy(gr.begin(), gr.end(), param_grad + po);
+            po += gr.size();
+        }
+        if (scalars) {
+            scalars[0] = rd_loss(mse, bits / double(npix), t->enc.lambda);
+            scalars[1] = mse;
+            scalars[2] = bits;
+        }
+        return CC_OK;
+    });
+}
+
+// ---------------------------------------------------------------------------
+// The reference's SOAP state (optim.hpp:122-141, NnOptimizer::soap) in the
+// layout of the product's ccb_soap_state (include/coolchic_b200_diag.h): per
+// tensor in for_each_param order L (r x r), R (c x c), QL, QR as doubles; m1,
+// v2 flat fp32; step counts.  Test infrastructure for the SOAP lock-step.
+// ---------------------------------------------------------------------------
+extern "C" int ccb_soap_state(cc_trainer* t, double* arena, float* m1, float* v2, int64_t* steps,
+                              int64_t* n_arena) {
+    return guarded([&] {
+        auto& nn = t->cur().nn;
+        if (!nn.use_soap) throw ConfigError("not a SOAP trainer (use_soap = false)");
+        size_t a = 0, o = 0;
+        for (size_t i = 0; i < nn.soap.size(); ++i) {
+            const SoapState& s = nn.soap[i];
+            for (const auto* v : {&s.lpre, &s.rpre, &s.ql, &s.qr}) {
+                if (arena) std::copy(v->begin(), v->end(), arena + a);
+                a += v->size();
+            }
+            if (m1) std::copy(s.m1.begin(), s.m1.end(), m1 + o);
+            if (v2) std::copy(s.v2.begin(), s.v2.end(), v2 + o);
+            o += s.m1.size();
+            if (steps) steps[i] = s.t;
+        }
+        if (n_arena) *n_arena = int64_t(a);
+        return CC_OK;
+    });
+}
+
+extern "C" int ccb_soap_set_state(cc_trainer* t, const double* arena, const float* m1, const float* v2,
+                                  const int64_t* steps) {
+    return guarded([&] {
+        auto& nn = t->cur().nn;
+        if (!nn.use_soap) throw ConfigError("not a SOAP trainer (use_soap = false)");
+        size_t a = 0, o = 0;
+        for (size_t i = 0; i < nn.soap.size(); ++i) {
+            SoapState& s = nn.soap[i];
+            for (auto* v : {&s.lpre, &s.rpre, &s.ql, &s.qr}) {
+                if (arena) std::copy(arena + a, arena + a + v->size(), v->begin());
+                a += v->size();
+            }
+            if (m1) std::copy(m1 + o, m1 + o + s.m1.size(), s.m1.begin());
+            if (v2) std::copy(v2 + o, v2 + o + s.v2.size(), s.v2.begin());
+            o += s.m1.size();
+            if (steps) s.t = steps[i];
+        }
+        return CC_OK;
+    });
+}

@@ -33,7 +33,7 @@ from .trainer import ConfigError, DecoderConfig, EncoderConfig, Trainer, _check
 
 
 def latent_levels(h: int, w: int) -> int:
-    """config.hpp:271: 7 levels below 1 Mpx, else 8."""
+    """config.hpp:84: 7 levels below 1 Mpx, else 8."""
     return 7 if h * w < 1_000_000 else 8
 
 

@@ -152,6 +152,7 @@ SIGNATURES = {
     "cc_trainer_train": (C.c_int, [_P, C.POINTER(TrainStatsC), _F, _I32, _F]),
     "cc_trainer_set_stream": (C.c_int, [_P, C.c_void_p]),
     "cc_trainer_enqueue_proxy_iterations": (C.c_int, [_P, C.c_int, _D, _D, _D]),
+    "cc_trainer_reserve_iterations": (C.c_int, [_P, C.c_int]),
     "cc_trainer_synchronize": (C.c_int, [_P]),
     "cc_trainer_last_records": (C.c_int, [_P, C.c_int, _D]),
 }
@@ -191,6 +192,7 @@ DIAG_SIGNATURES = {
     "ccb_counter_gauss": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, _F]),
     "ccb_timeline": (C.c_int, [_P, C.c_int, C.c_double, C.c_double, C.c_double, _D]),
     "ccb_soap_state": (C.c_int, [_P, _D, _F, _F, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "ccb_soap_set_state": (C.c_int, [_P, _D, _F, _F, C.POINTER(C.c_int64)]),
 }
 
 

@@ -594,40 +594,19 @@ static void configure_t() {
     cudaFuncSetAttribute(k_arm<DP, WP, kArmProxy>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
-// Opt in to > 48 KB dynamic shared memory on the CURRENT device.
-// The register-tiled kernel (cc_arm2.cu) is the default for every variant it
-// instantiates; CCB_ARM_V1=1 selects this per-latent kernel (A/B comparison).
+// The register-tiled kernel (cc_arm2.cu) runs every variant it instantiates;
+// this per-latent kernel is the fallback for the wide ARMs it does not.
 bool arm2_supported(int Dp, int Wp);
 size_t arm2_smem_bytes(int Dp, int Wp);
 void arm2_configure(int Dp, int Wp);
 void launch_arm2(const LaunchCtx& L, int mode);
 
-bool arm3_supported(int Dp, int Wp);
-size_t arm3_smem_bytes(int Dp, int Wp);
-void arm3_configure(int Dp, int Wp);
-void launch_arm3(const LaunchCtx& L, int mode);
+static bool use_arm2(int Dp, int Wp) { return arm2_supported(Dp, Wp); }
 
-static int arm_env_version() {  // CCB_ARM_V1=1 / CCB_ARM_V3=1: A/B against the default (2)
-    static const int v = [] {
-        const char* e1 = std::getenv("CCB_ARM_V1");
-        const char* e3 = std::getenv("CCB_ARM_V3");
-        if (e1 && e1[0] == '1') return 1;
-        if (e3 && e3[0] == '1') return 3;
-        return 2;
-    }();
-    return v;
-}
-// the tensor-core kernel (cc_arm3.cu) on request: measured slower than the
-// FFMA2 tile kernel at 512x768 (278 vs 265 us, 99 M vs 76 M warp instructions)
-static bool use_arm3(int Dp, int Wp) { return arm_env_version() == 3 && arm3_supported(Dp, Wp); }
-static bool use_arm2(int Dp, int Wp) { return !use_arm3(Dp, Wp) && arm_env_version() >= 2 && arm2_supported(Dp, Wp); }
-
-// both tiled kernels stage the same (P+1)-row window (row bands, halo <= 4)
-bool arm_uses_v2(int Dp, int Wp) { return use_arm3(Dp, Wp) || use_arm2(Dp, Wp); }
-bool arm_uses_v3(int Dp, int Wp) { return use_arm3(Dp, Wp); }
+// the tiled kernel stages a (P+1)-row window (row bands, halo <= 4)
+bool arm_uses_v2(int Dp, int Wp) { return use_arm2(Dp, Wp); }
 
 void arm_configure(int Dp, int Wp) {
-    if (use_arm3(Dp, Wp)) arm3_configure(Dp, Wp);
     if (use_arm2(Dp, Wp)) arm2_configure(Dp, Wp);
     if (Dp == 8 && Wp == 8) configure_t<8, 8>();
     else if (Dp == 16 && Wp == 12) configure_t<16, 12>();
@@ -649,7 +628,6 @@ static void launch_arm_mode(const LaunchCtx& L, int mode) {
 
 void launch_arm(const LaunchCtx& L, int mode) {
     const int Dp = L.host->Dp, Wp = L.host->Wp;
-    if (use_arm3(Dp, Wp)) return launch_arm3(L, mode);
     if (use_arm2(Dp, Wp)) return launch_arm2(L, mode);
     if (Dp == 8 && Wp == 8) launch_arm_mode<8, 8>(L, mode);
     else if (Dp == 16 && Wp == 12) launch_arm_mode<16, 12>(L, mode);
@@ -660,10 +638,6 @@ void launch_arm(const LaunchCtx& L, int mode) {
 }
 
 int arm_blocks_per_sm(int Dp, int Wp) {
-    if (use_arm3(Dp, Wp)) {  // __launch_bounds__(256, 2)
-        const int b = int((227 * 1024) / (arm3_smem_bytes(Dp, Wp) + 1024));
-        return b < 1 ? 1 : (b > 2 ? 2 : b);
-    }
     if (use_arm2(Dp, Wp)) {  // __launch_bounds__(128, 2)
         const int b = int((227 * 1024) / (arm2_smem_bytes(Dp, Wp) + 1024));
         return b < 1 ? 1 : (b > 2 ? 2 : b);

@@ -53,7 +53,7 @@ int guarded(F&& f) {
     }
 }
 
-// Schedule::value (config.hpp:210-216)
+// Schedule::value (config.hpp:23-29)
 double sched_value(double start, double end, bool cosine, int horizon, int iter) {
     if (iter <= 0) return start;
     if (iter >= horizon) return end;
@@ -208,7 +208,8 @@ void train(Trainer& tr, cc_train_stats* out) {
         }
         if (bad >= 0) {
             // encoder.hpp:365-372 — the later iterations of the chunk were
-            // no-ops (a non-finite cost leaves every state untouched)
+            // no-ops: k_finalize's sticky halt flag stops every step and
+            // counter update after the first non-finite cost of a batch
             if (st.restarts >= 2) break;
             ++st.restarts;
             lr_scale *= 0.5;
@@ -255,7 +256,7 @@ const char* cc_impl_name(void) { return "b200"; }
 
 int cc_decoder_config_preset(const char* name, cc_decoder_config* out) {
     const std::string n = name ? name : "";
-    // DecoderConfig::lop/mop/hop/vhop (config.hpp:240-243)
+    // DecoderConfig::lop/mop/hop/vhop (config.hpp:53-56)
     if (n == "lop") *out = {0, 6, 2, 8, 2, 8, 1, 1, 1};
     else if (n == "mop") *out = {1, 10, 4, 10, 2, 16, 2, 1, 1};
     else if (n == "hop") *out = {2, 14, 6, 20, 2, 48, 2, 1, 1};
@@ -574,6 +575,13 @@ int cc_trainer_enqueue_proxy_iterations(cc_trainer* t, int n, const double* lr,
     });
 }
 
+int cc_trainer_reserve_iterations(cc_trainer* t, int n) {
+    return guarded([&] {
+        t->tr->reserve_iterations(n);
+        return CC_OK;
+    });
+}
+
 int cc_trainer_synchronize(cc_trainer* t) {
     return guarded([&] {
         t->tr->synchronize();
@@ -653,6 +661,14 @@ int ccb_timeline(cc_trainer* t, int n, double lr, double temp, double noise, dou
 int ccb_soap_state(cc_trainer* t, double* arena, float* m1, float* v2, int64_t* steps, int64_t* n_arena) {
     return guarded([&] {
         t->tr->soap_state(arena, m1, v2, steps, n_arena);
+        return CC_OK;
+    });
+}
+
+int ccb_soap_set_state(cc_trainer* t, const double* arena, const float* m1, const float* v2,
+                       const int64_t* steps) {
+    return guarded([&] {
+        t->tr->set_soap_state(arena, m1, v2, steps);
         return CC_OK;
     });
 }

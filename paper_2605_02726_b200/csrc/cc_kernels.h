@@ -7,6 +7,8 @@
 
 namespace ccb {
 
+void cuda_check(cudaError_t e, const char* what);  // throws CudaError (cc_runtime.cu)
+
 struct LaunchCtx {
     const Plan* plan;      // device copy
     const Plan* host;      // host copy (same pointers)
@@ -43,7 +45,7 @@ inline void launch_pdl(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cuda
     cfg.stream = st;
     cfg.attrs = at;
     cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, k, static_cast<P>(args)...);
+    cuda_check(cudaLaunchKernelEx(&cfg, k, static_cast<P>(args)...), "cudaLaunchKernelEx");
 }
 
 enum ArmMode { kArmForward = 0, kArmHard = 1, kArmProxy = 2 };
@@ -69,7 +71,6 @@ void launch_pyramid(const LaunchCtx& L);
 int arm_blocks_per_sm(int Dp, int Wp);
 void arm_configure(int Dp, int Wp);
 bool arm_uses_v2(int Dp, int Wp);
-bool arm_uses_v3(int Dp, int Wp);  // the tensor-core kernel (cc_arm3.cu): fp64 quarter rows per CTA (Plan::arm_qs)
 void pyramid_configure(const Plan& H);
 
 // upsampling (cc_ups.cu)

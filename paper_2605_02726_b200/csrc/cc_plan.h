@@ -39,7 +39,7 @@ constexpr int kSynTile = 128;  // pixels per trunk-backward tile == threads per 
 struct GridGeom {
     int level, hyper, rows, cols;
     int stride;          // padded row stride, cols + 2P
-    int ifce_slot;       // -1 when unequipped (model.hpp:221-226)
+    int ifce_slot;       // -1 when unequipped (model.hpp:72-77)
     int rdim;            // IFCE source count for equipped grids
     int main_level;      // level if main grid, -1 if hyper
     int64_t pad_base;    // offset of element (0,0) inside yhat_pad
@@ -169,7 +169,6 @@ struct Plan {
     float* nn_m;
     float* nn_v;
     double* partials;
-    double* arm_qs;           // cc_arm3: the four latent-quarter rows of every ARM CTA (4 x arm CTAs x ARM params)
     double* bc_lat;           // per grid Adam bias corrections (2 per grid)
     double* bits_part;
     double* mse_part;
@@ -188,7 +187,7 @@ struct DevScalars {
     int cost_ok;              // isfinite(cost)
     int skipped;              // skipped_steps (encoder.hpp:72)
     int snap_take;            // hardround: take the pre-step snapshot
-    int pad0;
+    int halt;                 // set by a non-finite proxy cost: the rest of the batch are no-ops
     int64_t global_iter;      // encoder.hpp:71; keys the noise stream
     int64_t sched_pos;        // batched runs: index into the schedule arrays
     int64_t noise_iter;       // global_iter the noise_buf values belong to (-1: none)

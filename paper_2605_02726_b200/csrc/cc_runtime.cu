@@ -1,5 +1,5 @@
 // cc_runtime.cu — the B200 Trainer: geometry (build_latents latent.hpp:46-70,
-// make_model model.hpp:229-272, make_context_offsets entropy_model.hpp:24-45),
+// make_model model.hpp:80-123, make_context_offsets entropy_model.hpp:24-45),
 // one device arena per image, and the per-iteration launch sequences captured
 // once into CUDA graphs and replayed (no host work per kernel).
 #include "cc_runtime.h"
@@ -33,7 +33,7 @@ constexpr int kArmTileHost = kArmTile;
 constexpr int kRMaxHost = 12;
 constexpr int kFMaxHost = 8;
 constexpr int kSnapSlots = 8;
-constexpr float kBicubic[4] = {-0.0234375f, -0.0703125f, 0.2265625f, 0.8671875f};  // model.hpp:276
+constexpr float kBicubic[4] = {-0.0234375f, -0.0703125f, 0.2265625f, 0.8671875f};  // model.hpp:127
 
 int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -184,7 +184,7 @@ void Trainer::build_plan() {
     Plan& P = H_;
     const int h = P.H, w = P.W;
     const int hg = band_.on ? band_.hg : h;           // global image rows
-    P.L = int64_t(hg) * int64_t(w) < 1000000 ? 7 : 8;  // latent_levels, config.hpp:271
+    P.L = int64_t(hg) * int64_t(w) < 1000000 ? 7 : 8;  // latent_levels, config.hpp:84
     P.hyper = dec_.use_hyperlatents ? P.L - 4 : 0;     // kHyperCoarsestLevel = 4
     P.S = dec_.spatial_ctx;
     P.F = dec_.ifce_dim;
@@ -278,7 +278,7 @@ void Trainer::build_plan() {
         P.pix_own_hi = g0.own_hi;
     }
 
-    // ---- IFCE slots (model.hpp:244-251): main levels 0..min(3,L)-1 ----
+    // ---- IFCE slots (model.hpp:94-101): main levels 0..min(3,L)-1 ----
     P.n_slots = 0;
     int64_t df_cur = 0;
     if (P.F > 0) {
@@ -287,7 +287,7 @@ void Trainer::build_plan() {
             const int gi = P.main_gi[k];
             GridGeom& g = P.g[gi];
             g.ifce_slot = s;
-            g.rdim = P.hyper + (P.L - 1 - k);  // ifce_source_count, model.hpp:219
+            g.rdim = P.hyper + (P.L - 1 - k);  // ifce_source_count, model.hpp:70-71
             if (g.rdim > kRMaxHost) throw ConfigError("IFCE source count exceeds 12");
             if (g.rdim != gi) throw ConfigError("internal: IFCE sources must precede the grid");
             grids_[gi].ifce_slot = s;
@@ -545,9 +545,6 @@ void Trainer::allocate() {
     P.nn_m = f32(P.n_params);
     P.nn_v = f32(P.n_params);
     P.partials = static_cast<double*>(dalloc(sizeof(double) * size_t(sizes_.partials)));
-    P.arm_qs = arm_uses_v3(P.Dp, P.Wp)
-                   ? static_cast<double*>(dalloc(sizeof(double) * 4 * size_t(L_.arm_blocks) * size_t(P.arm_nvals)))
-                   : nullptr;
     P.bc_lat = static_cast<double*>(dalloc(sizeof(double) * 2 * kMaxGrids));
     P.bits_part = static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_bits_part)));
     P.mse_part = static_cast<double*>(dalloc(sizeof(double) * size_t(P.n_mse_part)));
@@ -596,7 +593,7 @@ void Trainer::zero_pads() {
     CCB_CUDA(cudaMemsetAsync(H_.yhat_pad, 0, sizeof(float) * size_t(sizes_.pad), stream_));
 }
 
-// init_model (model.hpp:286-305) — host side, bit-exact with the reference's
+// init_model (model.hpp:137-156) — host side, bit-exact with the reference's
 // contracted counter_uniform.
 void Trainer::init_params_host(uint64_t stream, std::vector<float>& out) const {
     const Plan& P = H_;
@@ -846,7 +843,7 @@ void Trainer::enqueue_true_cost() {
     launch_finalize(L_, kArmForward, -1);
 }
 
-void Trainer::run_graph(int which, int slot) {
+cudaGraphExec_t Trainer::ensure_graph(int which, int slot) {
     const int key = which == 3 ? 100 + slot : which;
     auto it = graphs_.find(key);
     if (it == graphs_.end()) {
@@ -862,7 +859,11 @@ void Trainer::run_graph(int which, int slot) {
         cudaGraphDestroy(g);
         it = graphs_.emplace(key, ex).first;
     }
-    CCB_CUDA(cudaGraphLaunch(it->second, stream_));
+    return it->second;
+}
+
+void Trainer::run_graph(int which, int slot) {
+    CCB_CUDA(cudaGraphLaunch(ensure_graph(which, slot), stream_));
 }
 
 void Trainer::read_scalars() {
@@ -878,6 +879,7 @@ double Trainer::proxy_iteration(double lr, double temp, double noise_std) {
     h_scal_->noise = noise_std;
     CCB_CUDA(cudaMemcpyAsync(&H_.scal->lr, &h_scal_->lr, 3 * sizeof(double),
                              cudaMemcpyHostToDevice, stream_));
+    CCB_CUDA(cudaMemsetAsync(&H_.scal->halt, 0, sizeof(int), stream_));
     run_graph(0);
     read_scalars();
     last_mse_ = h_scal_->mse;
@@ -946,6 +948,7 @@ double Trainer::band_finish(const double* nn_sums, double bits, double se, int* 
                              cudaMemcpyHostToDevice, stream_));
     CCB_CUDA(cudaMemcpyAsync(&H_.scal->cost_ok, &h_scal_->cost_ok, sizeof(int),
                              cudaMemcpyHostToDevice, stream_));
+    CCB_CUDA(cudaMemsetAsync(&H_.scal->halt, 0, sizeof(int), stream_));  // bands: the global cost decides
     launch_band_own_finite(L_);
     std::vector<int> lo(kMaxGrids);
     CCB_CUDA(cudaMemcpyAsync(lo.data(), H_.lat_ok, sizeof(int) * kMaxGrids, cudaMemcpyDeviceToHost,
@@ -1031,10 +1034,8 @@ void Trainer::set_stream(cudaStream_t s) {
     L_.stream = stream_;
 }
 
-void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* temp,
-                                       const double* noise) {
+void Trainer::reserve_iterations(int n) {
     require_loaded();
-    if (n <= 0) return;
     CCB_CUDA(cudaSetDevice(device_));
     if (n > sched_cap_) {
         synchronize();
@@ -1048,12 +1049,20 @@ void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* te
         if (h_sched_) cudaFreeHost(h_sched_);
         CCB_CUDA(cudaMallocHost(&h_sched_, sizeof(double) * 3 * size_t(n)));
         sched_cap_ = n;
-        auto it = graphs_.find(1);
+        auto it = graphs_.find(1);  // the batched graph bakes in d_sched_ / d_rec_
         if (it != graphs_.end()) {
             cudaGraphExecDestroy(it->second);
             graphs_.erase(it);
         }
     }
+    ensure_graph(1);
+}
+
+void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* temp,
+                                       const double* noise) {
+    require_loaded();
+    if (n <= 0) return;
+    reserve_iterations(n);  // no-op once sized: buffers and the graph are reused
     CCB_CUDA(cudaEventSynchronize(ev_sched_));  // the previous batch's upload has left h_sched_
     for (int i = 0; i < n; ++i) {  // the schedule goes up from pinned memory
         h_sched_[3 * i] = lr[i];
@@ -1064,6 +1073,7 @@ void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* te
                              stream_));
     CCB_CUDA(cudaEventRecord(ev_sched_, stream_));
     CCB_CUDA(cudaMemsetAsync(&H_.scal->sched_pos, 0, sizeof(int64_t), stream_));
+    CCB_CUDA(cudaMemsetAsync(&H_.scal->halt, 0, sizeof(int), stream_));
     // every iteration's record (cost, mse, bits, global_iter) is written by
     // the iteration's last kernel into mapped pinned host memory, without a
     // host synchronisation or a copy between the graphs
@@ -1430,6 +1440,21 @@ void Trainer::soap_state(double* arena, float* m1, float* v2, int64_t* t, int64_
     if (t)
         CCB_CUDA(cudaMemcpyAsync(t, H_.nn_t, sizeof(int64_t) * size_t(H_.n_tensors),
                                  cudaMemcpyDeviceToHost, stream_));
+    synchronize();
+}
+
+void Trainer::set_soap_state(const double* arena, const float* m1, const float* v2, const int64_t* t) {
+    require_loaded();
+    if (!H_.use_soap) throw ConfigError("not a SOAP trainer (use_soap = false)");
+    const size_t np = size_t(H_.n_params);
+    if (arena)
+        CCB_CUDA(cudaMemcpyAsync(H_.soap, arena, sizeof(double) * size_t(sizes_.soap),
+                                 cudaMemcpyHostToDevice, stream_));
+    if (m1) CCB_CUDA(cudaMemcpyAsync(H_.nn_m, m1, sizeof(float) * np, cudaMemcpyHostToDevice, stream_));
+    if (v2) CCB_CUDA(cudaMemcpyAsync(H_.nn_v, v2, sizeof(float) * np, cudaMemcpyHostToDevice, stream_));
+    if (t)
+        CCB_CUDA(cudaMemcpyAsync(H_.nn_t, t, sizeof(int64_t) * size_t(H_.n_tensors),
+                                 cudaMemcpyHostToDevice, stream_));
     synchronize();
 }
 

@@ -77,6 +77,9 @@ public:
     void proxy_iterations(int n, const double* lr, const double* temp, const double* noise,
                           double* rec);
     void enqueue_proxy_iterations(int n, const double* lr, const double* temp, const double* noise);
+    // size the batch buffers for n iterations and instantiate the batched graph
+    // (one-off setup kept out of enqueue_proxy_iterations' steady state)
+    void reserve_iterations(int n);
     void last_records(int n, double* rec);
     void set_stream(cudaStream_t s);
     void profile_stages(int n, double lr, double temp, double noise, double* ms);
@@ -121,6 +124,7 @@ public:
                    float* nv, int64_t* nt);
     void get_grads(float* lg, float* pg);
     void soap_state(double* arena, float* m1, float* v2, int64_t* t, int64_t* n_arena);
+    void set_soap_state(const double* arena, const float* m1, const float* v2, const int64_t* t);
     void set_q(const int32_t* q);
     void decode_terms(const float* params, int which, double* bits, double* mse);
     // (mu, sigma) of every quantised latent, params substituted (NULL: own)
@@ -153,6 +157,7 @@ private:
     void enqueue_hardround(int slot);
     void enqueue_true_cost();
     void run_graph(int which, int slot = -1);
+    cudaGraphExec_t ensure_graph(int which, int slot = -1);
     void read_scalars();
     void ensure_snapshot(int slot);
     void zero_pads();

@@ -45,8 +45,13 @@ __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, i
     DevScalars* s = P.scal;
     s->bits = bits;
     s->mse = mse;
-    s->cost = cost;
-    s->cost_ok = isfinite(cost) ? 1 : 0;
+    // once a proxy iteration of a batch came out non-finite, the remaining
+    // iterations of the batch take no step and advance no counter (train()
+    // restarts from the record of the first bad one, encoder.hpp:365-371)
+    const bool halted = mode == kArmProxy && s->halt;
+    s->cost = halted ? __longlong_as_double(0x7ff8000000000000LL) : cost;
+    s->cost_ok = (!halted && isfinite(cost)) ? 1 : 0;
+    if (mode == kArmProxy && !s->cost_ok) s->halt = 1;
     s->snap_take = (snap_slot >= 0 && s->cost_ok && cost < s->snap_cost[snap_slot]) ? 1 : 0;
 }
 

@@ -3,7 +3,7 @@
 Names, argument meaning and error behaviour follow
 ``coolcodec::detail::Trainer`` (encoder.hpp:59-306), ``warmup``
 (encoder.hpp:315-342), ``train`` (encoder.hpp:349-413) and the config structs
-(config.hpp:204-329).  The heavy lifting happens behind the C ABI: in the B200
+(config.hpp:17-142).  The heavy lifting happens behind the C ABI: in the B200
 library every call below runs sm_100a kernels; the host loop of ``train`` runs
 in that library's C++ runtime.  This module only marshals numpy buffers.
 """
@@ -63,7 +63,7 @@ def _ip(a: np.ndarray | None, t=C.c_int64):
 
 @dataclass
 class DecoderConfig:
-    """config.hpp:227-268 (default = HOP)."""
+    """config.hpp:40-81 (default = HOP)."""
 
     preset: int = 2
     spatial_ctx: int = 14
@@ -114,7 +114,7 @@ class DecoderConfig:
 
 @dataclass
 class EncoderConfig:
-    """config.hpp:280-329 (``lambda`` is spelled ``lmbda``)."""
+    """config.hpp:93-142 (``lambda`` is spelled ``lmbda``)."""
 
     warmup_candidates: int = 5
     warmup_keep: int = 2
@@ -130,7 +130,7 @@ class EncoderConfig:
     hardround_lr: float = 1e-4
     lmbda: float = 0.001
     seed: int = 0
-    use_soap: bool = False  # Adam on the NN params on both sides
+    use_soap: bool = True  # the reference default (config.hpp:107); benchmarks and parity runs clear it
     true_cost_interval: int = 1000
     log_path: str = ""
 
@@ -142,7 +142,7 @@ class EncoderConfig:
 
     @staticmethod
     def with_total(total: int) -> "EncoderConfig":
-        """EncoderConfig::with_total (config.hpp:314-328)."""
+        """EncoderConfig::with_total (config.hpp:127-141)."""
         cfg = EncoderConfig()
         if total == EncoderConfig().total_iters():
             return cfg
@@ -183,7 +183,7 @@ def _lround(x: float) -> int:
 
 @dataclass
 class Schedule:
-    """Schedule::value (config.hpp:204-217)."""
+    """Schedule::value (config.hpp:17-30)."""
 
     start: float
     end: float

@@ -16,10 +16,14 @@ def main(out: str, h: int, w: int, iters: int) -> None:
 
     lib = capi.load_product()
     img = make_synthetic_image(h, w, 3, lib)
-    enc = EncoderConfig(lmbda=1e-3, seed=5)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=5)
     with Trainer(img, enc, DecoderConfig.hop(), lib=lib) as tr:
         tr.fresh_candidate(0)
-        costs = [tr.proxy_iteration(1e-2, 0.35, 0.22) for _ in range(iters)]
+        # the batched path (graph 1: schedule load, PDL into the soft-quantiser,
+        # records into mapped host memory) that bench.py and train() use,
+        # then one synchronous iteration (graph 0)
+        costs = list(tr.proxy_iterations(np.full(iters - 1, 1e-2), 0.35, 0.22))
+        costs.append(tr.proxy_iteration(1e-2, 0.35, 0.22))
         st = tr.get_state()
         lg, pg = tr.get_grads()
     np.savez(out, costs=np.array(costs), latents=st["latents"], params=st["params"], lat_m=st["lat_m"],

@@ -57,7 +57,7 @@ def decoder_of(g):
 def replay(lib, name, iters=3) -> Report:
     g = load_case(name)
     h, w, seed = (int(x) for x in g["meta"])
-    enc = EncoderConfig(lmbda=float(g["lambda"]), seed=seed)
+    enc = EncoderConfig(use_soap=False, lmbda=float(g["lambda"]), seed=seed)
     rep = Report()
     with Trainer(g["image"], enc, decoder_of(g), lib=lib) as tr:
         tr.fresh_candidate(0)

@@ -40,3 +40,26 @@ def load_port():
     if not PORT_SO.exists():
         raise FileNotFoundError(f"{PORT_SO} missing: run `make -C oracle port`")
     return capi.load_library(PORT_SO)
+
+
+def truth_grads(ref_lib, tr, temp: float, noise_std: float):
+    """fp64 truth of the proxy-iteration gradients on `tr`'s current state
+    (a Trainer over the reference checker; oracle/ref_capi.cpp
+    ccref_truth_grads: the reference's own templated kernels instantiated
+    for double).  Returns (latent_grads, param_grads, [cost, mse, bits])."""
+    import ctypes as C
+
+    import numpy as np
+
+    fn = ref_lib.ccref_truth_grads
+    fn.restype = C.c_int
+    fn.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                   C.POINTER(C.c_double)]
+    lg = np.empty(tr.n_latents, np.float64)
+    pg = np.empty(tr.n_params, np.float64)
+    sc = np.empty(3, np.float64)
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    rc = fn(tr._h, temp, noise_std, dp(lg), dp(pg), dp(sc))
+    if rc != 0:
+        raise RuntimeError(ref_lib.cc_last_error().decode())
+    return lg, pg, sc

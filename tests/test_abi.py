@@ -143,7 +143,7 @@ def test_trainer_create_without_gpu_fails_loudly(product_lib):
     except Exception:  # noqa: BLE001
         pass
     img = np.zeros((3, 8, 8), np.float32)
-    ec, dc = EncoderConfig().to_c(), DecoderConfig.hop().to_c()
+    ec, dc = EncoderConfig(use_soap=False).to_c(), DecoderConfig.hop().to_c()
     h = C.c_void_p()
     rc = product_lib.cc_trainer_create(img.ctypes.data_as(capi._F), 8, 8, C.byref(ec), C.byref(dc),
                                        0, C.byref(h))

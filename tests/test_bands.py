@@ -178,7 +178,7 @@ def test_gloo_band_exchange(world, h, w):
 # ------------------------------------------------------------ GPU: exactness
 def _whole_and_bands(gpu_lib, h, w, n, halo, seed=0):
     img = make_image(gpu_lib, h, w, seed=seed)
-    enc = EncoderConfig(lmbda=1e-3, seed=seed)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=seed)
     dcfg = DecoderConfig.hop()
     whole = Trainer(img, enc, dcfg, lib=gpu_lib)
     lb = B.LocalBands(img, n, enc, dcfg, halo=halo, lib=gpu_lib)
@@ -191,7 +191,7 @@ def _whole_and_bands(gpu_lib, h, w, n, halo, seed=0):
 def test_band_grid_rows_match_runtime(gpu_lib):
     img = make_image(gpu_lib, 256, 192, seed=1)
     for r0, r1 in B.split_rows(256, 192, 2):
-        with B.BandTrainer(img, r0, r1, 6, EncoderConfig(), DecoderConfig.hop(), lib=gpu_lib) as t:
+        with B.BandTrainer(img, r0, r1, 6, EncoderConfig(use_soap=False), DecoderConfig.hop(), lib=gpu_lib) as t:
             for gi, g in enumerate(t.grids):
                 assert t.grid_rows(gi) == B.band_grid_rows(256, 192, r0, r1, 6, g.level)
 
@@ -231,7 +231,7 @@ def test_band_device_views_are_the_library_buffers(gpu_lib):
 
     img = make_image(gpu_lib, 256, 192, seed=2)
     r0, r1 = B.split_rows(256, 192, 2)[1]
-    with B.BandTrainer(img, r0, r1, 6, EncoderConfig(), DecoderConfig.hop(), lib=gpu_lib) as t:
+    with B.BandTrainer(img, r0, r1, 6, EncoderConfig(use_soap=False), DecoderConfig.hop(), lib=gpu_lib) as t:
         t.fresh_candidate(0)
         gi = len(t.grids) - 1
         gr = t.grid_rows(gi)

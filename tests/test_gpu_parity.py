@@ -17,7 +17,7 @@ import pytest
 from paper_2605_02726_b200 import capi
 from paper_2605_02726_b200.trainer import DecoderConfig, EncoderConfig, Trainer
 from tests import golden_util
-from tests.conftest import make_image, rel_l2
+from tests.conftest import GOLDEN, make_image, rel_l2
 
 pytestmark = pytest.mark.gpu
 
@@ -61,7 +61,7 @@ def test_cfg1_free_running_vs_golden(gpu_lib):
     """BASELINE config 1: 256x256, HOP, zero-initialised latents, 200 Adam
     iterations at lr 1e-2 — per-iteration cost / mse / bits vs the reference."""
     g = dict(np.load(golden_util.GOLDEN / "cfg1_scalars.npz"))
-    with Trainer(g["image"], EncoderConfig(lmbda=1e-3, seed=0), DecoderConfig.hop(),
+    with Trainer(g["image"], EncoderConfig(use_soap=False, lmbda=1e-3, seed=0), DecoderConfig.hop(),
                  lib=gpu_lib) as tr:
         tr.fresh_candidate(0)
         st = tr.get_state()
@@ -87,7 +87,7 @@ def test_cfg1_free_running_vs_golden(gpu_lib):
                                         (512, 768, "hop"), (1360, 2048, "cfg4")])
 def test_lockstep_vs_reference(gpu_lib, ref_lib, h, w, preset):
     img = make_image(ref_lib, h, w, seed=h + w)
-    enc = EncoderConfig(lmbda=1e-3, seed=h)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=h)
     dcfg = DecoderConfig.from_name(preset)
     with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
         tr_r.fresh_candidate(1)
@@ -133,9 +133,96 @@ def test_lockstep_vs_reference(gpu_lib, ref_lib, h, w, preset):
             assert tr_g.global_iter == tr_r.global_iter
 
 
+def test_lockstep_50_iterations_cfg1(gpu_lib, ref_lib):
+    """North star: per-iteration rate, distortion and gradients within 1e-4
+    over the first 50 iterations, at BASELINE config 1 (256x256, HOP,
+    zero-initialised latents, lr 1e-2, T 0.35, sigma 0.22).  Teacher-forced:
+    before every iteration the reference's full state (latents, parameters,
+    Adam moments and step counts, global_iter) is loaded into the device
+    trainer, because free-running fp32 trajectories diverge chaotically
+    (SURVEY 8(c)); after it, cost / mse / bits and every latent-grid and
+    NN-tensor gradient are compared."""
+    img = make_image(ref_lib, 256, 256, seed=0)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=0)
+    dcfg = DecoderConfig.hop()
+    worst_s, worst_l, worst_p = 0.0, 0.0, (0.0, "")
+    with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
+        tr_r.fresh_candidate(0)
+        st = tr_r.get_state()
+        st["latents"][:] = 0
+        tr_r.set_state(st)
+        for it in range(50):
+            tr_g.set_state(tr_r.get_state())
+            cr = tr_r.proxy_iteration(1e-2, 0.35, 0.22)
+            cg = tr_g.proxy_iteration(1e-2, 0.35, 0.22)
+            for a, b in zip((cg, *tr_g.last_terms()), (cr, *tr_r.last_terms())):
+                worst_s = max(worst_s, abs(a - b) / abs(b))
+            lr_, pr_ = tr_r.get_grads()
+            lg_, pg_ = tr_g.get_grads()
+            for gi in range(len(tr_r.grids)):
+                worst_l = max(worst_l, rel_l2(tr_g.grid_view(lg_, gi), tr_r.grid_view(lr_, gi)))
+            for ti, p in enumerate(tr_r.params):
+                e = rel_l2(tr_g.param_view(pg_, ti), tr_r.param_view(pr_, ti))
+                if e > worst_p[0]:
+                    worst_p = (e, f"{p.name}@{it}")
+            assert tr_g.global_iter == tr_r.global_iter
+    print(f"cfg1 50-iteration lock-step: scalars {worst_s:.2e}, latent grads {worst_l:.2e}, "
+          f"NN grads {worst_p}")
+    assert worst_s <= 1e-6
+    assert worst_l <= 1e-4
+    assert worst_p[0] <= 1e-4, worst_p
+
+
+def truth_report(gpu_lib, ref_lib, h, w, preset, seed=0, warm=1):
+    """Gradients of one proxy iteration on an identical state from (a) the
+    B200 library, (b) the reference's float Trainer, (c) the fp64 truth (the
+    reference's templated kernels in double, oracle/ref_capi.cpp
+    ccref_truth_grads).  Returns per-tensor rel-L2 of (a) and (b) vs (c)."""
+    from tests.oracle_util import truth_grads
+
+    img = make_image(ref_lib, h, w, seed=h + w + seed)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=h + seed)
+    dcfg = DecoderConfig.from_name(preset)
+    out = {"gpu": {}, "ref": {}, "scalars_gpu": None, "scalars_ref": None}
+    with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
+        tr_r.fresh_candidate(1)
+        for _ in range(warm):  # off the initial state (zero NN biases)
+            tr_r.proxy_iteration(1e-2, 0.35, 0.22)
+        tr_g.set_state(tr_r.get_state())
+        lt, pt, st = truth_grads(ref_lib, tr_r, 0.3, 0.2)
+        cr = tr_r.proxy_iteration(1e-2, 0.3, 0.2)
+        cg = tr_g.proxy_iteration(1e-2, 0.3, 0.2)
+        out["scalars_ref"] = [abs(a - b) / abs(b) for a, b in zip((cr, *tr_r.last_terms()), st)]
+        out["scalars_gpu"] = [abs(a - b) / abs(b) for a, b in zip((cg, *tr_g.last_terms()), st)]
+        for side, tr in (("gpu", tr_g), ("ref", tr_r)):
+            lg, pg = tr.get_grads()
+            for gi in range(len(tr.grids)):
+                out[side][f"grid{gi}"] = rel_l2(tr.grid_view(lg, gi), tr.grid_view(lt, gi))
+            for ti, p in enumerate(tr.params):
+                out[side][p.name] = rel_l2(tr.param_view(pg, ti), tr.param_view(pt, ti))
+    return out
+
+
+@pytest.mark.parametrize("h,w,preset", [(256, 256, "hop"), (512, 768, "hop"), (1360, 2048, "cfg4")])
+def test_grads_vs_fp64_truth(gpu_lib, ref_lib, h, w, preset):
+    """Every latent grid and every NN tensor within 1e-4 (relative L2) of the
+    fp64 truth, no positions dropped, at cfg1/cfg2 and at the cfg4 size and
+    decoder.  The reference's own float gradients are reported beside (its
+    weight gradients are sequential fp32 sums over all latents, so they drift
+    from the truth as n grows; the device sums per-tile partials in fp64)."""
+    rep = truth_report(gpu_lib, ref_lib, h, w, preset)
+    worst_g = max(rep["gpu"].items(), key=lambda kv: kv[1])
+    worst_r = max(rep["ref"].items(), key=lambda kv: kv[1])
+    print(f"{h}x{w} {preset}: gpu worst {worst_g}, ref worst {worst_r}, "
+          f"scalars gpu {rep['scalars_gpu']} ref {rep['scalars_ref']}")
+    assert max(rep["scalars_gpu"]) <= 1e-6
+    bad = {k: v for k, v in rep["gpu"].items() if not v <= 1e-4}
+    assert not bad, bad
+
+
 def test_quantize_bit_exact_for_identical_latents(gpu_lib, ref_lib):
     img = make_image(ref_lib, 96, 128, seed=1)
-    enc = EncoderConfig()
+    enc = EncoderConfig(use_soap=False)
     with Trainer(img, enc, DecoderConfig.hop(), lib=ref_lib) as tr_r, \
             Trainer(img, enc, DecoderConfig.hop(), lib=gpu_lib) as tr_g:
         tr_r.fresh_candidate(0)
@@ -155,7 +242,7 @@ def test_quantize_bit_exact_for_identical_latents(gpu_lib, ref_lib):
 def test_hardround_freezes_latents_bit_exact(gpu_lib):
     # tests/test_encoder.cpp:81-103
     img = make_image(gpu_lib, 32, 32, seed=21)
-    with Trainer(img, EncoderConfig(lmbda=1e-3, seed=2), DecoderConfig.lop(), lib=gpu_lib) as tr:
+    with Trainer(img, EncoderConfig(use_soap=False, lmbda=1e-3, seed=2), DecoderConfig.lop(), lib=gpu_lib) as tr:
         tr.fresh_candidate(0)
         for _ in range(20):
             tr.proxy_iteration(1e-2, 0.3, 0.2)
@@ -173,7 +260,7 @@ def test_bitwise_determinism(gpu_lib):
     img = make_image(gpu_lib, 80, 120, seed=5)
     outs = []
     for _ in range(2):
-        with Trainer(img, EncoderConfig(lmbda=4e-3, seed=17), DecoderConfig.hop(),
+        with Trainer(img, EncoderConfig(use_soap=False, lmbda=4e-3, seed=17), DecoderConfig.hop(),
                      lib=gpu_lib) as tr:
             tr.fresh_candidate(0)
             costs = tr.proxy_iterations(np.full(25, 1e-2), 0.35, 0.22)
@@ -187,7 +274,7 @@ def test_nonfinite_cost_returned_not_stepped(gpu_lib):
     # encoder.hpp:118: a non-finite cost is returned; no step, global_iter kept
     img = make_image(gpu_lib, 32, 48, seed=2)
     img[1, 5, 7] = np.nan  # a NaN target pixel makes the MSE (and the cost) NaN
-    with Trainer(img, EncoderConfig(), DecoderConfig.hop(), lib=gpu_lib) as tr:
+    with Trainer(img, EncoderConfig(use_soap=False), DecoderConfig.hop(), lib=gpu_lib) as tr:
         tr.fresh_candidate(0)
         st = tr.get_state()
         g0 = tr.global_iter
@@ -209,7 +296,7 @@ def test_nonfinite_behaviour_matches_reference(gpu_lib, ref_lib, inject):
     img = make_image(ref_lib, 32, 48, seed=2)
     if inject == "image_nan":
         img[0, 3, 4] = np.nan
-    enc, dcfg = EncoderConfig(lmbda=1e-3, seed=3), DecoderConfig.hop()
+    enc, dcfg = EncoderConfig(use_soap=False, lmbda=1e-3, seed=3), DecoderConfig.hop()
     with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
         tr_r.fresh_candidate(0)
         st = tr_r.get_state()
@@ -237,13 +324,13 @@ def test_nonfinite_behaviour_matches_reference(gpu_lib, ref_lib, inject):
 def test_warmup_budget_and_candidates(gpu_lib):
     # tests/test_encoder.cpp:56-79
     img = make_image(gpu_lib, 32, 32, seed=9)
-    enc = EncoderConfig(warmup_candidates=5, warmup_keep=2, warmup_iters=6, main_iters=1,
+    enc = EncoderConfig(use_soap=False, warmup_candidates=5, warmup_keep=2, warmup_iters=6, main_iters=1,
                         hardround_iters=1, lmbda=1e-3, seed=5)
     with Trainer(img, enc, DecoderConfig.lop(), lib=gpu_lib) as tr:
         tr.warmup()
         assert tr.global_iter == (5 + 2) * 6
         assert np.isfinite(tr.true_cost()[0])
-    enc1 = EncoderConfig(warmup_candidates=1, warmup_keep=2, warmup_iters=6, main_iters=1,
+    enc1 = EncoderConfig(use_soap=False, warmup_candidates=1, warmup_keep=2, warmup_iters=6, main_iters=1,
                          hardround_iters=1, lmbda=1e-3, seed=5)
     with Trainer(img, enc1, DecoderConfig.lop(), lib=gpu_lib) as tr:
         tr.warmup()
@@ -284,7 +371,7 @@ def test_cfg2_size_properties(gpu_lib):
     per-iteration records."""
     img = make_image(gpu_lib, 512, 768, seed=0)
     enc = EncoderConfig.with_total(10000)
-    enc.lmbda, enc.seed = 1e-3, 0
+    enc.lmbda, enc.seed, enc.use_soap = 1e-3, 0, False
     with Trainer(img, enc, DecoderConfig.hop(), lib=gpu_lib) as tr:
         tr.fresh_candidate(0)
         c = tr.proxy_iterations(np.full(40, 1e-2), 0.35, 0.22)
@@ -371,6 +458,81 @@ def test_soap_step_matches_restatement(gpu_lib):
                 assert off <= 1e-10 * max(np.abs(A).max(), 1e-300), (p.name, off)
 
 
+@pytest.mark.parametrize("h,w,preset", [(64, 96, "hop"), (256, 256, "hop")])
+def test_soap_lockstep_vs_reference(gpu_lib, ref_lib, h, w, preset):
+    """SOAP (the reference default) teacher-forced against the reference's
+    own soap_step (optim.hpp:189-254, via NnOptimizer::step optim.hpp:277-286):
+    before each iteration the reference's latents, parameters, latent Adam
+    state and full SOAP state (L, R EMAs, eigenbases QL / QR, m1, v2, t;
+    optim.hpp:122-141) are loaded into the device trainer; both take one
+    proxy iteration.  Steps t = 12..20 (no eigenbasis refresh) and the refresh
+    step t = 21 are compared: every parameter's update (p_after - p_before)
+    and the post-step preconditioner EMAs and moments within 1e-4 (relative
+    L2 per tensor).  At the refresh step the new eigenbases are compared as
+    subspaces only for eigenvalues separated by > 1e-6 of the spectrum (a
+    basis inside a degenerate eigenspace is arbitrary for Jacobi)."""
+    from tests.test_oracle import _soap_io, _soap_load
+
+    for name in ("ccb_soap_state", "ccb_soap_set_state"):
+        getattr(ref_lib, name).restype = C.c_int
+    img = make_image(ref_lib, h, w, seed=5)
+    enc = EncoderConfig(use_soap=True, lmbda=1e-3, seed=5)
+    dcfg = DecoderConfig.from_name(preset)
+    worst = {"dp": (0.0, ""), "L": 0.0, "m1": 0.0, "v2": 0.0}
+    with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
+        tr_r.fresh_candidate(0)
+        tr_g.fresh_candidate(0)
+        for _ in range(11):
+            tr_r.proxy_iteration(1e-2, 0.35, 0.22)
+        for it in range(10):  # SOAP steps t = 12 .. 21 (t = 21 refreshes the bases)
+            st = tr_r.get_state()
+            tr_g.set_state(st)
+            _soap_load(gpu_lib, tr_g, _soap_io(ref_lib, tr_r))
+            p0 = st["params"].astype(np.float64)
+            cr = tr_r.proxy_iteration(5e-3, 0.3, 0.2)
+            cg = tr_g.proxy_iteration(5e-3, 0.3, 0.2)
+            assert abs(cr - cg) / abs(cr) <= 1e-6
+            dr = tr_r.get_state()["params"].astype(np.float64) - p0
+            dg = tr_g.get_state()["params"].astype(np.float64) - p0
+            sr, sg = _soap_io(ref_lib, tr_r), _soap_io(gpu_lib, tr_g)
+            assert np.array_equal(sr["t"], sg["t"]) and np.all(sr["t"] == 12 + it)
+            refresh = (12 + it - 1) % 10 == 0
+            pos = 0
+            for ti, p in enumerate(tr_r.params):
+                sl = slice(p.offset, p.offset + p.size)
+                r, c = p.rows, p.cols
+                blocks = {}
+                for nm, n in (("L", r * r), ("R", c * c), ("QL", r * r), ("QR", c * c)):
+                    blocks[nm] = (sr["arena"][pos:pos + n], sg["arena"][pos:pos + n])
+                    pos += n
+                worst["L"] = max(worst["L"], rel_l2(blocks["L"][1], blocks["L"][0]),
+                                 rel_l2(blocks["R"][1], blocks["R"][0]))
+                worst["m1"] = max(worst["m1"], rel_l2(sg["m1"][sl], sr["m1"][sl]))
+                if not refresh:
+                    assert np.array_equal(blocks["QL"][0], blocks["QL"][1]), p.name
+                    worst["v2"] = max(worst["v2"], rel_l2(sg["v2"][sl], sr["v2"][sl]))
+                    e = rel_l2(dg[sl], dr[sl])
+                    if e > worst["dp"][0]:
+                        worst["dp"] = (e, f"{p.name}@t{12 + it}")
+                else:
+                    for nm, n in (("QL", r), ("QR", c)):
+                        A = blocks["L" if nm == "QL" else "R"][0].reshape(n, n)
+                        Qr, Qg = (x.reshape(n, n) for x in blocks[nm])
+                        ev = np.linalg.eigvalsh(A)
+                        scale = max(np.abs(ev).max(), 1e-300)
+                        dr_ = Qr.T @ A @ Qr
+                        for j in range(n):  # eigenvector j of the reference basis
+                            lam = dr_[j, j]
+                            if np.min(np.abs(np.delete(ev, np.argmin(np.abs(ev - lam))) - lam),
+                                      initial=np.inf) > 1e-6 * scale:
+                                cos = abs(Qr[:, j] @ Qg[:, j])
+                                assert cos >= 1 - 1e-6, (p.name, nm, j, cos)
+    print(f"SOAP lock-step {h}x{w}: worst update {worst['dp']}, L/R {worst['L']:.2e}, "
+          f"m1 {worst['m1']:.2e}, v2 {worst['v2']:.2e}")
+    assert worst["dp"][0] <= 1e-4, worst["dp"]
+    assert worst["L"] <= 1e-4 and worst["m1"] <= 1e-4 and worst["v2"] <= 1e-4
+
+
 def test_soap_full_train_final_rd(gpu_lib, ref_lib):
     """Full with_total schedule with SOAP on both sides.  SOAP's update along
     the null space of a rank-deficient preconditioner depends on the eigenbasis
@@ -400,7 +562,7 @@ def test_decode_terms_match_reference(gpu_lib, ref_lib):
     on identical quantised latents and substituted parameters, as the
     NN-quantisation search evaluates them (nn_coding.hpp:146-224)."""
     img = make_image(ref_lib, 64, 96, seed=11)
-    enc, dcfg = EncoderConfig(lmbda=1e-3, seed=2), DecoderConfig.hop()
+    enc, dcfg = EncoderConfig(use_soap=False, lmbda=1e-3, seed=2), DecoderConfig.hop()
     with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
         tr_r.fresh_candidate(0)
         for _ in range(20):
@@ -446,7 +608,7 @@ def test_latent_mu_sigma_bit_exact(gpu_lib, h, w, preset):
         pytest.skip("oracle/_ref/libccref_v3.so not built")
     ref_lib = capi.load_library(v3)
     img = make_image(ref_lib, h, w, seed=7)
-    enc, dcfg = EncoderConfig(lmbda=1e-3, seed=3), DecoderConfig.from_name(preset)
+    enc, dcfg = EncoderConfig(use_soap=False, lmbda=1e-3, seed=3), DecoderConfig.from_name(preset)
     with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
         tr_g.fresh_candidate(0)
         for _ in range(30):
@@ -478,37 +640,40 @@ def test_branches_match_serial_order(gpu_lib, tmp_path):
     import sys
 
     res = {}
-    for mode in ("0", "1"):
-        out = tmp_path / f"run{mode}.npz"
-        env = dict(os.environ, CCB_SERIAL=mode)
+    # concurrent + PDL / serial + PDL / serial without PDL: a hazard before a
+    # griddepcontrol.wait would show in the first two alike, so the third
+    # run (no programmatic launches at all) is the strict reference order
+    for mode, serial, pdl in (("conc", "0", "1"), ("ser", "1", "1"), ("ser_nopdl", "1", "0")):
+        out = tmp_path / f"run_{mode}.npz"
+        env = dict(os.environ, CCB_SERIAL=serial, CCB_PDL=pdl)
         subprocess.run([sys.executable, "-m", "tests.branch_run", str(out), "256", "384", "6"], env=env,
                        check=True, timeout=600, cwd=str(golden_util.GOLDEN.parents[1]))
         res[mode] = dict(np.load(out))
-    for k in res["0"]:
-        assert np.array_equal(res["0"][k], res["1"][k]), k
+    for other in ("ser", "ser_nopdl"):
+        for k in res["conc"]:
+            assert np.array_equal(res["conc"][k], res[other][k]), (other, k)
 
 
-def test_tensor_core_arm_matches_default(gpu_lib, tmp_path):
-    """The opt-in tensor-core ARM (cc_arm3.cu, mma.sync TF32 with a 3-term
-    split; CCB_ARM_V3=1) against the default FFMA2 kernel over a few
-    free-running batched iterations: costs within 1e-5, final state and
-    gradients within drift bounds, and its own runs bitwise deterministic."""
-    import os
-    import subprocess
-    import sys
+@pytest.mark.parametrize("name", ["lop96", "cfg1", "cfg2"])
+def test_full_schedule_final_rd_vs_golden(gpu_lib, name):
+    """North star: final true RD cost after a full with_total schedule within
+    0.5 % of the reference's train() (encoder.hpp:349-413) on the same image,
+    seed and decoder.  The reference results were produced here by
+    tools/make_golden_train.py from oracle/_ref (the unmodified reference;
+    cfg2 = BASELINE config 2, 512x768 HOP with_total(10000), ~2.5 h of CPU)."""
+    import json
 
-    res = {}
-    for tag, v3 in (("v2", "0"), ("v3a", "1"), ("v3b", "1")):
-        out = tmp_path / f"{tag}.npz"
-        env = dict(os.environ, CCB_ARM_V3=v3)
-        subprocess.run([sys.executable, "-m", "tests.branch_run", str(out), "256", "384", "6"], env=env,
-                       check=True, timeout=600, cwd=str(golden_util.GOLDEN.parents[1]))
-        res[tag] = dict(np.load(out))
-    for k in res["v3a"]:
-        assert np.array_equal(res["v3a"][k], res["v3b"][k]), k
-    a, b = res["v3a"], res["v2"]
-    assert np.max(np.abs(a["costs"] - b["costs"]) / np.abs(b["costs"])) <= 1e-5
-    assert rel_l2(a["latents"], b["latents"]) <= 1e-5
-    assert rel_l2(a["params"], b["params"]) <= 1e-5
-    assert rel_l2(a["pg"], b["pg"]) <= 1e-3
-    assert rel_l2(a["lg"], b["lg"]) <= 1e-3
+    p = GOLDEN / f"train_{name}.json"
+    if not p.exists():
+        pytest.skip(f"{p.name} not generated")
+    g = json.loads(p.read_text())
+    img = make_image(gpu_lib, g["h"], g["w"], seed=g["image_seed"])
+    enc = EncoderConfig.with_total(g["with_total"])
+    enc.lmbda, enc.seed, enc.use_soap = g["lmbda"], g["seed"], False
+    with Trainer(img, enc, DecoderConfig.from_name(g["decoder"]), lib=gpu_lib) as tr:
+        r = tr.train()
+    assert r.stats.iterations == g["iterations"]
+    rel = abs(r.stats.true_cost - g["true_cost"]) / g["true_cost"]
+    print(f"{name}: gpu {r.stats.true_cost:.6e} ref {g['true_cost']:.6e} rel {rel:.2e} "
+          f"psnr {r.stats.psnr:.3f}/{g['psnr']:.3f} bpp {r.stats.rate_bpp:.4f}/{g['rate_bpp']:.4f}")
+    assert rel <= 5e-3

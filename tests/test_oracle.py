@@ -17,7 +17,7 @@ import pytest
 from paper_2605_02726_b200 import capi
 from paper_2605_02726_b200.trainer import DecoderConfig, EncoderConfig, Trainer
 from tests import golden_util
-from tests.conftest import make_image
+from tests.conftest import make_image, rel_l2
 
 
 def _math(lib, prefix, fn, a, b=None, c=None):
@@ -127,9 +127,9 @@ def test_port_math_vectors(port_lib):
 def test_context_offsets_hop(ref_lib):
     # HOP causal offsets nearest-first — observed through the layout
     img = make_image(ref_lib, 16, 16)
-    with Trainer(img, EncoderConfig(), DecoderConfig.hop(), lib=ref_lib) as tr:
+    with Trainer(img, EncoderConfig(use_soap=False), DecoderConfig.hop(), lib=ref_lib) as tr:
         assert tr.layout.pad == 3
-    with Trainer(img, EncoderConfig(), DecoderConfig(spatial_ctx=26), lib=ref_lib) as tr:
+    with Trainer(img, EncoderConfig(use_soap=False), DecoderConfig(spatial_ctx=26), lib=ref_lib) as tr:
         assert tr.layout.pad == 4
 
 
@@ -138,7 +138,7 @@ def test_grid_shapes(ref_lib, port_lib, h, w, n_lat):
     # SURVEY 8(a) sizes (build_latents, latent.hpp:46-70)
     img = np.zeros((3, h, w), np.float32)
     for lib in (ref_lib, port_lib):
-        with Trainer(img, EncoderConfig(), DecoderConfig.hop(), lib=lib) as tr:
+        with Trainer(img, EncoderConfig(use_soap=False), DecoderConfig.hop(), lib=lib) as tr:
             assert tr.n_latents == n_lat
             assert tr.n_params == 1846
             assert [g.level for g in tr.grids] == [6, 5, 4, 6, 5, 4, 3, 2, 1, 0]
@@ -151,7 +151,7 @@ def test_zero_arm_rate_on_1x1(ref_lib, port_lib):
     img = np.full((3, 1, 1), 0.5, np.float32)
     per = ref_laplace_bits(0.0, 0.0, 1.0)
     for lib in (ref_lib, port_lib):
-        with Trainer(img, EncoderConfig(), DecoderConfig.hop(), lib=lib) as tr:
+        with Trainer(img, EncoderConfig(use_soap=False), DecoderConfig.hop(), lib=lib) as tr:
             tr.fresh_candidate(0)
             st = tr.get_state()
             st["latents"][:] = 0
@@ -182,7 +182,7 @@ def test_port_matches_reference_cfg1_prefix(port_lib):
     """Config 1 (256x256 HOP, zero latents): first 10 free-running iterations of
     the port against the reference's per-iteration scalars (golden)."""
     g = dict(np.load(golden_util.GOLDEN / "cfg1_scalars.npz"))
-    with Trainer(g["image"], EncoderConfig(lmbda=1e-3, seed=0), DecoderConfig.hop(),
+    with Trainer(g["image"], EncoderConfig(use_soap=False, lmbda=1e-3, seed=0), DecoderConfig.hop(),
                  lib=port_lib) as tr:
         tr.fresh_candidate(0)
         st = tr.get_state()
@@ -208,3 +208,69 @@ def test_fp32_sequential_sum_drift():
     assert abs(float(seq) - exact) / exact > 1e-3
     tiles = x.reshape(-1, 100).sum(axis=1, dtype=np.float32).astype(np.float64).sum()
     assert abs(tiles - exact) / exact < 1e-6
+
+
+def test_fp64_truth_matches_reference_float(ref_lib):
+    """The fp64 truth harness (ccref_truth_grads) against the reference's own
+    float proxy_iteration on the same state: they evaluate the same function,
+    so every gradient tensor agrees to float accuracy (~1e-6), and the
+    scalars to ~1e-7."""
+    from tests.oracle_util import truth_grads
+
+    img = make_image(ref_lib, 48, 80, seed=3)
+    with Trainer(img, EncoderConfig(use_soap=False, lmbda=1e-3, seed=3), DecoderConfig.hop(),
+                 lib=ref_lib) as tr:
+        tr.fresh_candidate(0)
+        tr.proxy_iteration(1e-2, 0.35, 0.22)  # move off the init
+        lt, pt, sc = truth_grads(ref_lib, tr, 0.3, 0.2)
+        c = tr.proxy_iteration(1e-2, 0.3, 0.2)
+        m, b = tr.last_terms()
+        lg, pg = tr.get_grads()
+        assert abs(c - sc[0]) / sc[0] < 1e-6 and abs(m - sc[1]) / sc[1] < 1e-6 and abs(b - sc[2]) / sc[2] < 1e-6
+        for gi in range(len(tr.grids)):
+            assert rel_l2(tr.grid_view(lg, gi), tr.grid_view(lt, gi)) < 2e-5, gi
+        for ti, p in enumerate(tr.params):
+            assert rel_l2(tr.param_view(pg, ti), tr.param_view(pt, ti)) < 2e-5, p.name
+
+
+def _soap_io(lib, tr):
+    n = C.c_int64()
+    assert lib.ccb_soap_state(tr._h, None, None, None, None, C.byref(n)) == 0
+    st = dict(arena=np.empty(n.value, np.float64), m1=np.empty(tr.n_params, np.float32),
+              v2=np.empty(tr.n_params, np.float32), t=np.empty(len(tr.params), np.int64))
+    assert lib.ccb_soap_state(tr._h, st["arena"].ctypes.data_as(C.POINTER(C.c_double)),
+                              st["m1"].ctypes.data_as(C.POINTER(C.c_float)),
+                              st["v2"].ctypes.data_as(C.POINTER(C.c_float)),
+                              st["t"].ctypes.data_as(C.POINTER(C.c_int64)), None) == 0
+    return st
+
+
+def _soap_load(lib, tr, st):
+    assert lib.ccb_soap_set_state(tr._h, st["arena"].ctypes.data_as(C.POINTER(C.c_double)),
+                                  st["m1"].ctypes.data_as(C.POINTER(C.c_float)),
+                                  st["v2"].ctypes.data_as(C.POINTER(C.c_float)),
+                                  st["t"].ctypes.data_as(C.POINTER(C.c_int64))) == 0
+
+
+def test_reference_soap_state_transfer_is_exact(ref_lib):
+    """The checker's SOAP-state accessors (oracle/ref_capi.cpp): a second
+    reference trainer loaded with the first one's latents, parameters and
+    SOAP state takes a bit-identical next step (soap_step, optim.hpp:189-254)."""
+    for name in ("ccb_soap_state", "ccb_soap_set_state"):
+        getattr(ref_lib, name).restype = C.c_int
+    img = make_image(ref_lib, 32, 48, seed=2)
+    enc = EncoderConfig(use_soap=True, lmbda=1e-3, seed=2)
+    with Trainer(img, enc, DecoderConfig.lop(), lib=ref_lib) as a, \
+            Trainer(img, enc, DecoderConfig.lop(), lib=ref_lib) as b:
+        a.fresh_candidate(0)
+        b.fresh_candidate(0)
+        for _ in range(12):
+            a.proxy_iteration(1e-2, 0.35, 0.22)
+        b.set_state(a.get_state())
+        _soap_load(ref_lib, b, _soap_io(ref_lib, a))
+        ca, cb = a.proxy_iteration(1e-2, 0.35, 0.22), b.proxy_iteration(1e-2, 0.35, 0.22)
+        assert ca == cb
+        assert np.array_equal(a.get_state()["params"], b.get_state()["params"])
+        sa, sb = _soap_io(ref_lib, a), _soap_io(ref_lib, b)
+        for k in sa:
+            assert np.array_equal(sa[k], sb[k]), k

@@ -49,7 +49,7 @@ def main():
     img = make_synthetic_image(h, w, 0, lib)
     bands = B.split_rows(h, w, world)
     r0, r1 = bands[rank]
-    enc, dcfg = EncoderConfig(lmbda=1e-3, seed=0), DecoderConfig.hop()
+    enc, dcfg = EncoderConfig(use_soap=False, lmbda=1e-3, seed=0), DecoderConfig.hop()
     tr = B.BandTrainer(img, r0, r1, a.halo, enc, dcfg, lib=lib, device=local)
     tr.fresh_candidate(0)
     hyper = any(g.hyper for g in tr.grids)

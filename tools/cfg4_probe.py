@@ -14,7 +14,7 @@ ref = oracle_util.load_reference()
 gpu = capi.load_product()
 h, w = 1360, 2048
 img = make_image(ref, h, w, seed=h + w)
-enc = EncoderConfig(lmbda=1e-3, seed=h)
+enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=h)
 dcfg = DecoderConfig.cfg4()
 r = Trainer(img, enc, dcfg, lib=ref)
 g = Trainer(img, enc, dcfg, lib=gpu)

@@ -42,7 +42,7 @@ SCHED = [(1e-2, 0.35, 0.22), (8e-3, 0.3, 0.2), (5e-3, 0.25, 0.18)]
 def run_case(lib, name, h, w, dcfg, seed, lam, zero):
     img = np.empty((3, h, w), np.float32)
     lib.cc_make_synthetic_image(h, w, seed, img.ctypes.data_as(capi._F))
-    enc = EncoderConfig(lmbda=lam, seed=seed)
+    enc = EncoderConfig(use_soap=False, lmbda=lam, seed=seed)
     tr = Trainer(img, enc, dcfg, lib=lib)
     tr.fresh_candidate(0)
     st0 = tr.get_state()
@@ -92,7 +92,7 @@ def cfg1_scalars(lib, iters=200):
     h = w = 256
     img = np.empty((3, h, w), np.float32)
     lib.cc_make_synthetic_image(h, w, 0, img.ctypes.data_as(capi._F))
-    tr = Trainer(img, EncoderConfig(lmbda=1e-3, seed=0), DecoderConfig.hop(), lib=lib)
+    tr = Trainer(img, EncoderConfig(use_soap=False, lmbda=1e-3, seed=0), DecoderConfig.hop(), lib=lib)
     tr.fresh_candidate(0)
     st = tr.get_state()
     st["latents"][:] = 0

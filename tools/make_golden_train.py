@@ -1,0 +1,60 @@
+"""Full-schedule golden results from the UNMODIFIED reference (oracle/_ref).
+
+`train()` (encoder.hpp:349-413) over EncoderConfig::with_total(N) with
+use_soap=false, run once here where /root/reference exists; the
+final true RD cost / PSNR / bpp land in tests/golden/train_<name>.json and the
+GPU test (`test_full_schedule_final_rd_vs_golden`) holds the device encode to
+0.5 % of it (north star).  cfg2 takes ~2.5 h of one core.
+
+    python tools/make_golden_train.py cfg1   # 256x256 HOP with_total(2000)
+    python tools/make_golden_train.py cfg2   # 512x768 HOP with_total(10000)
+"""
+from __future__ import annotations
+
+import json
+import platform
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(REPO))
+
+from paper_2605_02726_b200 import capi  # noqa: E402
+from paper_2605_02726_b200.trainer import DecoderConfig, EncoderConfig, Trainer  # noqa: E402
+from tests.oracle_util import load_reference, reference_path  # noqa: E402
+
+CASES = {
+    # name: (h, w, preset, total, seed, lambda)
+    "cfg1": (256, 256, "hop", 2000, 0, 1e-3),
+    "cfg2": (512, 768, "hop", 10000, 0, 1e-3),
+    "lop96": (96, 128, "lop", 1000, 2, 1e-3),
+}
+
+
+def main(name: str) -> None:
+    h, w, preset, total, seed, lam = CASES[name]
+    lib = load_reference()
+    img = np.empty((3, h, w), np.float32)
+    assert lib.cc_make_synthetic_image(h, w, seed, img.ctypes.data_as(capi._F)) == 0
+    enc = EncoderConfig.with_total(total)
+    enc.lmbda, enc.seed, enc.use_soap = lam, seed, False
+    t0 = time.time()
+    with Trainer(img, enc, DecoderConfig.from_name(preset), lib=lib) as tr:
+        r = tr.train()
+    out = dict(name=name, h=h, w=w, decoder=preset, with_total=total, image_seed=seed,
+               seed=seed, lmbda=lam, use_soap=False, iterations=r.stats.iterations,
+               true_cost=r.stats.true_cost, psnr=r.stats.psnr, rate_bpp=r.stats.rate_bpp,
+               restarts=r.stats.restarts, skipped_steps=r.stats.skipped_steps,
+               q_abs_sum=int(np.abs(r.q.astype(np.int64)).sum()),
+               generator=f"{reference_path().name} on {platform.processor() or platform.machine()}",
+               cpu_seconds=time.time() - t0)
+    p = REPO / "tests" / "golden" / f"train_{name}.json"
+    p.write_text(json.dumps(out, indent=1) + "\n")
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

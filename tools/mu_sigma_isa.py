@@ -12,7 +12,7 @@ from tests.oracle_util import REF_DIR
 from tests.conftest import make_image
 l3 = capi.load_library(REF_DIR / "libccref_v3.so"); l4 = capi.load_library(REF_DIR / "libccref_v4.so")
 img = make_image(l3, 64, 96, seed=7)
-enc, dcfg = EncoderConfig(lmbda=1e-3, seed=3), DecoderConfig.hop()
+enc, dcfg = EncoderConfig(use_soap=False, lmbda=1e-3, seed=3), DecoderConfig.hop()
 with Trainer(img, enc, dcfg, lib=l3) as t3, Trainer(img, enc, dcfg, lib=l4) as t4:
     t3.fresh_candidate(0)
     for _ in range(5): t3.proxy_iteration(1e-2, 0.35, 0.22)

@@ -21,7 +21,7 @@ def main():
     for m in range(M):
         img = make_synthetic_image(512, 768, m, lib)
         enc = EncoderConfig.with_total(10000)
-        enc.seed = m
+        enc.seed, enc.use_soap = m, False
         tr = Trainer(img, enc, DecoderConfig.hop(), lib=lib)
         tr.fresh_candidate(0)
         s = torch.cuda.Stream()

@@ -32,7 +32,7 @@ def main():
     gpu = capi.load_product()
     img = np.empty((3, H, W), np.float32)
     ref.cc_make_synthetic_image(H, W, 0, img.ctypes.data_as(capi._F))
-    enc = EncoderConfig(lmbda=1e-3, seed=0)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=0)
     dcfg = DecoderConfig.from_name(preset)
     tr_r = Trainer(img, enc, dcfg, lib=ref)
     tr_g = Trainer(img, enc, dcfg, lib=gpu)

@@ -7,7 +7,7 @@ from tests.conftest import make_image, rel_l2
 ref = oracle_util.load_reference(); gpu = capi.load_product()
 h, w = 1360, 2048
 img = make_image(ref, h, w, seed=h + w)
-enc = EncoderConfig(lmbda=1e-3, seed=h)
+enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=h)
 dcfg = DecoderConfig.from_name("cfg4")
 with Trainer(img, enc, dcfg, lib=ref) as tr_r, Trainer(img, enc, dcfg, lib=gpu) as tr_g:
     tr_r.fresh_candidate(1); tr_g.fresh_candidate(1)

@@ -15,7 +15,7 @@ NAMES = ["start", "softq", "ARM (side)", "pyramid (side)", "ups fwd", "syn fwd",
 lib = capi.load_product()
 h, w = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (512, 768)
 img = make_synthetic_image(h, w, 0, lib)
-enc = EncoderConfig(lmbda=1e-3, seed=0)
+enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=0)
 tr = Trainer(img, enc, DecoderConfig.hop(), lib=lib)
 tr.fresh_candidate(0)
 for _ in range(20):
