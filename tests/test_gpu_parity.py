@@ -148,6 +148,7 @@ def test_lockstep_50_iterations_cfg1(gpu_lib, ref_lib):
     worst_s, worst_l, worst_p = 0.0, 0.0, (0.0, "")
     with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
         tr_r.fresh_candidate(0)
+        tr_g.fresh_candidate(0)
         st = tr_r.get_state()
         st["latents"][:] = 0
         tr_r.set_state(st)
@@ -186,6 +187,7 @@ def truth_report(gpu_lib, ref_lib, h, w, preset, seed=0, warm=1):
     out = {"gpu": {}, "ref": {}, "scalars_gpu": None, "scalars_ref": None}
     with Trainer(img, enc, dcfg, lib=ref_lib) as tr_r, Trainer(img, enc, dcfg, lib=gpu_lib) as tr_g:
         tr_r.fresh_candidate(1)
+        tr_g.fresh_candidate(1)
         for _ in range(warm):  # off the initial state (zero NN biases)
             tr_r.proxy_iteration(1e-2, 0.35, 0.22)
         tr_g.set_state(tr_r.get_state())
