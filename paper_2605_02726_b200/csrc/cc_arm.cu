@@ -601,12 +601,28 @@ size_t arm2_smem_bytes(int Dp, int Wp);
 void arm2_configure(int Dp, int Wp);
 void launch_arm2(const LaunchCtx& L, int mode);
 
-static bool use_arm2(int Dp, int Wp) { return arm2_supported(Dp, Wp); }
+bool arm_tc_supported(int Dp, int Wp);
+size_t arm_tc_smem_bytes(int Dp, int Wp);
+void arm_tc_configure(int Dp, int Wp);
+void launch_arm_tc(const LaunchCtx& L, int mode);
 
-// the tiled kernel stages a (P+1)-row window (row bands, halo <= 4)
-bool arm_uses_v2(int Dp, int Wp) { return use_arm2(Dp, Wp); }
+// The tensor-core kernel (cc_arm_tc.cu) is the default; CCB_ARM=2 selects the
+// FFMA2 tile kernel (cc_arm2.cu) for A/B measurements.
+static int arm_env() {
+    static const int v = [] {
+        const char* e = std::getenv("CCB_ARM");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v;
+}
+static bool use_tc(int Dp, int Wp) { return arm_env() != 2 && arm_tc_supported(Dp, Wp); }
+static bool use_arm2(int Dp, int Wp) { return !use_tc(Dp, Wp) && arm2_supported(Dp, Wp); }
+
+// both tiled kernels stage a (P+1)-row window (row bands, halo <= 4)
+bool arm_uses_v2(int Dp, int Wp) { return use_tc(Dp, Wp) || use_arm2(Dp, Wp); }
 
 void arm_configure(int Dp, int Wp) {
+    if (use_tc(Dp, Wp)) arm_tc_configure(Dp, Wp);
     if (use_arm2(Dp, Wp)) arm2_configure(Dp, Wp);
     if (Dp == 8 && Wp == 8) configure_t<8, 8>();
     else if (Dp == 16 && Wp == 12) configure_t<16, 12>();
@@ -628,6 +644,7 @@ static void launch_arm_mode(const LaunchCtx& L, int mode) {
 
 void launch_arm(const LaunchCtx& L, int mode) {
     const int Dp = L.host->Dp, Wp = L.host->Wp;
+    if (use_tc(Dp, Wp)) return launch_arm_tc(L, mode);
     if (use_arm2(Dp, Wp)) return launch_arm2(L, mode);
     if (Dp == 8 && Wp == 8) launch_arm_mode<8, 8>(L, mode);
     else if (Dp == 16 && Wp == 12) launch_arm_mode<16, 12>(L, mode);
@@ -638,6 +655,10 @@ void launch_arm(const LaunchCtx& L, int mode) {
 }
 
 int arm_blocks_per_sm(int Dp, int Wp) {
+    if (use_tc(Dp, Wp)) {  // __launch_bounds__(256, 1), TMEM: 128 columns per CTA
+        const int b = int((227 * 1024) / (arm_tc_smem_bytes(Dp, Wp) + 1024));
+        return b < 1 ? 1 : (b > 2 ? 2 : b);
+    }
     if (use_arm2(Dp, Wp)) {  // __launch_bounds__(128, 2)
         const int b = int((227 * 1024) / (arm2_smem_bytes(Dp, Wp) + 1024));
         return b < 1 ? 1 : (b > 2 ? 2 : b);
