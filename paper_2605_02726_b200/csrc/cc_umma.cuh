@@ -7,13 +7,12 @@
 // 16 bytes (4 tf32) stored contiguously (128 B).  A tile is kept as
 //     [row / 8][k / 4][row % 8][k % 4]            (rows = M or N, k = K)
 // i.e. element (r, k) at byte ((r / 8) * KC + k / 4) * 128 + (r % 8) * 16 +
-// (k % 4) * 4 with KC = K / 4 core columns.  Read K-major (rows = M/N) it has
-// LBO = 128 (next core matrix along K) and SBO = KC * 128 (next 8 rows); the
-// SAME bytes read MN-major (the transposed operand, rows become K) have
-// SBO = 128 (next 4 elements along M/N) and LBO = KC * 128 (next 8 along K).
-// So an activation tile written once per latent row serves both the
-// per-latent layer GEMMs (latents = M) and the weight-gradient GEMMs
-// (latents = K) without a transpose.
+// (k % 4) * 4 with KC = K / 4 core columns, read K-major with LBO = 128 (next
+// core matrix along K) and SBO = KC * 128 (next 8 rows).  Measured on the
+// B200 (tools/micro/umma_probe*.cu): K-major M = 128 with N = 24..56 is exact;
+// the same bytes read MN-major (kind::tf32, SWIZZLE_NONE) return zeros, so a
+// transposed operand needs its own copy.  A operands can also come from TMEM
+// (lane = row, one column per k), written by the owning thread with tcgen05.st.
 #pragma once
 
 #include <cstdint>
@@ -51,6 +50,18 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B^T: A read from tensor memory (lane = row m, one
+// 32-bit column per k), B from shared memory (K-major descriptor)
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 
@@ -131,12 +142,33 @@ __device__ __forceinline__ void ld8(uint32_t taddr, float (&v)[8]) {
 }
 __device__ __forceinline__ void wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// registers -> this thread's TMEM lane, 8 / 4 consecutive 32-bit columns
+__device__ __forceinline__ void st8(uint32_t taddr, const float (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+                 "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void st4(uint32_t taddr, float a, float b, float c, float d) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "f"(a), "f"(b),
+                 "f"(c), "f"(d)
+                 : "memory");
+}
+__device__ __forceinline__ void wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 // fp32 -> (hi, lo) with hi exactly representable in tf32 (low 13 mantissa bits
 // cleared) and lo = x - hi exact; hi*hi' + hi*lo' + lo*hi' recovers the fp32
 // product to ~2^-21 relative (the "3xTF32" split)
 __device__ __forceinline__ void split(float x, float& hi, float& lo) {
     hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
     lo = x - hi;
+}
+// the same split with both parts rounded to nearest tf32: |x - hi - lo| <=
+// 2^-24 |x| (hi carries 11 bits, lo the next ~12, itself rounded), so the
+// three products recover the fp32 product to ~2^-23 instead of ~2^-21
+__device__ __forceinline__ uint32_t rn_tf32_bits(float x) { return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u; }
+__device__ __forceinline__ void split_rn(float x, float& hi, float& lo) {
+    hi = __uint_as_float(rn_tf32_bits(x));
+    lo = __uint_as_float(rn_tf32_bits(x - hi));
 }
 
 // byte offset of element (r, k) in a [r/8][k/4][r%8][k%4] tile with KC core columns
