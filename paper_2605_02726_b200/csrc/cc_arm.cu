@@ -620,6 +620,7 @@ static bool use_arm2(int Dp, int Wp) { return !use_tc(Dp, Wp) && arm2_supported(
 
 // both tiled kernels stage a (P+1)-row window (row bands, halo <= 4)
 bool arm_uses_v2(int Dp, int Wp) { return use_tc(Dp, Wp) || use_arm2(Dp, Wp); }
+bool arm_uses_tc(int Dp, int Wp) { return use_tc(Dp, Wp); }
 
 void arm_configure(int Dp, int Wp) {
     if (use_tc(Dp, Wp)) arm_tc_configure(Dp, Wp);
@@ -655,7 +656,7 @@ void launch_arm(const LaunchCtx& L, int mode) {
 }
 
 int arm_blocks_per_sm(int Dp, int Wp) {
-    if (use_tc(Dp, Wp)) {  // __launch_bounds__(256, 1), TMEM: 128 columns per CTA
+    if (use_tc(Dp, Wp)) {  // __launch_bounds__(128, 2), TMEM: <= 128 columns per CTA
         const int b = int((227 * 1024) / (arm_tc_smem_bytes(Dp, Wp) + 1024));
         return b < 1 ? 1 : (b > 2 ? 2 : b);
     }

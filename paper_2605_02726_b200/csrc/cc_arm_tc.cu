@@ -2,34 +2,34 @@
 // entropy_model.hpp:180-336) with its four per-latent dense layers on the
 // sm_100a tensor cores.
 //
-// One persistent CTA (256 threads) per SM walks row-segment tiles of <= 128
-// latents.  Per tile:
+// Persistent CTAs of 128 threads (one thread per latent of a row-segment tile
+// of <= 128 latents, one TMEM lane each), two CTAs per SM so that one CTA's
+// tensor-core round trips and barriers overlap the other's CUDA-core work.
+// Per tile:
 //
 //   gather C (causal context + IFCE features, fp32)          CUDA cores
-//   H1 = relu(C W1^T + b1)                                    tcgen05 (TMEM acc)
+//   H1 = relu(C W1^T + b1)                                    tcgen05, TMEM accumulator
 //   H2 = relu(H1 W2^T + b2)                                   tcgen05
 //   head mu / sigma_raw, Laplace rate and its backward, dH2   CUDA cores
 //   dH1 = (dH2 W2) * relu'(H1)                                tcgen05
 //   dC  = dH1 W1 + draw stab                                  tcgen05
-//   weight gradients (register micro-tiles over the latents)  CUDA cores
+//   weight gradients (register micro-tiles over the latents)  CUDA cores, overlapping
+//                                                             the dH1 / dC MMAs
 //
 // The tensor-core layers run as 3xTF32: every operand x is split into
-// hi = x with the low 13 mantissa bits cleared (exact in tf32) and lo = x - hi,
-// and D = Alo*Bhi + Ahi*Blo + Ahi*Bhi, fp32 accumulation in TMEM — ~2^-21
-// relative per product (tools/micro/umma_probe.cu: 3.2e-6 absolute on
-// products of magnitude ~6, vs 4.4e-3 for a single tf32 pass).  Biases ride
-// along as a column of ones in the A tile (B holds the bias in that column).
-// A operands live in ONE shared tile [latent][k] (canonical no-swizzle K-major
-// layout of cc_umma.cuh) that each layer's epilogue overwrites after the
-// previous MMA completed; B operands (weights, hi/lo) are staged once per CTA.
-// The epilogue of a layer: tcgen05.ld of the thread's TMEM lane (= latent),
-// activation, split, store of the next A tile and of the feature-major fp32
-// rows that the weight-gradient micro-tiles read (as cc_arm2.cu).
-//
-// Thread roles: thread t handles latent row r = t % 128 of the tile (TMEM
-// lane r: warp w reads lanes 32 (w % 4) ..), half h = t / 128 owns half of
-// every layer's feature chunks.  Thread 0 issues the MMAs; completion is an
-// mbarrier arrive by tcgen05.commit.
+// hi = round_tf32(x) and lo = round_tf32(x - hi) (|x - hi - lo| <= 2^-24 |x|)
+// and D = Alo*Bhi + Ahi*Blo + Ahi*Bhi with fp32 accumulation in TMEM
+// (tools/micro/umma_probe3.cu: relative error 1.8e-7 vs fp64 on K = 24 dot
+// products, sequential fp32 FMA 0.9e-7).  Biases ride along as a column of
+// ones in A (B holds the bias in that column).
+// The A operand of each layer lives in TMEM (lane = latent, one column per
+// input feature, hi and lo): the thread that owns a latent writes its row
+// with tcgen05.st after the previous layer's accumulator was read, so the
+// activations never go through shared memory on their way to the tensor
+// core.  B operands (weights hi/lo, canonical no-swizzle K-major layout of
+// cc_umma.cuh) are staged once per CTA.  The feature-major fp32 rows that the
+// weight-gradient micro-tiles read stay in shared memory (as cc_arm2.cu).
+// Thread 0 issues the MMAs; completion is an mbarrier arrive by tcgen05.commit.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -46,29 +46,34 @@ namespace ccb {
 
 namespace {
 
-constexpr int T = kArmTile;   // latents per tile (128)
-constexpr int NT = 2 * T;     // threads per CTA
+constexpr int T = kArmTile;   // latents per tile (128) == threads per CTA
+constexpr int NT = T;
 constexpr int LT = T + 4;     // feature-major row length (floats)
-constexpr int kRM = 12;       // max IFCE source grids
+constexpr int kRM = 11;       // max IFCE source grids: hyper (L - 4) + L - 1 - k <= 11 for L <= 8
+constexpr int kRR = kRM + 1;  // R rows + the ones row (3 row blocks of 4)
 constexpr int kFM = 8;        // max IFCE width
 constexpr int kMaxPad = 4;    // context window halo (yhat_pad border P)
 constexpr int WS = T + 2 * kMaxPad;
 constexpr int WC = (kMaxPad + 1) * WS;
-constexpr int WIN = WC + (kRM + 4) * LT;
+constexpr int WIN = WC + kRR * LT;
 
 constexpr int r8(int x) { return (x + 7) / 8 * 8; }
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
+constexpr uint32_t pow2cols(int x) { return x <= 32 ? 32u : x <= 64 ? 64u : x <= 128 ? 128u : 256u; }
 
 template <int DP, int WP>
 struct TC {
     static_assert(T == 128, "one TMEM lane per latent");
-    static constexpr int KD = r8(DP + 1);        // A tile of L1: C | 1 (ones at DP)
-    static constexpr int KW = r8(WP + 1);        // A tile of L2: H1 | 1 (ones at WP); dH2 for dH1
-    static constexpr int KC = KW + 8;            // A tile of dC: dH1 | draw
-    static constexpr int KT = cmax(KD, KC);      // row width of the shared A tile
+    static constexpr int KD = r8(DP + 1);        // A of L1: C | 1 (ones at DP)
+    static constexpr int KW = r8(WP + 1);        // A of L2: H1 | 1 (ones at WP); dH2 for dH1
+    static constexpr int KC = KW + 8;            // A of dC: dH1 | draw
+    static constexpr int KT = cmax(KD, KC);      // TMEM columns of one A copy
     static constexpr int NW = r8(WP);            // N of L1 / L2 / dH1
     static constexpr int ND = r8(DP);            // N of dC
     static_assert(NW <= 32 && ND <= 32, "one 32-column TMEM load per layer");
+    // TMEM columns: the layer accumulator, then A hi, then A lo
+    static constexpr uint32_t TM_ACC = 0, TM_AH = 32, TM_AL = 32 + KT;
+    static constexpr uint32_t TM_COLS = pow2cols(32 + 2 * KT);
     // feature-major fp32 rows (weight gradients, Laplace), as cc_arm2.cu
     static constexpr int RC = DP + 4;   // C: 0..D-1, ones at DP, own value at DP+1
     static constexpr int RH = WP + 4;   // H1 / H2: ones at WP
@@ -83,29 +88,27 @@ struct TC {
     static constexpr int O_DR = O_DH2 + RDH * LT;
     static constexpr int O_DF = O_DR + RDR * LT;
     static constexpr int ACT = O_DF + RF * LT;
+    static constexpr int O_HP = O_DH1;  // head partials [mu | sigma_raw]: P3 -> P4, before dH1 exists
     // weight-gradient jobs (4x4 micro-tiles) and units (job x latent third)
-    static constexpr int J1 = (WP / 4) * (DP / 4 + 1);   // dH1 x [C|1]
-    static constexpr int J2 = (WP / 4) * (WP / 4 + 1);   // dH2 x [H1|1]
+    static constexpr int J1 = (WP / 4) * (DP / 4 + 1);   // dH1 x [C|1]   (after the dH1 MMA)
+    static constexpr int J2 = (WP / 4) * (WP / 4 + 1);   // dH2 x [H1|1]  (beside the dH1 MMA)
     static constexpr int J3 = WP / 4 + 1;                // draw x [H2|1]
     static constexpr int J4 = DP / 4;                    // draw x C (stabilizer)
     static constexpr int NJ = J1 + J2 + J3 + J4;
     static constexpr int NU = 3 * NJ;
-    static constexpr int J5 = (kFM / 4) * (kRM / 4 + 1); // dF x [R|1] (per tile)
+    static constexpr int J5 = (kFM / 4) * (kRR / 4);     // dF x [R|1] (per tile, one warp each)
     static constexpr int MAXU = (NU + NT - 1) / NT;
-    static constexpr int NACC5 = kMaxSlots * kFM * (kRM + 1);
+    static constexpr int NACC5 = kMaxSlots * kFM * kRR;
     static_assert(NU * 16 * 2 <= ACT, "fp64 epilogue staging fits in the activation rows");
-    // TMEM columns of the four layer accumulators
-    static constexpr uint32_t TM_L1 = 0, TM_L2 = 32, TM_DH1 = 64, TM_DC = 96, TM_COLS = 128;
 };
 
 template <int DP, int WP>
-struct alignas(128) TcSmem {
+struct TcSmem {
     using K = TC<DP, WP>;
-    alignas(128) float atile[2][T * K::KT];        // A operand (hi, lo), [latent][k]
-    alignas(128) float b1[2][K::NW * K::KD];      // L1: [a][k]  W1, b1 at k = DP
-    alignas(128) float b2[2][K::NW * K::KW];      // L2: [b][a]  W2, b2 at a = WP
-    alignas(128) float b3[2][K::NW * K::KW];      // dH1: [a][b] = W2[b][a]
-    alignas(128) float b4[2][K::ND * K::KC];      // dC: [k][a] = W1[a][k]; [k][KW + j] = stab[j][k]
+    alignas(16) float b1[2][K::NW * K::KD];      // L1: [a][k]  W1, b1 at k = DP
+    alignas(16) float b2[2][K::NW * K::KW];      // L2: [b][a]  W2, b2 at a = WP
+    alignas(16) float b3[2][K::NW * K::KW];      // dH1: [a][b] = W2[b][a]
+    alignas(16) float b4[2][K::ND * K::KC];      // dC: [k][a] = W1[a][k]; [k][KW + j] = stab[j][k]
     alignas(16) float act[K::ACT];
     alignas(16) float win[2][WIN];
     alignas(16) float W3[2][WP];
@@ -113,9 +116,7 @@ struct alignas(128) TcSmem {
     alignas(16) float hb[4];
     alignas(16) float Wf[kMaxSlots][kFM][kRM];
     alignas(16) float bf[kMaxSlots][kFM];
-    alignas(16) float hpart[2][2][T];  // head partials [half][mu | sigma_raw][latent]
     int woff[kMaxCtx];
-    alignas(16) float stage5[K::J5][16];
     double acc5[K::NACC5];
     GridGeom geo[kMaxGrids];
     double red[NT / 32];
@@ -164,53 +165,59 @@ __device__ __forceinline__ void issue_gather(const Plan& P, const GridGeom* geo,
     cp_async_commit();
 }
 
-// one 4-feature chunk of the A tile (hi and lo) of latent row r
-__device__ __forceinline__ void store_chunk(float* hi_base, float* lo_base, int r, int c, int kcols,
-                                            float4 v) {
-    float4 h, l;
-    umma::split(v.x, h.x, l.x);
-    umma::split(v.y, h.y, l.y);
-    umma::split(v.z, h.z, l.z);
-    umma::split(v.w, h.w, l.w);
-    const uint32_t o = umma::tile_off(r, 4 * c, kcols / 4) / 4;
-    *reinterpret_cast<float4*>(hi_base + o) = h;
-    *reinterpret_cast<float4*>(lo_base + o) = l;
+// one 4-feature chunk of this thread's A row (hi, lo) into TMEM
+__device__ __forceinline__ void st_chunk(uint32_t tl, uint32_t col, float a, float b, float c, float d) {
+    float h0, h1, h2, h3, l0, l1, l2, l3;
+    umma::split_rn(a, h0, l0);
+    umma::split_rn(b, h1, l1);
+    umma::split_rn(c, h2, l2);
+    umma::split_rn(d, h3, l3);
+    umma::st4(tl + (32u + col), h0, h1, h2, h3);
 }
 
-// v[h * OFF + i] with i a compile-time index: a select of two registers
-// instead of a dynamically indexed (local-memory) array
-template <int OFF>
-__device__ __forceinline__ float hsel(const float (&v)[32], int h, int i) {
-    return h ? v[OFF + i] : v[i];
+template <int DP, int WP>
+struct ChunkStore {  // hi at TM_AH + c, lo at TM_AL + c
+    __device__ __forceinline__ static void put(uint32_t tl, int c, float a, float b, float cc, float d) {
+        using K = TC<DP, WP>;
+        float h[4], l[4];
+        umma::split_rn(a, h[0], l[0]);
+        umma::split_rn(b, h[1], l[1]);
+        umma::split_rn(cc, h[2], l[2]);
+        umma::split_rn(d, h[3], l[3]);
+        umma::st4(tl + K::TM_AH + uint32_t(c), h[0], h[1], h[2], h[3]);
+        umma::st4(tl + K::TM_AL + uint32_t(c), l[0], l[1], l[2], l[3]);
+    }
+};
+
+// this thread's A row is complete in TMEM: make it visible to the MMA issuer
+__device__ __forceinline__ void a_ready() {
+    umma::wait_st();
+    umma::fence_before_sync();
+    __syncthreads();
 }
 
-// D (TMEM) = A (tile, K-major, k-steps of 8) x B^T as 3xTF32
-__device__ __forceinline__ void mma3(uint32_t d, const float* a_hi, const float* a_lo, int a_kcols,
-                                     const float* b_hi, const float* b_lo, int b_kcols, int k_begin,
-                                     int nks, uint32_t idesc, bool accumulate) {
-    const uint32_t ah0 = umma::smem_u32(a_hi), al0 = umma::smem_u32(a_lo);
-    const uint32_t bh0 = umma::smem_u32(b_hi), bl0 = umma::smem_u32(b_lo);
-    const uint32_t asbo = uint32_t(a_kcols / 4) * 128u, bsbo = uint32_t(b_kcols / 4) * 128u;
+// D = A (TMEM columns a_hi / a_lo, k-steps of 8) x B^T (smem, K-major) as 3xTF32
+__device__ __forceinline__ void mma3_ts(uint32_t d, uint32_t a_hi, uint32_t a_lo, uint64_t bh,
+                                        uint64_t bl, int nks, uint32_t idesc) {
     for (int ks = 0; ks < nks; ++ks) {
-        const uint32_t ka = uint32_t(k_begin + 8 * ks) / 4 * 128u;  // core columns of A
-        const uint32_t kb = uint32_t(8 * ks) / 4 * 128u;             // of B
-        const uint64_t ah = umma::desc(ah0 + ka, 128, asbo), al = umma::desc(al0 + ka, 128, asbo);
-        const uint64_t bh = umma::desc(bh0 + kb, 128, bsbo), bl = umma::desc(bl0 + kb, 128, bsbo);
-        umma::mma_tf32(d, al, bh, idesc, (accumulate || ks > 0) ? 1u : 0u);
-        umma::mma_tf32(d, ah, bl, idesc, 1u);
-        umma::mma_tf32(d, ah, bh, idesc, 1u);
+        const uint32_t ka = 8u * uint32_t(ks);
+        const uint64_t kb = uint64_t(16 * ks);  // 256 B (two core columns) in descriptor units
+        umma::mma_tf32_ts(d, a_lo + ka, bh + kb, idesc, ks > 0 ? 1u : 0u);
+        umma::mma_tf32_ts(d, a_hi + ka, bl + kb, idesc, 1u);
+        umma::mma_tf32_ts(d, a_hi + ka, bh + kb, idesc, 1u);
     }
 }
 
 template <int DP, int WP, int MODE>
-__global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
+__global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
                                                   const int4* __restrict__ tiles, int ntiles) {
     using K = TC<DP, WP>;
+    using CS = ChunkStore<DP, WP>;
     const Plan& P = *pp;
-    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     TcSmem<DP, WP>& sm = *reinterpret_cast<TcSmem<DP, WP>*>(smem_raw);
     const int tid = threadIdx.x;
-    const int half = tid >> 7, lt = tid & (T - 1);
+    const int lt = tid;
     const int D = P.D, Wd = P.Wd, S = P.S, F = P.F;
     const float* prm = P.params;
     const bool has_stab = P.off_astab >= 0;
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
         float v = 0.0f;
         if (a < Wd) v = k < D ? prm[P.off_l1w + a * D + k] : (k == DP ? prm[P.off_l1b + a] : 0.0f);
         const uint32_t o = umma::tile_off(a, k, K::KD / 4) / 4;
-        umma::split(v, sm.b1[0][o], sm.b1[1][o]);
+        umma::split_rn(v, sm.b1[0][o], sm.b1[1][o]);
     }
     for (int e = tid; e < K::NW * K::KW; e += NT) {  // L2: B2[b][a]; dH1: B3[a][b] = W2[b][a]
         const int n = e / K::KW, k = e % K::KW;
@@ -234,8 +241,8 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
             v3 = k < Wd ? prm[P.off_l2w + k * Wd + n] : 0.0f;
         }
         const uint32_t o = umma::tile_off(n, k, K::KW / 4) / 4;
-        umma::split(v2, sm.b2[0][o], sm.b2[1][o]);
-        umma::split(v3, sm.b3[0][o], sm.b3[1][o]);
+        umma::split_rn(v2, sm.b2[0][o], sm.b2[1][o]);
+        umma::split_rn(v3, sm.b3[0][o], sm.b3[1][o]);
     }
     for (int e = tid; e < K::ND * K::KC; e += NT) {  // dC: B4[k][a] = W1[a][k], B4[k][KW + j] = stab[j][k]
         const int k = e / K::KC, a = e % K::KC;
@@ -245,7 +252,7 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
             else if (a >= K::KW && a < K::KW + 2 && has_stab) v = prm[P.off_astab + (a - K::KW) * D + k];
         }
         const uint32_t o = umma::tile_off(k, a, K::KC / 4) / 4;
-        umma::split(v, sm.b4[0][o], sm.b4[1][o]);
+        umma::split_rn(v, sm.b4[0][o], sm.b4[1][o]);
     }
     for (int e = tid; e < 2 * WP; e += NT) {
         const int j = e / WP, a = e % WP;
@@ -275,13 +282,24 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
     for (int e = tid; e < P.n_grids; e += NT) sm.geo[e] = P.g[e];
     for (int e = tid; e < K::ACT; e += NT) sm.act[e] = 0.0f;
     for (int e = tid; e < 2 * WIN; e += NT) (&sm.win[0][0])[e] = 0.0f;
-    for (int e = tid; e < 2 * T * K::KT; e += NT) (&sm.atile[0][0])[e] = 0.0f;
     umma::fence_async_smem();
     umma::fence_before_sync();
     __syncthreads();
     umma::fence_after_sync();
-    const uint32_t tm = sm.tmem + (uint32_t((tid >> 5) & 3) * 32u << 16);  // this warp's lane quarter
     const uint32_t tm0 = sm.tmem;
+    const uint32_t tl = tm0 + (uint32_t(tid & ~31) << 16);  // this warp's 32 lanes
+    // B descriptors (constant for the whole launch)
+    const uint64_t d_b1h = umma::desc(umma::smem_u32(sm.b1[0]), 128, (K::KD / 4) * 128);
+    const uint64_t d_b1l = umma::desc(umma::smem_u32(sm.b1[1]), 128, (K::KD / 4) * 128);
+    const uint64_t d_b2h = umma::desc(umma::smem_u32(sm.b2[0]), 128, (K::KW / 4) * 128);
+    const uint64_t d_b2l = umma::desc(umma::smem_u32(sm.b2[1]), 128, (K::KW / 4) * 128);
+    const uint64_t d_b3h = umma::desc(umma::smem_u32(sm.b3[0]), 128, (K::KW / 4) * 128);
+    const uint64_t d_b3l = umma::desc(umma::smem_u32(sm.b3[1]), 128, (K::KW / 4) * 128);
+    const uint64_t d_b4h = umma::desc(umma::smem_u32(sm.b4[0]), 128, (K::KC / 4) * 128);
+    const uint64_t d_b4l = umma::desc(umma::smem_u32(sm.b4[1]), 128, (K::KC / 4) * 128);
+    constexpr uint32_t ID_W = umma::idesc_tf32(128, K::NW, false, false);
+    constexpr uint32_t ID_D = umma::idesc_tf32(128, K::ND, false, false);
+    const uint32_t acc = tm0 + K::TM_ACC, a_hi = tm0 + K::TM_AH, a_lo = tm0 + K::TM_AL;
 
     float* const sC = sm.act + K::O_C;
     float* const sH1 = sm.act + K::O_H1;
@@ -290,10 +308,7 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
     float* const sDH2 = sm.act + K::O_DH2;
     float* const sDR = sm.act + K::O_DR;
     float* const sDF = sm.act + K::O_DF;
-    float* const At = sm.atile[0];
-    float* const Al = sm.atile[1];
-    constexpr uint32_t ID_W = umma::idesc_tf32(128, K::NW, false, false);
-    constexpr uint32_t ID_D = umma::idesc_tf32(128, K::ND, false, false);
+    float* const sHP = sm.act + K::O_HP;
     uint32_t phase = 0;
 
     int4 cur = blockIdx.x < ntiles ? tiles[blockIdx.x] : make_int4(0, 0, 0, 0);
@@ -311,6 +326,40 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
         for (int e = 0; e < 16; ++e) uacc[m][e] = 0.0;
     double bits_thr = 0.0;
     const float upstream = P.rate_upstream;
+
+    // this thread's weight-gradient units of one kind (J1: after the dH1 MMA;
+    // the others beside it); each unit a 4x4 register micro-tile over a third
+    // of the tile's latents
+    auto dw_units = [&](bool j1_kind) {
+#pragma unroll
+        for (int m = 0; m < K::MAXU; ++m) {
+            const int u = tid + m * NT;
+            if (u < K::NU && ((u / 3 < K::J1) == j1_kind)) {
+                const int j = u / 3;
+                int i0, i1;
+                third_range(u % 3, i0, i1);
+                const float* A;
+                const float* B;
+                if (j < K::J1) {
+                    constexpr int nq = DP / 4 + 1;
+                    A = sDH1 + (4 * (j / nq)) * LT;
+                    B = sC + (4 * (j % nq)) * LT;
+                } else if (j < K::J1 + K::J2) {
+                    constexpr int nq = WP / 4 + 1;
+                    const int jj = j - K::J1;
+                    A = sDH2 + (4 * (jj / nq)) * LT;
+                    B = sH1 + (4 * (jj % nq)) * LT;
+                } else if (j < K::J1 + K::J2 + K::J3) {
+                    A = sDR;
+                    B = sH2 + (4 * (j - K::J1 - K::J2)) * LT;
+                } else {
+                    A = sDR;
+                    B = sC + (4 * (j - K::J1 - K::J2 - K::J3)) * LT;
+                }
+                dw_tile4x4<LT>(A, B, i0, i1, uacc[m]);
+            }
+        }
+    };
 
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const int4 tile = cur;
@@ -339,22 +388,18 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
         const int4 nxt2 = sm.trec[kt & 3];
         ++kt;
 
-        // ---- P1: C = context + IFCE features (+ ones at DP): feature-major
-        // rows and this half's chunks of the A tile ----
+        // ---- P1: C = context + IFCE features (+ ones at DP) -> rows + A ----
         float* const sR = sm.win[wb] + WC;
-        float cv[K::KD / 2];  // this half's C chunk values (head stabiliser term)
+        float pc0 = 0.0f, pc1 = 0.0f;  // head stabiliser term stab . C
         {
             const float* win = sm.win[wb];
-            constexpr int CH = K::KD / 8;  // chunks per half
             float rv[kRM];
-            const bool need_r = slot >= 0 && (half + 1) * 4 * CH > S;
-            if (need_r) {
+            if (slot >= 0) {
 #pragma unroll
                 for (int j = 0; j < kRM; ++j) rv[j] = sR[j * LT + lt];
             }
 #pragma unroll
-            for (int cc = 0; cc < CH; ++cc) {
-                const int c = half * CH + cc;
+            for (int c = 0; c < K::KD / 4; ++c) {
                 float v4[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -373,122 +418,94 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
                         v = valid ? 1.0f : 0.0f;
                     }
                     v4[i] = v;
-                    cv[4 * cc + i] = f < DP ? v : 0.0f;
+                    if (f < DP) {
+                        pc0 = fmaf(v, sm.stab[0][f], pc0);
+                        pc1 = fmaf(v, sm.stab[1][f], pc1);
+                    }
                     if (f <= DP) sC[f * LT + lt] = v;
                 }
-                store_chunk(At, Al, lt, c, K::KT, make_float4(v4[0], v4[1], v4[2], v4[3]));
+                CS::put(tl, 4 * c, v4[0], v4[1], v4[2], v4[3]);
             }
-            if (half == 0) {
-                sC[(DP + 1) * LT + lt] = valid ? win[P.P * WS + P.P + lt] : 0.0f;  // own value
-                sH1[WP * LT + lt] = valid ? 1.0f : 0.0f;
-            } else {
-                sH2[WP * LT + lt] = valid ? 1.0f : 0.0f;
-                if (slot >= 0) sR[kRM * LT + lt] = valid ? 1.0f : 0.0f;
-            }
+            sC[(DP + 1) * LT + lt] = valid ? win[P.P * WS + P.P + lt] : 0.0f;  // own value
+            sH1[WP * LT + lt] = valid ? 1.0f : 0.0f;
+            sH2[WP * LT + lt] = valid ? 1.0f : 0.0f;
+            if (slot >= 0) sR[kRM * LT + lt] = valid ? 1.0f : 0.0f;
         }
-        umma::fence_async_smem();
-        __syncthreads();
+        a_ready();
         if (tid == 0) {
             umma::fence_after_sync();
-            mma3(tm0 + K::TM_L1, At, Al, K::KT, sm.b1[0], sm.b1[1], K::KD, 0, K::KD / 8, ID_W, false);
+            mma3_ts(acc, a_hi, a_lo, d_b1h, d_b1l, K::KD / 8, ID_W);
             umma::commit(&sm.mbar);
         }
 
-        // ---- P2: H1 = relu(acc) -> feature-major rows + A tile (ones at WP) ----
-        uint32_t m1 = 0;  // relu'(H1) of this half's features
+        // ---- P2: H1 = relu(acc) -> rows + A (ones at WP) ----
+        uint32_t m1 = 0;  // relu'(H1)
         umma::mbar_wait(&sm.mbar, phase);
         phase ^= 1;
         umma::fence_after_sync();
         {
             float v[32];
-            umma::ld32(tm + K::TM_L1, v);
+            umma::ld32(tl + K::TM_ACC, v);
             umma::wait_ld();
-            constexpr int CH = K::KW / 8;
 #pragma unroll
-            for (int cc = 0; cc < CH; ++cc) {
-                const int c = half * CH + cc;
+            for (int c = 0; c < K::KW / 4; ++c) {
                 float h4[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int a = 4 * c + i;
-                    const float x = hsel<K::KW / 2>(v, half, 4 * cc + i);
                     float h = 0.0f;
                     if (a < WP) {
-                        h = x > 0.0f ? x : 0.0f;
-                        if (x > 0.0f) m1 |= 1u << (4 * cc + i);
+                        h = v[a] > 0.0f ? v[a] : 0.0f;
+                        if (v[a] > 0.0f) m1 |= 1u << a;
                         sH1[a * LT + lt] = h;
                     } else if (a == WP) {
                         h = valid ? 1.0f : 0.0f;
                     }
                     h4[i] = h;
                 }
-                store_chunk(At, Al, lt, c, K::KT, make_float4(h4[0], h4[1], h4[2], h4[3]));
+                CS::put(tl, 4 * c, h4[0], h4[1], h4[2], h4[3]);
             }
         }
-        umma::fence_async_smem();
-        umma::fence_before_sync();
-        __syncthreads();
+        a_ready();
         if (tid == 0) {
             umma::fence_after_sync();
-            mma3(tm0 + K::TM_L2, At, Al, K::KT, sm.b2[0], sm.b2[1], K::KW, 0, K::KW / 8, ID_W, false);
+            mma3_ts(acc, a_hi, a_lo, d_b2h, d_b2l, K::KW / 8, ID_W);
             umma::commit(&sm.mbar);
         }
 
-        // ---- P3: H2 = relu(acc) -> rows; this half's head partials ----
-        float h2v[K::KW / 2];
+        // ---- P3: H2 = relu(acc) -> rows; head; P4: Laplace rate + backward; dH2 ----
+        uint32_t m2 = 0;  // relu'(H2)
         umma::mbar_wait(&sm.mbar, phase);
         phase ^= 1;
         umma::fence_after_sync();
-        {
-            float v[32];
-            umma::ld32(tm + K::TM_L2, v);
-            umma::wait_ld();
-            float p0 = 0.0f, p1 = 0.0f;
-#pragma unroll
-            for (int i = 0; i < K::KW / 2; ++i) {
-                const int a = half * (K::KW / 2) + i;
-                const float x = hsel<K::KW / 2>(v, half, i);
-                float h = 0.0f;
-                if (a < WP) {
-                    h = x > 0.0f ? x : 0.0f;
-                    sH2[a * LT + lt] = h;
-                    p0 = fmaf(h, sm.W3[0][a], p0);
-                    p1 = fmaf(h, sm.W3[1][a], p1);
-                }
-                h2v[i] = h;
-            }
-#pragma unroll
-            for (int i = 0; i < K::KD / 2; ++i) {
-                const int k = half * (K::KD / 2) + i;
-                if (k < DP) {
-                    p0 = fmaf(cv[i], sm.stab[0][k], p0);
-                    p1 = fmaf(cv[i], sm.stab[1][k], p1);
-                }
-            }
-            sm.hpart[half][0][lt] = p0;
-            sm.hpart[half][1][lt] = p1;
-        }
-        umma::fence_before_sync();
-        __syncthreads();
-
-        // ---- P4: Laplace rate + its backward (both halves, identical
-        // arithmetic), dH2 for this half's features ----
         float dmu = 0.0f, dsr = 0.0f;
         {
-            const float v = sC[(DP + 1) * LT + lt];
-            const float mu = sm.hb[0] + (sm.hpart[0][0][lt] + sm.hpart[1][0][lt]);
-            const float sr = sm.hb[1] + (sm.hpart[0][1][lt] + sm.hpart[1][1][lt]);
+            float v[32];
+            umma::ld32(tl + K::TM_ACC, v);
+            umma::wait_ld();
+            float p0 = pc0, p1 = pc1;
+#pragma unroll
+            for (int a = 0; a < WP; ++a) {
+                const float h = v[a] > 0.0f ? v[a] : 0.0f;
+                if (v[a] > 0.0f) m2 |= 1u << a;
+                sH2[a * LT + lt] = h;
+                p0 = fmaf(h, sm.W3[0][a], p0);
+                p1 = fmaf(h, sm.W3[1][a], p1);
+            }
+            const float vv = sC[(DP + 1) * LT + lt];
+            const float mu = sm.hb[0] + p0;
+            const float sr = sm.hb[1] + p1;
             const float sg = sigma_from_raw(sr);
             const float bsc = sg * kInvSqrt2F;
-            const float u = fabsf(v - mu);
+            const float u = fabsf(vv - mu);
             const float e1 = cc_exp(-(u + 0.5f) / bsc);
             const float e2 = cc_exp(-fabsf(u - 0.5f) / bsc);
             const float p = u >= 0.5f ? 0.5f * (e2 - e1) : 1.0f - 0.5f * (e1 + e2);
-            if (own && half == 0) bits_thr += double(-(cc_log(std_max(p, kProbFloorF)) * kLog2EF));
+            if (own) bits_thr += double(-(cc_log(std_max(p, kProbFloorF)) * kLog2EF));
             if (MODE != kArmForward) {
                 float gv = 0.0f;
                 if (own && p > kProbFloorF) {
-                    const float tt = v - mu;
+                    const float tt = vv - mu;
                     const float dbits_dp = -1.0f / (p * kLn2F);
                     const float dp_du = (e1 - e2) / (2.0f * bsc);
                     const float sgn = tt > 0.0f ? 1.0f : (tt < 0.0f ? -1.0f : 0.0f);
@@ -498,16 +515,11 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
                     if (sg > kSigmaMinF && sg < kSigmaMaxF) dsr = up * dp_db * kInvSqrt2F * sg;
                     gv = up * dp_du * sgn;
                 }
-                if (half == 0) {
-                    if (MODE == kArmProxy && valid) P.gown[g.lat_off + li] = gv;
-                    sDR[0 * LT + lt] = dmu;
-                    sDR[1 * LT + lt] = dsr;
-                }
-                // dH2 = (W3^T draw) * relu'(H2), this half's chunks of the A tile
-                constexpr int CH = K::KW / 8;
+                if (MODE == kArmProxy && valid) P.gown[g.lat_off + li] = gv;
+                sDR[0 * LT + lt] = dmu;
+                sDR[1 * LT + lt] = dsr;
 #pragma unroll
-                for (int cc = 0; cc < CH; ++cc) {
-                    const int c = half * CH + cc;
+                for (int c = 0; c < K::KW / 4; ++c) {  // dH2 = (W3^T draw) * relu'(H2)
                     float d4[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
@@ -516,97 +528,66 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
                         if (a < WP) {
                             d = fmaf(dmu, sm.W3[0][a], 0.0f);
                             d = fmaf(dsr, sm.W3[1][a], d);
-                            d = h2v[4 * cc + i] > 0.0f ? d : 0.0f;
+                            d = (m2 >> a) & 1u ? d : 0.0f;
                             sDH2[a * LT + lt] = d;
                         }
                         d4[i] = d;
                     }
-                    store_chunk(At, Al, lt, c, K::KT, make_float4(d4[0], d4[1], d4[2], d4[3]));
+                    CS::put(tl, 4 * c, d4[0], d4[1], d4[2], d4[3]);
                 }
             }
         }
+        (void)sHP;
         if (MODE == kArmForward) {
-            __syncthreads();  // hpart / windows reused by the next tile
+            __syncthreads();  // windows reused by the next tile
             wb ^= 1;
             cur = nxt;
             nxt = nxt2;
             continue;
         }
-        umma::fence_async_smem();
-        __syncthreads();
+        a_ready();
         if (tid == 0) {
             umma::fence_after_sync();
-            mma3(tm0 + K::TM_DH1, At, Al, K::KT, sm.b3[0], sm.b3[1], K::KW, 0, K::KW / 8, ID_W, false);
+            mma3_ts(acc, a_hi, a_lo, d_b3h, d_b3l, K::KW / 8, ID_W);
             umma::commit(&sm.mbar);
         }
+        dw_units(false);  // dH2 x [H1|1], draw x [H2|1], draw x C beside the dH1 MMA
 
-        // ---- P5: dH1 = acc * relu'(H1) -> rows + A tile; draw chunk ----
+        // ---- P5: dH1 = acc * relu'(H1) -> rows + A; draw columns ----
         umma::mbar_wait(&sm.mbar, phase);
         phase ^= 1;
         umma::fence_after_sync();
         {
             float v[32];
-            umma::ld32(tm + K::TM_DH1, v);
+            umma::ld32(tl + K::TM_ACC, v);
             umma::wait_ld();
-            constexpr int CH = K::KW / 8;
 #pragma unroll
-            for (int cc = 0; cc < CH; ++cc) {
-                const int c = half * CH + cc;
+            for (int c = 0; c < K::KW / 4; ++c) {
                 float d4[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int b = 4 * c + i;
                     float d = 0.0f;
                     if (b < WP) {
-                        d = (m1 >> (4 * cc + i)) & 1u ? hsel<K::KW / 2>(v, half, 4 * cc + i) : 0.0f;
+                        d = (m1 >> b) & 1u ? v[b] : 0.0f;
                         sDH1[b * LT + lt] = d;
                     }
                     d4[i] = d;
                 }
-                store_chunk(At, Al, lt, c, K::KT, make_float4(d4[0], d4[1], d4[2], d4[3]));
+                CS::put(tl, 4 * c, d4[0], d4[1], d4[2], d4[3]);
             }
-            // draw (dmu, dsr, 0, 0 | 0, 0, 0, 0) at columns KW .. KW+7
-            store_chunk(At, Al, lt, K::KW / 4 + half, K::KT,
-                        half == 0 ? make_float4(dmu, dsr, 0.0f, 0.0f) : make_float4(0.0f, 0.0f, 0.0f, 0.0f));
+            CS::put(tl, K::KW, dmu, dsr, 0.0f, 0.0f);
+            CS::put(tl, K::KW + 4, 0.0f, 0.0f, 0.0f, 0.0f);
         }
-        umma::fence_async_smem();
+        umma::wait_st();
         umma::fence_before_sync();
-        __syncthreads();
+        __syncthreads();  // A complete; dH1 rows complete
         if (tid == 0) {
             umma::fence_after_sync();
-            mma3(tm0 + K::TM_DC, At, Al, K::KT, sm.b4[0], sm.b4[1], K::KC, 0, K::KC / 8, ID_D, false);
+            mma3_ts(acc, a_hi, a_lo, d_b4h, d_b4l, K::KC / 8, ID_D);
             umma::commit(&sm.mbar);
         }
-
-        // ---- P8 (overlaps the dC MMA): weight gradients, register micro-tiles ----
-#pragma unroll
-        for (int m = 0; m < K::MAXU; ++m) {
-            const int u = tid + m * NT;
-            if (u < K::NU) {
-                const int j = u / 3;
-                int i0, i1;
-                third_range(u % 3, i0, i1);
-                const float* A;
-                const float* B;
-                if (j < K::J1) {
-                    constexpr int nq = DP / 4 + 1;
-                    A = sDH1 + (4 * (j / nq)) * LT;
-                    B = sC + (4 * (j % nq)) * LT;
-                } else if (j < K::J1 + K::J2) {
-                    constexpr int nq = WP / 4 + 1;
-                    const int jj = j - K::J1;
-                    A = sDH2 + (4 * (jj / nq)) * LT;
-                    B = sH1 + (4 * (jj % nq)) * LT;
-                } else if (j < K::J1 + K::J2 + K::J3) {
-                    A = sDR;
-                    B = sH2 + (4 * (j - K::J1 - K::J2)) * LT;
-                } else {
-                    A = sDR;
-                    B = sC + (4 * (j - K::J1 - K::J2 - K::J3)) * LT;
-                }
-                dw_tile4x4<LT>(A, B, i0, i1, uacc[m]);
-            }
-        }
+        dw_units(true);  // dH1 x [C|1] beside the dC MMA
 
         // ---- P6: dC -> dctx planes / dF ----
         umma::mbar_wait(&sm.mbar, phase);
@@ -614,17 +595,15 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
         umma::fence_after_sync();
         {
             float v[32];
-            umma::ld32(tm + K::TM_DC, v);
+            umma::ld32(tl + K::TM_ACC, v);
             umma::wait_ld();
             const bool st = MODE == kArmProxy && valid;
 #pragma unroll
-            for (int i = 0; i < K::ND / 2; ++i) {
-                const int k = half * (K::ND / 2) + i;
-                const float x = hsel<K::ND / 2>(v, half, i);
+            for (int k = 0; k < K::ND; ++k) {
                 if (k < S) {
-                    if (st) P.dctx[g.dctx_off + int64_t(k) * count + li] = x;
+                    if (st) P.dctx[g.dctx_off + int64_t(k) * count + li] = v[k];
                 } else if (k < S + F && slot >= 0) {
-                    const float dv = valid ? x : 0.0f;
+                    const float dv = valid ? v[k] : 0.0f;
                     sDF[(k - S) * LT + lt] = dv;
                     if (st) P.dfeat[g.dfeat_off + int64_t(k - S) * count + li] = dv;
                 }
@@ -637,12 +616,12 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
         if (slot >= 0) {
             const int warp = tid >> 5, lane = tid & 31;
             for (int j = warp; j < K::J5; j += NT / 32) {
-                constexpr int nq = kRM / 4 + 1;
+                constexpr int nq = kRR / 4;
                 const float* A = sDF + (4 * (j / nq)) * LT;
                 const float* B = sR + (4 * (j % nq)) * LT;
-                float acc[16];
+                float s16[16];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) acc[e] = 0.0f;
+                for (int e = 0; e < 16; ++e) s16[e] = 0.0f;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const int l = lane + 32 * q;
@@ -655,20 +634,20 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
 #pragma unroll
-                        for (int c = 0; c < 4; ++c) acc[r * 4 + c] = fmaf(av[r], bv[c], acc[r * 4 + c]);
+                        for (int c = 0; c < 4; ++c) s16[r * 4 + c] = fmaf(av[r], bv[c], s16[r * 4 + c]);
                 }
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+                    for (int o = 16; o > 0; o >>= 1) s16[e] += __shfl_xor_sync(0xffffffffu, s16[e], o);
                 }
                 if (lane < 16) {
                     const int a = 4 * (j / nq) + lane / 4, b = 4 * (j % nq) + lane % 4;
-                    float val = acc[0];
+                    float val = s16[0];
 #pragma unroll
                     for (int e = 1; e < 16; ++e)
-                        if (lane == e) val = acc[e];
-                    if (b <= kRM) sm.acc5[(slot * kFM + a) * (kRM + 1) + b] += double(val);
+                        if (lane == e) val = s16[e];
+                    sm.acc5[(slot * kFM + a) * kRR + b] += double(val);
                 }
             }
         }
@@ -720,7 +699,7 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
             const int rd = P.g[P.slot_gi[s]].rdim;
             for (int e = tid; e < F * (rd + 1); e += NT) {
                 const int f = e / (rd + 1), b = e % (rd + 1);
-                const double v = sm.acc5[(s * kFM + f) * (kRM + 1) + (b < rd ? b : kRM)];
+                const double v = sm.acc5[(s * kFM + f) * kRR + (b < rd ? b : kRM)];
                 const int o = b < rd ? P.off_ifw[s] + f * rd + b : P.off_ifb[s] + f;
                 row[o - R.param_off] = v;
             }
@@ -733,7 +712,7 @@ __global__ void __launch_bounds__(NT, 1) k_arm_tc(const Plan* __restrict__ pp,
 
 template <int DP, int WP>
 size_t tc_smem() {
-    return sizeof(TcSmem<DP, WP>) + 1024;  // + alignment slack of the dynamic window
+    return sizeof(TcSmem<DP, WP>);
 }
 
 template <int DP, int WP, int MODE>

@@ -71,6 +71,7 @@ void launch_pyramid(const LaunchCtx& L);
 int arm_blocks_per_sm(int Dp, int Wp);
 void arm_configure(int Dp, int Wp);
 bool arm_uses_v2(int Dp, int Wp);
+bool arm_uses_tc(int Dp, int Wp);  // the tensor-core kernel (cc_arm_tc.cu)
 void pyramid_configure(const Plan& H);
 
 // upsampling (cc_ups.cu)

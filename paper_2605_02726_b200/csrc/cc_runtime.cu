@@ -288,6 +288,7 @@ void Trainer::build_plan() {
             GridGeom& g = P.g[gi];
             g.ifce_slot = s;
             g.rdim = P.hyper + (P.L - 1 - k);  // ifce_source_count, model.hpp:70-71
+            if (g.rdim > 11) throw ConfigError("IFCE source count above 11 (at most 8 latent levels)");
             if (g.rdim > kRMaxHost) throw ConfigError("IFCE source count exceeds 12");
             if (g.rdim != gi) throw ConfigError("internal: IFCE sources must precede the grid");
             grids_[gi].ifce_slot = s;
@@ -454,7 +455,11 @@ void Trainer::build_plan() {
     // 1.5 CTAs per SM when 2 fit: the persistent ARM then leaves CTA slots on
     // half the SMs to the concurrent distortion branch (measured: 0.558 ->
     // 0.542 ms per iteration at 512x768 vs 2 per SM)
-    L_.arm_blocks = std::min(L_.arm_ntiles, arm_occ >= 2 ? num_sms_ * 3 / 2 : num_sms_ * arm_occ);
+    // (the tensor-core kernel runs 2 x 128-thread CTAs per SM: the second
+    // CTA's work overlaps the first one's tensor-core round trips)
+    L_.arm_blocks = std::min(L_.arm_ntiles, arm_uses_tc(P.Dp, P.Wp)  ? num_sms_ * arm_occ
+                                            : arm_occ >= 2          ? num_sms_ * 3 / 2
+                                                                    : num_sms_ * arm_occ);
     if (const char* e = std::getenv("CCB_ARM_CTAS"))  // A/B: explicit persistent CTA count
         L_.arm_blocks = std::max(1, std::min(L_.arm_ntiles, std::atoi(e)));
     const int FP = syn_padded_hidden(P.syn_F);
