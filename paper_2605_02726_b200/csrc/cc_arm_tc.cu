@@ -96,7 +96,7 @@ struct TC {
     static constexpr int J4 = DP / 4;                    // draw x C (stabilizer)
     static constexpr int NJ = J1 + J2 + J3 + J4;
     static constexpr int NU = 3 * NJ;
-    static constexpr int J5 = (kFM / 4) * (kRR / 4);     // dF x [R|1] (per tile, one warp each)
+    static constexpr int J5 = (kFM / 4) * (kRR / 4);     // dF x [R|1] (per tile, 8 latent slices each)
     static constexpr int MAXU = (NU + NT - 1) / NT;
     static constexpr int NACC5 = kMaxSlots * kFM * kRR;
     static_assert(NU * 16 * 2 <= ACT, "fp64 epilogue staging fits in the activation rows");
@@ -118,6 +118,7 @@ struct TcSmem {
     alignas(16) float bf[kMaxSlots][kFM];
     int woff[kMaxCtx];
     double acc5[K::NACC5];
+    alignas(16) float st5[K::J5 * 8][16];  // IFCE dW slice partials of one tile
     GridGeom geo[kMaxGrids];
     double red[NT / 32];
     alignas(16) int4 trec[4];
@@ -165,25 +166,15 @@ __device__ __forceinline__ void issue_gather(const Plan& P, const GridGeom* geo,
     cp_async_commit();
 }
 
-// one 4-feature chunk of this thread's A row (hi, lo) into TMEM
-__device__ __forceinline__ void st_chunk(uint32_t tl, uint32_t col, float a, float b, float c, float d) {
-    float h0, h1, h2, h3, l0, l1, l2, l3;
-    umma::split_rn(a, h0, l0);
-    umma::split_rn(b, h1, l1);
-    umma::split_rn(c, h2, l2);
-    umma::split_rn(d, h3, l3);
-    umma::st4(tl + (32u + col), h0, h1, h2, h3);
-}
-
 template <int DP, int WP>
 struct ChunkStore {  // hi at TM_AH + c, lo at TM_AL + c
     __device__ __forceinline__ static void put(uint32_t tl, int c, float a, float b, float cc, float d) {
         using K = TC<DP, WP>;
         float h[4], l[4];
-        umma::split_rn(a, h[0], l[0]);
-        umma::split_rn(b, h[1], l[1]);
-        umma::split_rn(cc, h[2], l[2]);
-        umma::split_rn(d, h[3], l[3]);
+        umma::split_rn_fast(a, h[0], l[0]);
+        umma::split_rn_fast(b, h[1], l[1]);
+        umma::split_rn_fast(cc, h[2], l[2]);
+        umma::split_rn_fast(d, h[3], l[3]);
         umma::st4(tl + K::TM_AH + uint32_t(c), h[0], h[1], h[2], h[3]);
         umma::st4(tl + K::TM_AL + uint32_t(c), l[0], l[1], l[2], l[3]);
     }
@@ -611,44 +602,27 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
         }
         umma::fence_before_sync();
         __syncthreads();
-        // ---- P9: IFCE weight gradient dF x [R|1]: one warp per 4x4 job,
-        // lanes over latents, fixed shuffle tree, fp64 per slot ----
+        // ---- P9: IFCE weight gradient dF x [R|1]: 6 4x4 jobs x 8 slices of
+        // 16 latents (48 threads), slices summed in order, fp64 per slot ----
         if (slot >= 0) {
-            const int warp = tid >> 5, lane = tid & 31;
-            for (int j = warp; j < K::J5; j += NT / 32) {
-                constexpr int nq = kRR / 4;
-                const float* A = sDF + (4 * (j / nq)) * LT;
-                const float* B = sR + (4 * (j % nq)) * LT;
-                float s16[16];
+            constexpr int nq = kRR / 4;
+            if (tid < K::J5 * 8) {
+                const int j = tid >> 3, sl = tid & 7;
+                float part[16];
 #pragma unroll
-                for (int e = 0; e < 16; ++e) s16[e] = 0.0f;
+                for (int e = 0; e < 16; ++e) part[e] = 0.0f;
+                dw_tile4x4<LT>(sDF + (4 * (j / nq)) * LT, sR + (4 * (j % nq)) * LT, 16 * sl, 16 * sl + 16, part);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int l = lane + 32 * q;
-                    float av[4], bv[4];
+                for (int e = 0; e < 16; ++e) sm.st5[tid][e] = part[e];
+            }
+            __syncthreads();
+            if (tid < K::J5 * 16) {
+                const int j = tid >> 4, q = tid & 15;
+                float v = sm.st5[8 * j][q];
 #pragma unroll
-                    for (int r = 0; r < 4; ++r) {
-                        av[r] = A[r * LT + l];
-                        bv[r] = B[r * LT + l];
-                    }
-#pragma unroll
-                    for (int r = 0; r < 4; ++r)
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) s16[r * 4 + c] = fmaf(av[r], bv[c], s16[r * 4 + c]);
-                }
-#pragma unroll
-                for (int e = 0; e < 16; ++e) {
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) s16[e] += __shfl_xor_sync(0xffffffffu, s16[e], o);
-                }
-                if (lane < 16) {
-                    const int a = 4 * (j / nq) + lane / 4, b = 4 * (j % nq) + lane % 4;
-                    float val = s16[0];
-#pragma unroll
-                    for (int e = 1; e < 16; ++e)
-                        if (lane == e) val = s16[e];
-                    sm.acc5[(slot * kFM + a) * kRR + b] += double(val);
-                }
+                for (int sl = 1; sl < 8; ++sl) v += sm.st5[8 * j + sl][q];
+                const int a = 4 * (j / nq) + q / 4, b = 4 * (j % nq) + q % 4;
+                sm.acc5[(slot * kFM + a) * kRR + b] += double(v);
             }
         }
         __syncthreads();  // windows / dF rows reused by the next tile
