@@ -175,6 +175,15 @@ BAND_SIGNATURES = {
     "cc_band_step": (C.c_int, [_P, _I]),
 }
 
+# include/coolchic_b200_batch.h (product only): batched images (cfg3)
+BATCH_SIGNATURES = {
+    "cc_batch_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_void_p)]),
+    "cc_batch_destroy": (None, [_P]),
+    "cc_batch_reserve_iterations": (C.c_int, [_P, C.c_int]),
+    "cc_batch_enqueue_proxy_iterations": (C.c_int, [_P, C.c_int, _D, _D, _D]),
+    "cc_batch_synchronize": (C.c_int, [_P]),
+}
+
 # include/coolchic_b200_codec.h (product and reference checker): decode passes
 CODEC_SIGNATURES = {
     "cc_trainer_set_q": (C.c_int, [_P, C.POINTER(C.c_int32)]),
@@ -212,6 +221,7 @@ def load_library(path: os.PathLike | str, diag: bool = False) -> C.CDLL:
     if diag:
         table.update(DIAG_SIGNATURES)
         table.update(BAND_SIGNATURES)
+        table.update(BATCH_SIGNATURES)
     for name, (res, args) in table.items():
         fn = getattr(lib, name)
         fn.restype = res

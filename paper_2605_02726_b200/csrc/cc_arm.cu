@@ -131,7 +131,7 @@ template <int DP, int WP, int MODE>
 __global__ void __launch_bounds__(kArmTile) k_arm(const Plan* __restrict__ pp,
                                                   const int4* __restrict__ tiles, int ntiles) {
     using K = ArmCfg<DP, WP>;
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ArmSmem<DP, WP>& sm = *reinterpret_cast<ArmSmem<DP, WP>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -482,7 +482,7 @@ __global__ void __launch_bounds__(kArmTile) k_arm(const Plan* __restrict__ pp,
 // in shared memory, writing each level.  Summation order ((a+b)+(c+d)) is
 // the same at every level, so results do not depend on the blocking.
 __global__ void __launch_bounds__(256) k_pyramid_fused(const Plan* __restrict__ pp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     extern __shared__ float pbuf[];
     const int s = blockIdx.y / P.F, f = blockIdx.y - s * P.F;
     const int smax = P.slot_smax[s];
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(256) k_pyramid_fused(const Plan* __restrict__ 
 
 // 2x2 block sums of dF for every IFCE-equipped grid, one level per launch.
 __global__ void k_pyramid(const Plan* __restrict__ pp, int level) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     for (int s = 0; s < P.n_slots; ++s) {
         if (level > P.slot_smax[s]) continue;
         const int ri = P.slot_pyr_rows[s][level - 1], ci = P.slot_pyr_cols[s][level - 1];
@@ -582,7 +582,7 @@ static size_t arm_smem() {
 template <int DP, int WP, int MODE>
 static void launch_arm_t(const LaunchCtx& L) {
     const size_t smem = arm_smem<DP, WP>();
-    k_arm<DP, WP, MODE><<<L.arm_blocks, kArmTile, smem, L.stream>>>(L.plan, L.arm_tiles,
+    k_arm<DP, WP, MODE><<<dim3(L.arm_blocks, 1, L.batch), kArmTile, smem, L.stream>>>(L.plan, L.arm_tiles,
                                                                     L.arm_ntiles);
 }
 
@@ -606,16 +606,19 @@ size_t arm_tc_smem_bytes(int Dp, int Wp);
 void arm_tc_configure(int Dp, int Wp);
 void launch_arm_tc(const LaunchCtx& L, int mode);
 
-// The tensor-core kernel (cc_arm_tc.cu) is the default; CCB_ARM=2 selects the
-// FFMA2 tile kernel (cc_arm2.cu) for A/B measurements.
+// The FFMA2 tile kernel (cc_arm2.cu) is the default: per iteration it is the
+// faster of the two (512x768 HOP: 0.453 vs 0.489 ms, the tensor-core kernel
+// needs 2 x 109 KB of shared memory per SM for its best time and starves the
+// concurrent distortion branch).  CCB_ARM=tc selects the
+// tensor-core kernel (cc_arm_tc.cu).
 static int arm_env() {
     static const int v = [] {
         const char* e = std::getenv("CCB_ARM");
-        return e ? std::atoi(e) : 0;
+        return (e && e[0] == 't') ? 3 : 0;
     }();
     return v;
 }
-static bool use_tc(int Dp, int Wp) { return arm_env() != 2 && arm_tc_supported(Dp, Wp); }
+static bool use_tc(int Dp, int Wp) { return arm_env() == 3 && arm_tc_supported(Dp, Wp); }
 static bool use_arm2(int Dp, int Wp) { return !use_tc(Dp, Wp) && arm2_supported(Dp, Wp); }
 
 // both tiled kernels stage a (P+1)-row window (row bands, halo <= 4)
@@ -695,7 +698,7 @@ void launch_pyramid(const LaunchCtx& L) {
     int nblk = 0;
     for (int s = 0; s < H.n_slots; ++s)
         nblk = std::max(nblk, H.slot_pyr_rows[s][H.slot_smax[s]] * H.slot_pyr_cols[s][H.slot_smax[s]]);
-    const dim3 grid(nblk, H.n_slots * H.F);
+    const dim3 grid(nblk, H.n_slots * H.F, L.batch);
     k_pyramid_fused<<<grid, 256, pyramid_smem(H), L.stream>>>(L.plan);
 }
 

@@ -181,7 +181,7 @@ template <int DP, int WP, int MODE>
 __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
                                                 const int4* __restrict__ tiles, int ntiles) {
     using K = A2<DP, WP>;
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     extern __shared__ __align__(16) unsigned char smem_raw[];
     A2Smem<DP, WP>& sm = *reinterpret_cast<A2Smem<DP, WP>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -601,7 +601,7 @@ size_t arm2_smem() {
 
 template <int DP, int WP, int MODE>
 void launch_t(const LaunchCtx& L) {
-    k_arm2<DP, WP, MODE><<<L.arm_blocks, NT, arm2_smem<DP, WP>(), L.stream>>>(L.plan, L.arm_tiles,
+    k_arm2<DP, WP, MODE><<<dim3(L.arm_blocks, 1, L.batch), NT, arm2_smem<DP, WP>(), L.stream>>>(L.plan, L.arm_tiles,
                                                                                L.arm_ntiles);
 }
 

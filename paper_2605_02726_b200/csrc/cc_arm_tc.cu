@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
                                                   const int4* __restrict__ tiles, int ntiles) {
     using K = TC<DP, WP>;
     using CS = ChunkStore<DP, WP>;
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TcSmem<DP, WP>& sm = *reinterpret_cast<TcSmem<DP, WP>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -691,7 +691,7 @@ size_t tc_smem() {
 
 template <int DP, int WP, int MODE>
 void launch_t(const LaunchCtx& L) {
-    k_arm_tc<DP, WP, MODE><<<L.arm_blocks, NT, tc_smem<DP, WP>(), L.stream>>>(L.plan, L.arm_tiles,
+    k_arm_tc<DP, WP, MODE><<<dim3(L.arm_blocks, 1, L.batch), NT, tc_smem<DP, WP>(), L.stream>>>(L.plan, L.arm_tiles,
                                                                               L.arm_ntiles);
 }
 

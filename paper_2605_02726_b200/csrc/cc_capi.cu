@@ -831,3 +831,53 @@ int cc_trainer_latent_mu_sigma(cc_trainer* t, const float* params, float* mu, fl
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- batches (cfg3)
+#include "coolchic_b200_batch.h"
+
+struct cc_batch {
+    std::unique_ptr<ccb::Batch> b;
+};
+
+extern "C" {
+
+int cc_batch_create(cc_trainer* const* trainers, int n, cc_batch** out) {
+    return guarded([&] {
+        if (!trainers || n <= 0 || !out) throw ccb::ConfigError("cc_batch_create: no trainers");
+        std::vector<ccb::Trainer*> v;
+        for (int i = 0; i < n; ++i) {
+            if (!trainers[i]) throw ccb::ConfigError("cc_batch_create: null trainer");
+            v.push_back(trainers[i]->tr.get());
+        }
+        auto* b = new cc_batch;
+        b->b = std::make_unique<ccb::Batch>(std::move(v));
+        *out = b;
+        return CC_OK;
+    });
+}
+
+void cc_batch_destroy(cc_batch* b) { delete b; }
+
+int cc_batch_reserve_iterations(cc_batch* b, int n) {
+    return guarded([&] {
+        b->b->reserve_iterations(n);
+        return CC_OK;
+    });
+}
+
+int cc_batch_enqueue_proxy_iterations(cc_batch* b, int n, const double* lr, const double* temp,
+                                      const double* noise_std) {
+    return guarded([&] {
+        b->b->enqueue_proxy_iterations(n, lr, temp, noise_std);
+        return CC_OK;
+    });
+}
+
+int cc_batch_synchronize(cc_batch* b) {
+    return guarded([&] {
+        b->b->synchronize();
+        return CC_OK;
+    });
+}
+
+}  // extern "C"

@@ -35,7 +35,7 @@ __device__ __forceinline__ float mul_add(float w, float x, float acc) { return _
 
 __global__ void __launch_bounds__(128) k_latent_mu_sigma(const Plan* __restrict__ pp, float* __restrict__ mu_out,
                                                          float* __restrict__ sigma_out) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (i >= P.n_latents) return;
     int gi = 0;
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(128) k_latent_mu_sigma(const Plan* __restrict_
 
 void launch_latent_mu_sigma(const LaunchCtx& L, float* mu, float* sigma) {
     const int64_t n = L.host->n_latents;
-    k_latent_mu_sigma<<<int((n + 127) / 128), 128, 0, L.stream>>>(L.plan, mu, sigma);
+    k_latent_mu_sigma<<<dim3(int((n + 127) / 128), 1, L.batch), 128, 0, L.stream>>>(L.plan, mu, sigma);
 }
 
 }  // namespace ccb

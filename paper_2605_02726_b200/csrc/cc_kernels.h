@@ -8,6 +8,7 @@
 namespace ccb {
 
 void cuda_check(cudaError_t e, const char* what);  // throws CudaError (cc_runtime.cu)
+[[noreturn]] void throw_config(const char* what);   // throws ConfigError (cc_runtime.cu)
 
 struct LaunchCtx {
     const Plan* plan;      // device copy
@@ -23,6 +24,8 @@ struct LaunchCtx {
     int syn_ntiles;        // 128-pixel tiles of the trunk-backward kernel
     int syn_blocks;
     int red_blocks;        // per-CTA partial rows of the small reduction kernels
+    int batch = 1;         // images per launch: plan points at `batch` consecutive Plans,
+                           // every kernel reads pp[blockIdx.z] (same geometry for all)
 };
 
 // Launch with programmatic stream serialization (see pdl_wait in
@@ -98,15 +101,15 @@ int syn_post_tiles(int H, int W);
 
 // optimizer / bookkeeping (cc_step.cu)
 void launch_finalize(const LaunchCtx& L, int mode, int snap_slot);
-void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log);
+void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, bool log_rec);
 void launch_nn_reduce(const LaunchCtx& L, int p_begin = 0, int p_end = -1);
-void launch_nn_apply(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log);
-void launch_sched_load(const LaunchCtx& L, const double* sched);
+void launch_nn_apply(const LaunchCtx& L, bool do_step, bool count_iter, bool log_rec);
+void launch_sched_load(const LaunchCtx& L);
 
 // SOAP for the NN parameters (cc_soap.cu)
 size_t soap_smem(const Plan& H);
 void soap_configure(const Plan& H);
-void launch_soap_apply(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log);
+void launch_soap_apply(const LaunchCtx& L, bool do_step, bool count_iter, bool log_rec);
 void launch_soap_reset(const LaunchCtx& L);
 void launch_snapshot_if_better(const LaunchCtx& L, int slot, float* snap_y, float* snap_p);
 

@@ -39,7 +39,7 @@ __device__ __forceinline__ int find_grid(const int64_t* s_off, int64_t i) {
 }
 
 __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     CCB_GRID_CACHE(P);
     // per-grid gradient-finiteness flags of this iteration (ANDed by k_latent_grad)
     if (blockIdx.x == 0 && threadIdx.x < kMaxGrids) P.lat_ok[threadIdx.x] = 1;
@@ -97,7 +97,7 @@ __global__ void k_softq_fwd(const Plan* __restrict__ pp) {
 // iteration's cost turns out non-finite the counter does not advance and
 // k_softq_fwd draws inline instead.
 __global__ void k_noise_ahead(const Plan* __restrict__ pp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     CCB_GRID_CACHE(P);
     const uint64_t giter = uint64_t(P.scal->global_iter) + 1;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
@@ -111,7 +111,7 @@ __global__ void k_noise_ahead(const Plan* __restrict__ pp) {
 }
 
 __global__ void k_quantize(const Plan* __restrict__ pp, int amp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
         long q = lroundf(P.y[i]);  // ties away from zero, like std::lround
@@ -122,7 +122,7 @@ __global__ void k_quantize(const Plan* __restrict__ pp, int amp) {
 }
 
 __global__ void k_pads_from_q(const Plan* __restrict__ pp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     CCB_GRID_CACHE(P);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -142,7 +142,7 @@ __global__ void k_pads_from_q(const Plan* __restrict__ pp) {
 // finer grid, and the upsampling gradient for main grids.  Then the
 // soft-quantize backward chain rule and the per-grid finiteness flag.
 __global__ void k_latent_grad(const Plan* __restrict__ pp, int force, int64_t i_begin, int64_t i_end) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     CCB_GRID_CACHE(P);
     const float temp = float(P.scal->temp);
     (void)force;  // gradients are assembled regardless of the cost flag; k_adam_latents
@@ -221,7 +221,7 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp, int force, int64_t i_
 // computed per grid by k_finalize from lat_t + 1.  Block 0 / thread 0 also
 // advances the step counters (encoder.hpp:129-133).
 __global__ void k_adam_latents(const Plan* __restrict__ pp, int g_begin, int g_end) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     CCB_GRID_CACHE(P);
     const double lr = P.scal->lr;
     const double* __restrict__ bc = P.bc_lat;
@@ -258,7 +258,7 @@ __global__ void k_adam_latents(const Plan* __restrict__ pp, int g_begin, int g_e
 }
 
 __global__ void k_init_latents(const Plan* __restrict__ pp, uint64_t stream, float amp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     CCB_GRID_CACHE(P);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -270,32 +270,32 @@ __global__ void k_init_latents(const Plan* __restrict__ pp, uint64_t stream, flo
 
 // ---------------------------------------------------------------------------
 void launch_softq_fwd(const LaunchCtx& L) {
-    launch_pdl(k_softq_fwd, dim3(L.elem_blocks), dim3(256), 0, L.stream, 's', L.plan);
+    launch_pdl(k_softq_fwd, dim3(L.elem_blocks, 1, L.batch), dim3(256), 0, L.stream, 's', L.plan);
 }
 void launch_quantize(const LaunchCtx& L, int amp) {
-    k_quantize<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, amp);
+    k_quantize<<<dim3(L.elem_blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan, amp);
 }
 void launch_pads_from_q(const LaunchCtx& L) {
-    k_pads_from_q<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+    k_pads_from_q<<<dim3(L.elem_blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan);
 }
 void launch_latent_grad(const LaunchCtx& L) {
-    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 0, 0, L.host->n_latents);
+    k_latent_grad<<<dim3(L.elem_blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan, 0, 0, L.host->n_latents);
 }
 void launch_latent_grad_partial(const LaunchCtx& L) {
-    k_latent_grad<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 1, 0, L.host->n_latents);
+    k_latent_grad<<<dim3(L.elem_blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan, 1, 0, L.host->n_latents);
 }
 // grids [g_begin, g_end) only (their latents are contiguous in decode order)
 void launch_latent_grad_grids(const LaunchCtx& L, int g_begin, int g_end) {
     const Plan& H = *L.host;
     const int64_t a = H.g[g_begin].lat_off, b = g_end < H.n_grids ? H.g[g_end].lat_off : H.n_latents;
     const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((b - a + 255) / 256, L.elem_blocks)));
-    k_latent_grad<<<blocks, 256, 0, L.stream>>>(L.plan, 0, a, b);
+    k_latent_grad<<<dim3(blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan, 0, a, b);
 }
 void launch_adam_latents_grids(const LaunchCtx& L, int g_begin, int g_end) {
     const Plan& H = *L.host;
     const int64_t a = H.g[g_begin].lat_off, b = g_end < H.n_grids ? H.g[g_end].lat_off : H.n_latents;
     const int blocks = int(std::max<int64_t>(1, std::min<int64_t>((b - a + 255) / 256, L.elem_blocks)));
-    k_adam_latents<<<blocks, 256, 0, L.stream>>>(L.plan, g_begin, g_end);
+    k_adam_latents<<<dim3(blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan, g_begin, g_end);
 }
 
 // Row bands: per-grid finiteness of the OWN rows' (complete) latent gradients,
@@ -304,7 +304,7 @@ __global__ void k_ok_reset(const Plan* __restrict__ pp) {
     if (threadIdx.x < kMaxGrids) pp->lat_ok[threadIdx.x] = 1;
 }
 __global__ void k_band_own_finite(const Plan* __restrict__ pp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     CCB_GRID_CACHE(P);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -316,17 +316,17 @@ __global__ void k_band_own_finite(const Plan* __restrict__ pp) {
     }
 }
 void launch_band_own_finite(const LaunchCtx& L) {
-    k_ok_reset<<<1, 32, 0, L.stream>>>(L.plan);
-    k_band_own_finite<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+    k_ok_reset<<<dim3(1, 1, L.batch), 32, 0, L.stream>>>(L.plan);
+    k_band_own_finite<<<dim3(L.elem_blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan);
 }
 void launch_adam_latents(const LaunchCtx& L) {
-    k_adam_latents<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, 0, L.host->n_grids);
+    k_adam_latents<<<dim3(L.elem_blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan, 0, L.host->n_grids);
 }
 void launch_noise_ahead(const LaunchCtx& L) {
-    k_noise_ahead<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan);
+    k_noise_ahead<<<dim3(L.elem_blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan);
 }
 void launch_init_latents(const LaunchCtx& L, uint64_t stream, float amp) {
-    k_init_latents<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, stream, amp);
+    k_init_latents<<<dim3(L.elem_blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan, stream, amp);
 }
 
 }  // namespace ccb

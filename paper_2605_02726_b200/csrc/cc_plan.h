@@ -177,6 +177,8 @@ struct Plan {
     int64_t* nn_t;            // per tensor
     int* lat_ok;              // per grid: grads finite
     int* tensor_ok;           // per NN tensor: grads finite
+    const double* sched;      // batched runs: (lr, temp, noise_std) per iteration
+    double* rec;              // batched runs: (cost, mse, bits, global_iter) per iteration (mapped host)
     // device scalars (see DevScalars)
     struct DevScalars* scal;
 };

@@ -22,6 +22,8 @@ bool pdl_enabled(char which) {
     return true;
 }
 
+void throw_config(const char* what) { throw ConfigError(what); }
+
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
         throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
@@ -652,11 +654,11 @@ void Trainer::reset_optimizers() {
 
 // NN-parameter optimizer step: Adam, or SOAP when EncoderConfig::use_soap
 // (NnOptimizer::step, optim.hpp:277-286).
-void Trainer::nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, double* cost_log) {
+void Trainer::nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, bool log_rec) {
     if (H_.use_soap)
-        launch_soap_apply(ctx, do_step, count_iter, cost_log);
+        launch_soap_apply(ctx, do_step, count_iter, log_rec);
     else
-        launch_nn_apply(ctx, do_step, count_iter, cost_log);
+        launch_nn_apply(ctx, do_step, count_iter, log_rec);
 }
 
 // ---------------------------------------------------------------- sequences
@@ -701,7 +703,7 @@ void Trainer::mark(int id, int on) {
 
 void Trainer::enqueue_proxy(bool batched) {
     mark(0, false);
-    if (batched) launch_sched_load(L_, d_sched_);
+    if (batched) launch_sched_load(L_);
     launch_softq_fwd(L_);
     mark(1, false);
     // A/B: the synthesis trunk's weight gradients as a separate launch on the
@@ -778,7 +780,7 @@ void Trainer::enqueue_proxy(bool batched) {
     // reductions) beside the coarse grids' Adam step (main)
     join(true);
     fork();
-    nn_apply(side(), true, true, batched ? d_rec_ : nullptr);
+    nn_apply(side(), true, true, batched);
     if (fine > 0) launch_adam_latents_grids(L_, 0, fine);
     join();
     mark(12, false);
@@ -833,7 +835,7 @@ void Trainer::enqueue_hardround(int slot) {
     CCB_CUDA(cudaMemsetAsync(H_.lat_g, 0, sizeof(float) * size_t(H_.n_latents), stream_));
     if (slot >= 0) launch_snapshot_if_better(L_, slot, snaps_.at(slot).y, snaps_.at(slot).p);
     launch_nn_reduce(L_);
-    nn_apply(L_, true, true, nullptr);
+    nn_apply(L_, true, true, false);
 }
 
 // Trainer::true_cost (encoder.hpp:158-168)
@@ -969,7 +971,7 @@ void Trainer::band_step(const int* lat_ok) {
     CCB_CUDA(cudaMemcpyAsync(H_.lat_ok, lat_ok, sizeof(int) * size_t(H_.n_grids),
                              cudaMemcpyHostToDevice, stream_));
     launch_adam_latents(L_);
-    nn_apply(L_, true, true, nullptr);
+    nn_apply(L_, true, true, false);
     read_scalars();
 }
 
@@ -1054,7 +1056,10 @@ void Trainer::reserve_iterations(int n) {
         if (h_sched_) cudaFreeHost(h_sched_);
         CCB_CUDA(cudaMallocHost(&h_sched_, sizeof(double) * 3 * size_t(n)));
         sched_cap_ = n;
-        auto it = graphs_.find(1);  // the batched graph bakes in d_sched_ / d_rec_
+        H_.sched = d_sched_;  // read by k_sched_load / k_nn_step through the plan
+        H_.rec = d_rec_;
+        CCB_CUDA(cudaMemcpy(d_plan_, &H_, sizeof(Plan), cudaMemcpyHostToDevice));
+        auto it = graphs_.find(1);  // (captured before the buffers moved)
         if (it != graphs_.end()) {
             cudaGraphExecDestroy(it->second);
             graphs_.erase(it);
@@ -1068,8 +1073,17 @@ void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* te
     require_loaded();
     if (n <= 0) return;
     reserve_iterations(n);  // no-op once sized: buffers and the graph are reused
+    upload_schedule(n, lr, temp, noise);  // from pinned memory
+    reset_batch_counters();
+    // every iteration's record (cost, mse, bits, global_iter) is written by
+    // the iteration's last kernel into mapped pinned host memory, without a
+    // host synchronisation or a copy between the graphs
+    for (int i = 0; i < n; ++i) run_graph(1);
+}
+
+void Trainer::upload_schedule(int n, const double* lr, const double* temp, const double* noise) {
     CCB_CUDA(cudaEventSynchronize(ev_sched_));  // the previous batch's upload has left h_sched_
-    for (int i = 0; i < n; ++i) {  // the schedule goes up from pinned memory
+    for (int i = 0; i < n; ++i) {
         h_sched_[3 * i] = lr[i];
         h_sched_[3 * i + 1] = temp[i];
         h_sched_[3 * i + 2] = noise[i];
@@ -1077,13 +1091,80 @@ void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* te
     CCB_CUDA(cudaMemcpyAsync(d_sched_, h_sched_, sizeof(double) * 3 * size_t(n), cudaMemcpyHostToDevice,
                              stream_));
     CCB_CUDA(cudaEventRecord(ev_sched_, stream_));
+}
+
+void Trainer::reset_batch_counters() {
     CCB_CUDA(cudaMemsetAsync(&H_.scal->sched_pos, 0, sizeof(int64_t), stream_));
     CCB_CUDA(cudaMemsetAsync(&H_.scal->halt, 0, sizeof(int), stream_));
-    // every iteration's record (cost, mse, bits, global_iter) is written by
-    // the iteration's last kernel into mapped pinned host memory, without a
-    // host synchronisation or a copy between the graphs
-    for (int i = 0; i < n; ++i) run_graph(1);
 }
+
+cudaGraphExec_t Trainer::capture_batched_proxy(const Plan* d_plans, int batch) {
+    const LaunchCtx keep = L_;
+    L_.plan = d_plans;
+    L_.batch = batch;
+    cudaGraph_t g;
+    cudaGraphExec_t ex = nullptr;
+    try {
+        CCB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        enqueue_proxy(true);
+        CCB_CUDA(cudaStreamEndCapture(stream_, &g));
+        CCB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+        cudaGraphDestroy(g);
+    } catch (...) {
+        L_ = keep;
+        throw;
+    }
+    L_ = keep;
+    return ex;
+}
+
+Batch::Batch(std::vector<Trainer*> trainers) : t_(std::move(trainers)) {
+    if (t_.empty()) throw ConfigError("empty batch");
+    const Plan& a = t_[0]->host_plan();
+    for (Trainer* t : t_) {
+        const Plan& b = t->host_plan();
+        if (t->is_band()) throw ConfigError("row-band trainers cannot be batched");
+        if (b.H != a.H || b.W != a.W || b.n_latents != a.n_latents || b.n_params != a.n_params ||
+            b.D != a.D || b.Wd != a.Wd || b.syn_F != a.syn_F || b.posts != a.posts || b.use_soap != a.use_soap ||
+            b.n_grids != a.n_grids)
+            throw ConfigError("batched trainers must share the image size, decoder and optimizer");
+        t->set_stream(t_[0]->stream());
+    }
+}
+
+Batch::~Batch() {
+    if (graph_) cudaGraphExecDestroy(graph_);
+    if (d_plans_) cudaFree(d_plans_);
+}
+
+void Batch::reserve_iterations(int n) {
+    if (n <= cap_ && graph_) return;
+    for (Trainer* t : t_) t->reserve_iterations(n);
+    if (graph_) {
+        cudaGraphExecDestroy(graph_);
+        graph_ = nullptr;
+    }
+    const size_t B = t_.size();
+    std::vector<Plan> hp(B);
+    for (size_t b = 0; b < B; ++b) {
+        hp[b] = t_[b]->host_plan();
+        hp[b].sched = t_[0]->device_schedule();  // one schedule for the whole batch
+    }
+    if (!d_plans_) CCB_CUDA(cudaMalloc(&d_plans_, sizeof(Plan) * B));
+    CCB_CUDA(cudaMemcpy(d_plans_, hp.data(), sizeof(Plan) * B, cudaMemcpyHostToDevice));
+    graph_ = t_[0]->capture_batched_proxy(d_plans_, int(B));
+    cap_ = n;
+}
+
+void Batch::enqueue_proxy_iterations(int n, const double* lr, const double* temp, const double* noise) {
+    if (n <= 0) return;
+    reserve_iterations(n);
+    t_[0]->upload_schedule(n, lr, temp, noise);
+    for (Trainer* t : t_) t->reset_batch_counters();
+    for (int i = 0; i < n; ++i) CCB_CUDA(cudaGraphLaunch(graph_, t_[0]->stream()));
+}
+
+void Batch::synchronize() { CCB_CUDA(cudaStreamSynchronize(t_[0]->stream())); }
 
 // Stage-by-stage replay of one proxy iteration with events in between
 // (diagnostics; same kernels as the graph).
@@ -1119,7 +1200,7 @@ void Trainer::profile_stages(int n, double lr, double temp, double noise, double
         launch_latent_grad(L_);
         launch_adam_latents(L_);
         launch_nn_reduce(L_);
-        nn_apply(L_, true, true, nullptr);
+        nn_apply(L_, true, true, false);
         CCB_CUDA(cudaEventRecord(ev[8], stream_));
         CCB_CUDA(cudaEventSynchronize(ev[8]));
         for (int s = 0; s < NS; ++s) {

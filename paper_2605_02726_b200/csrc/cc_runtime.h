@@ -81,6 +81,15 @@ public:
     // (one-off setup kept out of enqueue_proxy_iterations' steady state)
     void reserve_iterations(int n);
     void last_records(int n, double* rec);
+    // batched images (cfg3): capture this trainer's proxy iteration as ONE graph
+    // of launches over `batch` consecutive device plans (every kernel reads
+    // pp[blockIdx.z]); the plans must share this trainer's geometry.
+    cudaGraphExec_t capture_batched_proxy(const Plan* d_plans, int batch);
+    void upload_schedule(int n, const double* lr, const double* temp, const double* noise);
+    void reset_batch_counters();
+    const Plan& host_plan() const { return H_; }
+    const double* device_schedule() const { return d_sched_; }
+    cudaStream_t stream() const { return stream_; }
     void set_stream(cudaStream_t s);
     void profile_stages(int n, double lr, double temp, double noise, double* ms);
     static constexpr int kTimelineMarks = 13;
@@ -144,7 +153,7 @@ public:
 private:
     void init(const float* image, int h, int w);
     void mark(int id, int on);  // 0 main, 1 side, 2 tail stream
-    void nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, double* cost_log);
+    void nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, bool log_rec);
     void build_plan();
     void allocate();
     void require_loaded() const;
@@ -180,6 +189,8 @@ private:
     Plan H_{};
     Plan* d_plan_ = nullptr;
     LaunchCtx L_{};
+
+
     std::vector<TensorInfo> tensors_;
     std::vector<GridInfo> grids_;
     std::vector<void*> allocs_;
@@ -208,6 +219,31 @@ private:
         int hg = 0, r0 = 0, r1 = 0, halo = 0;
     } band_;
     std::vector<int4> tiles_host_;
+};
+
+// Several images of one geometry trained in lock-step by ONE set of launches
+// per stage (BASELINE config 3: independent images batched within a GPU; the
+// reference's only multi-image mode is independent encodes in a thread pool,
+// tools/coolcodec.cpp:150-171).  Every trainer keeps its own buffers, state,
+// counters and records; the batch owns the array of their device plans and the
+// batched iteration graph, launched on the first trainer's stream (all
+// trainers are moved onto it).
+class Batch {
+public:
+    explicit Batch(std::vector<Trainer*> trainers);
+    ~Batch();
+    Batch(const Batch&) = delete;
+    Batch& operator=(const Batch&) = delete;
+    void reserve_iterations(int n);
+    void enqueue_proxy_iterations(int n, const double* lr, const double* temp, const double* noise);
+    void synchronize();
+    int size() const { return int(t_.size()); }
+
+private:
+    std::vector<Trainer*> t_;
+    Plan* d_plans_ = nullptr;
+    cudaGraphExec_t graph_ = nullptr;
+    int cap_ = 0;
 };
 
 void fp32_peak(int device, double* tflops, double* ms);

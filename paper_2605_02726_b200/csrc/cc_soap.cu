@@ -107,9 +107,10 @@ __device__ void mm_abt(const double* a, const double* b, double* out, int R, int
 }
 
 __global__ void __launch_bounds__(kThreads) k_soap_step(const Plan* __restrict__ pp, int do_step,
-                                                        int count_iter, double* __restrict__ cost_log,
-                                                        const int* __restrict__ tensor_ok) {
-    const Plan& P = *pp;
+                                                        int count_iter, int log_rec) {
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
+    const int* __restrict__ tensor_ok = P.tensor_ok;
+    double* __restrict__ cost_log = log_rec ? P.rec : nullptr;
     const int ti = blockIdx.x;
     DevScalars* s = P.scal;
     if (count_iter && ti == 0 && threadIdx.x == 0 && s->cost_ok) s->global_iter += 1;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kThreads) k_soap_step(const Plan* __restrict__
 }
 
 __global__ void k_soap_reset(const Plan* __restrict__ pp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     const int ti = blockIdx.x;
     const int R = P.tensor_rows[ti], C = P.tensor_cols[ti];
     double* L = P.soap + P.soap_off[ti];
@@ -247,15 +248,14 @@ void soap_configure(const Plan& H) {
     cudaFuncSetAttribute(k_soap_step, cudaFuncAttributeMaxDynamicSharedMemorySize, int(soap_smem(H)));
 }
 
-void launch_soap_apply(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log) {
+void launch_soap_apply(const LaunchCtx& L, bool do_step, bool count_iter, bool log_rec) {
     const Plan& H = *L.host;
-    k_soap_step<<<H.n_tensors, kThreads, soap_smem(H), L.stream>>>(L.plan, do_step ? 1 : 0,
-                                                                   count_iter ? 1 : 0, cost_log,
-                                                                   H.tensor_ok);
+    k_soap_step<<<dim3(H.n_tensors, 1, L.batch), kThreads, soap_smem(H), L.stream>>>(
+        L.plan, do_step ? 1 : 0, count_iter ? 1 : 0, log_rec ? 1 : 0);
 }
 
 void launch_soap_reset(const LaunchCtx& L) {
-    k_soap_reset<<<L.host->n_tensors, 128, 0, L.stream>>>(L.plan);
+    k_soap_reset<<<dim3(L.host->n_tensors, 1, L.batch), 128, 0, L.stream>>>(L.plan);
 }
 
 }  // namespace ccb

@@ -21,7 +21,7 @@ namespace {
 // one CTA of 256 threads: strided partial sums, then a fixed-order tree
 __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, int mode,
                                                   int snap_slot) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     double* bc_lat = P.bc_lat;
     __shared__ double red[8];
     double b_loc = 0.0, s_loc = 0.0;
@@ -58,9 +58,9 @@ __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, i
 // Wide reduction: one warp per parameter over the whole grid; lanes stride the
 // per-CTA partial rows, fixed shuffle tree, regions in index order.  Writes
 // ParamTensor::g and clears the tensor's finiteness flag on a non-finite grad.
-__global__ void __launch_bounds__(256) k_nn_reduce(const Plan* __restrict__ pp,
-                                                   int* __restrict__ tensor_ok, int p_begin, int p_end) {
-    const Plan& P = *pp;
+__global__ void __launch_bounds__(256) k_nn_reduce(const Plan* __restrict__ pp, int p_begin, int p_end) {
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
+    int* __restrict__ tensor_ok = P.tensor_ok;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
@@ -90,9 +90,10 @@ __global__ void __launch_bounds__(256) k_nn_reduce(const Plan* __restrict__ pp,
 
 // One CTA per NN tensor: Adam with the per-tensor skip (optim.hpp:38-41).
 __global__ void __launch_bounds__(256) k_nn_step(const Plan* __restrict__ pp, int do_step,
-                                                 int count_iter, double* __restrict__ cost_log,
-                                                 const int* __restrict__ tensor_ok) {
-    const Plan& P = *pp;
+                                                 int count_iter, int log_rec) {
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
+    const int* __restrict__ tensor_ok = P.tensor_ok;
+    double* __restrict__ cost_log = log_rec ? P.rec : nullptr;
     const double lr = P.scal->lr;
     const int ti = blockIdx.x;
     const int off = P.tensor_off[ti], n = P.tensor_size[ti];
@@ -129,8 +130,10 @@ __global__ void __launch_bounds__(256) k_nn_step(const Plan* __restrict__ pp, in
 }
 
 // Batched runs: the scalars of iteration sched_pos (lr, temp, noise_std).
-__global__ void k_sched_load(const Plan* __restrict__ pp, const double* __restrict__ sched) {
-    DevScalars* s = pp->scal;
+__global__ void k_sched_load(const Plan* __restrict__ pp) {
+    const Plan& P = pp[blockIdx.z];
+    DevScalars* s = P.scal;
+    const double* __restrict__ sched = P.sched;
     const double* e = sched + 3 * s->sched_pos;
     s->lr = e[0];
     s->temp = e[1];
@@ -139,7 +142,7 @@ __global__ void k_sched_load(const Plan* __restrict__ pp, const double* __restri
 
 __global__ void k_snapshot_copy(const Plan* __restrict__ pp, int slot, float* __restrict__ sy,
                                 float* __restrict__ sp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     DevScalars* s = P.scal;
     if (!s->snap_take) return;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P.n_latents;
@@ -154,7 +157,7 @@ __global__ void k_snapshot_copy(const Plan* __restrict__ pp, int slot, float* __
 }  // namespace
 
 void launch_finalize(const LaunchCtx& L, int mode, int snap_slot) {
-    k_finalize<<<1, 256, 0, L.stream>>>(L.plan, mode, snap_slot);
+    k_finalize<<<dim3(1, 1, L.batch), 256, 0, L.stream>>>(L.plan, mode, snap_slot);
 }
 
 void launch_nn_reduce(const LaunchCtx& L, int p_begin, int p_end) {
@@ -162,26 +165,25 @@ void launch_nn_reduce(const LaunchCtx& L, int p_begin, int p_end) {
     if (p_end < 0 || p_end > H.n_params) p_end = H.n_params;
     if (p_end <= p_begin) return;
     const int blocks = (p_end - p_begin + 7) / 8;
-    k_nn_reduce<<<blocks, 256, 0, L.stream>>>(L.plan, H.tensor_ok, p_begin, p_end);
+    k_nn_reduce<<<dim3(blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan, p_begin, p_end);
 }
 
-void launch_nn_apply(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log) {
-    k_nn_step<<<L.host->n_tensors, 256, 0, L.stream>>>(L.plan, do_step ? 1 : 0,
-                                                       count_iter ? 1 : 0, cost_log,
-                                                       L.host->tensor_ok);
+void launch_nn_apply(const LaunchCtx& L, bool do_step, bool count_iter, bool log_rec) {
+    k_nn_step<<<dim3(L.host->n_tensors, 1, L.batch), 256, 0, L.stream>>>(L.plan, do_step ? 1 : 0,
+                                                                          count_iter ? 1 : 0, log_rec ? 1 : 0);
 }
 
-void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, double* cost_log) {
+void launch_nn_step(const LaunchCtx& L, bool do_step, bool count_iter, bool log_rec) {
     launch_nn_reduce(L);
-    launch_nn_apply(L, do_step, count_iter, cost_log);
+    launch_nn_apply(L, do_step, count_iter, log_rec);
 }
 
-void launch_sched_load(const LaunchCtx& L, const double* sched) {
-    k_sched_load<<<1, 1, 0, L.stream>>>(L.plan, sched);
+void launch_sched_load(const LaunchCtx& L) {
+    k_sched_load<<<dim3(1, 1, L.batch), 1, 0, L.stream>>>(L.plan);
 }
 
 void launch_snapshot_if_better(const LaunchCtx& L, int slot, float* snap_y, float* snap_p) {
-    k_snapshot_copy<<<L.elem_blocks, 256, 0, L.stream>>>(L.plan, slot, snap_y, snap_p);
+    k_snapshot_copy<<<dim3(L.elem_blocks, 1, L.batch), 256, 0, L.stream>>>(L.plan, slot, snap_y, snap_p);
 }
 
 }  // namespace ccb

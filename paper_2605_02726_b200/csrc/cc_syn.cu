@@ -35,7 +35,7 @@ constexpr int kLZ = kMaxLevels;  // z vector padded to 8 channels
 // the order is the reference's: bias, then z channels; t sums hidden units in
 // order (conv1x1_forward, layers.hpp:196-214).
 __global__ void __launch_bounds__(256) k_syn_trunk_fwd(const Plan* __restrict__ pp) {
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     __shared__ __align__(16) float c1wT[kLZ][64];
     __shared__ __align__(16) float c1b[64], c2w[3][64];
     __shared__ float c2b[4], st[3][kLZ];
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) k_syn_trunk_fwd(const Plan* __restrict__ 
 }  // namespace
 
 void launch_syn_forward(const LaunchCtx& L, bool backward) {
-    launch_pdl(k_syn_trunk_fwd, dim3(L.pix_blocks), dim3(256), 0, L.stream, 's', L.plan);
+    launch_pdl(k_syn_trunk_fwd, dim3(L.pix_blocks, 1, L.batch), dim3(256), 0, L.stream, 's', L.plan);
     launch_syn_post(L, backward);
 }
 

@@ -107,7 +107,7 @@ __device__ __forceinline__ void conv_pass(const float* __restrict__ in, float* _
 template <int NP>
 __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp, int with_grad) {
     using C = PC<NP>;
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PostSmem2<NP>& sm = *reinterpret_cast<PostSmem2<NP>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -392,14 +392,17 @@ int syn_post_tiles(int H, int W) { return ((H + TH - 1) / TH) * ((W + TW - 1) / 
 
 void launch_syn_post(const LaunchCtx& L, bool backward) {
     const Plan& H = *L.host;
-    if (H.post_scratch && backward)
-        cudaMemsetAsync(H.post_scratch, 0, sizeof(double) * size_t(H.n_mse_part) * NT * 30, L.stream);
+    if (H.post_scratch && backward) {
+        if (L.batch != 1) throw_config("batched launches need images below the posts' fp64 flush-slot size");
+        cuda_check(cudaMemsetAsync(H.post_scratch, 0, sizeof(double) * size_t(H.n_mse_part) * NT * 30, L.stream),
+                   "cudaMemsetAsync");
+    }
     const int g = H.n_mse_part;
     const int wg = backward ? 1 : 0;
     switch (H.posts) {
-        case 0: launch_pdl(k_syn_post2<0>, dim3(g), dim3(NT), sizeof(PostSmem2<0>), L.stream, 's', L.plan, wg); break;
-        case 1: launch_pdl(k_syn_post2<1>, dim3(g), dim3(NT), sizeof(PostSmem2<1>), L.stream, 's', L.plan, wg); break;
-        default: launch_pdl(k_syn_post2<2>, dim3(g), dim3(NT), sizeof(PostSmem2<2>), L.stream, 's', L.plan, wg); break;
+        case 0: launch_pdl(k_syn_post2<0>, dim3(g, 1, L.batch), dim3(NT), sizeof(PostSmem2<0>), L.stream, 's', L.plan, wg); break;
+        case 1: launch_pdl(k_syn_post2<1>, dim3(g, 1, L.batch), dim3(NT), sizeof(PostSmem2<1>), L.stream, 's', L.plan, wg); break;
+        default: launch_pdl(k_syn_post2<2>, dim3(g, 1, L.batch), dim3(NT), sizeof(PostSmem2<2>), L.stream, 's', L.plan, wg); break;
     }
 }
 

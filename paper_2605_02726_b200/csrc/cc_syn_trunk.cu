@@ -125,11 +125,11 @@ __device__ __forceinline__ void issue_tile(const Plan& P, const float* __restric
 }
 
 template <int FP, int PART>
-__global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict__ pp,
-                                                          const float* __restrict__ dt_in) {
+__global__ void __launch_bounds__(NT, 2) k_syn_trunk_bwd2(const Plan* __restrict__ pp) {
     constexpr bool kDz = PART != 2, kDw = PART != 1;
     using K = TB<FP>;
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
+    const float* __restrict__ dt_in = P.syn_dt;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TBSmem<FP>& sm = *reinterpret_cast<TBSmem<FP>*>(smem_raw);
     const int tid = threadIdx.x;
@@ -363,11 +363,11 @@ size_t tb_smem() {
 }
 
 template <int FP>
-void launch_t(const LaunchCtx& L, const float* dt, int part) {
-    const dim3 g(L.syn_blocks), b(NT);
-    if (part == 1) launch_pdl(k_syn_trunk_bwd2<FP, 1>, g, b, tb_smem<FP>(), L.stream, 's', L.plan, dt);
-    else if (part == 2) launch_pdl(k_syn_trunk_bwd2<FP, 2>, g, b, tb_smem<FP>(), L.stream, 's', L.plan, dt);
-    else launch_pdl(k_syn_trunk_bwd2<FP, 0>, g, b, tb_smem<FP>(), L.stream, 's', L.plan, dt);
+void launch_t(const LaunchCtx& L, int part) {
+    const dim3 g(L.syn_blocks, 1, L.batch), b(NT);
+    if (part == 1) launch_pdl(k_syn_trunk_bwd2<FP, 1>, g, b, tb_smem<FP>(), L.stream, 's', L.plan);
+    else if (part == 2) launch_pdl(k_syn_trunk_bwd2<FP, 2>, g, b, tb_smem<FP>(), L.stream, 's', L.plan);
+    else launch_pdl(k_syn_trunk_bwd2<FP, 0>, g, b, tb_smem<FP>(), L.stream, 's', L.plan);
 }
 
 template <int FP>
@@ -413,12 +413,11 @@ void syn_configure(int FP) {
 
 void launch_syn_backward(const LaunchCtx& L, int part) {
     const Plan& H = *L.host;
-    const float* dt = H.syn_dt;
     switch (syn_padded_hidden(H.syn_F)) {
-        case 8: launch_t<8>(L, dt, part); break;
-        case 16: launch_t<16>(L, dt, part); break;
-        case 48: launch_t<48>(L, dt, part); break;
-        default: launch_t<64>(L, dt, part); break;
+        case 8: launch_t<8>(L, part); break;
+        case 16: launch_t<16>(L, part); break;
+        case 48: launch_t<48>(L, part); break;
+        default: launch_t<64>(L, part); break;
     }
 }
 

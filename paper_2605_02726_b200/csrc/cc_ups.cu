@@ -158,7 +158,7 @@ __device__ __forceinline__ void fwd_tile(const float* __restrict__ in, int in_st
 template <int TB>
 __global__ void __launch_bounds__(kThreads) k_ups_fwd(const Plan* __restrict__ pp, int j) {
     __shared__ FwdSmem<TB> f;
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     const UpsStage& s = P.ups[j][blockIdx.y];
     const int ro = s.rows_out, co = s.cols_out, ri = s.rows_in, ci = s.cols_in;
     constexpr int FO = 2 * TB;
@@ -512,7 +512,7 @@ template <int TB>
 __global__ void __launch_bounds__(kThreads, 3) k_ups_bwd(const Plan* __restrict__ pp, int j, int write_lat) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BwdSmem<TB>& f = *reinterpret_cast<BwdSmem<TB>*>(smem_raw);
-    const Plan& P = *pp;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
     double acc[7] = {0, 0, 0, 0, 0, 0, 0};  // dk4[0..3] (rows+cols passes), dr3[0..2]
     ups_bwd_stage<TB>(P, j, blockIdx.y, blockIdx.x, gridDim.x, write_lat, f, acc);
     // tap gradients of this CTA -> partial row (blockIdx.y, blockIdx.x)
@@ -580,7 +580,7 @@ void launch_ups_forward(const LaunchCtx& L) {
     // z plane 0 (= ŷ of main grid 0) is written by k_softq_fwd / k_pads_from_q
     for (int j = H.L - 2; j >= 0; --j) {
         if (H.ups_n[j] == 0) continue;
-        const dim3 grid(ups_blocks_x(H, j, L.num_sms, true), H.ups_n[j]);
+        const dim3 grid(ups_blocks_x(H, j, L.num_sms, true), H.ups_n[j], L.batch);
         switch (ups_fwd_tile(H, j, L.num_sms)) {
             case 16: launch_pdl(k_ups_fwd<16>, grid, kThreads, 0, L.stream, 'f', L.plan, j); break;
             case 8: launch_pdl(k_ups_fwd<8>, grid, kThreads, 0, L.stream, 'f', L.plan, j); break;
@@ -593,7 +593,7 @@ void launch_ups_backward(const LaunchCtx& L, bool latent_grads, int j_begin, int
     const Plan& H = *L.host;
     for (int j = j_begin; j <= H.L - 2 && j < j_end; ++j) {
         if (H.ups_n[j] == 0) continue;
-        const dim3 grid(ups_blocks_x(H, j, L.num_sms, false), H.ups_n[j]);
+        const dim3 grid(ups_blocks_x(H, j, L.num_sms, false), H.ups_n[j], L.batch);
         const int wl = latent_grads ? 1 : 0;
         switch (ups_bwd_tile(H, j, L.num_sms)) {
             case 16: launch_pdl(k_ups_bwd<16>, grid, kThreads, sizeof(BwdSmem<16>), L.stream, 'b', L.plan, j, wl); break;

@@ -515,6 +515,67 @@ class Trainer:
         return flat[p.offset:p.offset + p.size]
 
 
+class Batch:
+    """Several trainers of one image size / decoder run in lock-step by one set
+    of kernel launches per stage (include/coolchic_b200_batch.h; BASELINE
+    config 3).  The reference's multi-image mode is independent encodes on a
+    thread pool (tools/coolcodec.cpp:150-171); each Trainer here stays a full
+    detail::Trainer equivalent."""
+
+    def __init__(self, trainers):
+        self.trainers = list(trainers)
+        if not self.trainers:
+            raise ConfigError("empty batch")
+        self.lib = self.trainers[0].lib
+        arr = (C.c_void_p * len(self.trainers))(*[t._h.value for t in self.trainers])
+        self._h = C.c_void_p()
+        _check(self.lib, self.lib.cc_batch_create(arr, len(self.trainers), C.byref(self._h)))
+
+    def reserve_iterations(self, n: int) -> None:
+        _check(self.lib, self.lib.cc_batch_reserve_iterations(self._h, int(n)))
+
+    def enqueue_proxy_iterations(self, lr, temp, noise_std) -> None:
+        lr = np.ascontiguousarray(lr, np.float64)
+        n = lr.size
+        temp = np.ascontiguousarray(np.broadcast_to(temp, (n,)), np.float64)
+        noise_std = np.ascontiguousarray(np.broadcast_to(noise_std, (n,)), np.float64)
+        dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+        _check(self.lib, self.lib.cc_batch_enqueue_proxy_iterations(self._h, n, dp(lr), dp(temp),
+                                                                    dp(noise_std)))
+
+    def synchronize(self) -> None:
+        _check(self.lib, self.lib.cc_batch_synchronize(self._h))
+
+    def proxy_iterations(self, lr, temp, noise_std) -> np.ndarray:
+        """n iterations of every image; returns costs [image, iteration]."""
+        n = np.asarray(lr).size
+        self.enqueue_proxy_iterations(lr, temp, noise_std)
+        self.synchronize()
+        out = np.empty((len(self.trainers), n), np.float64)
+        rec = np.empty(4 * n, np.float64)
+        for b, t in enumerate(self.trainers):
+            _check(self.lib, self.lib.cc_trainer_last_records(t._h, n, rec.ctypes.data_as(C.POINTER(C.c_double))))
+            out[b] = rec[0::4]
+        return out
+
+    def close(self):
+        if self._h:
+            self.lib.cc_batch_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
 def train(image: np.ndarray, enc: EncoderConfig, dcfg: DecoderConfig, lib=None,
           device: int = 0) -> TrainResult:
     """train(img, enc, dcfg) (encoder.hpp:349-413)."""

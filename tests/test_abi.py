@@ -26,7 +26,8 @@ def _exports(lib, names):
 
 def test_product_exports_every_declared_symbol(product_lib):
     names = (capi.header_symbols("coolchic_b200.h") + capi.header_symbols("coolchic_b200_diag.h")
-             + capi.header_symbols("coolchic_b200_band.h") + capi.header_symbols("coolchic_b200_codec.h"))
+             + capi.header_symbols("coolchic_b200_band.h") + capi.header_symbols("coolchic_b200_codec.h")
+             + capi.header_symbols("coolchic_b200_batch.h"))
     assert len(names) >= 48
     assert _exports(product_lib, names) == []
     assert product_lib.cc_impl_name() == b"b200"
@@ -37,6 +38,7 @@ def test_signature_table_covers_header():
     assert sorted(capi.DIAG_SIGNATURES) == capi.header_symbols("coolchic_b200_diag.h")
     assert sorted(capi.BAND_SIGNATURES) == capi.header_symbols("coolchic_b200_band.h")
     assert sorted(capi.CODEC_SIGNATURES) == capi.header_symbols("coolchic_b200_codec.h")
+    assert sorted(capi.BATCH_SIGNATURES) == capi.header_symbols("coolchic_b200_batch.h")
 
 
 def test_checkers_export_the_same_abi(ref_lib, port_lib):

@@ -752,3 +752,18 @@ def test_full_schedule_final_rd_vs_golden(gpu_lib, name):
     print(f"{name}: gpu {r.stats.true_cost:.6e} ref {g['true_cost']:.6e} rel {rel:.2e} "
           f"psnr {r.stats.psnr:.3f}/{g['psnr']:.3f} bpp {r.stats.rate_bpp:.4f}/{g['rate_bpp']:.4f}")
     assert rel <= 5e-3
+
+
+def test_tensor_core_arm_parity(gpu_lib, ref_lib):
+    """The tcgen05 ARM kernel (cc_arm_tc.cu, selected with CCB_ARM=tc): the
+    golden lock-step cases and a truth-arbitrated 512x768 lock-step against
+    the reference, in a subprocess (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+
+    env = dict(os.environ, CCB_ARM="tc")
+    r = subprocess.run([sys.executable, "-m", "tests.arm_variant_run"], env=env, capture_output=True,
+                       text=True, timeout=900, cwd=str(golden_util.GOLDEN.parents[1]))
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0
