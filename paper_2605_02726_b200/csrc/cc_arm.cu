@@ -603,6 +603,7 @@ void launch_arm2(const LaunchCtx& L, int mode);
 
 bool arm_tc_supported(int Dp, int Wp);
 size_t arm_tc_smem_bytes(int Dp, int Wp);
+int arm_tc_blocks_per_sm(int Dp, int Wp);
 void arm_tc_configure(int Dp, int Wp);
 void launch_arm_tc(const LaunchCtx& L, int mode);
 
@@ -659,10 +660,7 @@ void launch_arm(const LaunchCtx& L, int mode) {
 }
 
 int arm_blocks_per_sm(int Dp, int Wp) {
-    if (use_tc(Dp, Wp)) {  // __launch_bounds__(128, 2), TMEM: <= 128 columns per CTA
-        const int b = int((227 * 1024) / (arm_tc_smem_bytes(Dp, Wp) + 1024));
-        return b < 1 ? 1 : (b > 2 ? 2 : b);
-    }
+    if (use_tc(Dp, Wp)) return std::min(2, arm_tc_blocks_per_sm(Dp, Wp));  // TMEM: <= 128 columns per CTA
     if (use_arm2(Dp, Wp)) {  // __launch_bounds__(128, 2)
         const int b = int((227 * 1024) / (arm2_smem_bytes(Dp, Wp) + 1024));
         return b < 1 ? 1 : (b > 2 ? 2 : b);

@@ -2,9 +2,11 @@
 // entropy_model.hpp:180-336) with its four per-latent dense layers on the
 // sm_100a tensor cores.
 //
-// Persistent CTAs of 128 threads (one thread per latent of a row-segment tile
-// of <= 128 latents, one TMEM lane each), two CTAs per SM so that one CTA's
-// tensor-core round trips and barriers overlap the other's CUDA-core work.
+// Persistent CTAs of 256 threads over row-segment tiles of <= 128 latents: a
+// latent is one TMEM lane, shared by two threads (warps w and w + 4 address the
+// same lane quarter) that each own half of every layer's features; two CTAs
+// per SM so that one CTA's tensor-core round trips and barriers overlap the
+// other's CUDA-core work.
 // Per tile:
 //
 //   gather C (causal context + IFCE features, fp32)          CUDA cores
@@ -46,8 +48,8 @@ namespace ccb {
 
 namespace {
 
-constexpr int T = kArmTile;   // latents per tile (128) == threads per CTA
-constexpr int NT = T;
+constexpr int T = kArmTile;   // latents per tile (128)
+constexpr int NT = 2 * T;     // two threads per latent: half h owns half of every layer's features
 constexpr int LT = T + 4;     // feature-major row length (floats)
 constexpr int kRM = 11;       // max IFCE source grids: hyper (L - 4) + L - 1 - k <= 11 for L <= 8
 constexpr int kRR = kRM + 1;  // R rows + the ones row (3 row blocks of 4)
@@ -100,6 +102,9 @@ struct TC {
     static constexpr int MAXU = (NU + NT - 1) / NT;
     static constexpr int NACC5 = kMaxSlots * kFM * kRR;
     static_assert(NU * 16 * 2 <= ACT, "fp64 epilogue staging fits in the activation rows");
+    // two CTAs per SM (128 registers) unless the weight-gradient units need a
+    // second register-accumulated set (wide ARM inputs, e.g. the cfg4 decoder)
+    static constexpr int MINB = MAXU > 1 ? 1 : 2;
 };
 
 template <int DP, int WP>
@@ -180,6 +185,13 @@ struct ChunkStore {  // hi at TM_AH + c, lo at TM_AL + c
     }
 };
 
+// v[h * OFF + i] with i a compile-time index: a select of two registers
+// instead of a dynamically indexed (local-memory) array
+template <int OFF>
+__device__ __forceinline__ float hsel(const float (&v)[32], int h, int i) {
+    return h ? v[OFF + i] : v[i];
+}
+
 // this thread's A row is complete in TMEM: make it visible to the MMA issuer
 __device__ __forceinline__ void a_ready() {
     umma::wait_st();
@@ -200,7 +212,7 @@ __device__ __forceinline__ void mma3_ts(uint32_t d, uint32_t a_hi, uint32_t a_lo
 }
 
 template <int DP, int WP, int MODE>
-__global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
+__global__ void __launch_bounds__(NT, TC<DP, WP>::MINB) k_arm_tc(const Plan* __restrict__ pp,
                                                   const int4* __restrict__ tiles, int ntiles) {
     using K = TC<DP, WP>;
     using CS = ChunkStore<DP, WP>;
@@ -208,7 +220,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
     extern __shared__ __align__(16) unsigned char smem_raw[];
     TcSmem<DP, WP>& sm = *reinterpret_cast<TcSmem<DP, WP>*>(smem_raw);
     const int tid = threadIdx.x;
-    const int lt = tid;
+    const int half = tid >> 7, lt = tid & (T - 1);
     const int D = P.D, Wd = P.Wd, S = P.S, F = P.F;
     const float* prm = P.params;
     const bool has_stab = P.off_astab >= 0;
@@ -278,7 +290,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
     __syncthreads();
     umma::fence_after_sync();
     const uint32_t tm0 = sm.tmem;
-    const uint32_t tl = tm0 + (uint32_t(tid & ~31) << 16);  // this warp's 32 lanes
+    const uint32_t tl = tm0 + (uint32_t(tid & 96) << 16);  // this warp's lane quarter (warps w, w + 4 share it)
     // B descriptors (constant for the whole launch)
     const uint64_t d_b1h = umma::desc(umma::smem_u32(sm.b1[0]), 128, (K::KD / 4) * 128);
     const uint64_t d_b1l = umma::desc(umma::smem_u32(sm.b1[1]), 128, (K::KD / 4) * 128);
@@ -379,18 +391,22 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
         const int4 nxt2 = sm.trec[kt & 3];
         ++kt;
 
-        // ---- P1: C = context + IFCE features (+ ones at DP) -> rows + A ----
+        // ---- P1: C = context + IFCE features (+ ones at DP): this half's
+        // chunks -> feature-major rows + A ----
         float* const sR = sm.win[wb] + WC;
-        float pc0 = 0.0f, pc1 = 0.0f;  // head stabiliser term stab . C
+        float pc0 = 0.0f, pc1 = 0.0f;  // this half's share of the stabiliser term stab . C
         {
             const float* win = sm.win[wb];
+            constexpr int CH = K::KD / 8;  // chunks per half
             float rv[kRM];
-            if (slot >= 0) {
+            const bool need_r = slot >= 0 && (half + 1) * 4 * CH > S;
+            if (need_r) {
 #pragma unroll
                 for (int j = 0; j < kRM; ++j) rv[j] = sR[j * LT + lt];
             }
 #pragma unroll
-            for (int c = 0; c < K::KD / 4; ++c) {
+            for (int cc = 0; cc < CH; ++cc) {
+                const int c = half * CH + cc;
                 float v4[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -399,10 +415,17 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
                     if (f < S) {
                         v = valid ? win[sm.woff[f] + lt] : 0.0f;
                     } else if (f < D) {
-                        if (slot >= 0 && valid) {
+                        if (need_r && valid) {
+                            const float4* wf = reinterpret_cast<const float4*>(sm.Wf[slot][f - S]);
                             float a = sm.bf[slot][f - S];  // gemm_xwt_fast order: bias, then j
 #pragma unroll
-                            for (int j = 0; j < kRM; ++j) a = fmaf(rv[j], sm.Wf[slot][f - S][j], a);
+                            for (int q = 0; q < (kRM + 3) / 4; ++q) {
+                                const float4 w4 = wf[q];
+                                a = fmaf(rv[4 * q], w4.x, a);
+                                if (4 * q + 1 < kRM) a = fmaf(rv[4 * q + 1], w4.y, a);
+                                if (4 * q + 2 < kRM) a = fmaf(rv[4 * q + 2], w4.z, a);
+                                if (4 * q + 3 < kRM) a = fmaf(rv[4 * q + 3], w4.w, a);
+                            }
                             v = a;
                         }
                     } else if (f == DP) {
@@ -417,10 +440,13 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
                 }
                 CS::put(tl, 4 * c, v4[0], v4[1], v4[2], v4[3]);
             }
-            sC[(DP + 1) * LT + lt] = valid ? win[P.P * WS + P.P + lt] : 0.0f;  // own value
-            sH1[WP * LT + lt] = valid ? 1.0f : 0.0f;
-            sH2[WP * LT + lt] = valid ? 1.0f : 0.0f;
-            if (slot >= 0) sR[kRM * LT + lt] = valid ? 1.0f : 0.0f;
+            if (half == 0) {
+                sC[(DP + 1) * LT + lt] = valid ? win[P.P * WS + P.P + lt] : 0.0f;  // own value
+                sH1[WP * LT + lt] = valid ? 1.0f : 0.0f;
+            } else {
+                sH2[WP * LT + lt] = valid ? 1.0f : 0.0f;
+                if (slot >= 0) sR[kRM * LT + lt] = valid ? 1.0f : 0.0f;
+            }
         }
         a_ready();
         if (tid == 0) {
@@ -429,8 +455,8 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
             umma::commit(&sm.mbar);
         }
 
-        // ---- P2: H1 = relu(acc) -> rows + A (ones at WP) ----
-        uint32_t m1 = 0;  // relu'(H1)
+        // ---- P2: H1 = relu(acc) -> rows + A (ones at WP), this half's chunks ----
+        uint32_t m1 = 0;  // relu'(H1) of this half's features
         umma::mbar_wait(&sm.mbar, phase);
         phase ^= 1;
         umma::fence_after_sync();
@@ -438,16 +464,19 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
             float v[32];
             umma::ld32(tl + K::TM_ACC, v);
             umma::wait_ld();
+            constexpr int CH = K::KW / 8;
 #pragma unroll
-            for (int c = 0; c < K::KW / 4; ++c) {
+            for (int cc = 0; cc < CH; ++cc) {
+                const int c = half * CH + cc;
                 float h4[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int a = 4 * c + i;
+                    const float x = hsel<K::KW / 2>(v, half, 4 * cc + i);
                     float h = 0.0f;
                     if (a < WP) {
-                        h = v[a] > 0.0f ? v[a] : 0.0f;
-                        if (v[a] > 0.0f) m1 |= 1u << a;
+                        h = x > 0.0f ? x : 0.0f;
+                        if (x > 0.0f) m1 |= 1u << (4 * cc + i);
                         sH1[a * LT + lt] = h;
                     } else if (a == WP) {
                         h = valid ? 1.0f : 0.0f;
@@ -464,35 +493,48 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
             umma::commit(&sm.mbar);
         }
 
-        // ---- P3: H2 = relu(acc) -> rows; head; P4: Laplace rate + backward; dH2 ----
-        uint32_t m2 = 0;  // relu'(H2)
+        // ---- P3: H2 = relu(acc) -> rows; this half's head partials ----
+        uint32_t m2 = 0;  // relu'(H2) of this half's features
         umma::mbar_wait(&sm.mbar, phase);
         phase ^= 1;
         umma::fence_after_sync();
-        float dmu = 0.0f, dsr = 0.0f;
         {
             float v[32];
             umma::ld32(tl + K::TM_ACC, v);
             umma::wait_ld();
             float p0 = pc0, p1 = pc1;
 #pragma unroll
-            for (int a = 0; a < WP; ++a) {
-                const float h = v[a] > 0.0f ? v[a] : 0.0f;
-                if (v[a] > 0.0f) m2 |= 1u << a;
-                sH2[a * LT + lt] = h;
-                p0 = fmaf(h, sm.W3[0][a], p0);
-                p1 = fmaf(h, sm.W3[1][a], p1);
+            for (int i = 0; i < K::KW / 2; ++i) {
+                const int a = half * (K::KW / 2) + i;
+                const float x = hsel<K::KW / 2>(v, half, i);
+                if (a < WP) {
+                    const float h = x > 0.0f ? x : 0.0f;
+                    if (x > 0.0f) m2 |= 1u << i;
+                    sH2[a * LT + lt] = h;
+                    p0 = fmaf(h, sm.W3[0][a], p0);
+                    p1 = fmaf(h, sm.W3[1][a], p1);
+                }
             }
+            sHP[(2 * half) * LT + lt] = p0;
+            sHP[(2 * half + 1) * LT + lt] = p1;
+        }
+        umma::fence_before_sync();
+        __syncthreads();
+
+        // ---- P4: Laplace rate + its backward (both halves, identical
+        // arithmetic), dH2 for this half's features ----
+        float dmu = 0.0f, dsr = 0.0f;
+        {
             const float vv = sC[(DP + 1) * LT + lt];
-            const float mu = sm.hb[0] + p0;
-            const float sr = sm.hb[1] + p1;
+            const float mu = sm.hb[0] + (sHP[lt] + sHP[2 * LT + lt]);
+            const float sr = sm.hb[1] + (sHP[LT + lt] + sHP[3 * LT + lt]);
             const float sg = sigma_from_raw(sr);
             const float bsc = sg * kInvSqrt2F;
             const float u = fabsf(vv - mu);
             const float e1 = cc_exp(-(u + 0.5f) / bsc);
             const float e2 = cc_exp(-fabsf(u - 0.5f) / bsc);
             const float p = u >= 0.5f ? 0.5f * (e2 - e1) : 1.0f - 0.5f * (e1 + e2);
-            if (own) bits_thr += double(-(cc_log(std_max(p, kProbFloorF)) * kLog2EF));
+            if (own && half == 0) bits_thr += double(-(cc_log(std_max(p, kProbFloorF)) * kLog2EF));
             if (MODE != kArmForward) {
                 float gv = 0.0f;
                 if (own && p > kProbFloorF) {
@@ -506,11 +548,15 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
                     if (sg > kSigmaMinF && sg < kSigmaMaxF) dsr = up * dp_db * kInvSqrt2F * sg;
                     gv = up * dp_du * sgn;
                 }
-                if (MODE == kArmProxy && valid) P.gown[g.lat_off + li] = gv;
-                sDR[0 * LT + lt] = dmu;
-                sDR[1 * LT + lt] = dsr;
+                if (half == 0) {
+                    if (MODE == kArmProxy && valid) P.gown[g.lat_off + li] = gv;
+                    sDR[0 * LT + lt] = dmu;
+                    sDR[1 * LT + lt] = dsr;
+                }
+                constexpr int CH = K::KW / 8;
 #pragma unroll
-                for (int c = 0; c < K::KW / 4; ++c) {  // dH2 = (W3^T draw) * relu'(H2)
+                for (int cc = 0; cc < CH; ++cc) {  // dH2 = (W3^T draw) * relu'(H2)
+                    const int c = half * CH + cc;
                     float d4[4];
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
@@ -519,7 +565,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
                         if (a < WP) {
                             d = fmaf(dmu, sm.W3[0][a], 0.0f);
                             d = fmaf(dsr, sm.W3[1][a], d);
-                            d = (m2 >> a) & 1u ? d : 0.0f;
+                            d = (m2 >> (4 * cc + i)) & 1u ? d : 0.0f;
                             sDH2[a * LT + lt] = d;
                         }
                         d4[i] = d;
@@ -528,9 +574,8 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
                 }
             }
         }
-        (void)sHP;
         if (MODE == kArmForward) {
-            __syncthreads();  // windows reused by the next tile
+            __syncthreads();  // windows / head partials reused by the next tile
             wb ^= 1;
             cur = nxt;
             nxt = nxt2;
@@ -552,23 +597,26 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
             float v[32];
             umma::ld32(tl + K::TM_ACC, v);
             umma::wait_ld();
+            constexpr int CH = K::KW / 8;
 #pragma unroll
-            for (int c = 0; c < K::KW / 4; ++c) {
+            for (int cc = 0; cc < CH; ++cc) {
+                const int c = half * CH + cc;
                 float d4[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int b = 4 * c + i;
                     float d = 0.0f;
                     if (b < WP) {
-                        d = (m1 >> b) & 1u ? v[b] : 0.0f;
+                        d = (m1 >> (4 * cc + i)) & 1u ? hsel<K::KW / 2>(v, half, 4 * cc + i) : 0.0f;
                         sDH1[b * LT + lt] = d;
                     }
                     d4[i] = d;
                 }
                 CS::put(tl, 4 * c, d4[0], d4[1], d4[2], d4[3]);
             }
-            CS::put(tl, K::KW, dmu, dsr, 0.0f, 0.0f);
-            CS::put(tl, K::KW + 4, 0.0f, 0.0f, 0.0f, 0.0f);
+            // draw (dmu, dsr, 0, 0 | 0, 0, 0, 0) at columns KW .. KW+7
+            if (half == 0) CS::put(tl, K::KW, dmu, dsr, 0.0f, 0.0f);
+            else CS::put(tl, K::KW + 4, 0.0f, 0.0f, 0.0f, 0.0f);
         }
         umma::wait_st();
         umma::fence_before_sync();
@@ -589,12 +637,15 @@ __global__ void __launch_bounds__(NT, 2) k_arm_tc(const Plan* __restrict__ pp,
             umma::ld32(tl + K::TM_ACC, v);
             umma::wait_ld();
             const bool st = MODE == kArmProxy && valid;
+            float* const dcp = P.dctx + g.dctx_off + li;
 #pragma unroll
-            for (int k = 0; k < K::ND; ++k) {
+            for (int i = 0; i < K::ND / 2; ++i) {
+                const int k = half * (K::ND / 2) + i;
+                const float x = hsel<K::ND / 2>(v, half, i);
                 if (k < S) {
-                    if (st) P.dctx[g.dctx_off + int64_t(k) * count + li] = v[k];
+                    if (st) dcp[int64_t(k) * count] = x;
                 } else if (k < S + F && slot >= 0) {
-                    const float dv = valid ? v[k] : 0.0f;
+                    const float dv = valid ? x : 0.0f;
                     sDF[(k - S) * LT + lt] = dv;
                     if (st) P.dfeat[g.dfeat_off + int64_t(k - S) * count + li] = dv;
                 }
@@ -715,6 +766,26 @@ void configure_t() {
 bool arm_tc_supported(int Dp, int Wp) {
     return (Dp == 8 && Wp == 8) || (Dp == 16 && Wp == 12) || (Dp == 20 && Wp == 20) ||
            (Dp == 28 && Wp == 28) || (Dp == 32 && Wp == 20);
+}
+
+template <int DP, int WP>
+void configure_t();
+
+template <int DP, int WP>
+int occ_t() {
+    configure_t<DP, WP>();  // the >48 KB shared-memory opt-in the occupancy query needs
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_arm_tc<DP, WP, kArmProxy>, NT, tc_smem<DP, WP>());
+    return b < 1 ? 1 : b;
+}
+
+// resident CTAs per SM of the proxy variant (registers and shared memory)
+int arm_tc_blocks_per_sm(int Dp, int Wp) {
+    if (Dp == 8 && Wp == 8) return occ_t<8, 8>();
+    if (Dp == 16 && Wp == 12) return occ_t<16, 12>();
+    if (Dp == 20 && Wp == 20) return occ_t<20, 20>();
+    if (Dp == 28 && Wp == 28) return occ_t<28, 28>();
+    return occ_t<32, 20>();
 }
 
 size_t arm_tc_smem_bytes(int Dp, int Wp) {
