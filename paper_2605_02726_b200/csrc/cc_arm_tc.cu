@@ -761,22 +761,19 @@ void configure_t() {
     cudaFuncSetAttribute(k_arm_tc<DP, WP, kArmProxy>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
-}  // namespace
-
-bool arm_tc_supported(int Dp, int Wp) {
-    return (Dp == 8 && Wp == 8) || (Dp == 16 && Wp == 12) || (Dp == 20 && Wp == 20) ||
-           (Dp == 28 && Wp == 28) || (Dp == 32 && Wp == 20);
-}
-
-template <int DP, int WP>
-void configure_t();
-
 template <int DP, int WP>
 int occ_t() {
     configure_t<DP, WP>();  // the >48 KB shared-memory opt-in the occupancy query needs
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_arm_tc<DP, WP, kArmProxy>, NT, tc_smem<DP, WP>());
     return b < 1 ? 1 : b;
+}
+
+}  // namespace
+
+bool arm_tc_supported(int Dp, int Wp) {
+    return (Dp == 8 && Wp == 8) || (Dp == 16 && Wp == 12) || (Dp == 20 && Wp == 20) ||
+           (Dp == 28 && Wp == 28) || (Dp == 32 && Wp == 20);
 }
 
 // resident CTAs per SM of the proxy variant (registers and shared memory)
