@@ -119,7 +119,7 @@ struct TcSmem {
     alignas(16) float W3[2][WP];
     alignas(16) float stab[2][DP];
     alignas(16) float hb[4];
-    alignas(16) float Wf[kMaxSlots][kFM][kRM];
+    alignas(16) float Wf[kMaxSlots][kFM][kRR];  // rows padded to 12 (float4 loads); column 11 zero
     alignas(16) float bf[kMaxSlots][kFM];
     int woff[kMaxCtx];
     double acc5[K::NACC5];
@@ -266,8 +266,8 @@ __global__ void __launch_bounds__(NT, TC<DP, WP>::MINB) k_arm_tc(const Plan* __r
         sm.stab[j][k] = (has_stab && k < D) ? prm[P.off_astab + j * D + k] : 0.0f;
     }
     if (tid < 4) sm.hb[tid] = tid < 2 ? prm[P.off_hb + tid] : 0.0f;
-    for (int e = tid; e < kMaxSlots * kFM * kRM; e += NT) {
-        const int s = e / (kFM * kRM), r = e % (kFM * kRM), f = r / kRM, j = r % kRM;
+    for (int e = tid; e < kMaxSlots * kFM * kRR; e += NT) {
+        const int s = e / (kFM * kRR), r = e % (kFM * kRR), f = r / kRR, j = r % kRR;
         float v = 0.0f;
         if (s < P.n_slots) {
             const int rd = P.g[P.slot_gi[s]].rdim;
