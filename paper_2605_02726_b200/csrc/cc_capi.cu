@@ -8,6 +8,7 @@
 #include <cstring>
 #include <fstream>
 #include <limits>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -118,6 +119,119 @@ void run_fixed(Trainer& tr, int n, double lr, double temp, double noise) {
 
 namespace ccb {
 
+namespace {
+
+// One candidate's full trainer state (CandidateState, encoder.hpp:42-48) from
+// one trainer into another of the same geometry.
+void copy_candidate(Trainer& src, Trainer& dst) {
+    const Plan& p = src.plan();
+    const size_t nl = size_t(p.n_latents), np = size_t(p.n_params);
+    std::vector<float> lat(nl), lm(nl), lv(nl), par(np), nm(np), nv(np);
+    std::vector<int64_t> lt(static_cast<size_t>(p.n_grids)), nt(static_cast<size_t>(p.n_tensors));
+    const bool soap = p.use_soap != 0;
+    src.get_state(lat.data(), par.data(), lm.data(), lv.data(), lt.data(), soap ? nullptr : nm.data(),
+                  soap ? nullptr : nv.data(), soap ? nullptr : nt.data());
+    dst.set_state(lat.data(), par.data(), lm.data(), lv.data(), lt.data(), soap ? nullptr : nm.data(),
+                  soap ? nullptr : nv.data(), soap ? nullptr : nt.data());
+    if (soap) {
+        int64_t na = 0;
+        src.soap_state(nullptr, nullptr, nullptr, nullptr, &na);
+        std::vector<double> arena(static_cast<size_t>(na));
+        src.soap_state(arena.data(), nm.data(), nv.data(), nt.data(), nullptr);
+        dst.set_soap_state(arena.data(), nm.data(), nv.data(), nt.data());
+    }
+}
+
+bool serial_warmup_forced() {
+    static const bool v = [] {
+        const char* e = std::getenv("CCB_WARMUP_SERIAL");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
+}  // namespace
+
+// warmup (encoder.hpp:315-342) with the candidates of each round trained
+// CONCURRENTLY ("warm-up candidates are embarrassingly
+// parallel"): candidate ci lives in its own trainer (the caller's for ci = 0),
+// the round runs as one batched graph (Batch), and every candidate starts from
+// the global_iter the sequential loop would give it, so its noise stream —
+// and therefore every value — is what the sequential warm-up computes.
+// Returns false (state of `tr` reset to a fresh start) when that
+// equivalence cannot be guaranteed: a non-finite iteration leaves global_iter
+// behind, which shifts the later candidates' noise keys in the sequential
+// order; warmup() then runs the sequential loop.
+bool warmup_batched(Trainer& tr, const float* image, int h, int w, const cc_decoder_config& dec, int device) {
+    const cc_encoder_config& enc = tr.enc();
+    const int K = enc.warmup_candidates, it = enc.warmup_iters;
+    if (K <= 1 || it <= 0 || serial_warmup_forced()) return false;
+    const int64_t g0 = tr.global_iter();
+    const int s0 = tr.skipped_steps();
+    std::vector<std::unique_ptr<Trainer>> helpers;
+    std::vector<Trainer*> all{&tr};
+    for (int ci = 1; ci < K; ++ci) {
+        helpers.push_back(std::make_unique<Trainer>(image, h, w, enc, dec, device));
+        all.push_back(helpers.back().get());
+    }
+    const size_t nit = static_cast<size_t>(it);
+    const std::vector<double> lr(nit, enc.lr_start), tp(nit, enc.temp_start), ns(nit, enc.noise_std_start);
+    auto run_round = [&](const std::vector<Trainer*>& ts, const std::vector<int64_t>& start) {
+        for (size_t i = 0; i < ts.size(); ++i) ts[i]->set_counters(start[i], 0);
+        {
+            Batch b(ts);
+            b.enqueue_proxy_iterations(it, lr.data(), tp.data(), ns.data());
+            b.synchronize();
+        }
+        bool ok = true;
+        for (size_t i = 0; i < ts.size(); ++i) ok = ok && ts[i]->global_iter() == start[i] + it;
+        return ok;
+    };
+    int skipped = 0;
+    // round 1: every candidate, fresh (encoder.hpp:317-323)
+    std::vector<int64_t> start(static_cast<size_t>(K));
+    for (int ci = 0; ci < K; ++ci) {
+        all[ci]->fresh_candidate(ci);
+        start[size_t(ci)] = g0 + int64_t(ci) * it;
+    }
+    auto restart = [&] {
+        tr.fresh_candidate(0);
+        tr.set_counters(g0, s0);
+        return false;
+    };
+    if (!run_round(all, start)) return restart();
+    struct C {
+        int idx;
+        double cost;
+    };
+    std::vector<C> cands;
+    for (int ci = 0; ci < K; ++ci) {
+        skipped += all[ci]->skipped_steps();
+        cands.push_back({ci, all[ci]->true_cost(nullptr, nullptr)});
+    }
+    std::stable_sort(cands.begin(), cands.end(), [](const C& a, const C& b) { return a.cost < b.cost; });
+    const int keep = std::min<int>(enc.warmup_keep, int(cands.size()));
+    cands.resize(size_t(keep));
+    // round 2: the kept candidates in sorted order (encoder.hpp:331-336)
+    std::vector<Trainer*> kept;
+    std::vector<int64_t> start2;
+    for (int j = 0; j < keep; ++j) {
+        kept.push_back(all[size_t(cands[size_t(j)].idx)]);
+        start2.push_back(g0 + int64_t(K + j) * it);
+    }
+    if (!run_round(kept, start2)) return restart();
+    for (int j = 0; j < keep; ++j) {
+        skipped += kept[size_t(j)]->skipped_steps();
+        cands[size_t(j)].cost = kept[size_t(j)]->true_cost(nullptr, nullptr);
+    }
+    std::stable_sort(cands.begin(), cands.end(), [](const C& a, const C& b) { return a.cost < b.cost; });
+    Trainer* best = all[size_t(cands[0].idx)];
+    if (best != &tr) copy_candidate(*best, tr);
+    tr.set_counters(g0 + int64_t(K + keep) * it, s0 + skipped);
+    tr.set_current_cost(cands[0].cost);
+    return true;
+}
+
 // warmup (encoder.hpp:315-342): candidates live in device candidate slots.
 void warmup(Trainer& tr) {
     const cc_encoder_config& enc = tr.enc();
@@ -156,12 +270,13 @@ void warmup(Trainer& tr) {
 }
 
 // train (encoder.hpp:349-413) on a trainer whose counters were reset.
-void train(Trainer& tr, cc_train_stats* out) {
+void train(Trainer& tr, cc_train_stats* out, const float* image, int h, int w, const cc_decoder_config* dec,
+           int device) {
     const auto t0 = std::chrono::steady_clock::now();
     const cc_encoder_config& enc = tr.enc();
     const double npix = double(tr.plan().npix);
     Log log(tr.log_path());
-    warmup(tr);
+    if (!(image && dec && warmup_batched(tr, image, h, w, *dec, device))) warmup(tr);
 
     const int horizon = std::max(1, enc.main_iters - 1);
     cc_train_stats st{};
@@ -675,7 +790,7 @@ int ccb_soap_set_state(cc_trainer* t, const double* arena, const float* m1, cons
 
 int cc_trainer_warmup(cc_trainer* t) {
     return guarded([&] {
-        ccb::warmup(*t->tr);
+        if (!ccb::warmup_batched(*t->tr, t->image.data(), t->h, t->w, t->dec, t->device)) ccb::warmup(*t->tr);
         return CC_OK;
     });
 }
@@ -688,7 +803,7 @@ int cc_trainer_train(cc_trainer* t, cc_train_stats* stats, float* latents, int32
         e.log_path = t->log_path.c_str();
         t->tr.reset();
         t->tr = std::make_unique<Trainer>(t->image.data(), t->h, t->w, e, t->dec, t->device);
-        ccb::train(*t->tr, stats);
+        ccb::train(*t->tr, stats, t->image.data(), t->h, t->w, &t->dec, t->device);
         if (latents || q || params) {
             std::vector<float> lat(size_t(t->tr->plan().n_latents));
             t->tr->get_state(lat.data(), params, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);

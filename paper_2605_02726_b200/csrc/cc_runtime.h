@@ -252,6 +252,10 @@ void gauss(uint64_t stream, uint64_t idx0, int n, float* out);
 
 // warmup / train (encoder.hpp:315-413) over the B200 Trainer.
 void warmup(Trainer& tr);
-void train(Trainer& tr, cc_train_stats* stats);
+// train: with the host image (image != NULL) the warm-up candidates of each
+// round run concurrently in helper trainers (warmup_batched).
+void train(Trainer& tr, cc_train_stats* stats, const float* image = nullptr, int h = 0, int w = 0,
+           const cc_decoder_config* dec = nullptr, int device = 0);
+bool warmup_batched(Trainer& tr, const float* image, int h, int w, const cc_decoder_config& dec, int device);
 
 }  // namespace ccb

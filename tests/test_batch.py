@@ -8,7 +8,7 @@ import pytest
 
 from paper_2605_02726_b200 import capi
 from paper_2605_02726_b200.trainer import Batch, DecoderConfig, EncoderConfig, Trainer
-from tests.conftest import make_image
+from tests.conftest import REPO as GOLDEN_ROOT, make_image
 
 
 def test_batch_header_declares_the_python_table():
@@ -61,3 +61,25 @@ def test_batch_rejects_mixed_geometry(gpu_lib):
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("soap", [0, 1])
+def test_batched_warmup_is_the_sequential_warmup(gpu_lib, tmp_path, soap):
+    """train()'s warm-up runs each round's candidates concurrently (one batched
+    graph); every candidate starts from the global_iter the
+    sequential loop (encoder.hpp:315-342) gives it, so the whole encode must
+    be bit-identical to the sequential warm-up (CCB_WARMUP_SERIAL=1)."""
+    import os
+    import subprocess
+    import sys
+
+    res = {}
+    for mode in ("0", "1"):
+        out = tmp_path / f"w{mode}.npz"
+        env = dict(os.environ, CCB_WARMUP_SERIAL=mode)
+        subprocess.run([sys.executable, "-m", "tests.warmup_run", str(out), str(soap)], env=env, check=True,
+                       timeout=600, cwd=str(GOLDEN_ROOT))
+        res[mode] = dict(np.load(out))
+    for k in res["0"]:
+        assert np.array_equal(res["0"][k], res["1"][k]), k
