@@ -51,6 +51,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-full-schedule", action="store_true")
+    ap.add_argument("--no-cfg3", action="store_true")
+    ap.add_argument("--cfg3-line", action="store_true", help="print the N>1 (config 3) line even at N=1")
+    ap.add_argument("--images", type=int, default=24, help="cfg3: images in total (sharded over the GPUs)")
     return ap.parse_args()
 
 
@@ -209,6 +212,8 @@ def run_b200(args, rank, world, local_rank):
 
     lib = capi.load_product()
     h, w = args.height, args.width
+    if world > 1 or args.cfg3_line:
+        return run_cfg3_line(args, lib, rank, world, dev, dist)
     img = make_synthetic_image(h, w, args.seed + rank, lib)
     enc = EncoderConfig.with_total(10000)
     enc.lmbda, enc.seed, enc.use_soap = 1e-3, args.seed + rank, False
@@ -390,6 +395,17 @@ def run_b200(args, rank, world, local_rank):
                 "timing": "host wall clock around the synchronous call, max over ranks"}
         finite = finite and math.isfinite(res.stats.true_cost)
 
+    # BASELINE config 3 on this one GPU: 24 images batched in one graph
+    cfg3 = None
+    if world == 1 and not args.no_cfg3:
+        tr.close()
+        r3 = run_cfg3(args, lib, args.images, args.seed, dev, None, min(K, 20), W)
+        cfg3 = {"value": r3["value"], "unit": UNIT, "ms_per_step": r3["ms_per_step"],
+                "images_per_gpu": r3["images_per_gpu"], "steps": r3["steps"], "e2e": r3["e2e"],
+                "costs_finite": r3["costs_finite"],
+                "workload": f"cfg3: {args.images} independent {h}x{w} synthetic images batched in one graph "
+                            "(include/coolchic_b200_batch.h), device-timed steady state"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -413,11 +429,148 @@ def run_b200(args, rank, world, local_rank):
             "it_per_s_per_image": K / (ms_max / 1e3),
             "value_l2_flushed": value_flushed,
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "full_schedule": full,
+            "cfg3_one_gpu": cfg3,
             "gpu_launches": int(kpi.value) * K, "kernels_per_step": int(kpi.value),
             "clocks": clocks, "costs_finite": finite,
         }
         print(json.dumps(line), flush=True)
     tr.close()
+
+
+def run_cfg3(args, lib, n_img, seed0, dev, dist, K, W):
+    """BASELINE config 3 on this GPU: n_img independent 512x768 images trained
+    in lock-step by one batched graph (include/coolchic_b200_batch.h).
+    Device-timed steady state (CUDA events on the batch's stream) and end to
+    end (images up from pinned host memory, records back) through the C ABI."""
+    import torch
+
+    from paper_2605_02726_b200.trainer import Batch
+
+    h, w = args.height, args.width
+    dcfg = DecoderConfig.from_name(args.preset)
+    imgs, trs = [], []
+    for m in range(n_img):
+        enc = EncoderConfig.with_total(10000)
+        enc.lmbda, enc.seed, enc.use_soap = 1e-3, seed0 + m, False
+        imgs.append(make_synthetic_image(h, w, seed0 + m, lib))
+        t = Trainer(imgs[-1], enc, dcfg, lib=lib, device=dev.index)
+        t.fresh_candidate(0)
+        trs.append(t)
+    stream = torch.cuda.Stream(device=dev)
+    if lib.cc_trainer_set_stream(trs[0]._h, C.c_void_p(stream.cuda_stream)) != 0:
+        raise RuntimeError(lib.cc_last_error().decode())
+    b = Batch(trs)  # every trainer moves onto the first one's stream
+    b.reserve_iterations(max(K, W))
+    lr, tp, ns = schedule(EncoderConfig.with_total(10000), W + K)
+    b.enqueue_proxy_iterations(lr[:W], tp[:W], ns[:W])
+    b.synchronize()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    b.enqueue_proxy_iterations(lr[W:W + K], tp[W:W + K], ns[W:W + K])
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    world = dist.get_world_size() if dist else 1
+    value = world * n_img * h * w * K / (ms / 1e3) / 1e9
+    rec = np.empty(4 * K, np.float64)
+    finite = True
+    for tr in trs:
+        lib.cc_trainer_last_records(tr._h, K, _dp(rec))
+        finite = finite and bool(np.all(np.isfinite(rec[0::4])))
+    # end to end: every image up from pinned host memory, the batched steps,
+    # every image's records read back
+    pinned = [torch.empty((3, h, w), dtype=torch.float32, pin_memory=True) for _ in range(n_img)]
+    for pm, im in zip(pinned, imgs):
+        pm.numpy()[...] = im
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for tr, pm in zip(trs, pinned):
+        tr.upload_image(pm.numpy())
+    b.enqueue_proxy_iterations(lr[W:W + K], tp[W:W + K], ns[W:W + K])
+    for tr in trs:
+        lib.cc_trainer_last_records(tr._h, K, _dp(rec))
+    e1.record(stream)
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e = world * n_img * h * w * K / (float(t.item()) / 1e3) / 1e9
+    kpi = C.c_int()
+    lib.ccb_kernels_per_iteration(trs[0]._h, C.byref(kpi))
+    b.close()
+    for tr in trs:
+        tr.close()
+    return {"value": value, "ms_per_step": ms / K, "images_per_gpu": n_img, "steps": K,
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": (n_img * 3 * h * w * 4 + K * 24) / K,
+                    "d2h_bytes_per_step": n_img * 32,
+                    "api": "cc_trainer_upload_image per image + cc_batch_enqueue_proxy_iterations + "
+                           "cc_trainer_last_records per image"},
+            "kernels_per_step": int(kpi.value), "costs_finite": finite}
+
+
+def run_cfg3_line(args, lib, rank, world, dev, dist):
+    """N > 1: BASELINE config 3 — 24 images sharded evenly over the ranks
+    (no collective on the data path), batched within each GPU."""
+    import torch
+
+    total = args.images
+    if total % world:
+        raise SystemExit(f"--images {total} does not split over {world} GPUs")
+    n_img = total // world
+    K, W = args.steps, max(3, args.warmup)
+    sampler = ClockSampler(None)
+    sampler.start()
+    r = run_cfg3(args, lib, n_img, args.seed + rank * n_img, dev, dist, K, W)
+    clocks = sampler.stop()
+    if rank == 0:
+        cfg = config_dict(args)
+        cfg.update({"workload": f"cfg3: {total} independent {args.height}x{args.width} synthetic images, "
+                                f"{n_img} per GPU batched in one graph, HOP, proxy_iteration (NN params Adam)",
+                    "images_per_gpu": n_img, "images_total": total,
+                    "parallelism": f"image-sharded x{world} (no collective), batched within each GPU"})
+        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+                "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+                "e2e": r["e2e"], "gpu_launches": r["kernels_per_step"] * K, "kernels_per_step": r["kernels_per_step"],
+                "clocks": clocks, "costs_finite": r["costs_finite"]}
+        print(json.dumps(line), flush=True)
+
+
+def capi_macs(lib, dcfg, h, w):def run_cfg3_line(args, lib, rank, world, dev, dist):
+    """N > 1: BASELINE config 3 — 24 images sharded evenly over the ranks
+    (no collective on the data path), batched within each GPU."""
+    import torch
+
+    total = args.images
+    if total % world:
+        raise SystemExit(f"--images {total} does not split over {world} GPUs")
+    n_img = total // world
+    K, W = args.steps, max(3, args.warmup)
+    sampler = ClockSampler(None)
+    sampler.start()
+    r = run_cfg3(args, lib, n_img, args.seed + rank * n_img, dev, dist, K, W)
+    clocks = sampler.stop()
+    if rank == 0:
+        cfg = config_dict(args)
+        cfg.update({"workload": f"cfg3: {total} independent {args.height}x{args.width} synthetic images, "
+                                f"{n_img} per GPU batched in one graph, HOP, proxy_iteration (NN params Adam)",
+                    "images_per_gpu": n_img, "images_total": total,
+                    "parallelism": f"image-sharded x{world} (no collective), batched within each GPU"})
+        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+                "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
+                "e2e": r["e2e"], "gpu_launches": r["kernels_per_step"] * K, "kernels_per_step": r["kernels_per_step"],
+                "clocks": clocks, "costs_finite": r["costs_finite"]}
+        print(json.dumps(line), flush=True)
 
 
 def capi_macs(lib, dcfg, h, w):
