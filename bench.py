@@ -545,34 +545,6 @@ def run_cfg3_line(args, lib, rank, world, dev, dist):
         print(json.dumps(line), flush=True)
 
 
-def capi_macs(lib, dcfg, h, w):def run_cfg3_line(args, lib, rank, world, dev, dist):
-    """N > 1: BASELINE config 3 — 24 images sharded evenly over the ranks
-    (no collective on the data path), batched within each GPU."""
-    import torch
-
-    total = args.images
-    if total % world:
-        raise SystemExit(f"--images {total} does not split over {world} GPUs")
-    n_img = total // world
-    K, W = args.steps, max(3, args.warmup)
-    sampler = ClockSampler(None)
-    sampler.start()
-    r = run_cfg3(args, lib, n_img, args.seed + rank * n_img, dev, dist, K, W)
-    clocks = sampler.stop()
-    if rank == 0:
-        cfg = config_dict(args)
-        cfg.update({"workload": f"cfg3: {total} independent {args.height}x{args.width} synthetic images, "
-                                f"{n_img} per GPU batched in one graph, HOP, proxy_iteration (NN params Adam)",
-                    "images_per_gpu": n_img, "images_total": total,
-                    "parallelism": f"image-sharded x{world} (no collective), batched within each GPU"})
-        line = {"metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-                "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": cfg,
-                "e2e": r["e2e"], "gpu_launches": r["kernels_per_step"] * K, "kernels_per_step": r["kernels_per_step"],
-                "clocks": clocks, "costs_finite": r["costs_finite"]}
-        print(json.dumps(line), flush=True)
-
-
 def capi_macs(lib, dcfg, h, w):
     dc = dcfg.to_c()
     return lib.cc_count_macs_per_pixel(C.byref(dc), h, w)
