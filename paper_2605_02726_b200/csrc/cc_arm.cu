@@ -649,6 +649,11 @@ static void launch_arm_mode(const LaunchCtx& L, int mode) {
 
 void launch_arm(const LaunchCtx& L, int mode) {
     const int Dp = L.host->Dp, Wp = L.host->Wp;
+    static const bool skip = [] {  // timing diagnostic only (wrong results): the iteration without the ARM
+        const char* e = std::getenv("CCB_DIAG_SKIP_ARM");
+        return e && e[0] == '1';
+    }();
+    if (skip) return;
     if (use_tc(Dp, Wp)) return launch_arm_tc(L, mode);
     if (use_arm2(Dp, Wp)) return launch_arm2(L, mode);
     if (Dp == 8 && Wp == 8) launch_arm_mode<8, 8>(L, mode);

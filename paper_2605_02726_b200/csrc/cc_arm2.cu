@@ -32,6 +32,7 @@
 #include "cc_kernels.h"
 #include "cc_math.cuh"
 #include "cc_reduce.cuh"
+#include "cc_ctx.cuh"
 #include "cc_tile.cuh"
 
 namespace ccb {
@@ -85,6 +86,7 @@ struct A2 {
     static constexpr int MAXU = (NU + NU5 + NT - 1) / NT;  // units per thread (upper bound)
     static constexpr int NACC5 = kMaxSlots * kFM * (kRM + 1);
     static_assert(NU * 16 <= ACT, "epilogue staging fits in the activation buffers");
+    static_assert(2 * RH >= DP, "dC rows (S <= D <= DP) fit in the H1 / H2 rows");
 };
 
 template <int DP, int WP>
@@ -447,9 +449,10 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
             }
         }
         __syncthreads();
-        // ---- P7: dC = W1ᵀ·dH1 + stabᵀ·draw -> dctx / dF ----
+        // ---- P7: dC = W1ᵀ·dH1 + stabᵀ·draw -> dF now, context rows after P8 ----
+        float2 dcacc[K::ND];
         {
-            float2 acc[K::ND];
+            float2 (&acc)[K::ND] = dcacc;
 #pragma unroll
             for (int n = 0; n < K::ND; ++n) acc[n] = make_float2(0.0f, 0.0f);
             tile_gemm<K::ND, WP>(sDH1, sm.W1, pr, grp, acc);
@@ -460,15 +463,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
             for (int n = 0; n < K::ND; ++n) {
                 const int k = grp * K::ND + n;
                 if (k < S) {
-                    if (MODE == kArmProxy) {
-                        float* dcp = P.dctx + g.dctx_off + int64_t(k) * count + l0;
-                        if (v1 && (reinterpret_cast<uintptr_t>(dcp) & 7) == 0) {
-                            *reinterpret_cast<float2*>(dcp) = acc[n];
-                        } else {
-                            if (v0) dcp[0] = acc[n].x;
-                            if (v1) dcp[1] = acc[n].y;
-                        }
-                    }
+                    // kept in registers: written as row partials after P8
                 } else if (k < S + F && slot >= 0) {
                     const float2 dv = make_float2(v0 ? acc[n].x : 0.0f, v1 ? acc[n].y : 0.0f);
                     *reinterpret_cast<float2*>(sDF + (k - S) * LT + 2 * pr) = dv;
@@ -535,6 +530,19 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
                 if (b <= kRM) sm.acc5[(slot * kFM + a) * (kRM + 1) + b] += double(v);
             }
             // stage5 is rewritten only after the next tile's five barriers
+        }
+        if (MODE == kArmProxy) {
+            // ---- P9: the context gradient as row partials (cc_ctx.cuh); the
+            // H1 / H2 rows are dead here and hold dC[o][latent] ----
+            float* const sDC = sm.act + K::O_H1;
+#pragma unroll
+            for (int n = 0; n < K::ND; ++n) {
+                const int k = grp * K::ND + n;
+                if (k < S) *reinterpret_cast<float2*>(sDC + k * LT + 2 * pr) = dcacc[n];
+            }
+            __syncthreads();
+            ctx_store_partials(P, g, tile, sDC, LT, tid, NT);
+            // (the next tile's P0 barrier orders these reads before P1's writes)
         }
         wb ^= 1;
         cur = nxt;

@@ -41,6 +41,7 @@
 #include "cc_kernels.h"
 #include "cc_math.cuh"
 #include "cc_reduce.cuh"
+#include "cc_ctx.cuh"
 #include "cc_tile.cuh"
 #include "cc_umma.cuh"
 
@@ -91,6 +92,7 @@ struct TC {
     static constexpr int O_DF = O_DR + RDR * LT;
     static constexpr int ACT = O_DF + RF * LT;
     static constexpr int O_HP = O_DH1;  // head partials [mu | sigma_raw]: P3 -> P4, before dH1 exists
+    static_assert(2 * RH >= DP, "dC rows (S <= D <= DP) fit in the H1 / H2 rows");
     // weight-gradient jobs (4x4 micro-tiles) and units (job x latent third)
     static constexpr int J1 = (WP / 4) * (DP / 4 + 1);   // dH1 x [C|1]   (after the dH1 MMA)
     static constexpr int J2 = (WP / 4) * (WP / 4 + 1);   // dH2 x [H1|1]  (beside the dH1 MMA)
@@ -637,13 +639,13 @@ __global__ void __launch_bounds__(NT, TC<DP, WP>::MINB) k_arm_tc(const Plan* __r
             umma::ld32(tl + K::TM_ACC, v);
             umma::wait_ld();
             const bool st = MODE == kArmProxy && valid;
-            float* const dcp = P.dctx + g.dctx_off + li;
+            float* const sDC = sm.act + K::O_H1;  // H1 / H2 rows are dead: dC[o][latent]
 #pragma unroll
             for (int i = 0; i < K::ND / 2; ++i) {
                 const int k = half * (K::ND / 2) + i;
                 const float x = hsel<K::ND / 2>(v, half, i);
                 if (k < S) {
-                    if (st) dcp[int64_t(k) * count] = x;
+                    sDC[k * LT + lt] = x;
                 } else if (k < S + F && slot >= 0) {
                     const float dv = valid ? x : 0.0f;
                     sDF[(k - S) * LT + lt] = dv;
@@ -653,6 +655,8 @@ __global__ void __launch_bounds__(NT, TC<DP, WP>::MINB) k_arm_tc(const Plan* __r
         }
         umma::fence_before_sync();
         __syncthreads();
+        // the context gradient as row partials (cc_ctx.cuh)
+        if (MODE == kArmProxy) ctx_store_partials(P, g, tile, sm.act + K::O_H1, LT, tid, NT);
         // ---- P9: IFCE weight gradient dF x [R|1]: 6 4x4 jobs x 8 slices of
         // 16 latents (48 threads), slices summed in order, fp64 per slot ----
         if (slot >= 0) {

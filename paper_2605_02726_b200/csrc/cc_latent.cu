@@ -16,6 +16,7 @@
 #include <cstdint>
 
 #include "cc_kernels.h"
+#include "cc_ctx.cuh"
 #include "cc_math.cuh"
 
 namespace ccb {
@@ -175,7 +176,9 @@ __global__ void k_latent_grad(const Plan* __restrict__ pp, int force, int64_t i_
         else if (g.main_level > 0)
             zterm = P.dups[i];
         const float* dc = P.dctx + g.dctx_off + li;
-        for (int o0 = 0; o0 < S; o0 += 8) {
+        if (P.ctx_part) {  // row partials of the tiled ARM kernels (cc_ctx.cuh)
+            acc += ctx_gather(P, g, r, c);
+        } else for (int o0 = 0; o0 < S; o0 += 8) {
             float v[8];
 #pragma unroll
             for (int k = 0; k < 8; ++k) {

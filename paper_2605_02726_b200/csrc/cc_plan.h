@@ -9,8 +9,14 @@
 //              border is written once at allocation and never touched again.
 //   y, m, v, g, th1, th2, gown, dups, q(int32) : flat latent layout (grids in
 //              decode order, unpadded row-major) — LatentSet, latent.hpp:30-44.
-//   dctx     : per grid S planes of the ARM context gradient dC (S x rows x cols)
-//              consumed by the deterministic gather (no float atomics).
+//   dctx     : the ARM's context gradient dC on its way to the latents it came
+//              from, consumed by a deterministic gather (no float atomics).
+//              Tiled ARM kernels (ctx_part = 1): per grid, ROW PARTIALS
+//              [source row r][d = 0..P][row tile q][T + 2P]: for the targets
+//              of source row r that lie d rows up (column c0 - P .. c0 + T + P
+//              of tile q), the sum over the context offsets with dy = -d;
+//              ~4.2 floats per latent (P = 3) instead of S = 14 planes.
+//              Per-latent kernel (ctx_part = 0): S planes (S x rows x cols).
 //   dfeat    : per IFCE-equipped grid, F planes of dF plus its 2x2 block-sum
 //              pyramid (levels 1..smax), see cc_arm.cu.
 //   z, dz    : (L, H, W) dense upsampled latents and their gradient.
@@ -44,7 +50,7 @@ struct GridGeom {
     int main_level;      // level if main grid, -1 if hyper
     int64_t pad_base;    // offset of element (0,0) inside yhat_pad
     int64_t lat_off;     // offset inside the flat latent layout
-    int64_t dctx_off;    // offset of this grid's S planes inside dctx
+    int64_t dctx_off;    // offset of this grid's context-gradient rows / planes inside dctx
     int64_t dfeat_off;   // equipped grids: offset of dF level 0 inside dfeat
     // row bands (cfg5): this grid holds global rows [row0, row0 + rows) of a
     // grid with `grows` rows; local rows [own_lo, own_hi) are owned (rate terms,
@@ -94,6 +100,7 @@ struct Plan {
     int64_t npix_global;
     int64_t zpix[kMaxLevels];    // z / dz plane k: offset of local pixel (0,0)
     int zvec;                    // npix and all zpix are multiples of 4 (16-byte loads)
+    int ctx_part;                // dctx holds row partials (tiled ARM kernels), see above
     int slot_pyr_a[kMaxSlots];   // global row of the dF pyramid origin (aligned)
     uint64_t seed;
 

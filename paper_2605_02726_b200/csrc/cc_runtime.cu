@@ -237,6 +237,7 @@ void Trainer::build_plan() {
     P.n_grids = int(order.size());
     if (P.n_grids > kMaxGrids) throw ConfigError("too many grids");
     int64_t pad_cur = 0, lat_cur = 0, dctx_cur = 0;
+    P.ctx_part = arm_uses_v2(P.Dp, P.Wp) ? 1 : 0;
     for (int i = 0; i < kMaxLevels; ++i) P.main_gi[i] = -1;
     for (int gi = 0; gi < P.n_grids; ++gi) {
         GridGeom& g = P.g[gi];
@@ -263,7 +264,10 @@ void Trainer::build_plan() {
         g.lat_off = lat_cur;
         lat_cur += int64_t(g.rows) * g.cols;
         g.dctx_off = dctx_cur;
-        dctx_cur += int64_t(P.S) * g.rows * g.cols;
+        if (P.ctx_part)  // [row][d = 0..P][row tile][kArmTile + 2P]
+            dctx_cur += int64_t(g.rows) * (P.P + 1) * ceil_div(g.cols, kArmTileHost) * (kArmTileHost + 2 * P.P);
+        else
+            dctx_cur += int64_t(P.S) * g.rows * g.cols;
         g.main_level = g.hyper ? -1 : g.level;
         if (!g.hyper) P.main_gi[g.level] = gi;
         g.ifce_slot = -1;
