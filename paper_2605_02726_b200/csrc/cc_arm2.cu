@@ -112,6 +112,7 @@ struct alignas(16) A2Smem {
     GridGeom geo[kMaxGrids];
     double red[NT / 32];
     alignas(16) int4 trec[4];  // tile records two ahead, landed by cp.async with the gathers
+    CtxTable ctxt;  // context offsets by target row (cc_ctx.cuh)
 };
 
 template <typename AccT>
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
         sm.woff[e] = e < S ? (P.P + P.ctx_dy[e]) * WS + P.P + P.ctx_dx[e] : 0;
     for (int e = tid; e < K::NACC5; e += NT) sm.acc5[e] = 0.0;
     for (int e = tid; e < P.n_grids; e += NT) sm.geo[e] = P.g[e];
+    if (tid == 0) ctx_table_build(P, sm.ctxt);
     // constant rows: zero padding of every activation array (written once);
     // windows zeroed so R rows past a grid's rdim are always finite
     for (int e = tid; e < K::ACT; e += NT) sm.act[e] = 0.0f;
@@ -541,7 +543,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
                 if (k < S) *reinterpret_cast<float2*>(sDC + k * LT + 2 * pr) = dcacc[n];
             }
             __syncthreads();
-            ctx_store_partials(P, g, tile, sDC, LT, tid, NT);
+            ctx_store_partials(P, g, tile, sDC, LT, sm.ctxt, tid, NT);
             // (the next tile's P0 barrier orders these reads before P1's writes)
         }
         wb ^= 1;

@@ -129,6 +129,7 @@ struct TcSmem {
     GridGeom geo[kMaxGrids];
     double red[NT / 32];
     alignas(16) int4 trec[4];
+    CtxTable ctxt;  // context offsets by target row (cc_ctx.cuh)
     uint64_t mbar;
     uint32_t tmem;
 };
@@ -285,6 +286,7 @@ __global__ void __launch_bounds__(NT, TC<DP, WP>::MINB) k_arm_tc(const Plan* __r
         sm.woff[e] = e < S ? (P.P + P.ctx_dy[e]) * WS + P.P + P.ctx_dx[e] : 0;
     for (int e = tid; e < K::NACC5; e += NT) sm.acc5[e] = 0.0;
     for (int e = tid; e < P.n_grids; e += NT) sm.geo[e] = P.g[e];
+    if (tid == 0) ctx_table_build(P, sm.ctxt);
     for (int e = tid; e < K::ACT; e += NT) sm.act[e] = 0.0f;
     for (int e = tid; e < 2 * WIN; e += NT) (&sm.win[0][0])[e] = 0.0f;
     umma::fence_async_smem();
@@ -656,7 +658,7 @@ __global__ void __launch_bounds__(NT, TC<DP, WP>::MINB) k_arm_tc(const Plan* __r
         umma::fence_before_sync();
         __syncthreads();
         // the context gradient as row partials (cc_ctx.cuh)
-        if (MODE == kArmProxy) ctx_store_partials(P, g, tile, sm.act + K::O_H1, LT, tid, NT);
+        if (MODE == kArmProxy) ctx_store_partials(P, g, tile, sm.act + K::O_H1, LT, sm.ctxt, tid, NT);
         // ---- P9: IFCE weight gradient dF x [R|1]: 6 4x4 jobs x 8 slices of
         // 16 latents (48 threads), slices summed in order, fp64 per slot ----
         if (slot >= 0) {

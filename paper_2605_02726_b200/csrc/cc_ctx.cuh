@@ -17,26 +17,44 @@
 
 namespace ccb {
 
+// The context offsets grouped by target row: for d = 0 .. P, the offsets
+// o (ascending) with dy_o = -d and their dx.  Built once per CTA.
+struct CtxTable {
+    int n[5];
+    int o[5][12];
+    int dx[5][12];
+};
+
+__device__ __forceinline__ void ctx_table_build(const Plan& P, CtxTable& t) {  // one thread
+    for (int d = 0; d < 5; ++d) t.n[d] = 0;
+    for (int o = 0; o < P.S; ++o) {
+        const int d = -P.ctx_dy[o];
+        if (d < 0 || d > 4 || t.n[d] >= 12) continue;  // (context offsets: dy <= 0, |d| <= pad <= 4)
+        t.o[d][t.n[d]] = o;
+        t.dx[d][t.n[d]] = P.ctx_dx[o];
+        ++t.n[d];
+    }
+}
+
 // dC: shared memory, rows o = 0 .. S-1 (stride ldc floats) over the tile's
 // latents 0 .. len-1.  All nthreads threads of the CTA call it.
 __device__ __forceinline__ void ctx_store_partials(const Plan& P, const GridGeom& g, int4 tile,
-                                                   const float* __restrict__ dC, int ldc, int tid,
-                                                   int nthreads) {
+                                                   const float* __restrict__ dC, int ldc, const CtxTable& tb,
+                                                   int tid, int nthreads) {
     constexpr int T = kArmTile;
     const int pad = P.P, W2 = T + 2 * pad, nd = pad + 1;
     const int r = tile.z, len = tile.w, c0 = tile.y - r * g.cols, q = c0 / T;
     const int ntr = (g.cols + T - 1) / T;
-    const int S = P.S;
-    float* const base = P.dctx + g.dctx_off;
+    float* const base = P.dctx + g.dctx_off + (int64_t(r) * nd * ntr + q) * W2;
     for (int e = tid; e < nd * W2; e += nthreads) {
         const int d = e / W2, j = e - d * W2;
         float acc = 0.0f;
-        for (int o = 0; o < S; ++o) {
-            if (-P.ctx_dy[o] != d) continue;
-            const int c = j - pad - P.ctx_dx[o];  // source latent of this target column
-            if (c >= 0 && c < len) acc += dC[o * ldc + c];
+        const int n = tb.n[d];
+        for (int i = 0; i < n; ++i) {
+            const int c = j - pad - tb.dx[d][i];  // source latent of this target column
+            if (c >= 0 && c < len) acc += dC[tb.o[d][i] * ldc + c];
         }
-        base[((int64_t(r) * nd + d) * ntr + q) * W2 + j] = acc;
+        base[int64_t(d) * ntr * W2 + j] = acc;
     }
 }
 

@@ -34,9 +34,12 @@ CASES = {
 }
 
 
-def main(name: str) -> None:
+def main(name: str, isa: str = "") -> None:
     h, w, preset, total, seed, lam = CASES[name]
-    lib = load_reference()
+    if isa:  # the other ISA build of the reference (spread between equally valid fp32 evaluations)
+        lib = capi.load_library(REPO / "oracle" / "_ref" / f"libccref_{isa}.so")
+    else:
+        lib = load_reference()
     img = np.empty((3, h, w), np.float32)
     assert lib.cc_make_synthetic_image(h, w, seed, img.ctypes.data_as(capi._F)) == 0
     enc = EncoderConfig.with_total(total)
@@ -49,12 +52,13 @@ def main(name: str) -> None:
                true_cost=r.stats.true_cost, psnr=r.stats.psnr, rate_bpp=r.stats.rate_bpp,
                restarts=r.stats.restarts, skipped_steps=r.stats.skipped_steps,
                q_abs_sum=int(np.abs(r.q.astype(np.int64)).sum()),
-               generator=f"{reference_path().name} on {platform.processor() or platform.machine()}",
+               generator=f"{('libccref_' + isa + '.so') if isa else reference_path().name} on "
+                         f"{platform.processor() or platform.machine()}",
                cpu_seconds=time.time() - t0)
-    p = REPO / "tests" / "golden" / f"train_{name}.json"
+    p = REPO / "tests" / "golden" / (f"train_{name}.json" if not isa else f"train_{name}_{isa}.json")
     p.write_text(json.dumps(out, indent=1) + "\n")
     print(json.dumps(out))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "")
