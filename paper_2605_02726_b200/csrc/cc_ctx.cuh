@@ -29,7 +29,7 @@ __device__ __forceinline__ void ctx_table_build(const Plan& P, CtxTable& t) {  /
     for (int d = 0; d < 5; ++d) t.n[d] = 0;
     for (int o = 0; o < P.S; ++o) {
         const int d = -P.ctx_dy[o];
-        if (d < 0 || d > 4 || t.n[d] >= 12) continue;  // (context offsets: dy <= 0, |d| <= pad <= 4)
+        if (d < 0 || d > 4 || t.n[d] >= 9) continue;  // (context offsets: dy <= 0, -dy, |dx| <= pad <= 4)
         t.o[d][t.n[d]] = o;
         t.dx[d][t.n[d]] = P.ctx_dx[o];
         ++t.n[d];
@@ -46,15 +46,24 @@ __device__ __forceinline__ void ctx_store_partials(const Plan& P, const GridGeom
     const int r = tile.z, len = tile.w, c0 = tile.y - r * g.cols, q = c0 / T;
     const int ntr = (g.cols + T - 1) / T;
     float* const base = P.dctx + g.dctx_off + (int64_t(r) * nd * ntr + q) * W2;
-    for (int e = tid; e < nd * W2; e += nthreads) {
-        const int d = e / W2, j = e - d * W2;
-        float acc = 0.0f;
+    for (int d = 0; d < nd; ++d) {
         const int n = tb.n[d];
-        for (int i = 0; i < n; ++i) {
-            const int c = j - pad - tb.dx[d][i];  // source latent of this target column
-            if (c >= 0 && c < len) acc += dC[tb.o[d][i] * ldc + c];
+        int oo[9], xx[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {  // this row's offsets (<= 2P + 1 <= 9), padded with no-ops
+            oo[i] = i < n ? tb.o[d][i] : 0;
+            xx[i] = i < n ? tb.dx[d][i] : -(1 << 20);
         }
-        base[int64_t(d) * ntr * W2 + j] = acc;
+        float* const out = base + int64_t(d) * ntr * W2;
+        for (int j = tid; j < W2; j += nthreads) {
+            float acc = 0.0f;
+#pragma unroll
+            for (int i = 0; i < 9; ++i) {
+                const int c = j - pad - xx[i];  // source latent of this target column
+                if (unsigned(c) < unsigned(len)) acc += dC[oo[i] * ldc + c];
+            }
+            out[j] = acc;
+        }
     }
 }
 
