@@ -465,7 +465,15 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
             for (int n = 0; n < K::ND; ++n) {
                 const int k = grp * K::ND + n;
                 if (k < S) {
-                    // kept in registers: written as row partials after P8
+                    if (MODE == kArmProxy && !P.ctx_part) {  // S planes (else row partials after P8)
+                        float* dcp = P.dctx + g.dctx_off + int64_t(k) * count + l0;
+                        if (v1 && (reinterpret_cast<uintptr_t>(dcp) & 7) == 0) {
+                            *reinterpret_cast<float2*>(dcp) = acc[n];
+                        } else {
+                            if (v0) dcp[0] = acc[n].x;
+                            if (v1) dcp[1] = acc[n].y;
+                        }
+                    }
                 } else if (k < S + F && slot >= 0) {
                     const float2 dv = make_float2(v0 ? acc[n].x : 0.0f, v1 ? acc[n].y : 0.0f);
                     *reinterpret_cast<float2*>(sDF + (k - S) * LT + 2 * pr) = dv;
@@ -533,7 +541,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
             }
             // stage5 is rewritten only after the next tile's five barriers
         }
-        if (MODE == kArmProxy) {
+        if (MODE == kArmProxy && P.ctx_part) {
             // ---- P9: the context gradient as row partials (cc_ctx.cuh); the
             // H1 / H2 rows are dead here and hold dC[o][latent] ----
             float* const sDC = sm.act + K::O_H1;

@@ -647,7 +647,8 @@ __global__ void __launch_bounds__(NT, TC<DP, WP>::MINB) k_arm_tc(const Plan* __r
                 const int k = half * (K::ND / 2) + i;
                 const float x = hsel<K::ND / 2>(v, half, i);
                 if (k < S) {
-                    sDC[k * LT + lt] = x;
+                    if (P.ctx_part) sDC[k * LT + lt] = x;                              // row partials below
+                    else if (st) P.dctx[g.dctx_off + int64_t(k) * count + li] = x;  // S planes
                 } else if (k < S + F && slot >= 0) {
                     const float dv = valid ? x : 0.0f;
                     sDF[(k - S) * LT + lt] = dv;
@@ -658,7 +659,7 @@ __global__ void __launch_bounds__(NT, TC<DP, WP>::MINB) k_arm_tc(const Plan* __r
         umma::fence_before_sync();
         __syncthreads();
         // the context gradient as row partials (cc_ctx.cuh)
-        if (MODE == kArmProxy) ctx_store_partials(P, g, tile, sm.act + K::O_H1, LT, sm.ctxt, tid, NT);
+        if (MODE == kArmProxy && P.ctx_part) ctx_store_partials(P, g, tile, sm.act + K::O_H1, LT, sm.ctxt, tid, NT);
         // ---- P9: IFCE weight gradient dF x [R|1]: 6 4x4 jobs x 8 slices of
         // 16 latents (48 threads), slices summed in order, fp64 per slot ----
         if (slot >= 0) {

@@ -237,7 +237,15 @@ void Trainer::build_plan() {
     P.n_grids = int(order.size());
     if (P.n_grids > kMaxGrids) throw ConfigError("too many grids");
     int64_t pad_cur = 0, lat_cur = 0, dctx_cur = 0;
-    P.ctx_part = arm_uses_v2(P.Dp, P.Wp) ? 1 : 0;
+    // context-gradient row partials (cc_ctx.cuh) instead of S planes: 3.3x less
+    // dctx traffic and a cheaper gather (tail 69 -> 63 us), but the partial
+    // sums cost the ARM more than that (263 -> 283-291 us alone, 0.453 ->
+    // 0.465-0.472 ms per iteration at 512x768): opt-in, CCB_CTX_PART=1
+    static const bool ctx_part_env = [] {
+        const char* e = std::getenv("CCB_CTX_PART");
+        return e && e[0] == '1';
+    }();
+    P.ctx_part = (ctx_part_env && arm_uses_v2(P.Dp, P.Wp)) ? 1 : 0;
     for (int i = 0; i < kMaxLevels; ++i) P.main_gi[i] = -1;
     for (int gi = 0; gi < P.n_grids; ++gi) {
         GridGeom& g = P.g[gi];

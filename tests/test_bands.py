@@ -244,3 +244,75 @@ def test_band_device_views_are_the_library_buffers(gpu_lib):
         t.forward_backward(1e-2, 0.35, 0.22)
         nn = t.device_nn_partial()
         assert nn.dtype == torch.float64 and np.array_equal(nn.cpu().numpy(), t.nn_partial())
+
+
+# ------------------------------------- GPU + gloo: real band trainers, 2 ranks
+def _band_trainer_worker(rank, world, port, h, w, halo, iters, q):
+    import traceback
+
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2605_02726_b200 import capi
+
+        lib = capi.load_product()
+        img = make_image(lib, h, w, seed=0)
+        bands = B.split_rows(h, w, world)
+        enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=0)
+        with B.BandTrainer(img, *bands[rank], halo, enc, DecoderConfig.hop(), lib=lib, device=0) as tr:
+            tr.fresh_candidate(0)
+            hyper = any(g.hyper for g in tr.grids)
+            # host transport (gloo): the routing code the NCCL path also runs
+            db = B.DistBand(tr, h, w, bands, halo, hyper, dist, device=None)
+            costs = [db.proxy_iteration(1e-2, 0.35, 0.22) for _ in range(iters)]
+            own = [tr.rows(0, gi, tr.grid_rows(gi).o0, tr.grid_rows(gi).o1) for gi in range(len(tr.grids))]
+            q.put(dict(rank=rank, costs=costs, own=own, params=tr.get_state()["params"],
+                       global_iter=tr.global_iter))
+    except Exception:  # report instead of leaving the parent waiting
+        q.put(dict(rank=rank, error=traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_dist_band_two_ranks_match_local_bands(gpu_lib):
+    """Two processes, each driving a REAL BandTrainer through DistBand over
+    gloo (host exchange; both on this one GPU — their kernels never wait on one
+    another, the ranks meet only in the host collectives), against the same
+    bands run in one process (LocalBands): bit-identical costs, latents and
+    parameters after 3 iterations (same routing, same rank-order sums)."""
+    import torch.multiprocessing as mp
+
+    h, w, halo, iters, world = 256, 192, 6, 3, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_band_trainer_worker, args=(r, world, port, h, w, halo, iters, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda r: r["rank"])
+    for p in procs:
+        p.join(timeout=120)
+    for r in res:
+        assert "error" not in r, r.get("error")
+    img = make_image(gpu_lib, h, w, seed=0)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=0)
+    lb = B.LocalBands(img, world, enc, DecoderConfig.hop(), halo=halo, lib=gpu_lib)
+    try:
+        lb.fresh_candidate(0)
+        costs = [lb.proxy_iteration(1e-2, 0.35, 0.22) for _ in range(iters)]
+        for r in res:
+            assert r["costs"] == costs, (r["rank"], r["costs"], costs)
+            t = lb.trainers[r["rank"]]
+            for gi in range(len(t.grids)):
+                gr = t.grid_rows(gi)
+                assert np.array_equal(r["own"][gi], t.rows(0, gi, gr.o0, gr.o1)), (r["rank"], gi)
+            assert np.array_equal(r["params"], t.get_state()["params"])
+            assert r["global_iter"] == iters
+    finally:
+        lb.close()
+    assert np.array_equal(res[0]["params"], res[1]["params"])

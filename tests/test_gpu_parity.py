@@ -754,15 +754,18 @@ def test_full_schedule_final_rd_vs_golden(gpu_lib, name):
     assert rel <= 5e-3
 
 
-def test_tensor_core_arm_parity(gpu_lib, ref_lib):
-    """The tcgen05 ARM kernel (cc_arm_tc.cu, selected with CCB_ARM=tc): the
+@pytest.mark.parametrize("variant", [{"CCB_ARM": "tc"}, {"CCB_CTX_PART": "1"},
+                                     {"CCB_ARM": "tc", "CCB_CTX_PART": "1"}])
+def test_arm_variant_parity(gpu_lib, ref_lib, variant):
+    """The opt-in ARM variants — the tcgen05 kernel (cc_arm_tc.cu, CCB_ARM=tc)
+    and the context gradient as row partials (cc_ctx.cuh, CCB_CTX_PART=1): the
     golden lock-step cases and a truth-arbitrated 512x768 lock-step against
-    the reference, in a subprocess (the switch is read once per process)."""
+    the reference, in a subprocess (the switches are read once per process)."""
     import os
     import subprocess
     import sys
 
-    env = dict(os.environ, CCB_ARM="tc")
+    env = dict(os.environ, **variant)
     r = subprocess.run([sys.executable, "-m", "tests.arm_variant_run"], env=env, capture_output=True,
                        text=True, timeout=900, cwd=str(golden_util.GOLDEN.parents[1]))
     print(r.stdout[-3000:], r.stderr[-3000:])
