@@ -770,3 +770,24 @@ def test_arm_variant_parity(gpu_lib, ref_lib, variant):
                        text=True, timeout=900, cwd=str(golden_util.GOLDEN.parents[1]))
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0
+
+
+def test_cfg2_warmup_matches_reference(gpu_lib):
+    """BASELINE config 2 (512x768 HOP, with_total(10000), seed 0): the whole
+    warm-up (5 candidates x 40 iterations, the best 2 refined for 40 more,
+    encoder.hpp:315-342; here the concurrent batched version) ends on the same
+    winner as the reference's — its true cost within 1e-4 and its latents /
+    parameters within 1e-3 of the reference's state after 280 free-running
+    iterations (tests/golden/warm_cfg2.npz from tools/warmup_compare.py)."""
+    r = dict(np.load(GOLDEN / "warm_cfg2.npz"))
+    img = make_image(gpu_lib, 512, 768, seed=0)
+    enc = EncoderConfig.with_total(10000)
+    enc.lmbda, enc.seed, enc.use_soap = 1e-3, 0, False
+    with Trainer(img, enc, DecoderConfig.hop(), lib=gpu_lib) as tr:
+        tr.warmup()
+        st = tr.get_state()
+        tc = tr.true_cost()
+        assert tr.global_iter == int(r["gi"]) == 280
+    assert abs(tc[0] - r["tc"][0]) / r["tc"][0] <= 1e-4
+    assert rel_l2(st["latents"], r["latents"]) <= 1e-3
+    assert rel_l2(st["params"], r["params"]) <= 1e-3
