@@ -437,6 +437,18 @@ def run_b200(args, rank, world, local_rank):
     tr.close()
 
 
+def _max_over_ranks(dist, x, dev):
+    """max of a host scalar over the ranks (NCCL on the device; gloo on the host)."""
+    if not dist:
+        return float(x)
+    import torch
+
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_cfg3(args, lib, n_img, seed0, dev, dist, K, W):
     """BASELINE config 3 on this GPU: n_img independent 512x768 images trained
     in lock-step by one batched graph (include/coolchic_b200_batch.h).
@@ -473,10 +485,7 @@ def run_cfg3(args, lib, n_img, seed0, dev, dist, K, W):
     e1.record(stream)
     e1.synchronize()
     ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = _max_over_ranks(dist, ms, dev)
     world = dist.get_world_size() if dist else 1
     value = world * n_img * h * w * K / (ms / 1e3) / 1e9
     rec = np.empty(4 * K, np.float64)
@@ -500,10 +509,7 @@ def run_cfg3(args, lib, n_img, seed0, dev, dist, K, W):
         lib.cc_trainer_last_records(tr._h, K, _dp(rec))
     e1.record(stream)
     e1.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e = world * n_img * h * w * K / (float(t.item()) / 1e3) / 1e9
+    e2e = world * n_img * h * w * K / (_max_over_ranks(dist, e0.elapsed_time(e1), dev) / 1e3) / 1e9
     kpi = C.c_int()
     lib.ccb_kernels_per_iteration(trs[0]._h, C.byref(kpi))
     b.close()
@@ -555,6 +561,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook (tests/test_bench_ranks.py): several ranks on one GPU with a
+    # gloo process group — exercises the N>1 code path, not a timing
+    shared = os.environ.get("BENCH_SHARED_GPU") == "1"
+    if shared:
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -563,7 +574,10 @@ def main():
         import torch.distributed as dist
 
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_b200(args, rank, world, local_rank)
     finally:
