@@ -82,6 +82,7 @@ void launch_ups_forward(const LaunchCtx& L);
 void launch_ups_backward(const LaunchCtx& L, bool latent_grads, int j_begin = 0, int j_end = 1 << 30);
 int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward);
 int ups_coarse_from(const Plan& H);
+int ups_chain_ctas();  // CTAs per cascade of the coarse-chain launches
 int ups_bwd_tile(const Plan& H, int j, int num_sms);  // backward tile edge of stage j
 void ups_configure();
 

@@ -501,7 +501,8 @@ void Trainer::build_plan() {
     for (int j = 0; j < P.L - 1; ++j) {
         // k_ups_bwd writes one row per CTA: dk4 (row + column passes) and dr3;
         // fused coarse stages one row per cascade
-        const int nb = j >= P.ups_jc ? P.ups_n[j] : ups_blocks_x(P, j, num_sms_, false) * P.ups_n[j];
+        const int nb = j >= P.ups_jc ? ups_chain_ctas() * P.ups_n[j]
+                                     : ups_blocks_x(P, j, num_sms_, false) * P.ups_n[j];
         P.reg_ups_rows[j] = region(P.off_tconv[j], 4, nb);
         P.reg_ups_cols[j] = -1;
         P.reg_ups_ref[j] = region(P.off_refine[j], 3, nb);

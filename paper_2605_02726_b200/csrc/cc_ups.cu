@@ -528,6 +528,95 @@ __global__ void __launch_bounds__(kThreads, 3) k_ups_bwd(const Plan* __restrict_
     }
 }
 
+// ---------------------------------------------------------- coarse chains
+// The coarse stages j >= P.ups_jc (little work each, a latency-bound launch
+// apiece when run stage by stage) as ONE launch per direction: a thread-block
+// cluster per cascade k walks that cascade's coarse stages in order — tiles
+// of a stage spread over the cluster's CTAs, a cluster barrier
+// (release / acquire) between consecutive stages, which is exactly the
+// dependency (stage j of cascade k reads only stage j +- 1 of cascade k).
+// Every stage uses the same tile code as the per-stage kernels.
+constexpr int kChainCL = 8;  // CTAs per cluster (portable size)
+
+struct ChainTiles {
+    int tb[kMaxLevels];  // tile edge (4 / 8) of each stage
+};
+
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ int cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return int(r);
+}
+
+template <int TB>
+__device__ __forceinline__ void fwd_stage_tiles(const Plan& P, int j, int si, int t_begin, int t_step,
+                                                FwdSmem<TB>& f) {
+    const UpsStage& s = P.ups[j][si];
+    const int ro = s.rows_out, co = s.cols_out, ri = s.rows_in, ci = s.cols_in;
+    constexpr int FO = 2 * TB;
+    const int tiles_x = (co + FO - 1) / FO;
+    const int ntiles = tiles_x * ((ro + FO - 1) / FO);
+    const float* k4 = P.params + P.off_tconv[j];
+    const float* r3 = P.params + P.off_refine[j];
+    const float kk[4] = {k4[0], k4[1], k4[2], k4[3]};
+    const float kc = r3[0], ke = r3[1], ko = r3[2];
+    const float* in = stage_in(P, s);
+    float* out = stage_out(P, s);
+    for (int tile = t_begin; tile < ntiles; tile += t_step) {
+        const int U0 = (tile / tiles_x) * TB, V0 = (tile % tiles_x) * TB;
+        if (fwd_interior<TB>(U0, V0, ri, ci, ro, co))
+            fwd_tile<TB, false>(in, s.in_stride, out, ro, co, ri, ci, U0, V0, kk, kc, ke, ko, f);
+        else
+            fwd_tile<TB, true>(in, s.in_stride, out, ro, co, ri, ci, U0, V0, kk, kc, ke, ko, f);
+    }
+}
+
+// forward: cascade k = jc + 1 + blockIdx.y runs stages k-1 .. jc
+__global__ void __launch_bounds__(kThreads) k_ups_fwd_chain(const Plan* __restrict__ pp, ChainTiles ct) {
+    __shared__ FwdSmem<8> f8;
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
+    const int jc = P.ups_jc, k = jc + 1 + int(blockIdx.y), rank = cluster_rank();
+    pdl_wait();  // the inputs (the soft-quantised latents) come from the predecessor
+    pdl_trigger();
+    for (int j = k - 1; j >= jc; --j) {
+        const int si = k - j - 1;  // ups[j] lists the cascades k = j+1, j+2, ... in order
+        if (ct.tb[j] == 8) fwd_stage_tiles<8>(P, j, si, rank, kChainCL, f8);
+        else fwd_stage_tiles<4>(P, j, si, rank, kChainCL, *reinterpret_cast<FwdSmem<4>*>(&f8));
+        cluster_barrier();  // stage j's output is the next stage's input
+    }
+}
+
+// backward: cascade k = jc + 1 + blockIdx.y runs stages jc .. k-1; each
+// stage's tap gradients of this CTA -> partial row (si * kChainCL + rank)
+__global__ void __launch_bounds__(kThreads) k_ups_bwd_chain(const Plan* __restrict__ pp, int write_lat,
+                                                            ChainTiles ct) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BwdSmem<8>& f8 = *reinterpret_cast<BwdSmem<8>*>(smem_raw);
+    const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
+    const int jc = P.ups_jc, k = jc + 1 + int(blockIdx.y), rank = cluster_rank();
+    for (int j = jc; j < k; ++j) {
+        const int si = k - j - 1;
+        double acc[7] = {0, 0, 0, 0, 0, 0, 0};
+        if (ct.tb[j] == 8) ups_bwd_stage<8>(P, j, si, rank, kChainCL, write_lat, f8, acc);
+        else ups_bwd_stage<4>(P, j, si, rank, kChainCL, write_lat, *reinterpret_cast<BwdSmem<4>*>(smem_raw), acc);
+        __syncthreads();
+        block_sum_vec<7>(acc, f8.red, f8.tot);
+        __syncthreads();
+        const int row = si * kChainCL + rank;
+        if (threadIdx.x < 4) {
+            const PartialRegion& R = P.region[P.reg_ups_rows[j]];
+            P.partials[R.base + int64_t(threadIdx.x) * R.nblocks + row] = f8.tot[threadIdx.x];
+        } else if (threadIdx.x < 7) {
+            const PartialRegion& R = P.region[P.reg_ups_ref[j]];
+            P.partials[R.base + int64_t(threadIdx.x - 4) * R.nblocks + row] = f8.tot[threadIdx.x];
+        }
+        cluster_barrier();  // stage j's input gradient is the next stage's output gradient
+    }
+}
+
 }  // namespace
 
 int ups_bwd_tile(const Plan& H, int j, int num_sms) {
@@ -566,19 +655,74 @@ int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward) {
     return best < cap ? best : cap;
 }
 
-// no fused coarse launch: every stage has its own (small-tile) launch
-int ups_coarse_from(const Plan& H) { return H.L - 1; }
+// first stage of the coarse chains (H.L - 1 = none): stages 2 .. L-2, which
+// carry a few percent of the upsampling work but a latency-bound launch each;
+// CCB_UPS_CHAIN=0 runs every stage as its own launch (A/B)
+int ups_coarse_from(const Plan& H) {
+    static const bool off = [] {
+        const char* e = std::getenv("CCB_UPS_CHAIN");
+        return e && e[0] == '0';
+    }();
+    return (off || H.L < 4) ? H.L - 1 : 2;
+}
+
+int ups_chain_ctas() { return kChainCL; }
+
+static ChainTiles chain_tiles(const Plan& H, int num_sms) {
+    ChainTiles ct{};
+    for (int j = 0; j < kMaxLevels; ++j) {
+        int t = 0;  // the chain's CTAs: kChainCL per cascade
+        for (int i = 0; i < H.ups_n[j]; ++i) t += bwd_tiles(H.ups[j][i], 8);
+        ct.tb[j] = t >= 2 * kChainCL * (H.ups_n[j] > 0 ? H.ups_n[j] : 1) ? 8 : 4;
+    }
+    (void)num_sms;
+    return ct;
+}
+
+static void launch_chain(const LaunchCtx& L, bool forward, int write_lat) {
+    const Plan& H = *L.host;
+    const int ncas = H.L - 1 - H.ups_jc;
+    if (ncas <= 0) return;
+    const ChainTiles ct = chain_tiles(H, L.num_sms);
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kChainCL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    int na = 1;
+    if (pdl_enabled(forward ? 'f' : 'b')) {
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        na = 2;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kChainCL, ncas, L.batch);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = L.stream;
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    if (forward) {
+        cfg.dynamicSmemBytes = 0;
+        cuda_check(cudaLaunchKernelEx(&cfg, k_ups_fwd_chain, L.plan, ct), "cudaLaunchKernelEx(ups fwd chain)");
+    } else {
+        cfg.dynamicSmemBytes = sizeof(BwdSmem<8>);
+        cuda_check(cudaLaunchKernelEx(&cfg, k_ups_bwd_chain, L.plan, write_lat, ct),
+                   "cudaLaunchKernelEx(ups bwd chain)");
+    }
+}
 
 void ups_configure() {
     cudaFuncSetAttribute(k_ups_bwd<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<16>)));
     cudaFuncSetAttribute(k_ups_bwd<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<8>)));
     cudaFuncSetAttribute(k_ups_bwd<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<4>)));
+    cudaFuncSetAttribute(k_ups_bwd_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<8>)));
 }
 
 void launch_ups_forward(const LaunchCtx& L) {
     const Plan& H = *L.host;
     // z plane 0 (= ŷ of main grid 0) is written by k_softq_fwd / k_pads_from_q
-    for (int j = H.L - 2; j >= 0; --j) {
+    launch_chain(L, true, 0);  // stages >= ups_jc, every cascade in one cluster launch
+    for (int j = std::min(H.L - 2, H.ups_jc - 1); j >= 0; --j) {
         if (H.ups_n[j] == 0) continue;
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, true), H.ups_n[j], L.batch);
         switch (ups_fwd_tile(H, j, L.num_sms)) {
@@ -593,6 +737,10 @@ void launch_ups_backward(const LaunchCtx& L, bool latent_grads, int j_begin, int
     const Plan& H = *L.host;
     for (int j = j_begin; j <= H.L - 2 && j < j_end; ++j) {
         if (H.ups_n[j] == 0) continue;
+        if (j >= H.ups_jc) {  // the coarse chain covers every remaining stage
+            launch_chain(L, false, latent_grads ? 1 : 0);
+            return;
+        }
         const dim3 grid(ups_blocks_x(H, j, L.num_sms, false), H.ups_n[j], L.batch);
         const int wl = latent_grads ? 1 : 0;
         switch (ups_bwd_tile(H, j, L.num_sms)) {
