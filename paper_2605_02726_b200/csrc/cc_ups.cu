@@ -536,7 +536,15 @@ __global__ void __launch_bounds__(kThreads, 3) k_ups_bwd(const Plan* __restrict_
 // (release / acquire) between consecutive stages, which is exactly the
 // dependency (stage j of cascade k reads only stage j +- 1 of cascade k).
 // Every stage uses the same tile code as the per-stage kernels.
-constexpr int kChainCL = 8;  // CTAs per cluster (portable size)
+// CTAs per cluster: CCB_UPS_CHAIN_CL (8 portable, 16 non-portable)
+static int chain_cl() {
+    static const int v = [] {
+        const char* e = std::getenv("CCB_UPS_CHAIN_CL");
+        const int c = e ? std::atoi(e) : 8;
+        return c == 16 ? 16 : (c == 4 ? 4 : 8);
+    }();
+    return v;
+}
 
 struct ChainTiles {
     int tb[kMaxLevels];  // tile edge (4 / 8) of each stage
@@ -583,8 +591,8 @@ __global__ void __launch_bounds__(kThreads) k_ups_fwd_chain(const Plan* __restri
     pdl_trigger();
     for (int j = k - 1; j >= jc; --j) {
         const int si = k - j - 1;  // ups[j] lists the cascades k = j+1, j+2, ... in order
-        if (ct.tb[j] == 8) fwd_stage_tiles<8>(P, j, si, rank, kChainCL, f8);
-        else fwd_stage_tiles<4>(P, j, si, rank, kChainCL, *reinterpret_cast<FwdSmem<4>*>(&f8));
+        if (ct.tb[j] == 8) fwd_stage_tiles<8>(P, j, si, rank, int(gridDim.x), f8);
+        else fwd_stage_tiles<4>(P, j, si, rank, int(gridDim.x), *reinterpret_cast<FwdSmem<4>*>(&f8));
         cluster_barrier();  // stage j's output is the next stage's input
     }
 }
@@ -600,12 +608,12 @@ __global__ void __launch_bounds__(kThreads) k_ups_bwd_chain(const Plan* __restri
     for (int j = jc; j < k; ++j) {
         const int si = k - j - 1;
         double acc[7] = {0, 0, 0, 0, 0, 0, 0};
-        if (ct.tb[j] == 8) ups_bwd_stage<8>(P, j, si, rank, kChainCL, write_lat, f8, acc);
-        else ups_bwd_stage<4>(P, j, si, rank, kChainCL, write_lat, *reinterpret_cast<BwdSmem<4>*>(smem_raw), acc);
+        if (ct.tb[j] == 8) ups_bwd_stage<8>(P, j, si, rank, int(gridDim.x), write_lat, f8, acc);
+        else ups_bwd_stage<4>(P, j, si, rank, int(gridDim.x), write_lat, *reinterpret_cast<BwdSmem<4>*>(smem_raw), acc);
         __syncthreads();
         block_sum_vec<7>(acc, f8.red, f8.tot);
         __syncthreads();
-        const int row = si * kChainCL + rank;
+        const int row = si * int(gridDim.x) + rank;
         if (threadIdx.x < 4) {
             const PartialRegion& R = P.region[P.reg_ups_rows[j]];
             P.partials[R.base + int64_t(threadIdx.x) * R.nblocks + row] = f8.tot[threadIdx.x];
@@ -663,17 +671,21 @@ int ups_coarse_from(const Plan& H) {
         const char* e = std::getenv("CCB_UPS_CHAIN");
         return e && e[0] == '0';
     }();
-    return (off || H.L < 4) ? H.L - 1 : 2;
+    static const int jc = [] {
+        const char* e = std::getenv("CCB_UPS_CHAIN");
+        return e ? std::atoi(e) : 3;
+    }();
+    return (off || jc < 1 || H.L < jc + 2) ? H.L - 1 : jc;
 }
 
-int ups_chain_ctas() { return kChainCL; }
+int ups_chain_ctas() { return chain_cl(); }
 
 static ChainTiles chain_tiles(const Plan& H, int num_sms) {
     ChainTiles ct{};
     for (int j = 0; j < kMaxLevels; ++j) {
         int t = 0;  // the chain's CTAs: kChainCL per cascade
         for (int i = 0; i < H.ups_n[j]; ++i) t += bwd_tiles(H.ups[j][i], 8);
-        ct.tb[j] = t >= 2 * kChainCL * (H.ups_n[j] > 0 ? H.ups_n[j] : 1) ? 8 : 4;
+        ct.tb[j] = t >= 2 * chain_cl() * (H.ups_n[j] > 0 ? H.ups_n[j] : 1) ? 8 : 4;
     }
     (void)num_sms;
     return ct;
@@ -686,7 +698,7 @@ static void launch_chain(const LaunchCtx& L, bool forward, int write_lat) {
     const ChainTiles ct = chain_tiles(H, L.num_sms);
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = kChainCL;
+    at[0].val.clusterDim.x = chain_cl();
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     int na = 1;
@@ -696,7 +708,7 @@ static void launch_chain(const LaunchCtx& L, bool forward, int write_lat) {
         na = 2;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kChainCL, ncas, L.batch);
+    cfg.gridDim = dim3(chain_cl(), ncas, L.batch);
     cfg.blockDim = dim3(kThreads);
     cfg.stream = L.stream;
     cfg.attrs = at;
@@ -716,6 +728,8 @@ void ups_configure() {
     cudaFuncSetAttribute(k_ups_bwd<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<8>)));
     cudaFuncSetAttribute(k_ups_bwd<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<4>)));
     cudaFuncSetAttribute(k_ups_bwd_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(BwdSmem<8>)));
+    cudaFuncSetAttribute(k_ups_bwd_chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_ups_fwd_chain, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
 }
 
 void launch_ups_forward(const LaunchCtx& L) {
