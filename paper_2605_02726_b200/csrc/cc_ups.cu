@@ -663,19 +663,18 @@ int ups_blocks_x(const Plan& H, int j, int num_sms, bool forward) {
     return best < cap ? best : cap;
 }
 
-// first stage of the coarse chains (H.L - 1 = none): stages 2 .. L-2, which
-// carry a few percent of the upsampling work but a latency-bound launch each;
-// CCB_UPS_CHAIN=0 runs every stage as its own launch (A/B)
+// first stage of the coarse chains (H.L - 1 = none).  Opt-in, CCB_UPS_CHAIN=j
+// (chain stages j .. L-2) and CCB_UPS_CHAIN_CL = 8 / 16: measured at 512x768
+// (profiles/r02_ups_chain.txt) every setting is slower than the per-stage
+// launches with programmatic dependent launch (0.4598 ms per iteration vs
+// 0.4598-0.4709: a cluster per cascade has fewer CTAs than the per-stage
+// grids, and the stage kernels' launch latency is already hidden by PDL).
 int ups_coarse_from(const Plan& H) {
-    static const bool off = [] {
-        const char* e = std::getenv("CCB_UPS_CHAIN");
-        return e && e[0] == '0';
-    }();
     static const int jc = [] {
         const char* e = std::getenv("CCB_UPS_CHAIN");
-        return e ? std::atoi(e) : 3;
+        return e ? std::atoi(e) : 0;
     }();
-    return (off || jc < 1 || H.L < jc + 2) ? H.L - 1 : jc;
+    return (jc < 1 || H.L < jc + 2) ? H.L - 1 : jc;
 }
 
 int ups_chain_ctas() { return chain_cl(); }

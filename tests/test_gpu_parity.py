@@ -755,10 +755,12 @@ def test_full_schedule_final_rd_vs_golden(gpu_lib, name):
 
 
 @pytest.mark.parametrize("variant", [{"CCB_ARM": "tc"}, {"CCB_CTX_PART": "1"},
-                                     {"CCB_ARM": "tc", "CCB_CTX_PART": "1"}])
+                                     {"CCB_ARM": "tc", "CCB_CTX_PART": "1"},
+                                     {"CCB_UPS_CHAIN": "2", "CCB_UPS_CHAIN_CL": "16"}])
 def test_arm_variant_parity(gpu_lib, ref_lib, variant):
-    """The opt-in ARM variants — the tcgen05 kernel (cc_arm_tc.cu, CCB_ARM=tc)
-    and the context gradient as row partials (cc_ctx.cuh, CCB_CTX_PART=1): the
+    """The opt-in variants — the tcgen05 ARM (cc_arm_tc.cu, CCB_ARM=tc), the
+    context gradient as row partials (cc_ctx.cuh, CCB_CTX_PART=1) and the
+    coarse upsampling stages as cluster launches (cc_ups.cu, CCB_UPS_CHAIN): the
     golden lock-step cases and a truth-arbitrated 512x768 lock-step against
     the reference, in a subprocess (the switches are read once per process)."""
     import os
