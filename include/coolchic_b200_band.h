@@ -66,6 +66,34 @@ int cc_band_finish(cc_trainer* tr, const double* nn_sums, double bits, double sq
 /* Adam steps with the per-grid finiteness ANDed over ranks. */
 int cc_band_step(cc_trainer* tr, const int* lat_ok);
 
+/* ---- device-resident band iteration (csrc/cc_band.h) ----------------------
+ * The same iteration with the exchange inside the library, on the band
+ * trainers' streams: a run of n proxy iterations is enqueued without any host
+ * synchronisation; each band trainer keeps the per-iteration records
+ * (cc_trainer_last_records: cost, mse, bits, global_iter — identical on every
+ * band).  Results are bit-identical to the host-driven phases above.
+ *
+ *   local group: every band of the image in this process (trainers on one
+ *                GPU or several), ordered by events between their streams;
+ *   NCCL group:  one band per process; `nccl_id` (128 bytes) comes from
+ *                cc_band_nccl_unique_id on one rank and is shared by the
+ *                caller (e.g. torch.distributed.broadcast_object_list);
+ *                `edges` = the nranks+1 band row edges (edges[r], edges[r+1]
+ *                = rank r's rows).  libnccl.so.2 is resolved at run time. */
+typedef struct cc_band_group cc_band_group;
+int cc_band_group_local(cc_trainer* const* bands, int nbands, cc_band_group** out);
+int cc_band_nccl_unique_id(void* id128);
+int cc_band_group_nccl(cc_trainer* band, const void* id128, int nranks, int rank, const int* edges,
+                       cc_band_group** out);
+/* buffers for up to n iterations per enqueue (optional: enqueue grows them) */
+int cc_band_group_reserve(cc_band_group* g, int n);
+/* n proxy iterations with per-iteration (lr, temp, noise_std); returns
+ * without waiting for the device */
+int cc_band_group_enqueue_proxy_iterations(cc_band_group* g, int n, const double* lr,
+                                           const double* temp, const double* noise_std);
+int cc_band_group_synchronize(cc_band_group* g);
+int cc_band_group_destroy(cc_band_group* g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,9 @@ int ccb_soap_state(cc_trainer* tr, double* arena, float* m1, float* v2, int64_t*
  * reference's soap_step, optim.hpp:189-254).  Any input may be NULL. */
 int ccb_soap_set_state(cc_trainer* tr, const double* arena, const float* m1, const float* v2,
                        const int64_t* t);
+/* Host waits on the device the library has issued so far in this process
+ * (stream / event synchronisations): the band iteration's sync budget. */
+int ccb_host_sync_count(int64_t* n);
 
 #ifdef __cplusplus
 }

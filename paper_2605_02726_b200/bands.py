@@ -15,8 +15,12 @@ the routing of halo rows, and two transports —
 
   * LocalBands: all bands in one process (one GPU or several), exchange by
     host copies; used by the single-GPU equivalence test;
-  * DistBand: one band per rank over torch.distributed (NCCL between GPUs,
-    gloo on CPU); the collectives are all_gather + paired send/recv.
+  * DistBand: one band per rank over torch.distributed (gloo on CPU: host
+    routing; CUDA band trainers: the library's NCCL band group below);
+  * DeviceBands / the NCCL band group: the same iteration with the exchange
+    inside the library on the trainers' streams (csrc/cc_band.h) — a run of
+    iterations is enqueued without host synchronisation, bit-identical to the
+    host-routed transports.
 
 The routing logic is transport-independent (``halo_plan``), so the gloo
 world-size-2 tests exercise exactly what the NCCL path runs.
@@ -273,6 +277,81 @@ class LocalBands:
                                for t in self.trainers])
 
 
+def _sched(lr, temp, noise):
+    lr = np.ascontiguousarray(np.atleast_1d(lr), np.float64)
+    n = lr.size
+    temp = np.ascontiguousarray(np.broadcast_to(temp, (n,)), np.float64)
+    noise = np.ascontiguousarray(np.broadcast_to(noise, (n,)), np.float64)
+    return n, lr, temp, noise
+
+
+class _Group:
+    """A library band group (cc_band_group_*): enqueue / synchronise / records."""
+
+    def __init__(self, lib, handle: C.c_void_p, record_trainer):
+        self.lib, self._h, self._rec_tr = lib, handle, record_trainer
+
+    def reserve(self, n: int) -> None:
+        _check(self.lib, self.lib.cc_band_group_reserve(self._h, n))
+
+    def enqueue_proxy_iterations(self, lr, temp, noise) -> int:
+        n, lr, temp, noise = _sched(lr, temp, noise)
+        dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+        _check(self.lib, self.lib.cc_band_group_enqueue_proxy_iterations(self._h, n, dp(lr), dp(temp),
+                                                                         dp(noise)))
+        return n
+
+    def synchronize(self) -> None:
+        _check(self.lib, self.lib.cc_band_group_synchronize(self._h))
+
+    def records(self, n: int) -> np.ndarray:
+        """(n, 4): cost, mse, bits, global_iter of the last n iterations (waits)."""
+        rec = np.empty(4 * n, np.float64)
+        _check(self.lib, self.lib.cc_trainer_last_records(self._rec_tr._h, n,
+                                                          rec.ctypes.data_as(C.POINTER(C.c_double))))
+        return rec.reshape(n, 4)
+
+    def proxy_iterations(self, lr, temp, noise) -> np.ndarray:
+        n = self.enqueue_proxy_iterations(lr, temp, noise)
+        return self.records(n)[:, 0]
+
+    def close(self) -> None:
+        if self._h:
+            self.lib.cc_band_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+
+def host_sync_count(lib) -> int:
+    n = C.c_int64()
+    _check(lib, lib.ccb_host_sync_count(C.byref(n)))
+    return n.value
+
+
+class DeviceBands(LocalBands):
+    """All bands of one image in this process with the exchange inside the
+    library (cc_band_group_local): a run of iterations is enqueued without
+    host synchronisation; results are bit-identical to LocalBands."""
+
+    def __init__(self, image: np.ndarray, nbands: int, enc: EncoderConfig, dcfg: DecoderConfig,
+                 halo: int = 8, devices: list[int] | None = None, lib=None):
+        super().__init__(image, nbands, enc, dcfg, halo=halo, devices=devices, lib=lib)
+        lib = self.trainers[0].lib
+        arr = (C.c_void_p * nbands)(*[t._h.value for t in self.trainers])
+        h = C.c_void_p()
+        _check(lib, lib.cc_band_group_local(arr, nbands, C.byref(h)))
+        self.group = _Group(lib, h, self.trainers[0])
+
+    def proxy_iterations(self, lr, temp, noise) -> np.ndarray:
+        return self.group.proxy_iterations(lr, temp, noise)
+
+    def proxy_iteration(self, lr: float, temp: float, noise: float) -> float:
+        return float(self.group.proxy_iterations([lr], temp, noise)[0])
+
+    def close(self):
+        self.group.close()
+        super().close()
+
+
 class DistBand:
     """This rank's band over torch.distributed (NCCL device tensors between
     GPUs; gloo host tensors on CPU).  ``tr`` is any object with the
@@ -282,7 +361,9 @@ class DistBand:
     def __init__(self, tr, h: int, w: int, bands, halo: int, hyper: bool, dist, device=None):
         self.tr, self.dist, self.device = tr, dist, device
         self.rank, self.world = dist.get_rank(), dist.get_world_size()
+        self.bands = list(bands)
         self.plan = halo_plan(h, w, bands, halo, hyper, self.rank)
+        self.group = None
 
     def _t(self, a: np.ndarray):
         import torch
@@ -330,52 +411,42 @@ class DistBand:
         self.dist.all_gather(bufs, t)
         return [self._np(x) for x in bufs]
 
-    # ---- device-direct path (NCCL on the library's own buffers, no host staging)
+    # ---- device path: the library's NCCL band group (cc_band_group_nccl) runs
+    # the exchange on the trainer's stream; torch.distributed only shares the
+    # NCCL unique id
     def _device_ok(self) -> bool:
         return self.device is not None and hasattr(self.tr, "device_rows")
 
-    def _p2p(self, sends, recvs):
-        ops = [self.dist.P2POp(self.dist.isend, t, peer) for t, peer in sends if t.numel()]
-        ops += [self.dist.P2POp(self.dist.irecv, t, peer) for t, peer in recvs if t.numel()]
-        if ops:
-            for r in self.dist.batch_isend_irecv(ops):
-                r.wait()
+    def _nccl_group(self) -> _Group:
+        if self.group is None:
+            lib = self.tr.lib
+            uid = (C.c_char * 128)()
+            if self.rank == 0:
+                _check(lib, lib.cc_band_nccl_unique_id(uid))
+            box = [bytes(uid)]
+            self.dist.broadcast_object_list(box, src=0)
+            uid = (C.c_char * 128).from_buffer_copy(box[0])
+            edges = (C.c_int * (self.world + 1))(*([r0 for r0, _ in self.bands] + [self.bands[-1][1]]))
+            h = C.c_void_p()
+            _check(lib, lib.cc_band_group_nccl(self.tr._h, uid, self.world, self.rank, edges, C.byref(h)))
+            self.group = _Group(lib, h, self.tr)
+        return self.group
 
-    def _refresh_halos_device(self) -> None:
-        sends, recvs = [], []
-        for gi, d in enumerate(self.plan):  # one message per grid and direction
-            if self.rank > 0:
-                sends.append((self.tr.device_rows(0, gi, *d["send_up"]), self.rank - 1))
-                recvs.append((self.tr.device_rows(0, gi, *d["halo_up"]), self.rank - 1))
-            if self.rank + 1 < self.world:
-                sends.append((self.tr.device_rows(0, gi, *d["send_down"]), self.rank + 1))
-                recvs.append((self.tr.device_rows(0, gi, *d["halo_down"]), self.rank + 1))
-        self._p2p(sends, recvs)
+    def proxy_iterations(self, lr, temp, noise) -> np.ndarray:
+        """n iterations enqueued at once (device path: one host wait at the end)."""
+        if self._device_ok():
+            return self._nccl_group().proxy_iterations(lr, temp, noise)
+        n, lr, temp, noise = _sched(lr, temp, noise)
+        return np.array([self.proxy_iteration(lr[i], temp[i], noise[i]) for i in range(n)])
 
-    def _return_grads_device(self) -> None:
-        import torch
-
-        sends, recvs, adds = [], [], []
-        for gi, d in enumerate(self.plan):
-            if self.rank > 0:
-                sends.append((self.tr.device_rows(1, gi, *d["halo_up"]), self.rank - 1))
-                own = self.tr.device_rows(1, gi, *d["send_up"])
-                tmp = torch.empty_like(own)
-                recvs.append((tmp, self.rank - 1))
-                adds.append((own, tmp))
-            if self.rank + 1 < self.world:
-                sends.append((self.tr.device_rows(1, gi, *d["halo_down"]), self.rank + 1))
-                own = self.tr.device_rows(1, gi, *d["send_down"])
-                tmp = torch.empty_like(own)
-                recvs.append((tmp, self.rank + 1))
-                adds.append((own, tmp))
-        self._p2p(sends, recvs)
-        for own, tmp in adds:
-            own.add_(tmp)
+    def close(self) -> None:
+        if self.group is not None:
+            self.group.close()
+            self.group = None
 
     def proxy_iteration(self, lr: float, temp: float, noise: float) -> float:
         if self._device_ok():
-            return self._proxy_iteration_device(lr, temp, noise)
+            return float(self._nccl_group().proxy_iterations([lr], temp, noise)[0])
         self.refresh_halos()
         bits, se = self.tr.forward_backward(lr, temp, noise)
         up, dn = self._swap(_pack(self.tr, 1, self.plan, "halo_up"),
@@ -392,25 +463,4 @@ class DistBand:
         cost, ok = self.tr.finish(tot[:-2], float(tot[-2]), float(tot[-1]))
         oks = self._gather(ok.astype(np.int32))
         self.tr.step(np.minimum.reduce(oks))
-        return cost
-
-    def _proxy_iteration_device(self, lr: float, temp: float, noise: float) -> float:
-        import torch
-
-        self._refresh_halos_device()
-        torch.cuda.synchronize(self.device)
-        bits, se = self.tr.forward_backward(lr, temp, noise)  # returns with the band's work done
-        self._return_grads_device()
-        nn = self.tr.device_nn_partial()
-        mine = torch.cat([nn, torch.tensor([bits, se], dtype=torch.float64, device=nn.device)])
-        parts = [torch.empty_like(mine) for _ in range(self.world)]
-        self.dist.all_gather(parts, mine)
-        tot = parts[0].clone()
-        for p in parts[1:]:  # rank order: identical sums on every rank
-            tot += p
-        oks = [torch.empty(len(self.plan), dtype=torch.int32, device=nn.device) for _ in range(self.world)]
-        tot_h = tot.cpu().numpy()  # synchronises the NCCL stream
-        cost, ok = self.tr.finish(tot_h[:-2], float(tot_h[-2]), float(tot_h[-1]))
-        self.dist.all_gather(oks, torch.from_numpy(ok.astype(np.int32)).to(nn.device))
-        self.tr.step(np.minimum.reduce([o.cpu().numpy() for o in oks]))
         return cost

@@ -61,7 +61,7 @@ def build_product(verbose: bool = False, ptxas_v: bool = False) -> Path:
         with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
             list(ex.map(run, cmds))
     if _newer(OUT, objs):
-        cmd = [nvcc, *ARCH, "-shared", "-o", str(OUT), *map(str, objs), "-lcudart"]
+        cmd = [nvcc, *ARCH, "-shared", "-o", str(OUT), *map(str, objs), "-lcudart", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

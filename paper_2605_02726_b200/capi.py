@@ -173,6 +173,13 @@ BAND_SIGNATURES = {
     "cc_band_nn_partial": (C.c_int, [_P, _D]),
     "cc_band_finish": (C.c_int, [_P, _D, C.c_double, C.c_double, _D, _I]),
     "cc_band_step": (C.c_int, [_P, _I]),
+    "cc_band_group_local": (C.c_int, [C.POINTER(_P), C.c_int, C.POINTER(_P)]),
+    "cc_band_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "cc_band_group_nccl": (C.c_int, [_P, C.c_void_p, C.c_int, C.c_int, _I, C.POINTER(_P)]),
+    "cc_band_group_reserve": (C.c_int, [_P, C.c_int]),
+    "cc_band_group_enqueue_proxy_iterations": (C.c_int, [_P, C.c_int, _D, _D, _D]),
+    "cc_band_group_synchronize": (C.c_int, [_P]),
+    "cc_band_group_destroy": (C.c_int, [_P]),
 }
 
 # include/coolchic_b200_batch.h (product only): batched images (cfg3)
@@ -202,6 +209,7 @@ DIAG_SIGNATURES = {
     "ccb_timeline": (C.c_int, [_P, C.c_int, C.c_double, C.c_double, C.c_double, _D]),
     "ccb_soap_state": (C.c_int, [_P, _D, _F, _F, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "ccb_soap_set_state": (C.c_int, [_P, _D, _F, _F, C.POINTER(C.c_int64)]),
+    "ccb_host_sync_count": (C.c_int, [C.POINTER(C.c_int64)]),
 }
 
 

@@ -16,9 +16,17 @@
 #include "../../include/coolchic_b200.h"
 #include "../../include/coolchic_b200_diag.h"
 #include "../../include/coolchic_synth.h"
+#include "cc_band.h"
 #include "cc_runtime.h"
 
 using ccb::Trainer;
+
+struct cc_batch {
+    std::unique_ptr<ccb::Batch> b;
+};
+struct cc_band_group {
+    std::unique_ptr<ccb::BandGroup> g;
+};
 
 struct cc_trainer {
     std::unique_ptr<Trainer> tr;
@@ -788,6 +796,13 @@ int ccb_soap_set_state(cc_trainer* t, const double* arena, const float* m1, cons
     });
 }
 
+int ccb_host_sync_count(int64_t* n) {
+    return guarded([&] {
+        *n = ccb::host_sync_count();
+        return CC_OK;
+    });
+}
+
 int cc_trainer_warmup(cc_trainer* t) {
     return guarded([&] {
         if (!ccb::warmup_batched(*t->tr, t->image.data(), t->h, t->w, t->dec, t->device)) ccb::warmup(*t->tr);
@@ -915,6 +930,69 @@ int cc_band_step(cc_trainer* t, const int* lat_ok) {
     });
 }
 
+int cc_band_group_local(cc_trainer* const* bands, int nbands, cc_band_group** out) {
+    return guarded([&] {
+        if (!bands || nbands < 1 || !out) throw ccb::ConfigError("bad band list");
+        std::vector<Trainer*> v;
+        for (int b = 0; b < nbands; ++b) {
+            if (!bands[b]) throw ccb::ConfigError("null band trainer");
+            v.push_back(bands[b]->tr.get());
+        }
+        auto g = std::make_unique<cc_band_group>();
+        g->g = std::make_unique<ccb::BandGroup>(v);
+        *out = g.release();
+        return CC_OK;
+    });
+}
+
+int cc_band_nccl_unique_id(void* id128) {
+    return guarded([&] {
+        if (!id128) throw ccb::ConfigError("null id buffer");
+        ccb::BandGroup::nccl_unique_id(id128);
+        return CC_OK;
+    });
+}
+
+int cc_band_group_nccl(cc_trainer* band, const void* id128, int nranks, int rank, const int* edges,
+                       cc_band_group** out) {
+    return guarded([&] {
+        if (!band || !id128 || !edges || !out) throw ccb::ConfigError("null argument");
+        auto g = std::make_unique<cc_band_group>();
+        g->g = std::make_unique<ccb::BandGroup>(band->tr.get(), id128, nranks, rank, edges);
+        *out = g.release();
+        return CC_OK;
+    });
+}
+
+int cc_band_group_reserve(cc_band_group* g, int n) {
+    return guarded([&] {
+        g->g->reserve(n);
+        return CC_OK;
+    });
+}
+
+int cc_band_group_enqueue_proxy_iterations(cc_band_group* g, int n, const double* lr, const double* temp,
+                                           const double* noise_std) {
+    return guarded([&] {
+        g->g->enqueue_proxy_iterations(n, lr, temp, noise_std);
+        return CC_OK;
+    });
+}
+
+int cc_band_group_synchronize(cc_band_group* g) {
+    return guarded([&] {
+        g->g->synchronize();
+        return CC_OK;
+    });
+}
+
+int cc_band_group_destroy(cc_band_group* g) {
+    return guarded([&] {
+        delete g;
+        return CC_OK;
+    });
+}
+
 }  // extern "C"
 
 // ---------------------------------------------------------------- decode passes
@@ -950,9 +1028,6 @@ int cc_trainer_latent_mu_sigma(cc_trainer* t, const float* params, float* mu, fl
 // ---------------------------------------------------------------- batches (cfg3)
 #include "coolchic_b200_batch.h"
 
-struct cc_batch {
-    std::unique_ptr<ccb::Batch> b;
-};
 
 extern "C" {
 

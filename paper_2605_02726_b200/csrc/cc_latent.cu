@@ -304,7 +304,7 @@ void launch_adam_latents_grids(const LaunchCtx& L, int g_begin, int g_end) {
 // Row bands: per-grid finiteness of the OWN rows' (complete) latent gradients,
 // the per-tensor check of adam_step (optim.hpp:38-41) restricted to this band.
 __global__ void k_ok_reset(const Plan* __restrict__ pp) {
-    if (threadIdx.x < kMaxGrids) pp->lat_ok[threadIdx.x] = 1;
+    if (threadIdx.x < kMaxGrids) pp[blockIdx.z].lat_ok[threadIdx.x] = 1;
 }
 __global__ void k_band_own_finite(const Plan* __restrict__ pp) {
     const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image

@@ -5,6 +5,7 @@
 #include "cc_runtime.h"
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -596,7 +597,15 @@ void Trainer::allocate() {
     if (P.use_soap) soap_configure(H_);
 }
 
-void Trainer::synchronize() { CCB_CUDA(cudaStreamSynchronize(stream_)); }
+// host waits on the device issued by the library (ccb_host_sync_count)
+static std::atomic<int64_t> g_host_syncs{0};
+int64_t host_sync_count() { return g_host_syncs.load(); }
+void count_host_sync() { g_host_syncs.fetch_add(1); }
+
+void Trainer::synchronize() {
+    count_host_sync();
+    CCB_CUDA(cudaStreamSynchronize(stream_));
+}
 
 void Trainer::upload_image(const float* image) {
     CCB_CUDA(cudaSetDevice(device_));
@@ -980,6 +989,43 @@ double Trainer::band_finish(const double* nn_sums, double bits, double se, int* 
     return cost;
 }
 
+// Device-resident band iteration: the schedule entry, the forward/backward
+// and the step read everything from device memory, so a whole run of
+// iterations is enqueued without host synchronisation (BandGroup, cc_band.cu).
+void Trainer::band_reserve(int n) {
+    require_loaded();
+    if (!band_.on) throw StateError("not a band trainer");
+    reserve_iterations(n);  // band trainers: buffers only, no iteration graph
+}
+
+void Trainer::band_dev_forward_backward() {
+    require_loaded();
+    if (!band_.on) throw StateError("not a band trainer");
+    if (sched_cap_ <= 0) throw StateError("band_reserve before the device-resident band iteration");
+    CCB_CUDA(cudaSetDevice(device_));
+    launch_sched_load(L_);
+    launch_softq_fwd(L_);
+    fork();
+    launch_arm(side(), kArmProxy);
+    launch_pyramid(side());
+    launch_ups_forward(L_);
+    launch_syn_forward(L_, true);
+    launch_syn_backward(L_);
+    launch_ups_backward(L_, true);
+    join();
+    launch_finalize(L_, kArmProxy, -1);
+    launch_latent_grad_partial(L_);
+    launch_nn_reduce(L_);
+    CCB_CUDA(cudaGetLastError());
+}
+
+void Trainer::band_dev_step() {
+    CCB_CUDA(cudaSetDevice(device_));
+    launch_adam_latents(L_);
+    nn_apply(L_, true, true, true);  // + the iteration's record, sched_pos += 1
+    CCB_CUDA(cudaGetLastError());
+}
+
 void Trainer::band_step(const int* lat_ok) {
     CCB_CUDA(cudaMemcpyAsync(H_.lat_ok, lat_ok, sizeof(int) * size_t(H_.n_grids),
                              cudaMemcpyHostToDevice, stream_));
@@ -1078,7 +1124,7 @@ void Trainer::reserve_iterations(int n) {
             graphs_.erase(it);
         }
     }
-    ensure_graph(1);
+    if (!band_.on) ensure_graph(1);
 }
 
 void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* temp,
@@ -1095,7 +1141,10 @@ void Trainer::enqueue_proxy_iterations(int n, const double* lr, const double* te
 }
 
 void Trainer::upload_schedule(int n, const double* lr, const double* temp, const double* noise) {
-    CCB_CUDA(cudaEventSynchronize(ev_sched_));  // the previous batch's upload has left h_sched_
+    if (cudaEventQuery(ev_sched_) != cudaSuccess) {  // the previous batch's upload has left h_sched_
+        count_host_sync();
+        CCB_CUDA(cudaEventSynchronize(ev_sched_));
+    }
     for (int i = 0; i < n; ++i) {
         h_sched_[3 * i] = lr[i];
         h_sched_[3 * i + 1] = temp[i];
@@ -1177,7 +1226,10 @@ void Batch::enqueue_proxy_iterations(int n, const double* lr, const double* temp
     for (int i = 0; i < n; ++i) CCB_CUDA(cudaGraphLaunch(graph_, t_[0]->stream()));
 }
 
-void Batch::synchronize() { CCB_CUDA(cudaStreamSynchronize(t_[0]->stream())); }
+void Batch::synchronize() {
+    count_host_sync();
+    CCB_CUDA(cudaStreamSynchronize(t_[0]->stream()));
+}
 
 // Stage-by-stage replay of one proxy iteration with events in between
 // (diagnostics; same kernels as the graph).

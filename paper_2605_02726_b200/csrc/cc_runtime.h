@@ -117,6 +117,9 @@ public:
 
     // row bands (cfg5): see cc_runtime.cu
     bool is_band() const { return band_.on; }
+    void band_spec(int* hg, int* r0, int* r1, int* halo) const {
+        *hg = band_.hg, *r0 = band_.r0, *r1 = band_.r1, *halo = band_.halo;
+    }
     void band_forward_backward(double lr, double temp, double noise, double* bits, double* se);
     void band_nn_partial(double* out);
     double band_finish(const double* nn_sums, double bits, double se, int* lat_ok_own);
@@ -125,6 +128,14 @@ public:
     void band_grid_rows(int gi, int* out4) const;
     void* band_device_rows(int which, int gi, int rb, int re, int64_t* count);
     double* nn_partial_device() { return H_.grads_d; }
+    // device-resident band iteration (cc_band.cu drives the exchange between
+    // the phases; no host synchronisation inside an iteration)
+    void band_reserve(int n);          // schedule + record buffers for n iterations
+    void band_dev_forward_backward();  // iteration sched_pos: forward + backward on the band
+    void band_dev_step();              // latent + NN Adam with the exchanged flags
+    const Plan* device_plan() const { return d_plan_; }
+    const LaunchCtx& launch_ctx() const { return L_; }
+    int device() const { return device_; }
 
     // state transfer
     void set_state(const float* lat, const float* par, const float* lm, const float* lv,
@@ -245,6 +256,9 @@ private:
     cudaGraphExec_t graph_ = nullptr;
     int cap_ = 0;
 };
+
+int64_t host_sync_count();  // host waits on the device issued by the library so far
+void count_host_sync();
 
 void fp32_peak(int device, double* tflops, double* ms);
 void eval_math(int fn, int n, const float* a, const float* b, const float* c, float* out);

@@ -18,6 +18,8 @@ from paper_2605_02726_b200.trainer import ConfigError, DecoderConfig, EncoderCon
 
 from .conftest import make_image, rel_l2
 
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
 
 # ------------------------------------------------------------------ layout
 def test_split_rows_aligned():
@@ -316,3 +318,110 @@ def test_dist_band_two_ranks_match_local_bands(gpu_lib):
     finally:
         lb.close()
     assert np.array_equal(res[0]["params"], res[1]["params"])
+
+
+# ----------------------------- GPU: the exchange inside the library (cc_band.h)
+def _states(tr):
+    st = tr.get_state()
+    own = [tr.rows(0, gi, tr.grid_rows(gi).o0, tr.grid_rows(gi).o1) for gi in range(len(tr.grids))]
+    return own, st["params"], tr.global_iter
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("h,w,n", [(256, 192, 2), (1536, 256, 3)])
+def test_device_bands_match_local_bands(gpu_lib, h, w, n):
+    """The device-resident band iteration (cc_band_group_local: halo rows,
+    gradient return, rank-order gathers and the flag AND on the trainers'
+    streams) is bit-identical to the host-routed LocalBands, and a run of
+    iterations costs ONE host synchronisation (the records read)."""
+    img = make_image(gpu_lib, h, w, seed=3)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=3)
+    lr = np.array([1e-2, 9e-3, 8e-3, 7e-3, 6e-3])
+    tp = np.array([0.35, 0.33, 0.31, 0.29, 0.27])
+    ns = np.array([0.22, 0.21, 0.2, 0.19, 0.18])
+    lb = B.LocalBands(img, n, enc, DecoderConfig.hop(), halo=6, lib=gpu_lib)
+    db = B.DeviceBands(img, n, enc, DecoderConfig.hop(), halo=6, lib=gpu_lib)
+    try:
+        lb.fresh_candidate(0)
+        db.fresh_candidate(0)
+        db.group.reserve(len(lr))
+        host = [lb.proxy_iteration(lr[i], tp[i], ns[i]) for i in range(len(lr))]
+        s0 = B.host_sync_count(gpu_lib)
+        dev = db.proxy_iterations(lr, tp, ns)
+        syncs = B.host_sync_count(gpu_lib) - s0
+        assert list(dev) == host, (list(dev), host)
+        assert syncs <= 1, syncs
+        for b in range(n):
+            o1, p1, g1 = _states(lb.trainers[b])
+            o2, p2, g2 = _states(db.trainers[b])
+            for gi in range(len(o1)):
+                assert np.array_equal(o1[gi], o2[gi]), (b, gi)
+            assert np.array_equal(p1, p2), b
+            assert g1 == g2 == len(lr)
+        # one more iteration at a time through the same group
+        assert db.proxy_iteration(5e-3, 0.25, 0.17) == lb.proxy_iteration(5e-3, 0.25, 0.17)
+    finally:
+        db.close()
+        lb.close()
+
+
+_NCCL1 = r"""
+import json, os, sys
+import numpy as np
+import torch, torch.distributed as dist
+sys.path.insert(0, os.getcwd())
+from paper_2605_02726_b200 import bands as B, capi
+from paper_2605_02726_b200.trainer import DecoderConfig, EncoderConfig
+from tests.conftest import make_image
+torch.cuda.set_device(0)
+dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda:0"))
+lib = capi.load_product()
+h, w = 256, 192
+img = make_image(lib, h, w, seed=4)
+enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=4)
+lr = np.array([1e-2, 9e-3, 8e-3]); tp = np.array([0.35, 0.33, 0.31]); ns = np.array([0.22, 0.21, 0.2])
+with B.BandTrainer(img, 0, h, 6, enc, DecoderConfig.hop(), lib=lib, device=0) as tr:
+    tr.fresh_candidate(0)
+    hyper = any(g.hyper for g in tr.grids)
+    db = B.DistBand(tr, h, w, [(0, h)], 6, hyper, dist, device=0)
+    costs = list(db.proxy_iterations(lr, tp, ns))
+    st = tr.get_state()
+    db.close()
+    out = dict(costs=costs, params=st["params"].tolist(), lat=st["latents"].tolist(), global_iter=tr.global_iter)
+dist.destroy_process_group()
+print("RESULT " + json.dumps(out))
+"""
+
+
+@pytest.mark.gpu
+def test_nccl_band_group_single_rank_matches_local(gpu_lib, tmp_path):
+    """The NCCL transport of the band group (dlopen'ed libnccl, unique id over
+    torch.distributed, ncclAllGather of the partials, ncclAllReduce(min) of the
+    flags on the trainer's stream) at world size 1 — the one configuration a
+    single GPU can run — against the local group: bit-identical."""
+    import json
+    import subprocess
+    import sys
+
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    script = tmp_path / "nccl1.py"
+    script.write_text(_NCCL1)
+    r = subprocess.run([sys.executable, str(script)], cwd=str(ROOT), env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-4000:]
+    line = [x for x in r.stdout.splitlines() if x.startswith("RESULT ")][-1]
+    got = json.loads(line[7:])
+    h, w = 256, 192
+    img = make_image(gpu_lib, h, w, seed=4)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=4)
+    db = B.DeviceBands(img, 1, enc, DecoderConfig.hop(), halo=6, lib=gpu_lib)
+    try:
+        db.fresh_candidate(0)
+        costs = list(db.proxy_iterations([1e-2, 9e-3, 8e-3], [0.35, 0.33, 0.31], [0.22, 0.21, 0.2]))
+        st = db.trainers[0].get_state()
+        assert got["costs"] == costs
+        assert np.array_equal(np.array(got["params"], np.float32), st["params"])
+        assert np.array_equal(np.array(got["lat"], np.float32), st["latents"])
+        assert got["global_iter"] == 3
+    finally:
+        db.close()
