@@ -691,6 +691,56 @@ void Trainer::nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, bool
 // assembly.
 // CCB_SERIAL=1 runs every branch on the main stream in program order (the
 // race check of tests/test_gpu_parity.py::test_branches_match_serial_order).
+// graphs honour the per-node priorities captured from the branch streams
+// (main = greatest, side / tail = least) instead of the launch stream's
+static unsigned graph_flags() {
+    static const unsigned f = [] {
+        const char* e = std::getenv("CCB_NODE_PRIO");
+        return (e && (e[0] == '1' || e[0] == '2')) ? unsigned(cudaGraphInstantiateFlagUseNodePriority) : 0u;
+    }();
+    return f;
+}
+
+static bool node_priorities() { return graph_flags() != 0u; }
+
+// while capturing: the node(s) just added on `st` run at the least priority
+void Trainer::note_low_priority(cudaStream_t st) {
+    if (!node_priorities()) return;
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t nd = 0;
+    CCB_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd));
+    if (cs != cudaStreamCaptureStatusActive) return;
+    for (size_t i = 0; i < nd; ++i) low_nodes_.push_back(deps[i]);
+}
+
+// every other kernel node of a captured graph at the greatest priority, so
+// the critical (distortion) chain's CTAs are dispatched before pending
+// low-priority (ARM) CTAs whenever an SM frees up
+void Trainer::apply_node_priorities(cudaGraph_t g) {
+    if (!node_priorities()) return;
+    int least = 0, greatest = 0;
+    CCB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    size_t n = 0;
+    CCB_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CCB_CUDA(cudaGraphGetNodes(g, nodes.data(), &n));
+    for (cudaGraphNode_t nd : nodes) {
+        cudaGraphNodeType t;
+        CCB_CUDA(cudaGraphNodeGetType(nd, &t));
+        if (t != cudaGraphNodeTypeKernel) continue;
+        const bool low = std::find(low_nodes_.begin(), low_nodes_.end(), nd) != low_nodes_.end();
+        cudaKernelNodeAttrValue v{};
+        static const bool invert = [] {  // CCB_NODE_PRIO=2: the ARM first instead
+            const char* e = std::getenv("CCB_NODE_PRIO");
+            return e && e[0] == '2';
+        }();
+        v.priority = (low != invert) ? least : greatest;
+        CCB_CUDA(cudaGraphKernelNodeSetAttribute(nd, cudaLaunchAttributePriority, &v));
+    }
+    low_nodes_.clear();
+}
+
 static bool serial_branches() {
     static const bool on = [] {
         const char* e = std::getenv("CCB_SERIAL");
@@ -739,6 +789,7 @@ void Trainer::enqueue_proxy(bool batched) {
     }();
     fork();
     launch_arm(side(), kArmProxy);
+    note_low_priority(side().stream);
     mark(2, true);
     if (mode != 2) {
         launch_pyramid(side());
@@ -827,7 +878,8 @@ void Trainer::timeline(int n, double lr, double temp, double noise, double* ms) 
     CCB_CUDA(cudaStreamEndCapture(stream_, &g));
     tl_ev_ = nullptr;
     cudaGraphExec_t ex;
-    CCB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+    apply_node_priorities(g);
+        CCB_CUDA(cudaGraphInstantiate(&ex, g, graph_flags()));
     cudaGraphDestroy(g);
     std::vector<double> acc(kTimelineMarks, 0.0);
     for (int it = 0; it < n; ++it) {
@@ -884,7 +936,8 @@ cudaGraphExec_t Trainer::ensure_graph(int which, int slot) {
         else enqueue_hardround(slot);
         CCB_CUDA(cudaStreamEndCapture(stream_, &g));
         cudaGraphExec_t ex;
-        CCB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+        apply_node_priorities(g);
+        CCB_CUDA(cudaGraphInstantiate(&ex, g, graph_flags()));
         cudaGraphDestroy(g);
         it = graphs_.emplace(key, ex).first;
     }
@@ -1170,7 +1223,8 @@ cudaGraphExec_t Trainer::capture_batched_proxy(const Plan* d_plans, int batch) {
         CCB_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
         enqueue_proxy(true);
         CCB_CUDA(cudaStreamEndCapture(stream_, &g));
-        CCB_CUDA(cudaGraphInstantiate(&ex, g, 0));
+        apply_node_priorities(g);
+        CCB_CUDA(cudaGraphInstantiate(&ex, g, graph_flags()));
         cudaGraphDestroy(g);
     } catch (...) {
         L_ = keep;

@@ -179,6 +179,8 @@ private:
     void run_graph(int which, int slot = -1);
     cudaGraphExec_t ensure_graph(int which, int slot = -1);
     void read_scalars();
+    void note_low_priority(cudaStream_t st);
+    void apply_node_priorities(cudaGraph_t g);
     void ensure_snapshot(int slot);
     void zero_pads();
     void* dalloc(size_t bytes);
@@ -230,6 +232,7 @@ private:
         int hg = 0, r0 = 0, r1 = 0, halo = 0;
     } band_;
     std::vector<int4> tiles_host_;
+    std::vector<cudaGraphNode_t> low_nodes_;  // captured nodes to run at the least priority
 };
 
 // Several images of one geometry trained in lock-step by ONE set of launches
