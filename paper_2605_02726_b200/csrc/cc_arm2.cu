@@ -46,8 +46,11 @@ constexpr int kRM = 12;       // max IFCE source grids
 constexpr int kFM = 8;        // max IFCE width
 constexpr int kMaxPad = 4;    // context window halo (yhat_pad border P)
 constexpr int WS = T + 2 * kMaxPad;  // context window row: columns c0-P .. c0+len-1+P
+static_assert(WS == kArmWinCols, "the window row is the TMA box row (Trainer::make_pad_maps)");
 constexpr int WC = (kMaxPad + 1) * WS;  // context part of a window
-constexpr int WIN = WC + (kRM + 4) * LT;  // + R rows [j][latent]: sources, ones at kRM, zeros
+// + R rows [j][latent]: sources, ones at kRM, zeros; a multiple of 32 floats
+// so that both window buffers start on the 128 bytes the TMA destination needs
+constexpr int WIN = (WC + (kRM + 4) * LT + 31) & ~31;
 
 template <int DP, int WP>
 struct A2 {
@@ -90,7 +93,7 @@ struct A2 {
 };
 
 template <int DP, int WP>
-struct alignas(16) A2Smem {
+struct alignas(128) A2Smem {
     using K = A2<DP, WP>;
     alignas(16) float W1T[DP][32];   // [k][out a] (forward l1), group stride 8
     alignas(16) float W1[WP][32];    // [a][out k] (backward dC)
@@ -105,13 +108,14 @@ struct alignas(16) A2Smem {
     alignas(16) float Wf[kMaxSlots][kFM][kRM];
     alignas(16) float bf[kMaxSlots][kFM];
     alignas(16) float act[K::ACT];
-    alignas(16) float win[2][WIN];   // gather windows: this tile's, the next tile's
+    alignas(128) float win[2][WIN];  // gather windows: this tile's, the next tile's
     int woff[kMaxCtx];               // context offset o -> window position
     alignas(16) float stage5[K::NU5][16];
     double acc5[K::NACC5];  // IFCE dW (+db), per slot, fp64
     GridGeom geo[kMaxGrids];
     double red[NT / 32];
     alignas(16) int4 trec[4];  // tile records two ahead, landed by cp.async with the gathers
+    alignas(8) uint64_t wbar[2];  // TMA completion of each window buffer's context rows
     CtxTable ctxt;  // context offsets by target row (cc_ctx.cuh)
 };
 
@@ -140,31 +144,49 @@ __device__ __forceinline__ void third_range(int s, int& i0, int& i1) {
     i1 = s == 2 ? T : i0 + 44;
 }
 
-__device__ __forceinline__ void cp_async4_zfill(float* smem, const float* gmem, bool full) {
-    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "r"(full ? 4 : 0)
-                 : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+
+struct alignas(64) CUtensorMapOpaque {  // CUtensorMap (cuda.h): 128 opaque bytes
+    unsigned long long opaque[16];
+};
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, unsigned parity) {
+    const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}\n" ::"r"(sb),
+        "r"(parity)
+        : "memory");
+}
 
 // Asynchronous gather of one row-segment tile (grid tile.x, latents
 // tile.y .. tile.y+len-1 = row r, columns c0 .. c0+len-1) into a window
-// buffer: the P+1 padded rows r-P .. r over columns c0-P .. c0+len-1+P (the
-// causal context of every latent of the tile, zero border included), and on
-// IFCE grids the R rows [j][latent] = ŷ of coarser grid j < rdim at
+// buffer: the P+1 padded rows r-P .. r over columns c0-P .. c0-P+WS-1 (the
+// causal context of every latent of the tile, zero border included) as ONE
+// TMA box load (cp.async.bulk.tensor.2d from the grid's padded array,
+// Trainer::make_pad_maps; zero fill past the array) completing on `bar`, and
+// on IFCE grids the R rows [j][latent] = ŷ of coarser grid j < rdim at
 // (r >> sh, c >> sh) (global rows, clamped to the band) — one warp per
-// source grid.  All 256 threads; always commits one cp.async group.
+// source grid, cp.async.  All 256 threads; always commits one cp.async group.
 __device__ __forceinline__ void issue_gather(const Plan& P, const GridGeom* geo, int4 tile, float* win,
-                                             int tid) {
+                                             uint64_t* bar, int tid) {
     const GridGeom& g = geo[tile.x];
     const int r = tile.z, len = tile.w, c0 = tile.y - r * g.cols;
-    const int pad = P.P;
-    const float* base = P.yhat_pad + g.pad_base + int64_t(r - pad) * g.stride + (c0 - pad);
-    const int lenw = len + 2 * pad;
-    for (int e = tid; e < (pad + 1) * WS; e += NT) {
-        const int i = e / WS, x = e - i * WS;
-        const bool full = x < lenw;
-        cp_async4_zfill(win + e, full ? base + int64_t(i) * g.stride + x : base, full);
+    if (tid == 0) {
+        const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(bar));
+        const unsigned sw = static_cast<unsigned>(__cvta_generic_to_shared(win));
+        const unsigned bytes = unsigned(WS) * unsigned(P.P + 1) * 4u;
+        const CUtensorMapOpaque* map = static_cast<const CUtensorMapOpaque*>(P.pad_maps) + tile.x;
+        // the buffer's previous (generic-proxy) readers are ordered before the async-proxy write
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sb), "r"(bytes) : "memory");
+        // box origin in padded coordinates: column c0 (= c0 - P unpadded), row r (= r - P)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(sw),
+            "l"(map), "r"(c0), "r"(r), "r"(sb)
+            : "memory");
     }
     if (g.ifce_slot >= 0) {
         float* wr = win + WC;
@@ -185,7 +207,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
                                                 const int4* __restrict__ tiles, int ntiles) {
     using K = A2<DP, WP>;
     const Plan& P = pp[blockIdx.z];  // batched launches: one plan per image
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     A2Smem<DP, WP>& sm = *reinterpret_cast<A2Smem<DP, WP>*>(smem_raw);
     const int tid = threadIdx.x;
     const int half = tid >> 7, lt = tid & (T - 1);   // per-latent roles
@@ -242,7 +264,14 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
         sm.woff[e] = e < S ? (P.P + P.ctx_dy[e]) * WS + P.P + P.ctx_dx[e] : 0;
     for (int e = tid; e < K::NACC5; e += NT) sm.acc5[e] = 0.0;
     for (int e = tid; e < P.n_grids; e += NT) sm.geo[e] = P.g[e];
-    if (tid == 0) ctx_table_build(P, sm.ctxt);
+    if (tid == 0) {
+        ctx_table_build(P, sm.ctxt);
+        for (int b = 0; b < 2; ++b) {
+            const unsigned sb = static_cast<unsigned>(__cvta_generic_to_shared(&sm.wbar[b]));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sb) : "memory");
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     // constant rows: zero padding of every activation array (written once);
     // windows zeroed so R rows past a grid's rdim are always finite
     for (int e = tid; e < K::ACT; e += NT) sm.act[e] = 0.0f;
@@ -264,7 +293,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
     int wb = 0;  // window buffer of the current tile
     if (tid == 0)  // ring slot of the first tile's record two ahead; later ones by cp.async
         sm.trec[0] = blockIdx.x + 2 * gridDim.x < ntiles ? tiles[blockIdx.x + 2 * gridDim.x] : make_int4(0, 0, 0, 0);
-    if (blockIdx.x < ntiles) issue_gather(P, sm.geo, cur, sm.win[0], tid);
+    if (blockIdx.x < ntiles) issue_gather(P, sm.geo, cur, sm.win[0], &sm.wbar[0], tid);
     int kt = 0;  // tile count of this CTA (ring index)
 
     // persistent weight-gradient accumulators of this thread's units
@@ -297,10 +326,11 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
                          : "memory");
         }
         if (t + int(gridDim.x) < ntiles)
-            issue_gather(P, sm.geo, nxt, sm.win[wb ^ 1], tid);
+            issue_gather(P, sm.geo, nxt, sm.win[wb ^ 1], &sm.wbar[wb ^ 1], tid);
         else
             cp_async_commit();
         asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        mbar_wait_parity(&sm.wbar[wb], unsigned(kt >> 1) & 1u);  // this tile's context rows (TMA)
         __syncthreads();
         const int4 nxt2 = sm.trec[kt & 3];
         ++kt;

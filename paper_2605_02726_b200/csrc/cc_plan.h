@@ -33,6 +33,7 @@
 namespace ccb {
 
 constexpr int kMaxGrids = 16;
+constexpr int kArmWinCols = 136;  // ARM context window row: a 128-latent tile + 2 x 4 halo columns
 constexpr int kMaxLevels = 8;
 constexpr int kMaxCtx = 64;
 constexpr int kMaxTensors = 64;
@@ -144,6 +145,7 @@ struct Plan {
 
     // ---- device buffers ----
     float* yhat_pad;
+    const void* pad_maps;     // CUtensorMap[kMaxGrids]: TMA descriptors of the padded grids
     float* y;
     float* lat_m;
     float* lat_v;

@@ -4,6 +4,9 @@
 // once into CUDA graphs and replayed (no host work per kernel).
 #include "cc_runtime.h"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -267,7 +270,10 @@ void Trainer::build_plan() {
             g.own_lo = o0 - w0;
             g.own_hi = o1 - w0;
         }
-        g.stride = g.cols + 2 * P.P;
+        // row stride rounded to 16 bytes: every grid's padded array is a
+        // valid TMA tensor (16-byte aligned base and row pitch; the extra
+        // columns belong to the zero border)
+        g.stride = (g.cols + 2 * P.P + 3) & ~3;
         g.pad_base = pad_cur + int64_t(P.P) * g.stride + P.P;
         pad_cur += int64_t(g.rows + 2 * P.P) * g.stride;
         g.lat_off = lat_cur;
@@ -525,11 +531,44 @@ void Trainer::build_plan() {
     tiles_host_ = tiles;
 }
 
+// One TMA descriptor per grid over its zero-bordered padded array
+// ((rows + 2P) x stride fp32): the ARM loads a tile's causal-context window
+// (P + 1 rows x kArmWinCols columns, zero fill past the array) with one
+// cp.async.bulk.tensor instead of per-thread 4-byte copies.
+void Trainer::make_pad_maps() {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CCB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) throw CudaError("cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    Plan& P = H_;
+    std::vector<CUtensorMap> maps(kMaxGrids);
+    std::memset(maps.data(), 0, sizeof(CUtensorMap) * maps.size());
+    for (int gi = 0; gi < P.n_grids; ++gi) {
+        const GridGeom& g = P.g[gi];
+        float* base = P.yhat_pad + g.pad_base - int64_t(P.P) * g.stride - P.P;
+        const cuuint64_t dims[2] = {cuuint64_t(g.stride), cuuint64_t(g.rows + 2 * P.P)};
+        const cuuint64_t strides[1] = {cuuint64_t(g.stride) * sizeof(float)};
+        const cuuint32_t box[2] = {cuuint32_t(kArmWinCols), cuuint32_t(P.P + 1)};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode(&maps[size_t(gi)], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims, strides, box, estr,
+                                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed for grid " + std::to_string(gi));
+    }
+    auto* d = static_cast<CUtensorMap*>(dalloc(sizeof(CUtensorMap) * maps.size()));
+    CCB_CUDA(cudaMemcpy(d, maps.data(), sizeof(CUtensorMap) * maps.size(), cudaMemcpyHostToDevice));
+    P.pad_maps = d;
+}
+
 void Trainer::allocate() {
     Plan& P = H_;
     const int64_t nl = P.n_latents, np = P.npix;
     auto f32 = [&](int64_t n) { return static_cast<float*>(dalloc(sizeof(float) * size_t(n))); };
     P.yhat_pad = f32(sizes_.pad);
+    make_pad_maps();
     P.y = f32(nl);
     P.lat_m = f32(nl);
     P.lat_v = f32(nl);

@@ -167,6 +167,7 @@ private:
     void nn_apply(const LaunchCtx& ctx, bool do_step, bool count_iter, bool log_rec);
     void build_plan();
     void allocate();
+    void make_pad_maps();
     void require_loaded() const;
     void init_params_host(uint64_t stream, std::vector<float>& out) const;
     void enqueue_proxy(bool batched);
