@@ -259,8 +259,12 @@ class LocalBands:
         nn = np.zeros(self.trainers[0].n_params, np.float64)
         for t in self.trainers:
             nn = nn + t.nn_partial()
-        bits = float(sum(s[0] for s in sums))
-        se = float(sum(s[1] for s in sums))
+        # rank-order sums, as the device band group (k_band_finish); Python's
+        # sum() of floats is compensated (3.12+) and would round differently
+        bits = se = 0.0
+        for s in sums:
+            bits += float(s[0])
+            se += float(s[1])
         oks = []
         cost = None
         for t in self.trainers:

@@ -28,6 +28,9 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
+#include <vector>
+#include <mutex>
 
 #include "cc_kernels.h"
 #include "cc_math.cuh"
@@ -615,7 +618,7 @@ void launch_arm_tc(const LaunchCtx& L, int mode);
 static int arm_env() {
     static const int v = [] {
         const char* e = std::getenv("CCB_ARM");
-        return (e && e[0] == 't') ? 3 : 0;
+        return (e && e[0] == 't') ? 3 : (e && e[0] == '2') ? 2 : 0;
     }();
     return v;
 }
@@ -647,6 +650,177 @@ static void launch_arm_mode(const LaunchCtx& L, int mode) {
         launch_arm_t<DP, WP, kArmProxy>(L);
 }
 
+
+// IFCE weight gradients of the constant-bank ARM's plans (Plan::ifce_sep),
+// from the dF block-sum pyramid (entropy_model.hpp:318-321):
+//   dW_f[s][f][j] = sum over latents of IFCE grid s of dF[f] * yhat_j(r >> sh, c >> sh)
+//                 = sum over the positions (R, C) of source grid j of
+//                   yhat_j(R, C) * P_sh[f](R, C),
+// P_sh = level sh = level_j - level_s of the pyramid of dF (the same block
+// sums k_latent_grad scatters as dR, aligned the same way), and
+//   db_f[s][f] = sum of dF[f] = sum over the deepest pyramid level.
+// One CTA per work item (s, j, e0, e1) — a chunk of <= kIfceChunk positions
+// of source grid j (j = kIfceBias: the deepest pyramid level, for the bias),
+// built by the runtime (ifce_dw_items); the item writes its F sums and zeros
+// for the rest of its row of slot s's partial region (fixed-order reduction).
+constexpr int kIfceThreads = 128;
+constexpr int kIfceF = 8;
+
+__global__ void __launch_bounds__(kIfceThreads) k_ifce_dw(const Plan* __restrict__ pp) {
+    const Plan& P = pp[blockIdx.z];
+    const int4 it = P.ifce_items[blockIdx.x];
+    const int s = it.x, j = it.y, e0 = it.z, e1 = it.w;
+    const GridGeom& g = P.g[P.slot_gi[s]];
+    const int rd = g.rdim, F = P.F;
+    const bool bias = j == kIfceBias;
+    const int sh = bias ? P.slot_smax[s] : P.g[j].level - g.level;
+    const int prows = P.slot_pyr_rows[s][sh], cols = P.slot_pyr_cols[s][sh];
+    const float* pyr = P.dfeat + P.slot_pyr_off[s][sh];
+    const int64_t pc = int64_t(prows) * cols;
+    const FDivU cdiv(cols);
+    float acc[kIfceF];
+#pragma unroll
+    for (int f = 0; f < kIfceF; ++f) acc[f] = 0.0f;
+#pragma unroll 4
+    for (int e = e0 + threadIdx.x; e < e1; e += kIfceThreads) {
+        const int r = cdiv.div(e), c = e - r * cols;
+        float w = 1.0f;
+        int R = r;
+        if (!bias) {
+            const GridGeom& sg = P.g[j];
+            R = sg.row0 + r - (P.slot_pyr_a[s] >> sh);  // as k_latent_grad's dR gather
+            if (R < 0 || R >= prows) continue;
+            w = P.yhat_pad[sg.pad_base + int64_t(r) * sg.stride + c];
+        }
+        const float* q = pyr + int64_t(R) * cols + c;
+#pragma unroll
+        for (int f = 0; f < kIfceF; ++f)
+            if (f < F) acc[f] = fmaf(w, q[int64_t(f) * pc], acc[f]);
+    }
+    __shared__ float part[kIfceF][kIfceThreads + 1];
+#pragma unroll
+    for (int f = 0; f < kIfceF; ++f) part[f][threadIdx.x] = acc[f];
+    __syncthreads();
+    const PartialRegion& Rg = P.region[P.reg_ifce[s]];
+    const PartialRow row(P, Rg, blockIdx.x - P.ifce_item0[s]);
+    for (int x = threadIdx.x; x < F * (rd + 1); x += kIfceThreads) {
+        const int f = x / (rd + 1), b = x % (rd + 1);
+        double v = 0.0;
+        if ((b < rd && b == j) || (b == rd && bias))
+            for (int t = 0; t < kIfceThreads; ++t) v += double(part[f][t]);
+        const int o = b < rd ? P.off_ifw[s] + f * rd + b : P.off_ifb[s] + f;
+        row[o - Rg.param_off] = v;
+    }
+}
+
+static void launch_ifce_dw(const LaunchCtx& L) {
+    const Plan& H = *L.host;
+    if (!H.ifce_sep) return;
+    k_ifce_dw<<<dim3(H.n_ifce_items, 1, L.batch), kIfceThreads, 0, L.stream>>>(L.plan);
+}
+
+// the work items of k_ifce_dw (row x of slot s's region = item ifce_item0[s] + x)
+std::vector<int4> ifce_dw_items(const Plan& P, int* item0) {
+    std::vector<int4> v;
+    for (int s = 0; s < P.n_slots; ++s) {
+        item0[s] = int(v.size());
+        const GridGeom& g = P.g[P.slot_gi[s]];
+        for (int j = 0; j <= g.rdim; ++j) {
+            const bool bias = j == g.rdim;
+            const int sh = bias ? P.slot_smax[s] : P.g[j].level - g.level;
+            const int n = (bias ? P.slot_pyr_rows[s][sh] : P.g[j].rows) * P.slot_pyr_cols[s][sh];
+            for (int e = 0; e < n; e += kIfceChunk)
+                v.push_back(make_int4(s, bias ? kIfceBias : j, e, std::min(n, e + kIfceChunk)));
+        }
+    }
+    return v;
+}
+
+
+
+// The constant-bank ARM (cc_armc.cuh) is the default for the dims it
+// instantiates: one constant slot per translation unit cc_armc_s<k>.cu.
+// CCB_ARM=2 selects the FFMA2 tile kernel, CCB_ARM=tc the tensor-core one.
+#define CCB_ARMC_DECL(k)                                 \
+    void armc_launch_s##k(const LaunchCtx& L, int mode); \
+    void armc_prep_s##k(const LaunchCtx& L);             \
+    void armc_configure_s##k(int Dp, int Wp);
+CCB_ARMC_DECL(0)
+CCB_ARMC_DECL(1)
+CCB_ARMC_DECL(2)
+CCB_ARMC_DECL(3)
+CCB_ARMC_DECL(4)
+CCB_ARMC_DECL(5)
+CCB_ARMC_DECL(6)
+CCB_ARMC_DECL(7)
+#undef CCB_ARMC_DECL
+static_assert(kArmcSlots == 8, "one translation unit per slot");
+using ArmcLaunch = void (*)(const LaunchCtx&, int);
+using ArmcPrep = void (*)(const LaunchCtx&);
+using ArmcConf = void (*)(int, int);
+static const ArmcLaunch g_armc_launch[kArmcSlots] = {armc_launch_s0, armc_launch_s1, armc_launch_s2, armc_launch_s3,
+                                                     armc_launch_s4, armc_launch_s5, armc_launch_s6, armc_launch_s7};
+static const ArmcPrep g_armc_prep[kArmcSlots] = {armc_prep_s0, armc_prep_s1, armc_prep_s2, armc_prep_s3,
+                                                 armc_prep_s4, armc_prep_s5, armc_prep_s6, armc_prep_s7};
+static const ArmcConf g_armc_conf[kArmcSlots] = {armc_configure_s0, armc_configure_s1, armc_configure_s2,
+                                                 armc_configure_s3, armc_configure_s4, armc_configure_s5,
+                                                 armc_configure_s6, armc_configure_s7};
+
+size_t armc_smem_s0(int Dp, int Wp);
+
+int armc_blocks_per_sm(int Dp, int Wp) {  // resident 64-thread CTAs per SM (shared-memory bound)
+    const int b = int((228 * 1024) / (armc_smem_s0(Dp, Wp) + 1024));
+    return std::max(1, std::min(kArmcPerSm, b));
+}
+
+bool armc_supported(int Dp, int Wp) {
+    return arm_env() == 0 && ((Dp == 20 && Wp == 20) || (Dp == 32 && Wp == 20));
+}
+
+// Slots are handed out to trainers for their lifetime.  When all are taken
+// a trainer SHARES one (round robin): its weights and the other owner's then
+// pass through the same constant slot, which is safe as long as the two do
+// not run an ARM at the same time on different streams — true inside the
+// library (a batch runs its images one after another on one stream; the band
+// trainers of one image hold bit-identical weights), and documented for
+// callers that run more than kArmcSlots independent trainers concurrently.
+static std::mutex g_armc_mu;
+static int g_armc_users[kArmcSlots] = {};
+static int g_armc_rr = 0;
+
+int armc_acquire_slot() {
+    std::lock_guard<std::mutex> lk(g_armc_mu);
+    for (int s = 0; s < kArmcSlots; ++s)
+        if (g_armc_users[s] == 0) {
+            g_armc_users[s] = 1;
+            return s;
+        }
+    const int s = g_armc_rr;
+    g_armc_rr = (g_armc_rr + 1) % kArmcSlots;
+    ++g_armc_users[s];
+    return s;
+}
+
+void armc_release_slot(int slot) {
+    if (slot < 0 || slot >= kArmcSlots) return;
+    std::lock_guard<std::mutex> lk(g_armc_mu);
+    if (g_armc_users[slot] > 0) --g_armc_users[slot];
+}
+
+void armc_configure(int Dp, int Wp) {
+    for (int s = 0; s < kArmcSlots; ++s) g_armc_conf[s](Dp, Wp);
+}
+
+bool launch_arm_prep(const LaunchCtx& L) {
+    static const bool skip = [] {
+        const char* e = std::getenv("CCB_DIAG_SKIP_ARM");
+        return e && e[0] == '1';
+    }();
+    if (L.arm_cslot < 0 || skip) return false;
+    g_armc_prep[L.arm_cslot](L);
+    return true;
+}
+
 void launch_arm(const LaunchCtx& L, int mode) {
     const int Dp = L.host->Dp, Wp = L.host->Wp;
     static const bool skip = [] {  // timing diagnostic only (wrong results): the iteration without the ARM
@@ -654,6 +828,20 @@ void launch_arm(const LaunchCtx& L, int mode) {
         return e && e[0] == '1';
     }();
     if (skip) return;
+    if (L.arm_cslot >= 0) {
+        g_armc_launch[L.arm_cslot](L, mode);
+        // hardround: the IFCE weight gradients need the dF pyramid (the proxy
+        // iteration launches it after the ARM anyway)
+        if (mode == kArmHard) launch_pyramid(L);
+        return;
+    }
+    struct IfceAfter {  // the tile kernels below write zeros for the IFCE parameters when ifce_sep
+        const LaunchCtx& L;
+        int mode;
+        ~IfceAfter() {
+            if (mode == kArmHard && L.host->ifce_sep) launch_pyramid(L);
+        }
+    } ifce_after{L, mode};
     if (use_tc(Dp, Wp)) return launch_arm_tc(L, mode);
     if (use_arm2(Dp, Wp)) return launch_arm2(L, mode);
     if (Dp == 8 && Wp == 8) launch_arm_mode<8, 8>(L, mode);
@@ -703,6 +891,7 @@ void launch_pyramid(const LaunchCtx& L) {
         nblk = std::max(nblk, H.slot_pyr_rows[s][H.slot_smax[s]] * H.slot_pyr_cols[s][H.slot_smax[s]]);
     const dim3 grid(nblk, H.n_slots * H.F, L.batch);
     k_pyramid_fused<<<grid, 256, pyramid_smem(H), L.stream>>>(L.plan);
+    launch_ifce_dw(L);  // constant-bank ARM: the IFCE weight gradients from the pyramid
 }
 
 }  // namespace ccb

@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
                 } else if (k < S + F && slot >= 0) {
                     const float2 dv = make_float2(v0 ? acc[n].x : 0.0f, v1 ? acc[n].y : 0.0f);
                     *reinterpret_cast<float2*>(sDF + (k - S) * LT + 2 * pr) = dv;
-                    if (MODE == kArmProxy) {
+                    if (MODE == kArmProxy || (MODE == kArmHard && P.ifce_sep)) {  // k_ifce_dw reads dF
                         float* dfp = P.dfeat + g.dfeat_off + int64_t(k - S) * count + l0;
                         if (v1 && (reinterpret_cast<uintptr_t>(dfp) & 7) == 0) {
                             *reinterpret_cast<float2*>(dfp) = dv;
@@ -635,7 +635,7 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
         const int rd = P.g[P.slot_gi[s]].rdim;
         for (int e = tid; e < F * (rd + 1); e += NT) {
             const int f = e / (rd + 1), b = e % (rd + 1);
-            const double v = sm.acc5[(s * kFM + f) * (kRM + 1) + (b < rd ? b : kRM)];
+            const double v = P.ifce_sep ? 0.0 : sm.acc5[(s * kFM + f) * (kRM + 1) + (b < rd ? b : kRM)];
             const int o = b < rd ? P.off_ifw[s] + f * rd + b : P.off_ifb[s] + f;
             row[o - R.param_off] = v;
         }

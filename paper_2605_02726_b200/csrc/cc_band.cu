@@ -44,7 +44,8 @@ __global__ void __launch_bounds__(256) k_band_finish(const Plan* __restrict__ pp
             se += parts[r * stride + P.n_params + 1];
         }
         const double mse = se / double(3 * P.npix_global);
-        const double cost = mse + P.lambda * (bits / double(P.npix_global));  // encoder.hpp:115
+        // encoder.hpp:115, contracted as the reference build (-ffp-contract=fast) and k_finalize do
+        const double cost = fma(P.lambda, bits / double(P.npix_global), mse);
         DevScalars* s = P.scal;
         s->bits = bits;
         s->mse = mse;

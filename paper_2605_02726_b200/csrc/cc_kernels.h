@@ -5,6 +5,8 @@
 
 #include "cc_plan.h"
 
+#include <vector>
+
 namespace ccb {
 
 void cuda_check(cudaError_t e, const char* what);  // throws CudaError (cc_runtime.cu)
@@ -26,6 +28,9 @@ struct LaunchCtx {
     int red_blocks;        // per-CTA partial rows of the small reduction kernels
     int batch = 1;         // images per launch: plan points at `batch` consecutive Plans,
                            // every kernel reads pp[blockIdx.z] (same geometry for all)
+    int arm_cslot = -1;    // constant-bank ARM (cc_armc.cuh): the constant slot, -1 = not used
+    float* const* arm_cstages = nullptr;  // host array: each image's Plan::arm_cstage (launch time only)
+    bool arm_prepped = false;  // launch_arm_prep already packed the weights and filled the slot for image 0
 };
 
 // Launch with programmatic stream serialization (see pdl_wait in
@@ -70,12 +75,29 @@ void launch_noise_ahead(const LaunchCtx& L);
 bool arm_dims_supported(int D, int W);
 void arm_padded_dims(int D, int W, int* Dp, int* Wp);
 void launch_arm(const LaunchCtx& L, int mode);
+// constant-bank ARM: pack the weights and fill the slot for image 0 (returns
+// false when the launch context does not use it); launch_arm then skips that
+// with LaunchCtx::arm_prepped
+bool launch_arm_prep(const LaunchCtx& L);
+// IFCE weight gradients from the dF pyramid (Plan::ifce_sep): work items
+constexpr int kIfceChunk = 256;  // positions per item (two per thread: latency-bound gathers need many CTAs)
+constexpr int kIfceBias = 15;     // item source index of the bias sums
+std::vector<int4> ifce_dw_items(const Plan& P, int* item0);
 void launch_pyramid(const LaunchCtx& L);
 int arm_blocks_per_sm(int Dp, int Wp);
 void arm_configure(int Dp, int Wp);
 bool arm_uses_v2(int Dp, int Wp);
 bool arm_uses_tc(int Dp, int Wp);  // the tensor-core kernel (cc_arm_tc.cu)
 void pyramid_configure(const Plan& H);
+// constant-bank ARM (cc_armc.cuh, one constant slot per translation unit)
+constexpr int kArmcSlots = 8;
+constexpr int kArmcSlotFloats = 2560;
+constexpr int kArmcPerSm = 4;       // 64-thread CTAs per SM (at most)
+bool armc_supported(int Dp, int Wp);
+int armc_blocks_per_sm(int Dp, int Wp);
+int armc_acquire_slot();             // a free slot, else a shared one (cc_arm.cu)
+void armc_release_slot(int slot);
+void armc_configure(int Dp, int Wp);
 
 // upsampling (cc_ups.cu)
 void launch_ups_forward(const LaunchCtx& L);

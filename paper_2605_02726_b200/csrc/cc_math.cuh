@@ -111,6 +111,20 @@ struct FDiv {
     __device__ __forceinline__ int div(int e) const { return int((float(e) + 0.5f) * inv); }
 };
 
+// e / n for 0 <= e < 2^31, 1 <= n < 2^31: m = ceil(2^63 / n), e / n =
+// (m * 2e) >> 64 — the rounding error e * (m - 2^63/n) / 2^63 < 2^-32 stays
+// below the 1/n gap to the next integer, so the quotient is exact.
+struct FDivU {
+    unsigned long long m;
+    __device__ __forceinline__ explicit FDivU(int n) {
+        const unsigned long long t = 1ull << 63;
+        m = t / (unsigned long long)n + (t % (unsigned long long)n != 0 ? 1ull : 0ull);
+    }
+    __device__ __forceinline__ int div(int e) const {
+        return int(__umul64hi(m, 2ull * (unsigned long long)e));
+    }
+};
+
 // Asynchronous 4-byte global -> shared copy (LDGSTS): window staging keeps
 // every load of a tile in flight at once instead of load/wait/store.
 __device__ __forceinline__ void cp_async4(float* smem, const float* gmem) {

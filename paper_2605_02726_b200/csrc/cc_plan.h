@@ -132,6 +132,11 @@ struct Plan {
     int n_regions;
     PartialRegion region[kMaxPartialRegions];
     int reg_arm;              // region index of the ARM kernel (ARM + IFCE params)
+    int ifce_sep;             // IFCE weight gradients from k_ifce_dw (constant-bank ARM); the ARM kernels write zeros
+    int reg_ifce[kMaxSlots];  // its regions (one per IFCE slot): one row per work item of the slot
+    int n_ifce_items;         // k_ifce_dw work items (slot, source j or kIfceBias, first, end position)
+    int ifce_item0[kMaxSlots];  // first item of each slot (row 0 of its region)
+    const int4* ifce_items;
     int reg_syn_trunk;        // syn c1,c2,stab
     int reg_post[2];          // syn post i (w + b)
     int reg_ups_rows[kMaxLevels], reg_ups_cols[kMaxLevels], reg_ups_ref[kMaxLevels];
@@ -163,6 +168,7 @@ struct Plan {
     float* ups_grad;
     float* ups_grad2;
     float* image;
+    float* arm_cstage;        // constant-bank ARM: this image's padded weight image (cc_armc.cuh)
     float* syn_t;
     float* syn_p[2];
     float* syn_sz;

@@ -132,6 +132,7 @@ void Trainer::init(const float* image, int h, int w) {
 Trainer::~Trainer() {
     cudaSetDevice(device_);
     if (stream_) cudaStreamSynchronize(stream_);
+    armc_release_slot(armc_slot_);
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     for (auto& kv : cands_) {
         for (float* p : {kv.second.y, kv.second.m, kv.second.v, kv.second.p, kv.second.nm, kv.second.nv})
@@ -250,6 +251,11 @@ void Trainer::build_plan() {
         return e && e[0] == '1';
     }();
     P.ctx_part = (ctx_part_env && arm_uses_v2(P.Dp, P.Wp)) ? 1 : 0;
+    // the constant-bank ARM (cc_armc.cuh) where it instantiates the dims; its
+    // launch geometry (kArmcPerSm x 64-thread CTAs per SM) sizes the ARM's
+    // partial rows even when no constant slot is free (then the FFMA2 tile
+    // kernel runs on the same grid)
+    armc_on_ = armc_supported(P.Dp, P.Wp) && !P.ctx_part;
     for (int i = 0; i < kMaxLevels; ++i) P.main_gi[i] = -1;
     for (int gi = 0; gi < P.n_grids; ++gi) {
         GridGeom& g = P.g[gi];
@@ -481,6 +487,11 @@ void Trainer::build_plan() {
     L_.arm_blocks = std::min(L_.arm_ntiles, arm_uses_tc(P.Dp, P.Wp)  ? num_sms_ * arm_occ
                                             : arm_occ >= 2          ? num_sms_ * 3 / 2
                                                                     : num_sms_ * arm_occ);
+    if (armc_on_) {
+        int per = armc_blocks_per_sm(P.Dp, P.Wp);
+        if (const char* e = std::getenv("CCB_ARMC_OCC")) per = std::max(1, std::min(per, std::atoi(e)));
+        L_.arm_blocks = std::min(L_.arm_ntiles, num_sms_ * per);
+    }
     if (const char* e = std::getenv("CCB_ARM_CTAS"))  // A/B: explicit persistent CTA count
         L_.arm_blocks = std::max(1, std::min(L_.arm_ntiles, std::atoi(e)));
     const int FP = syn_padded_hidden(P.syn_F);
@@ -504,6 +515,22 @@ void Trainer::build_plan() {
     };
     P.arm_nvals = P.off_tconv[0];
     P.reg_arm = region(0, P.arm_nvals, L_.arm_blocks);
+    // constant-bank ARM: the IFCE weight gradients come from k_ifce_dw (its
+    // own partial rows; the ARM kernels write zeros for those parameters)
+    P.ifce_sep = (armc_on_ && P.n_slots > 0 && P.F > 0) ? 1 : 0;
+    for (int s = 0; s < kMaxSlots; ++s) P.reg_ifce[s] = -1;
+    P.n_ifce_items = 0;
+    ifce_items_host_.clear();
+    if (P.ifce_sep) {
+        ifce_items_host_ = ifce_dw_items(P, P.ifce_item0);
+        P.n_ifce_items = int(ifce_items_host_.size());
+        for (int s = 0; s < P.n_slots; ++s) {
+            const int rd = P.g[P.slot_gi[s]].rdim;
+            if (P.off_ifb[s] != P.off_ifw[s] + P.F * rd) throw ConfigError("IFCE parameters are not contiguous");
+            const int end = s + 1 < P.n_slots ? P.ifce_item0[s + 1] : P.n_ifce_items;
+            P.reg_ifce[s] = region(P.off_ifw[s], P.F * rd + P.F, end - P.ifce_item0[s]);
+        }
+    }
     P.ups_jc = ups_coarse_from(P);
     for (int j = 0; j < P.L - 1; ++j) {
         // k_ups_bwd writes one row per CTA: dk4 (row + column passes) and dr3;
@@ -616,6 +643,15 @@ void Trainer::allocate() {
     d_tiles_ = static_cast<int4*>(dalloc(sizeof(int4) * tiles_host_.size()));
     CCB_CUDA(cudaMemcpy(d_tiles_, tiles_host_.data(), sizeof(int4) * tiles_host_.size(),
                         cudaMemcpyHostToDevice));
+    P.arm_cstage = armc_on_ ? f32(kArmcSlotFloats) : nullptr;
+    P.ifce_items = nullptr;
+    if (!ifce_items_host_.empty()) {
+        int4* d = static_cast<int4*>(dalloc(sizeof(int4) * ifce_items_host_.size()));
+        CCB_CUDA(cudaMemcpy(d, ifce_items_host_.data(), sizeof(int4) * ifce_items_host_.size(),
+                            cudaMemcpyHostToDevice));
+        P.ifce_items = d;
+    }
+    if (armc_on_) armc_slot_ = armc_acquire_slot();
     d_plan_ = static_cast<Plan*>(dalloc(sizeof(Plan)));
     CCB_CUDA(cudaMemcpy(d_plan_, &H_, sizeof(Plan), cudaMemcpyHostToDevice));
     CCB_CUDA(cudaMallocHost(&h_scal_, sizeof(DevScalars)));
@@ -628,7 +664,10 @@ void Trainer::allocate() {
     L_.host = &H_;
     L_.stream = stream_;
     L_.arm_tiles = d_tiles_;
+    L_.arm_cslot = armc_slot_;
+    L_.arm_cstages = &H_.arm_cstage;
     arm_configure(P.Dp, P.Wp);
+    if (armc_on_) armc_configure(P.Dp, P.Wp);
     syn_configure(syn_padded_hidden(P.syn_F));
     ups_configure();
     syn_post_configure();
@@ -815,6 +854,10 @@ void Trainer::mark(int id, int on) {
 void Trainer::enqueue_proxy(bool batched) {
     mark(0, false);
     if (batched) launch_sched_load(L_);
+    // constant-bank ARM: the weights packed into its constant slot on the
+    // rate branch while the soft-quantiser runs
+    fork();
+    const bool prepped = launch_arm_prep(side());
     launch_softq_fwd(L_);
     mark(1, false);
     // A/B: the synthesis trunk's weight gradients as a separate launch on the
@@ -827,7 +870,11 @@ void Trainer::enqueue_proxy(bool batched) {
         return e ? std::atoi(e) : 0;
     }();
     fork();
-    launch_arm(side(), kArmProxy);
+    {
+        LaunchCtx rate = side();
+        rate.arm_prepped = prepped;
+        launch_arm(rate, kArmProxy);
+    }
     note_low_priority(side().stream);
     mark(2, true);
     if (mode != 2) {
@@ -1060,7 +1107,7 @@ double Trainer::band_finish(const double* nn_sums, double bits, double se, int* 
     CCB_CUDA(cudaMemcpyAsync(H_.tensor_ok, ok.data(), sizeof(int) * ok.size(),
                              cudaMemcpyHostToDevice, stream_));
     const double mse = se / double(3 * H_.npix_global);
-    const double cost = mse + H_.lambda * (bits / double(H_.npix_global));  // encoder.hpp:115
+    const double cost = std::fma(H_.lambda, bits / double(H_.npix_global), mse);  // encoder.hpp:115, as k_finalize
     h_scal_->bits = bits;
     h_scal_->mse = mse;
     h_scal_->cost = cost;
@@ -1252,10 +1299,11 @@ void Trainer::reset_batch_counters() {
     CCB_CUDA(cudaMemsetAsync(&H_.scal->halt, 0, sizeof(int), stream_));
 }
 
-cudaGraphExec_t Trainer::capture_batched_proxy(const Plan* d_plans, int batch) {
+cudaGraphExec_t Trainer::capture_batched_proxy(const Plan* d_plans, int batch, float* const* arm_cstages) {
     const LaunchCtx keep = L_;
     L_.plan = d_plans;
     L_.batch = batch;
+    L_.arm_cstages = arm_cstages;
     cudaGraph_t g;
     cudaGraphExec_t ex = nullptr;
     try {
@@ -1307,7 +1355,9 @@ void Batch::reserve_iterations(int n) {
     }
     if (!d_plans_) CCB_CUDA(cudaMalloc(&d_plans_, sizeof(Plan) * B));
     CCB_CUDA(cudaMemcpy(d_plans_, hp.data(), sizeof(Plan) * B, cudaMemcpyHostToDevice));
-    graph_ = t_[0]->capture_batched_proxy(d_plans_, int(B));
+    stages_.resize(B);
+    for (size_t b = 0; b < B; ++b) stages_[b] = hp[b].arm_cstage;
+    graph_ = t_[0]->capture_batched_proxy(d_plans_, int(B), stages_.data());
     cap_ = n;
 }
 

@@ -84,7 +84,7 @@ public:
     // batched images (cfg3): capture this trainer's proxy iteration as ONE graph
     // of launches over `batch` consecutive device plans (every kernel reads
     // pp[blockIdx.z]); the plans must share this trainer's geometry.
-    cudaGraphExec_t capture_batched_proxy(const Plan* d_plans, int batch);
+    cudaGraphExec_t capture_batched_proxy(const Plan* d_plans, int batch, float* const* arm_cstages);
     void upload_schedule(int n, const double* lr, const double* temp, const double* noise);
     void reset_batch_counters();
     const Plan& host_plan() const { return H_; }
@@ -203,6 +203,8 @@ private:
     Plan H_{};
     Plan* d_plan_ = nullptr;
     LaunchCtx L_{};
+    bool armc_on_ = false;   // the constant-bank ARM's launch geometry (cc_armc.cuh)
+    int armc_slot_ = -1;     // its constant slot (-1: none free, the FFMA2 tile kernel runs)
 
 
     std::vector<TensorInfo> tensors_;
@@ -233,6 +235,7 @@ private:
         int hg = 0, r0 = 0, r1 = 0, halo = 0;
     } band_;
     std::vector<int4> tiles_host_;
+    std::vector<int4> ifce_items_host_;  // k_ifce_dw work items (cc_arm.cu)
     std::vector<cudaGraphNode_t> low_nodes_;  // captured nodes to run at the least priority
 };
 
@@ -257,6 +260,7 @@ public:
 private:
     std::vector<Trainer*> t_;
     Plan* d_plans_ = nullptr;
+    std::vector<float*> stages_;  // each image's constant-bank ARM weight image (cc_armc.cuh)
     cudaGraphExec_t graph_ = nullptr;
     int cap_ = 0;
 };

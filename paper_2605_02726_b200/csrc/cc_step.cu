@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) k_finalize(const Plan* __restrict__ pp, i
     if (threadIdx.x != 0) return;
     const double bits = bits_all, se = se_all;
     const double mse = se / double(3 * P.npix_global);
-    const double cost = mse + P.lambda * (bits / double(P.npix_global));
+    const double cost = fma(P.lambda, bits / double(P.npix_global), mse);  // contracted (reference: -ffp-contract=fast)
     DevScalars* s = P.scal;
     s->bits = bits;
     s->mse = mse;
