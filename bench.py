@@ -308,7 +308,8 @@ def run_b200(args, rank, world, local_rank):
             traffic = json.loads(tf.read_text()).get("bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "fp32", "kernel": "k_arm2 (fused ARM+IFCE fwd/bwd, register-tiled)",
+    roofline = {"bound": "fp32", "kernel": "k_armc (ARM + IFCE fwd/bwd, weights in the constant bank; "
+                "timed with its weight pack and constant-slot fill)",
                 "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
                 "frac": achieved / peak.value, "traffic": traffic,
                 "flops_per_launch": arm_flops,

@@ -114,15 +114,24 @@ struct alignas(16) Smem {
     double red[NT / 32];
 };
 
-// job index -> family / groups
+// job index -> family / groups: the row-sum carriers (first B group of each
+// family) are jobs 0 .. 2 NGA (all in warp 0), so warp 1 skips the sums
 template <int DP, int WP>
 __device__ __forceinline__ void job_id(int j, int& fam, int& ga, int& gb) {
     using J = JB<DP, WP>;
-    if (j < J::N1) { fam = 0; ga = j / J::NGC; gb = j % J::NGC; return; }
-    j -= J::N1;
-    if (j < J::N2) { fam = 1; ga = j / J::NGW; gb = j % J::NGW; return; }
-    j -= J::N2;
-    fam = 2; ga = 0; gb = j;
+    if (j <= 2 * J::NGA) {
+        gb = 0;
+        fam = j < J::NGA ? 0 : (j < 2 * J::NGA ? 1 : 2);
+        ga = j < J::NGA ? j : (j < 2 * J::NGA ? j - J::NGA : 0);
+        return;
+    }
+    j -= 2 * J::NGA + 1;
+    constexpr int R1 = J::NGA * (J::NGC - 1), R2 = J::NGA * (J::NGW - 1);
+    if (j < R1) { fam = 0; ga = j / (J::NGC - 1); gb = 1 + j % (J::NGC - 1); return; }
+    j -= R1;
+    if (j < R2) { fam = 1; ga = j / (J::NGW - 1); gb = 1 + j % (J::NGW - 1); return; }
+    j -= R2;
+    fam = 2; ga = 0; gb = 1 + j;
 }
 
 template <int DP, int WP>
@@ -345,7 +354,7 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
                 h1[a] = make_float2(b, b);
             }
             const float* xp = &sm.C[0][l0];
-#pragma unroll 2
+#pragma unroll 4
             for (int k = 0; k < DP; ++k, xp += LT) {  // input outer (own column back from shared memory)
                 const float2 x = *reinterpret_cast<const float2*>(xp);
                 row_fma<WP>(x, W::W1T + k * WP, h1);
@@ -371,7 +380,7 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
                 h2[b] = make_float2(bb, bb);
             }
             const float* xp = &sm.H1[0][l0];
-#pragma unroll 2
+#pragma unroll 4
             for (int a = 0; a < WP; ++a, xp += LT) {
                 const float2 x = *reinterpret_cast<const float2*>(xp);
                 row_fma<WP>(x, W::W2T + a * WP, h2);
@@ -417,7 +426,7 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
 #pragma unroll
             for (int b = 0; b < WP; ++b) dh1[b] = make_float2(0.0f, 0.0f);
             const float* xp = &sm.DH2[0][l0];
-#pragma unroll 2
+#pragma unroll 4
             for (int a = 0; a < WP; ++a, xp += LT) {
                 const float2 x = *reinterpret_cast<const float2*>(xp);
                 row_fma<WP>(x, W::W2 + a * WP, dh1);
@@ -434,7 +443,7 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
 #pragma unroll
             for (int k = 0; k < DP; ++k) dc[k] = make_float2(0.0f, 0.0f);
             const float* xp = &sm.DH1[0][l0];
-#pragma unroll 2
+#pragma unroll 4
             for (int a = 0; a < WP; ++a, xp += LT) {
                 const float2 x = *reinterpret_cast<const float2*>(xp);
                 row_fma<DP>(x, W::W1 + a * DP, dc);

@@ -748,7 +748,9 @@ double ccb_arm_flops(cc_trainer* t) {
     for (int gi = 0; gi < P.n_grids; ++gi) {
         const double cnt = double(P.g[gi].rows) * P.g[gi].cols;
         macs += cnt * per;
-        if (P.g[gi].ifce_slot >= 0) macs += cnt * double(P.g[gi].rdim) * P.F;
+        // IFCE: forward + dF backward in the ARM kernel; its weight gradient
+        // is in the ARM kernel too unless k_ifce_dw takes it (Plan::ifce_sep)
+        if (P.g[gi].ifce_slot >= 0) macs += cnt * double(P.g[gi].rdim) * P.F * (P.ifce_sep ? 4.0 / 6.0 : 1.0);
     }
     return 6.0 * macs;
 }
