@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "cc_kernels.h"
 #include "cc_math.cuh"
@@ -91,6 +92,7 @@ struct JB {
     static constexpr int NJ = N1 + N2 + NH;
     static constexpr int NO = 4 * NB + 4;          // outputs per job
     static_assert(NJ <= 64, "one job per thread");
+    static_assert(2 * NGA + 1 <= 32, "the row-sum carriers fit in warp 0");
 };
 
 struct Job {
@@ -479,30 +481,36 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
                 for (int e = 0; e < 4 * NB; ++e) p[e] = make_float2(0.0f, 0.0f);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) s4[i] = make_float2(0.0f, 0.0f);
+                // the row-sum carriers are all in warp 0 (job_id): warp 1 runs
+                // the loop without the sums (a warp-uniform branch)
+                auto quads = [&](auto with_sums) {
 #pragma unroll 2
-                for (int q = 0; q < T / 4; ++q) {
-                    float4 av[4], bv[NB];
+                    for (int q = 0; q < T / 4; ++q) {
+                        float4 av[4], bv[NB];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) av[i] = *reinterpret_cast<const float4*>(jb.a[i] + 4 * q);
+                        for (int i = 0; i < 4; ++i) av[i] = *reinterpret_cast<const float4*>(jb.a[i] + 4 * q);
 #pragma unroll
-                    for (int c = 0; c < NB; ++c) bv[c] = *reinterpret_cast<const float4*>(jb.b[c] + 4 * q);
+                        for (int c = 0; c < NB; ++c) bv[c] = *reinterpret_cast<const float4*>(jb.b[c] + 4 * q);
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
+                        for (int i = 0; i < 4; ++i)
 #pragma unroll
-                        for (int c = 0; c < NB; ++c) {
-                            float2 t = p[i * NB + c];
-                            t = ffma2(make_float2(av[i].x, av[i].y), make_float2(bv[c].x, bv[c].y), t);
-                            t = ffma2(make_float2(av[i].z, av[i].w), make_float2(bv[c].z, bv[c].w), t);
-                            p[i * NB + c] = t;
-                        }
-                    if (sums) {
+                            for (int c = 0; c < NB; ++c) {
+                                float2 t = p[i * NB + c];
+                                t = ffma2(make_float2(av[i].x, av[i].y), make_float2(bv[c].x, bv[c].y), t);
+                                t = ffma2(make_float2(av[i].z, av[i].w), make_float2(bv[c].z, bv[c].w), t);
+                                p[i * NB + c] = t;
+                            }
+                        if (decltype(with_sums)::value && sums) {
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            s4[i] = fadd2(s4[i], make_float2(av[i].x, av[i].y));
-                            s4[i] = fadd2(s4[i], make_float2(av[i].z, av[i].w));
+                            for (int i = 0; i < 4; ++i) {
+                                s4[i] = fadd2(s4[i], make_float2(av[i].x, av[i].y));
+                                s4[i] = fadd2(s4[i], make_float2(av[i].z, av[i].w));
+                            }
                         }
                     }
-                }
+                };
+                if (tid < 32) quads(std::true_type{});
+                else quads(std::false_type{});
                 {
 #pragma unroll
                     for (int e = 0; e < 4 * NB; ++e) acc[e] += double(p[e].x + p[e].y);

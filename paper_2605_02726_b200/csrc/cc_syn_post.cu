@@ -54,17 +54,22 @@ struct alignas(16) PostSmem2 {
     float img[3][C::PL];
     float wf[C::NPL][3 * 27];    // forward weights  [co][ci][tap]
     float wb[C::NPL][3 * 27];    // transposed       [ci][co][flipped tap]
+    float2 wfp[C::NPL][27];      // (co 0, co 1) pairs of wf per [ci][tap]: FFMA2 operands
+    float2 wbp[C::NPL][27];      // the same for wb
     float bias[C::NPL][4];
     double red[NT / 32];
 };
 
 // out[co] over window W_h (virtual coords) from the 3 planes `in`:
 //   out = (bias) + sum_{ci,tap} wk[co][ci][tap] * in[ci][v + off(tap)] + in[co][v]
-// `wk` is [co][27] in shared memory; one thread = one column x RS rows.
+// `wk` is [co][27] in shared memory, `wkp` its (co 0, co 1) pairs per
+// [ci][tap]: output channels 0 and 1 are the two FFMA2 lanes (the input value
+// the broadcast operand), channel 2 a plain FMA — the per-channel order of
+// the terms (ci, then tap) is unchanged.  One thread = one column x RS rows.
 template <int NP, int h>
 __device__ __forceinline__ void conv_pass(const float* __restrict__ in, float* __restrict__ out,
-                                          const float* __restrict__ wk, const float* __restrict__ bias,
-                                          int tid) {
+                                          const float* __restrict__ wk, const float2* __restrict__ wkp,
+                                          const float* __restrict__ bias, int tid) {
     using C = PC<NP>;
     constexpr int w = TW + 2 * h, hh = TH + 2 * h;
     constexpr int NS = (NT / w) < hh ? (NT / w) : hh;
@@ -82,26 +87,42 @@ __device__ __forceinline__ void conv_pass(const float* __restrict__ in, float* _
 #pragma unroll
             for (int cc = 0; cc < 3; ++cc)
                 x[ci][rr][cc] = (ra - 1 + rr <= rb) ? in[ci * C::PL + (ra - 1 + rr) * C::PW + vc - 1 + cc] : 0.0f;
+    float2 v01[RS];
+    float v2[RS];
+    {
+        const float b0 = bias ? bias[0] : 0.0f, b1 = bias ? bias[1] : 0.0f, b2 = bias ? bias[2] : 0.0f;
 #pragma unroll
-    for (int co = 0; co < 3; ++co) {
-        float v[RS];
-        const float b = bias ? bias[co] : 0.0f;
+        for (int rr = 0; rr < RS; ++rr) {
+            v01[rr] = make_float2(b0, b1);
+            v2[rr] = b2;
+        }
+    }
 #pragma unroll
-        for (int rr = 0; rr < RS; ++rr) v[rr] = b;
+    for (int ci = 0; ci < 3; ++ci) {
+        float2 wp[9];
+        float w2[9];
 #pragma unroll
-        for (int ci = 0; ci < 3; ++ci) {
-            float wv[9];
-#pragma unroll
-            for (int q = 0; q < 9; ++q) wv[q] = wk[co * 27 + ci * 9 + q];
-#pragma unroll
-            for (int rr = 0; rr < RS; ++rr)
-#pragma unroll
-                for (int q = 0; q < 9; ++q) v[rr] = fmaf(wv[q], x[ci][rr + q / 3][q % 3], v[rr]);
+        for (int q = 0; q < 9; ++q) {
+            wp[q] = wkp[ci * 9 + q];
+            w2[q] = wk[2 * 27 + ci * 9 + q];
         }
 #pragma unroll
         for (int rr = 0; rr < RS; ++rr)
-            if (ra + rr < rb) out[co * C::PL + (ra + rr) * C::PW + vc] = v[rr] + x[co][rr + 1][1];
+#pragma unroll
+            for (int q = 0; q < 9; ++q) {
+                const float xv = x[ci][rr + q / 3][q % 3];
+                v01[rr] = ffma2(wp[q], make_float2(xv, xv), v01[rr]);
+                v2[rr] = fmaf(w2[q], xv, v2[rr]);
+            }
     }
+#pragma unroll
+    for (int rr = 0; rr < RS; ++rr)
+        if (ra + rr < rb) {
+            float* o = out + (ra + rr) * C::PW + vc;
+            o[0] = v01[rr].x + x[0][rr + 1][1];
+            o[C::PL] = v01[rr].y + x[1][rr + 1][1];
+            o[2 * C::PL] = v2[rr] + x[2][rr + 1][1];
+        }
 }
 
 template <int NP>
@@ -119,6 +140,9 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
             const int co = e / 27, ci = (e / 9) % 3, q = e % 9;
             sm.wf[i][e] = v;
             sm.wb[i][ci * 27 + co * 9 + (8 - q)] = v;
+            // FFMA2 pairs: wf as [ci][tap] (co 0 | co 1), wb as [co][flipped tap] (ci 0 | ci 1)
+            if (co < 2) reinterpret_cast<float*>(&sm.wfp[i][ci * 9 + q])[co] = v;
+            if (ci < 2) reinterpret_cast<float*>(&sm.wbp[i][co * 9 + (8 - q)])[ci] = v;
         }
         if (tid < 4) sm.bias[i][tid] = tid < 3 ? P.params[P.off_pb[i] + tid] : 0.0f;
     }
@@ -174,7 +198,7 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
         __syncthreads();
         // ---- forward posts ----
         if constexpr (NP >= 1) {
-            conv_pass<NP, 2 * NP - 1>(sm.p[0][0], sm.p[1][0], sm.wf[0], sm.bias[0], tid);
+            conv_pass<NP, 2 * NP - 1>(sm.p[0][0], sm.p[1][0], sm.wf[0], sm.wfp[0], sm.bias[0], tid);
             __syncthreads();
             if (border) {  // re-clamp p_1 outside the image
                 constexpr int h = 2 * NP - 1;
@@ -191,7 +215,7 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
             }
         }
         if constexpr (NP >= 2) {
-            conv_pass<NP, 2 * NP - 2>(sm.p[1][0], sm.p[2][0], sm.wf[1], sm.bias[1], tid);
+            conv_pass<NP, 2 * NP - 2>(sm.p[1][0], sm.p[2][0], sm.wf[1], sm.wfp[1], sm.bias[1], tid);
             __syncthreads();
             // p_2 is only read on W_NP by the x̂ pass and in-image by dW: no re-clamp
         }
@@ -230,13 +254,13 @@ __global__ void __launch_bounds__(NT, 2) k_syn_post2(const Plan* __restrict__ pp
         auto back = [&](auto hconst, int i) {
             constexpr int hi = decltype(hconst)::value;  // window of d_i
             if (!border) {
-                conv_pass<NP, hi>(sm.d[i + 1][0], sm.d[i][0], sm.wb[i], nullptr, tid);
+                conv_pass<NP, hi>(sm.d[i + 1][0], sm.d[i][0], sm.wb[i], sm.wbp[i], nullptr, tid);
                 __syncthreads();
                 return;
             }
             // border tile: compute on W_{i+1} (covers the ring outside the
             // image next to W_i), fold the ring onto the edge, zero it
-            conv_pass<NP, hi + 1>(sm.d[i + 1][0], sm.d[i][0], sm.wb[i], nullptr, tid);
+            conv_pass<NP, hi + 1>(sm.d[i + 1][0], sm.d[i][0], sm.wb[i], sm.wbp[i], nullptr, tid);
             __syncthreads();
             constexpr int w = TW + 2 * hi, hh = TH + 2 * hi;
             float acc[3][3];
