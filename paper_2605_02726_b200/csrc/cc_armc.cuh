@@ -112,9 +112,27 @@ struct alignas(16) Smem {
     float DR[2][LT];
     float ZR[LT];                 // zero row (padding operand)
     GridGeom geo[kMaxGrids];
-    int cdy[DP], cdx[DP];
+    int coff[kMaxGrids][DP];      // context offset o of grid gi: dy * padded stride + dx
+    int64_t rsrc[2][kRM];         // IFCE source rows of the tile (double-buffered by tile parity):
+    int rsh[2][kRM];              //   yhat_pad offset of the source row, column shift
     double red[NT / 32];
 };
+
+// the IFCE source rows of tile `tile` (threads t0, t0 + step, ...): the row
+// of source grid j that latent row r maps to (global rows, clamped to the
+// band window, entropy_model.hpp:239-244) and the column shift
+template <int DP, int WP>
+__device__ __forceinline__ void ifce_rows(const Plan& P, Smem<DP, WP>& sm, int4 tile, int buf, int t0, int step) {
+    const GridGeom& g = sm.geo[tile.x];
+    if (g.ifce_slot < 0) return;
+    for (int j = t0; j < g.rdim; j += step) {
+        const GridGeom& sg = sm.geo[j];
+        const int sh = sg.level - g.level;
+        const int rs = min(max(((g.row0 + tile.z) >> sh) - sg.row0, 0), sg.rows - 1);
+        sm.rsrc[buf][j] = sg.pad_base + int64_t(rs) * sg.stride;
+        sm.rsh[buf][j] = sh;
+    }
+}
 
 // job index -> family / groups: the row-sum carriers (first B group of each
 // family) are jobs 0 .. 2 NGA (all in warp 0), so warp 1 skips the sums
@@ -273,11 +291,13 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
         constexpr int NR = DP + 4 * WP + 2 + 1;
         for (int e = tid; e < NR * LT; e += NT) rows[e] = 0.0f;
         for (int e = tid; e < P.n_grids; e += NT) sm.geo[e] = P.g[e];
-        for (int e = tid; e < DP; e += NT) {
-            sm.cdy[e] = e < S ? P.ctx_dy[e] : 0;
-            sm.cdx[e] = e < S ? P.ctx_dx[e] : 0;
+        for (int e = tid; e < kMaxGrids * DP; e += NT) {
+            const int gi = e / DP, o = e % DP;
+            sm.coff[gi][o] = (gi < P.n_grids && o < S) ? P.ctx_dy[o] * P.g[gi].stride + P.ctx_dx[o] : 0;
         }
     }
+    __syncthreads();
+    if (blockIdx.x < ntiles) ifce_rows(P, sm, tiles[blockIdx.x], 0, tid, NT);
     __syncthreads();
 
     // this thread's weight-gradient job (one per thread, persistent fp64
@@ -290,7 +310,8 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
     const float upstream = P.rate_upstream;
     const int l0 = 2 * tid;
 
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int par = 0;  // tile parity: rsrc / rsh buffer of the current tile
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, par ^= 1) {
         const int4 tile = tiles[t];
         const GridGeom& g = sm.geo[tile.x];
         const int r = tile.z, len = tile.w, c0 = tile.y - r * g.cols;
@@ -308,7 +329,7 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
 #pragma unroll
             for (int o = 0; o < DP; ++o) {
                 if (o < S) {
-                    const int off = sm.cdy[o] * stride + sm.cdx[o];
+                    const int off = sm.coff[tile.x][o];
                     cx[o] = make_float2(v0 ? __ldg(rowp + off + cA) : 0.0f, v1 ? __ldg(rowp + off + cB) : 0.0f);
                 }
             }
@@ -323,10 +344,17 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
             for (int j = 0; j < kRM; ++j) {
                 rv[j] = make_float2(0.0f, 0.0f);
                 if (j < g.rdim) {
-                    const GridGeom& sg = sm.geo[j];
-                    const int sh = sg.level - g.level;
-                    const int rs = min(max(((g.row0 + r) >> sh) - sg.row0, 0), sg.rows - 1);
-                    const float* src = P.yhat_pad + sg.pad_base + int64_t(rs) * sg.stride;
+                    const float* src;
+                    int sh;
+                    if (MODE == kArmForward) {  // no per-tile barrier in this mode: rows computed here
+                        const GridGeom& sg = sm.geo[j];
+                        sh = sg.level - g.level;
+                        const int rs = min(max(((g.row0 + r) >> sh) - sg.row0, 0), sg.rows - 1);
+                        src = P.yhat_pad + sg.pad_base + int64_t(rs) * sg.stride;
+                    } else {
+                        src = P.yhat_pad + sm.rsrc[par][j];
+                        sh = sm.rsh[par][j];
+                    }
                     rv[j] = make_float2(v0 ? __ldg(src + (cA >> sh)) : 0.0f, v1 ? __ldg(src + (cB >> sh)) : 0.0f);
                 }
             }
@@ -457,10 +485,11 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
             }
             const int64_t count = int64_t(g.rows) * g.cols;
             const int64_t li = int64_t(tile.y) + l0;
+            float* dcp = P.dctx + g.dctx_off + li;
 #pragma unroll
-            for (int k = 0; k < DP; ++k) {
+            for (int k = 0; k < DP; ++k, dcp += count) {
                 if (k < S) {
-                    if (MODE == kArmProxy) store2(P.dctx + g.dctx_off + int64_t(k) * count + li, dc[k], v0, v1);
+                    if (MODE == kArmProxy) store2(dcp, dc[k], v0, v1);
                 } else if (k < S + F && slot >= 0) {
                     // dF: the dR pyramid (k_pyramid_fused) and the IFCE weight gradient (k_ifce_dw)
                     const float2 dv = make_float2(v0 ? dc[k].x : 0.0f, v1 ? dc[k].y : 0.0f);
@@ -470,7 +499,10 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
         }
         __syncthreads();  // every activation row of the tile is in shared memory
 
-        // ---- P7: this thread's weight-gradient job over the tile ----
+        // ---- P7: this thread's weight-gradient job over the tile; the
+        // threads without a job prepare the next tile's IFCE source rows ----
+        if (!has_job && t + int(gridDim.x) < ntiles)
+            ifce_rows(P, sm, tiles[t + gridDim.x], par ^ 1, tid - J::NJ, NT - J::NJ);
         if (has_job) {
             const Job jb = job_rows<DP, WP>(sm, tid);
             {
