@@ -631,11 +631,11 @@ __global__ void __launch_bounds__(NT, 2) k_arm2(const Plan* __restrict__ pp,
         }
         if (o >= 0) row[o - R.param_off] = v;
     }
-    for (int s = 0; s < P.n_slots; ++s) {
+    for (int s = 0; s < (P.ifce_sep ? 0 : P.n_slots); ++s) {  // ifce_sep: k_ifce_dw's own region
         const int rd = P.g[P.slot_gi[s]].rdim;
         for (int e = tid; e < F * (rd + 1); e += NT) {
             const int f = e / (rd + 1), b = e % (rd + 1);
-            const double v = P.ifce_sep ? 0.0 : sm.acc5[(s * kFM + f) * (kRM + 1) + (b < rd ? b : kRM)];
+            const double v = sm.acc5[(s * kFM + f) * (kRM + 1) + (b < rd ? b : kRM)];
             const int o = b < rd ? P.off_ifw[s] + f * rd + b : P.off_ifb[s] + f;
             row[o - R.param_off] = v;
         }

@@ -600,15 +600,7 @@ __global__ void __launch_bounds__(NT, 4) k_armc(const Plan* __restrict__ pp, con
             }
         }
     }
-    // the IFCE weight gradients come from k_ifce_dw (Plan::ifce_sep): zeros here
-    for (int s = 0; s < P.n_slots; ++s) {
-        const int rd = P.g[P.slot_gi[s]].rdim;
-        for (int e = tid; e < F * (rd + 1); e += NT) {
-            const int f = e / (rd + 1), b = e % (rd + 1);
-            const int o = b < rd ? P.off_ifw[s] + f * rd + b : P.off_ifb[s] + f;
-            row[o - R.param_off] = 0.0;
-        }
-    }
+    // (the IFCE weight gradients: k_ifce_dw's own region, Plan::ifce_sep)
 }
 
 // the padded constant image of each image's ARM weights (one thread per entry)

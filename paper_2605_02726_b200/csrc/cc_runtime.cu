@@ -517,11 +517,11 @@ void Trainer::build_plan() {
         pbase += int64_t(count) * nblocks;
         return r;
     };
-    P.arm_nvals = P.off_tconv[0];
-    P.reg_arm = region(0, P.arm_nvals, L_.arm_blocks);
     // constant-bank ARM: the IFCE weight gradients come from k_ifce_dw (its
-    // own partial rows; the ARM kernels write zeros for those parameters)
+    // own partial rows); the ARM's region then ends before them
     P.ifce_sep = (armc_on_ && P.n_slots > 0 && P.F > 0) ? 1 : 0;
+    P.arm_nvals = P.ifce_sep ? P.off_ifw[0] : P.off_tconv[0];
+    P.reg_arm = region(0, P.arm_nvals, L_.arm_blocks);
     for (int s = 0; s < kMaxSlots; ++s) P.reg_ifce[s] = -1;
     P.n_ifce_items = 0;
     ifce_items_host_.clear();
