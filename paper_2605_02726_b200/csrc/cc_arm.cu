@@ -777,34 +777,27 @@ bool armc_supported(int Dp, int Wp) {
     return arm_env() == 0 && ((Dp == 20 && Wp == 20) || (Dp == 32 && Wp == 20));
 }
 
-// Slots are handed out to trainers for their lifetime.  When all are taken
-// a trainer SHARES one (round robin): its weights and the other owner's then
-// pass through the same constant slot, which is safe as long as the two do
-// not run an ARM at the same time on different streams — true inside the
-// library (a batch runs its images one after another on one stream; the band
-// trainers of one image hold bit-identical weights), and documented for
-// callers that run more than kArmcSlots independent trainers concurrently.
+// Slots are handed out to trainers for their lifetime, exclusively: a
+// trainer created while all 8 are taken runs the FFMA2 tile kernel
+// (cc_arm2.cu) on the same launch geometry — correct, slower — so any number
+// of trainers may run concurrently on any streams.
 static std::mutex g_armc_mu;
-static int g_armc_users[kArmcSlots] = {};
-static int g_armc_rr = 0;
+static bool g_armc_used[kArmcSlots] = {};
 
 int armc_acquire_slot() {
     std::lock_guard<std::mutex> lk(g_armc_mu);
     for (int s = 0; s < kArmcSlots; ++s)
-        if (g_armc_users[s] == 0) {
-            g_armc_users[s] = 1;
+        if (!g_armc_used[s]) {
+            g_armc_used[s] = true;
             return s;
         }
-    const int s = g_armc_rr;
-    g_armc_rr = (g_armc_rr + 1) % kArmcSlots;
-    ++g_armc_users[s];
-    return s;
+    return -1;
 }
 
 void armc_release_slot(int slot) {
     if (slot < 0 || slot >= kArmcSlots) return;
     std::lock_guard<std::mutex> lk(g_armc_mu);
-    if (g_armc_users[slot] > 0) --g_armc_users[slot];
+    g_armc_used[slot] = false;
 }
 
 void armc_configure(int Dp, int Wp) {

@@ -95,7 +95,7 @@ constexpr int kArmcSlotFloats = 2560;
 constexpr int kArmcPerSm = 4;       // 64-thread CTAs per SM (at most)
 bool armc_supported(int Dp, int Wp);
 int armc_blocks_per_sm(int Dp, int Wp);
-int armc_acquire_slot();             // a free slot, else a shared one (cc_arm.cu)
+int armc_acquire_slot();             // a free slot, or -1 (then the FFMA2 tile kernel runs)
 void armc_release_slot(int slot);
 void armc_configure(int Dp, int Wp);
 

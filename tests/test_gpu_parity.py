@@ -345,6 +345,31 @@ def test_bitwise_determinism(gpu_lib):
         assert np.array_equal(a, b)
 
 
+def test_more_trainers_than_constant_slots(gpu_lib, ref_lib):
+    """The constant-bank ARM hands out 8 constant slots exclusively; a ninth
+    live trainer runs the FFMA2 tile ARM on the same launch geometry.  Both
+    match the reference lock-step (the golden-free 64x96 HOP iteration), the
+    slot-less one also after the others are gone, and slots are reused."""
+    img = make_image(gpu_lib, 64, 96, seed=4)
+    enc = EncoderConfig(use_soap=False, lmbda=1e-3, seed=3)
+    with Trainer(img, enc, DecoderConfig.hop(), lib=ref_lib) as tr_r:
+        tr_r.fresh_candidate(0)
+        ref = [tr_r.proxy_iteration(1e-2, 0.35, 0.22) for _ in range(3)]
+    trs = [Trainer(img, enc, DecoderConfig.hop(), lib=gpu_lib) for _ in range(9)]
+    try:
+        for t in (trs[0], trs[8]):  # a slot holder and the slot-less ninth
+            t.fresh_candidate(0)
+            got = [t.proxy_iteration(1e-2, 0.35, 0.22) for _ in range(3)]
+            assert np.allclose(got, ref, rtol=1e-5, atol=0), (got, ref)
+    finally:
+        for t in trs:
+            t.close()
+    for _ in range(10):  # released slots are handed out again
+        with Trainer(img, enc, DecoderConfig.hop(), lib=gpu_lib) as t:
+            t.fresh_candidate(0)
+            assert abs(t.proxy_iteration(1e-2, 0.35, 0.22) - ref[0]) <= 1e-5 * abs(ref[0])
+
+
 def test_nonfinite_cost_returned_not_stepped(gpu_lib):
     # encoder.hpp:118: a non-finite cost is returned; no step, global_iter kept
     img = make_image(gpu_lib, 32, 48, seed=2)
