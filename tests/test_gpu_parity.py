@@ -832,11 +832,13 @@ def test_cfg2_full_schedule_within_reference_spread(gpu_lib):
     assert abs(rel.mean()) <= max(2.5 * se, 5e-3) and abs(rel.mean()) <= 0.03, (rel.mean(), se)
 
 
-@pytest.mark.parametrize("variant", [{"CCB_ARM": "tc"}, {"CCB_CTX_PART": "1"},
+@pytest.mark.parametrize("variant", [{"CCB_ARM": "2"}, {"CCB_ARM": "tc"}, {"CCB_CTX_PART": "1"},
                                      {"CCB_ARM": "tc", "CCB_CTX_PART": "1"},
                                      {"CCB_UPS_CHAIN": "2", "CCB_UPS_CHAIN_CL": "16"}])
 def test_arm_variant_parity(gpu_lib, ref_lib, variant):
-    """The opt-in variants — the tcgen05 ARM (cc_arm_tc.cu, CCB_ARM=tc), the
+    """The opt-in variants — the FFMA2 tile ARM (cc_arm2.cu, CCB_ARM=2; the
+    default is the constant-bank ARM, cc_armc.cuh), the tcgen05 ARM
+    (cc_arm_tc.cu, CCB_ARM=tc), the
     context gradient as row partials (cc_ctx.cuh, CCB_CTX_PART=1) and the
     coarse upsampling stages as cluster launches (cc_ups.cu, CCB_UPS_CHAIN): the
     golden lock-step cases and a truth-arbitrated 512x768 lock-step against
