@@ -2,33 +2,33 @@
 // entropy_model.hpp:180-336) with the weights in the CONSTANT BANK.
 //
 // Included by cc_armc_s<k>.cu with CCB_ARMC_SLOT = k: every translation unit
-// owns one constant slot (c_armw, 6 KB) and instantiates the kernels that read
-// it, so a kernel's weight operands are compile-time constant-bank addresses.
+// owns one constant slot (c_armw, 10 KB) and instantiates the kernels that
+// read it, so a kernel's weight operands are constant-bank addresses known at
+// compile time (unrolled code) or uniform-register relative (the rolled layer
+// loops).  A per-thread runtime slot index would compile to LDC and run 5-15x
+// slower (tools/micro/const_ffma.cu).
 //
 // Execution shape (one CTA = 64 threads = one 128-latent row-segment tile at a
 // time, persistent over the tile list):
 //   * a thread carries TWO adjacent latents through the whole chain in
 //     registers — context gather, IFCE, l1, l2, head, Laplace rate and its
 //     backward, dH2, dH1, dC — as packed FFMA2 with the two latents as the two
-//     lanes and the weight as a (w, w) uniform-register pair loaded straight
-//     from the constant bank (LDCU): no shared-memory traffic for weights, no
-//     barrier inside the chain (measured probe, tools/micro/const_ffma.cu: a
-//     20x20 layer chain at 57-66 TFLOP/s on the B200, vs 11 TFLOP/s for the
-//     whole shared-memory-tiled ARM of cc_arm2.cu);
+//     lanes and the weight as a uniform-register scalar loaded straight from
+//     the constant bank (LDCU; SASS FFMA2 R, R.F32x2, UR.F32, R): no shared-
+//     memory traffic for weights, no barrier inside the chain (probe: a 20x20
+//     layer chain at 57-66 TFLOP/s on the B200);
 //   * the chain leaves its activations FEATURE-MAJOR in shared memory ([row]
-//     [latent], latents contiguous): C, H1, H2, dH1, dH2, draw, dF, R;
-//   * the weight gradients are 4x4 register micro-tiles over the latent axis
-//     (dW1 = dH1 x C, dW2 = dH2 x H1, head = draw x [H2|C], IFCE = dF x R; the
-//     bias rows = row sums, folded into the first column group of each
-//     family).  The tile's 32 latent quads of every job are split evenly over
-//     the 64 threads; a job spans at most two threads, whose partials the
-//     owner (the thread holding the job's first quad) adds in a fixed order
-//     into fp64 accumulators that live in its registers across all tiles of
-//     the CTA — deterministic, no atomics;
-//   * per CTA one fp64 partial row of every ARM/IFCE parameter (k_nn_reduce
-//     sums the rows in order) and one fp64 bits partial.
-// Same outputs as cc_arm2.cu: dC as S planes (dctx), dF planes (dfeat), the
-// own-value gradient (gown), bits_part, the ARM partial region.
+//     [latent], latents contiguous): C, H1, H2, dH1, dH2, draw;
+//   * the weight gradients are ONE job per thread: a 4 x NB register
+//     micro-tile over the tile's latent axis (dW1 = dH1 x C, dW2 = dH2 x H1,
+//     head = draw x [H2 | C]; the bias rows = row sums of the A rows, in the
+//     first column group of each family), accumulated in fp64 registers
+//     across all tiles of the CTA — deterministic, no atomics;
+//   * per CTA one fp64 partial row of every ARM parameter (k_nn_reduce sums
+//     the rows in order) and one fp64 bits partial.  The IFCE weight
+//     gradients come from the dF pyramid (k_ifce_dw, cc_arm.cu).
+// Same data outputs as cc_arm2.cu: dC as S planes (dctx), dF planes (dfeat),
+// the own-value gradient (gown), bits_part.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -57,7 +57,7 @@ constexpr int kSlotFloats = 2560;
 // constant-slot layout (floats), padded dims, zero padded.  Every dense
 // layer's weights are stored with the OUTPUT index contiguous, in the order
 // the layer loop walks them (input outer, rolled; outputs inner, unrolled):
-// one LDCU.128 lands four (w, w) pairs' worth of weights.
+// consecutive outputs read consecutive constant words.
 template <int DP, int WP>
 struct CL {
     static constexpr int W1T = 0;                // [DP][WP]  l1.w[a][k] at (k, a): forward
