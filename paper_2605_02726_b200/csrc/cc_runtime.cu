@@ -488,13 +488,15 @@ void Trainer::build_plan() {
                                             : arm_occ >= 2          ? num_sms_ * 3 / 2
                                                                     : num_sms_ * arm_occ);
     if (armc_on_) {
-        // 3.5 CTAs per SM when 4 fit: the free slot on half the SMs lets the
-        // concurrent distortion branch start its kernels beside the ARM
-        // (512x768: 4 per SM 0.439 ms per iteration, 3.5 0.427, 3 0.430)
-        int per2 = 2 * armc_blocks_per_sm(P.Dp, P.Wp);
-        if (per2 >= 8) per2 = 7;
-        if (const char* e = std::getenv("CCB_ARMC_OCC")) per2 = 2 * std::max(1, std::min(per2 / 2, std::atoi(e)));
-        L_.arm_blocks = std::min(L_.arm_ntiles, num_sms_ * per2 / 2);
+        // 3.25 CTAs per SM when 4 fit: the free slots on three quarters of
+        // the SMs let the concurrent distortion branch (the critical chain)
+        // run its kernels beside the ARM (512x768, the kernel at <= 168
+        // registers: 4 per SM 0.439 ms per iteration, 3.5 0.420, 3.25 0.413,
+        // 3 0.424)
+        int per4 = 4 * armc_blocks_per_sm(P.Dp, P.Wp);
+        if (per4 >= 16) per4 = 13;
+        if (const char* e = std::getenv("CCB_ARMC_OCC")) per4 = 4 * std::max(1, std::min(per4 / 4, std::atoi(e)));
+        L_.arm_blocks = std::min(L_.arm_ntiles, num_sms_ * per4 / 4);
     }
     if (const char* e = std::getenv("CCB_ARM_CTAS"))  // A/B: explicit persistent CTA count
         L_.arm_blocks = std::max(1, std::min(L_.arm_ntiles, std::atoi(e)));
