@@ -275,12 +275,12 @@ __device__ __forceinline__ void ifce_fwd(const float2 (&rv)[kRM], int F, float2 
     }
 }
 
-// register budget: 168 for the (20,20) kernel (__launch_bounds__ min 5 CTAs:
-// a few spills, the same speed, and room beside it for the concurrent
-// distortion kernels: 0.420 -> 0.413 ms per iteration at 512x768); the
+// register budget: 168 for the (20,20) kernel (__launch_bounds__ min 6 CTAs:
+// 128 bytes of spills, the same speed, and room beside it for the concurrent
+// distortion kernels: 0.420 -> 0.412 ms per iteration at 512x768); the
 // (32,20) kernel keeps its 227 (spilling it costs 9 %)
 template <int DP, int WP, int MODE>
-__global__ void __launch_bounds__(NT, DP > WP ? 4 : 5) k_armc(const Plan* __restrict__ pp, const int4* __restrict__ tiles,
+__global__ void __launch_bounds__(NT, DP > WP ? 4 : 6) k_armc(const Plan* __restrict__ pp, const int4* __restrict__ tiles,
                                                 int ntiles) {
     using W = CL<DP, WP>;
     using J = JB<DP, WP>;
