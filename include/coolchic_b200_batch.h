@@ -26,7 +26,8 @@ typedef struct cc_batch cc_batch;
 
 /* n trainers (borrowed; they must outlive the batch) of the same device, image
  * size, decoder and optimizer, each with a candidate loaded.  They are moved
- * onto the first trainer's CUDA stream. */
+ * onto the first trainer's CUDA stream until cc_batch_destroy, which moves
+ * them back onto their own streams. */
 int cc_batch_create(cc_trainer* const* trainers, int n, cc_batch** out);
 void cc_batch_destroy(cc_batch* b);
 /* size every trainer's record buffer for n iterations and instantiate the

@@ -131,7 +131,10 @@ void Trainer::init(const float* image, int h, int w) {
 
 Trainer::~Trainer() {
     cudaSetDevice(device_);
-    if (stream_) cudaStreamSynchronize(stream_);
+    // a trainer moved onto another's stream (a batch) must not touch that
+    // stream here: its owner may be gone already
+    if (stream_ && stream_ == own_stream_) cudaStreamSynchronize(stream_);
+    else if (stream_) cudaDeviceSynchronize();
     armc_release_slot(armc_slot_);
     for (auto& kv : graphs_) cudaGraphExecDestroy(kv.second);
     for (auto& kv : cands_) {
@@ -1344,6 +1347,13 @@ Batch::Batch(std::vector<Trainer*> trainers) : t_(std::move(trainers)) {
 Batch::~Batch() {
     if (graph_) cudaGraphExecDestroy(graph_);
     if (d_plans_) cudaFree(d_plans_);
+    // every trainer back on its own stream (they were moved onto trainers[0]'s)
+    for (size_t b = 1; b < t_.size(); ++b) {
+        try {
+            t_[b]->set_stream(nullptr);
+        } catch (...) {
+        }
+    }
 }
 
 void Batch::reserve_iterations(int n) {
