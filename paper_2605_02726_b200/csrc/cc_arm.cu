@@ -821,28 +821,19 @@ void launch_arm(const LaunchCtx& L, int mode) {
         return e && e[0] == '1';
     }();
     if (skip) return;
-    if (L.arm_cslot >= 0) {
-        g_armc_launch[L.arm_cslot](L, mode);
-        // hardround: the IFCE weight gradients need the dF pyramid (the proxy
-        // iteration launches it after the ARM anyway)
-        if (mode == kArmHard) launch_pyramid(L);
-        return;
-    }
-    struct IfceAfter {  // the tile kernels below write zeros for the IFCE parameters when ifce_sep
-        const LaunchCtx& L;
-        int mode;
-        ~IfceAfter() {
-            if (mode == kArmHard && L.host->ifce_sep) launch_pyramid(L);
-        }
-    } ifce_after{L, mode};
-    if (use_tc(Dp, Wp)) return launch_arm_tc(L, mode);
-    if (use_arm2(Dp, Wp)) return launch_arm2(L, mode);
-    if (Dp == 8 && Wp == 8) launch_arm_mode<8, 8>(L, mode);
+    if (L.arm_cslot >= 0) g_armc_launch[L.arm_cslot](L, mode);
+    else if (use_tc(Dp, Wp)) launch_arm_tc(L, mode);
+    else if (use_arm2(Dp, Wp)) launch_arm2(L, mode);
+    else if (Dp == 8 && Wp == 8) launch_arm_mode<8, 8>(L, mode);
     else if (Dp == 16 && Wp == 12) launch_arm_mode<16, 12>(L, mode);
     else if (Dp == 20 && Wp == 20) launch_arm_mode<20, 20>(L, mode);
     else if (Dp == 28 && Wp == 28) launch_arm_mode<28, 28>(L, mode);
     else if (Dp == 32 && Wp == 20) launch_arm_mode<32, 20>(L, mode);
     else launch_arm_mode<40, 40>(L, mode);
+    // Plan::ifce_sep: the IFCE weight gradients come from the dF pyramid
+    // (k_ifce_dw); the proxy iteration launches the pyramid after the ARM
+    // anyway, a hardround iteration needs it here
+    if (mode == kArmHard && L.host->ifce_sep) launch_pyramid(L);
 }
 
 int arm_blocks_per_sm(int Dp, int Wp) {
